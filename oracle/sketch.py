@@ -1,0 +1,25 @@
+"""Row sketch X = Gamma A (TEST INFRASTRUCTURE ONLY).
+
+Paper: Algorithm 2 line 2 "Construct a row sketch X = Gamma A";
+Table 1 for the cost model.  The oracle forms Gamma explicitly
+(oracle.omega) and multiplies -- the definition written out, with the library
+matmul as the one step (no blocking or reordering of the method).
+
+Layout: A is an (m, n) float64 array; X is returned as an (l, n) array.
+"""
+import numpy as np
+
+from . import omega
+
+
+def sketch(A, l, kind="gaussian", seed=0, zeta=8):
+    """X = Gamma A with Gamma from oracle.omega (P:176 / P:182)."""
+    A = np.asarray(A, dtype=np.float64)
+    m = A.shape[0]
+    G = omega.embedding(kind, seed, l, m, zeta)
+    return G @ A
+
+
+def sketch_columns(A_cols, l, kind="gaussian", seed=0, zeta=8):
+    """X[:, J] for a sample of columns A[:, J] (same Gamma; used for full-size spot checks)."""
+    return sketch(A_cols, l, kind, seed, zeta)

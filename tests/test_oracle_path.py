@@ -1,0 +1,305 @@
+"""Oracle pins for sketch, LUPP, CPQR, ID coefficients and residuals.
+
+Each test pins an oracle function to something other than itself: a closed form,
+a worked example (SPEC S:170, S:185, S:369 -- derived by hand in the test),
+a paper statement (Lemma 2, Theorem 4.1, Remark 2.1), an independent
+library routine (LAPACK getrf/geqp3/lstsq/solve via scipy/numpy) on tie-free
+inputs, or brute force on tiny inputs.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+from inputs import haar, kahan_witness, make_c1, make_lowrank
+from oracle import cpqr, idcoef, lupp, omega, residual, sketch
+
+U_RND = 2.0 ** -53
+
+
+# ----------------------------------------------------------------------------- sketch
+def test_sketch_closed_forms():
+    l, m, n = 12, 30, 7
+    G = omega.gaussian(4, l, m)
+    assert np.array_equal(sketch.sketch(np.zeros((m, n)), l, "gaussian", 4), np.zeros((l, n)))
+    np.testing.assert_allclose(sketch.sketch(np.eye(m), l, "gaussian", 4), G, rtol=0, atol=0)
+    E = np.zeros((m, n)); E[5, 3] = 1.0            # A = e_i e_j^T  =>  X(:, j) = Gamma(:, i)
+    X = sketch.sketch(E, l, "gaussian", 4)
+    np.testing.assert_array_equal(X[:, 3], G[:, 5])
+    assert np.count_nonzero(X[:, [0, 1, 2, 4, 5, 6]]) == 0
+
+
+def test_sketch_linearity_and_rank():
+    rng = np.random.default_rng(0)
+    m, n, l = 60, 40, 10
+    A, B = rng.standard_normal((m, n)), rng.standard_normal((m, n))
+    for kind in ("gaussian", "sparse_sign"):
+        XA = sketch.sketch(A, l, kind, 9)
+        XB = sketch.sketch(B, l, kind, 9)
+        XAB = sketch.sketch(2 * A - 3 * B, l, kind, 9)
+        np.testing.assert_allclose(XAB, 2 * XA - 3 * XB, atol=1e-12)
+    # Lemma 1: rank-r A, l <= r  =>  X full row rank; rank-r A, l > r => rank r
+    Ar = make_lowrank(m, n, np.array([3.0, 2.0, 1.0, 0.5]), rng)
+    X = sketch.sketch(Ar, 3, "gaussian", 1)
+    s = np.linalg.svd(X, compute_uv=False)
+    assert s[-1] > 1e-10 * s[0]
+    X = sketch.sketch(Ar, 8, "gaussian", 1)
+    s = np.linalg.svd(X, compute_uv=False)
+    assert s[4] < 1e-12 * s[0]
+
+
+def test_sparse_sketch_is_signed_row_sums():
+    rng = np.random.default_rng(2)
+    m, n, l, z = 50, 6, 16, 8
+    A = rng.standard_normal((m, n))
+    rows, signs = omega.sparse_sign_structure(3, l, m, z)
+    X = np.zeros((l, n))
+    for i in range(m):                                  # scatter form, independent of the matmul
+        for j in range(z):
+            X[rows[i, j]] += signs[i, j] * A[i] / math.sqrt(z)
+    np.testing.assert_allclose(sketch.sketch(A, l, "sparse_sign", 3, z), X, atol=1e-13)
+
+
+# ----------------------------------------------------------------------------- LUPP
+def test_lupp_spec_2x2_case():
+    # X = [[4,2],[1,3]] -> pivots [1,2] (1-based), L_l = [[4,0],[1,2.5]], R = [[1,.5],[0,1]].
+    X = np.array([[4.0, 2.0], [1.0, 3.0]])
+    piv, Lf, U, _ = lupp.select_cols(X, 2)
+    assert piv.tolist() == [0, 1]
+    np.testing.assert_array_equal(U.T, [[4.0, 0.0], [1.0, 2.5]])          # L_l = U^T
+    np.testing.assert_array_equal(Lf.T, [[1.0, 0.5], [0.0, 1.0]])         # R^{LU} = Lf^T
+
+
+def test_lupp_identity_and_ties_lowest_original_index():
+    piv, _, _, _ = lupp.select_cols(np.eye(6), 6)
+    assert piv.tolist() == list(range(6))
+    # tie demo: lowest ORIGINAL index wins -> [2, 0]; LAPACK's swapped order gives [2, 1]
+    X = np.array([[1.0, 1.0, 3.0], [5.0, -5.0, 0.0]])
+    piv, _, _, _ = lupp.select_cols(X, 2)
+    assert piv.tolist() == [2, 0]
+
+
+def test_lupp_factorization_and_bounds():
+    rng = np.random.default_rng(5)
+    for (n, k) in [(50, 8), (200, 30), (31, 31)]:
+        X = rng.standard_normal((k + 3, n))
+        piv, Lf, U, gaps = lupp.select_cols(X, k)
+        assert len(set(piv.tolist())) == k
+        assert np.max(np.abs(Lf)) <= 1.0 + 1e-15                        # |R^{LU}| <= 1
+        np.testing.assert_array_equal(Lf[piv, np.arange(k)], 1.0)
+        L1 = Lf[piv]
+        assert np.all(np.triu(L1, 1) == 0)                              # unit lower in pivot order
+        M = X[:k].T
+        err = np.max(np.abs(M - Lf @ U))
+        assert err <= 8 * k * U_RND * np.max(np.abs(M)) * 10
+        assert np.all(np.tril(U, -1) == 0)
+        assert np.all((gaps >= 0) & (gaps <= 1))
+
+
+def test_lupp_matches_lapack_getrf_tie_free():
+    # scipy's getrf on X^T (partial pivoting) picks the same k pivots on tie-free random input
+    rng = np.random.default_rng(6)
+    for trial in range(20):
+        n, k = 120, 25
+        X = rng.standard_normal((k, n))
+        piv, _, _, _ = lupp.select_cols(X, k)
+        lu, ipiv = sla.lu_factor(X.T.copy())
+        perm = np.arange(n)
+        for i, p in enumerate(ipiv):
+            perm[i], perm[p] = perm[p], perm[i]
+        assert piv.tolist() == perm[:k].tolist()
+
+
+def test_lupp_k_row_invariance_and_duality():
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((40, 300))
+    p_all = lupp.select_cols(X, 20)[0]
+    p_k = lupp.select_cols(X[:20], 20)[0]
+    assert p_all.tolist() == p_k.tolist()                              # reading R5
+    C = rng.standard_normal((8, 3))
+    assert lupp.select_rows(C, 3)[0].tolist() == lupp.select_cols(C.T, 3)[0].tolist()
+
+
+def test_lupp_kahan_witness_lemma2():
+    # Lemma 2 tightness: every step is a tie; pivots 0..l-1; max|R1^{-1}R2| = 2^{l-1},
+    # row-wise 2^{l-i} (1-based i).
+    for l in (5, 10, 20):
+        X = kahan_witness(l, l + 7)
+        piv, Lf, U, gaps = lupp.select_cols(X, l)
+        assert piv.tolist() == list(range(l))
+        assert np.all(gaps == 0.0)
+        g = lupp.growth(Lf, piv)
+        np.testing.assert_array_equal(g, 2.0 ** (l - 1 - np.arange(l)))
+        _, T, eta = idcoef.id_coeffs(Lf, piv)
+        assert np.max(np.abs(T)) == 2.0 ** (l - 1)
+        assert eta >= 2.0 ** (l - 1)
+
+
+def test_lupp_rank_deficiency():
+    rng = np.random.default_rng(8)
+    C = rng.standard_normal((30, 3)) @ rng.standard_normal((3, 4))      # rank 3
+    lupp.select_rows(C[:, :3], 3)
+    with pytest.raises(lupp.RankError) as e:
+        lupp.select_rows(C, 4)
+    assert e.value.step == 4
+
+
+# ----------------------------------------------------------------------------- CPQR
+def test_cpqr_spec_case():
+    # X = diag(3,4) padded with a zero column -> pivots [2,1,(3)] (1-based)
+    X = np.array([[3.0, 0.0, 0.0], [0.0, 4.0, 0.0]])
+    piv, R = cpqr.select_cols_cpqr(X, 2)
+    assert piv.tolist() == [1, 0]
+    assert abs(abs(R[0, 1]) - 4) < 1e-15 and abs(abs(R[1, 0]) - 3) < 1e-15
+
+
+def test_cpqr_matches_lapack_geqp3_and_factorizes():
+    rng = np.random.default_rng(10)
+    for trial in range(10):
+        l, n, k = 14, 90, 12
+        X = rng.standard_normal((l, n))
+        piv, R = cpqr.select_cols_cpqr(X, k)
+        _, Rq, P = sla.qr(X, pivoting=True, mode="economic")
+        assert piv.tolist() == P[:k].tolist()
+        d = np.abs(R[np.arange(k), piv])
+        assert np.all(np.diff(d) <= 1e-12)                              # |diag R1| non-increasing
+        np.testing.assert_allclose(d, np.abs(np.diag(Rq))[:k], rtol=1e-12)
+        # ||X Pi_1 - Q R11||: the leading k pivoted columns are spanned exactly
+        Q = np.linalg.qr(X[:, piv])[0]
+        np.testing.assert_allclose(np.abs(Q.T @ X[:, piv]), np.abs(R[:, piv]), atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- ID coefficients
+def test_idcoef_spec_eta_case():
+    # X = [[1,0,.5],[0,1,.5]], pivots [1,2] -> X1^+X2 = (.5,.5)^T -> eta = sqrt(1.5)
+    X = np.array([[1.0, 0.0, 0.5], [0.0, 1.0, 0.5]])
+    piv, Lf, _, _ = lupp.select_cols(X, 2)
+    Z, T, eta = idcoef.id_coeffs(Lf, piv)
+    assert piv.tolist() == [0, 1]
+    np.testing.assert_allclose(T[:, 0], [0.5, 0.5], atol=1e-16)
+    assert abs(eta - math.sqrt(1.5)) < 1e-15
+
+
+def test_idcoef_identity_block_and_library_solve():
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((30, 400))
+    k = 25
+    piv, Lf, _, _ = lupp.select_cols(X, k)
+    Z, T, eta = idcoef.id_coeffs(Lf, piv)
+    assert np.array_equal(Z[:, piv], np.eye(k))                         # bitwise identity block
+    rest = np.setdiff1d(np.arange(400), piv)
+    T_ref = np.linalg.solve(X[:k, piv], X[:k, rest])                    # X1^{-1} X2
+    np.testing.assert_allclose(T, T_ref, atol=1e-10 * np.max(np.abs(T_ref)))
+    # interpolation: X[:k] = X[:k, J] Z exactly up to rounding
+    np.testing.assert_allclose(X[:k, piv] @ Z, X[:k], atol=1e-10)
+    assert eta >= 1.0
+
+
+def test_theorem41_certificate():
+    # Theorem 4.1: ||A - CC^+A||_F <= eta ||A - A X^+ X||_F with X the k-row sketch (R5)
+    rng = np.random.default_rng(12)
+    for trial in range(30):
+        m, n, k = 60, 50, 6
+        sig = 0.7 ** np.arange(min(m, n))
+        A = make_lowrank(m, n, sig, rng)
+        X = sketch.sketch(A, k + 4, "gaussian", trial)
+        piv, Lf, _, _ = lupp.select_cols(X, k)
+        _, _, eta = idcoef.id_coeffs(Lf, piv)
+        res, _ = residual.residual(A, piv, kind="col_id")
+        Xk = X[:k]
+        rf = np.linalg.norm(A - A @ np.linalg.pinv(Xk) @ Xk)
+        assert res <= eta * rf * (1 + 1e-8)
+
+
+# ----------------------------------------------------------------------------- residuals
+def test_residual_closed_forms():
+    n, k = 40, 7
+    r, nA = residual.residual(np.eye(n), np.arange(k), kind="col_id")
+    assert abs(r - math.sqrt(n - k)) < 1e-13 and abs(nA - math.sqrt(n)) < 1e-13
+    r, _ = residual.residual(np.eye(n), Is=np.arange(k), kind="row_id")
+    assert abs(r - math.sqrt(n - k)) < 1e-13
+    # exact rank k: any independent skeleton gives a zero residual (SPEC acceptance 1)
+    rng = np.random.default_rng(13)
+    A = make_lowrank(80, 60, np.array([5.0, 3, 2, 1, 0.5]), rng)
+    X = sketch.sketch(A, 5, "gaussian", 3)
+    piv = lupp.select_cols(X, 5)[0]
+    Ipiv = lupp.select_rows(A[:, piv], 5)[0]
+    for kind in ("col_id", "row_id", "cur"):
+        r, nA = residual.residual(A, piv, Ipiv, kind=kind)
+        assert r <= 1e-13 * nA
+
+
+def test_residual_against_lstsq_and_eckart_young():
+    A, sigma = make_c1(seed=5, m=96, n=80)
+    k = 10
+    X = sketch.sketch(A, 20, "gaussian", 2)
+    piv, Lf, _, _ = lupp.select_cols(X, k)
+    r, nA = residual.residual(A, piv, kind="col_id")
+    C = A[:, piv]
+    r_ls = np.linalg.norm(A - C @ np.linalg.lstsq(C, A, rcond=None)[0])
+    assert abs(r - r_ls) <= 1e-10 * r
+    assert abs(nA - math.sqrt(np.sum(sigma ** 2))) < 1e-13
+    assert r >= residual.optimal_error(sigma, k) * (1 - 1e-12)            # Eckart-Young
+    Z, _, _ = idcoef.id_coeffs(Lf, piv)
+    r_z, _ = residual.residual(A, piv, kind="id_coeffs", Z=Z)
+    assert r_z >= r * (1 - 1e-12)                                           # CC^+A is the best C-based fit
+
+
+def test_remark21_sandwich_and_identity():
+    # Remark 2.1
+    rng = np.random.default_rng(14)
+    for trial in range(10):
+        A = make_lowrank(50, 40, 0.8 ** np.arange(40), rng)
+        k = 8
+        piv = lupp.select_cols(sketch.sketch(A, k, "gaussian", trial), k)[0]
+        Ipiv = lupp.select_rows(A[:, piv], k)[0]
+        rc, _ = residual.residual(A, piv, kind="col_id")
+        rr, _ = residual.residual(A, Is=Ipiv, kind="row_id")
+        rcur, _ = residual.residual(A, piv, Ipiv, kind="cur")
+        assert rc <= rcur * (1 + 1e-9)
+        assert rcur ** 2 <= (rc ** 2 + rr ** 2) * (1 + 1e-9)
+        Qc = residual.ortho(A[:, piv])
+        Qr = residual.ortho(A[Ipiv].T)
+        extra = np.linalg.norm(Qc @ Qc.T @ (A - A @ Qr @ Qr.T))
+        assert abs(rcur ** 2 - (rc ** 2 + extra ** 2)) <= 1e-9 * rcur ** 2
+
+
+def test_two_sided_id_equals_column_id():
+    # (C S^{-1}) S (C^+ A) = C C^+ A
+    rng = np.random.default_rng(15)
+    A = make_lowrank(40, 30, 0.6 ** np.arange(30), rng)
+    k = 5
+    piv = lupp.select_cols(sketch.sketch(A, k, "gaussian", 0), k)[0]
+    Ipiv = lupp.select_rows(A[:, piv], k)[0]
+    C = A[:, piv]
+    S = A[np.ix_(Ipiv, piv)]
+    tsid = np.linalg.solve(S.T, C.T).T @ S @ np.linalg.lstsq(C, A, rcond=None)[0]
+    r_ts = np.linalg.norm(A - tsid)
+    r, nA = residual.residual(A, piv, kind="col_id")
+    assert abs(r_ts - r) <= 1e-10 * nA
+
+
+def test_brute_force_subset_bounds():
+    # min_J ||A - CC^+A||_F <= sqrt(k+1) ||A - A_k||_F, and LUPP's subset is never below min_J
+    rng = np.random.default_rng(16)
+    k = 3
+    for trial in range(25):
+        A = rng.standard_normal((12, 10)) * (0.5 ** np.arange(10))
+        sv = np.linalg.svd(A, compute_uv=False)
+        opt = residual.optimal_error(sv, k)
+        best = min(residual.residual(A, list(J), kind="col_id")[0]
+                   for J in itertools.combinations(range(10), k))
+        assert opt <= best * (1 + 1e-12)
+        assert best <= math.sqrt(k + 1) * opt * (1 + 1e-12)
+        piv = lupp.select_cols(sketch.sketch(A, k + 2, "gaussian", trial), k)[0]
+        assert residual.residual(A, piv, kind="col_id")[0] >= best * (1 - 1e-12)
+
+
+def test_generators_spectra():
+    A, sigma = make_c1(seed=3, m=64, n=64)
+    s = np.linalg.svd(A, compute_uv=False)
+    np.testing.assert_allclose(s, sigma, rtol=1e-12, atol=1e-15)
+    Q = haar(50, 10, np.random.default_rng(0))
+    np.testing.assert_allclose(Q.T @ Q, np.eye(10), atol=1e-14)
