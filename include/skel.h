@@ -1,0 +1,180 @@
+/*
+ * skel.h -- C ABI of libskel.so: the B200 (sm_100a) hot path of randomized
+ * LUPP skeleton selection (Dong & Martinsson, "Simpler is better: a
+ * comparative study of randomized pivoting algorithms for CUR and
+ * interpolative decompositions", arXiv 2104.05877).
+ *
+ * Citations: P:<n> = line n of the paper text (PAPER.md, the LaTeX source);
+ * readings R<n> = DESIGN.md section 3, where every place the paper is silent
+ * or ambiguous is resolved.
+ *
+ * Conventions (all entry points)
+ *   - Matrices are IEEE FP64.  Indices are int64, 0-based (the paper is
+ *     1-based MATLAB).
+ *   - A is COLUMN-major m x n with leading dimension lda >= m.
+ *   - The sketch X is ROW-major l x n with row stride ldx >= n (== X^T
+ *     column-major n x l, the panel the LUPP works on).
+ *   - C (m x k), Lf (n x k), Z (k x n), R^T panels are column-major.
+ *   - Pointers are CUDA device pointers on the context's device unless the
+ *     argument is documented "host".  The caller owns every buffer; a context
+ *     owns only its workspace (grown on demand, reused, freed by sk_destroy).
+ *   - Every call is enqueued on the context's stream and returns without
+ *     synchronising, EXCEPT calls that write a host scalar (info, eta,
+ *     res_fro, ...), which synchronise that stream before returning.
+ *   - Errors: the return value.  SK_E_ARG for a bad size, leading dimension,
+ *     NULL required pointer or parameter out of range (checked before any
+ *     work is enqueued, nothing is written); SK_E_RANK when a pivot of
+ *     magnitude <= 1e-14 * max|panel| is met (R7), with *info = the 1-based
+ *     failing step (LAPACK style); SK_E_CUDA for a CUDA runtime error;
+ *     SK_E_NOMEM when the workspace cannot grow.  sk_last_error() returns a
+ *     human-readable message for the last non-OK status of the context.
+ *   - Thread safety: one context per (thread, stream).  Contexts are
+ *     independent; different contexts may run concurrently.
+ *   - There is no CPU fallback: every step runs in this library's kernels.
+ */
+#ifndef SKEL_H_
+#define SKEL_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sk_ctx sk_ctx;
+
+typedef enum {
+  SK_OK = 0,
+  SK_E_ARG = 1,
+  SK_E_RANK = 2,
+  SK_E_CUDA = 3,
+  SK_E_NCCL = 4,
+  SK_E_NOMEM = 5,
+  SK_E_STATE = 6
+} sk_status;
+
+/* Oblivious l2 embeddings Gamma.  Gaussian: i.i.d. N(0, 1/l)
+ * (R3).  Sparse sign: zeta nonzeros +-1/sqrt(zeta) per column at
+ * uniformly random distinct rows (R4); zeta = min(l, 8) in practice
+ * (P:185).  Both are regenerated on the fly from (seed, row, column) with
+ * Philox4x32-10 (R1, R2) and never stored in HBM. */
+typedef enum { SK_EMB_GAUSSIAN = 0, SK_EMB_SPARSE_SIGN = 1 } sk_embedding;
+
+/* Which approximation sk_residual measures (Frobenius norm, R12).
+ *   COL_ID    ||A - C C^+ A||              eq:def_column_id
+ *   ROW_ID    ||A - A R^+ R||              eq:def_row_id,
+ *   CUR       ||A - Q_C (Q_C^T A Q_R) Q_R^T||   stable CUR, Remark 2.3
+ *   ID_COEFFS ||A - C Z||                  eq:colID, with Z from sk_id_coeffs */
+typedef enum {
+  SK_RES_COL_ID = 0,
+  SK_RES_ROW_ID = 1,
+  SK_RES_CUR = 2,
+  SK_RES_ID_COEFFS = 3
+} sk_residual_kind;
+
+/* ---- context ----------------------------------------------------------- */
+
+/* Create a context on CUDA device `device`, enqueueing on `stream`
+ * (a cudaStream_t; NULL = the legacy default stream).  *ctx is set on success. */
+sk_status sk_create(sk_ctx** ctx, int device, void* stream);
+/* Re-target the context to another stream of the same device. */
+sk_status sk_set_stream(sk_ctx* ctx, void* stream);
+/* Release the workspace and the context (synchronises its stream). NULL is a no-op. */
+void sk_destroy(sk_ctx* ctx);
+/* Message of the last non-OK status returned through ctx ("" if none). Never NULL. */
+const char* sk_last_error(const sk_ctx* ctx);
+/* Library version string, e.g. "skel 0.1 sm_100a". */
+const char* sk_version(void);
+/* Bytes of device workspace currently held by ctx. */
+int64_t sk_workspace_bytes(const sk_ctx* ctx);
+/* Number of kernels this context has launched so far (for the bench's gpu_launches count). */
+int64_t sk_launch_count(const sk_ctx* ctx);
+
+/* ---- S0 + S1: sketch  (Algorithm 2 lines 1-2) ---------------- */
+
+/* X = Gamma A.  Gamma (l x m) is drawn from (emb, zeta, seed) on the fly.
+ *   A   m x n column-major (lda >= m), read only.
+ *   X   l x n row-major (ldx >= n), written.
+ *   Requires 1 <= l <= m, n >= 0; for SK_EMB_SPARSE_SIGN 2 <= zeta <= min(l, 64)
+ *   (zeta is ignored for SK_EMB_GAUSSIAN).  X must not alias A. */
+sk_status sk_sketch(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
+                    int64_t l, sk_embedding emb, int32_t zeta, uint64_t seed,
+                    double* X, int64_t ldx);
+
+/* ---- S2: column skeletons by LUPP on the sketch  (eq:def_LUPP; Alg. 2 line 3) ----
+ * k-step LU with partial pivoting on the n x k panel X^T(:, 0:k) = rows 0..k-1
+ * of X (R5: only those rows can influence the first k pivots).  Step t picks
+ * the active row j of the panel maximising |M(j, t)|, ties to the
+ * lowest original index (R6), then applies the Schur-complement update.
+ *   X     l x n row-major (ldx >= n); read only.  Requires 1 <= k <= l, k <= n.
+ *   Js    device int64[k]: the pivots in pivot order (J_s of eq:Js).
+ *   Lf    NULL or n x k column-major (ldlf >= n): Lf(i,t) = multiplier of row i
+ *         at step t (|Lf| <= 1), Lf(Js[t],t) = 1, Lf(Js[t],t') = 0 for t' > t.
+ *         X^T(:,0:k) = Lf U in exact arithmetic.
+ *   U     NULL or k x k column-major upper triangular (ldu >= k): row t = pivot row.
+ *   gaps  NULL or device double[k]: (a1 - a2)/a1 for the two largest candidate
+ *         magnitudes at step t (near-tie diagnostics).
+ *   info  NULL or host int64: 0, or the 1-based step of a rank failure (R7).
+ *         Non-NULL info synchronises the stream and makes a rank failure
+ *         return SK_E_RANK; with NULL the call is asynchronous and a rank
+ *         failure leaves Js[t..k-1] = -1. */
+sk_status sk_select_cols(sk_ctx* ctx, const double* X, int64_t l, int64_t n, int64_t ldx,
+                         int64_t k, int64_t* Js, double* Lf, int64_t ldlf, double* U,
+                         int64_t ldu, double* gaps, int64_t* info);
+
+/* ---- S2': column skeletons by CPQR on the sketch (eq:def_QRCP; Sec. 5 "Rand-CPQR") ----
+ * k steps of Householder QR with column pivoting on all l rows of X; the pivot
+ * is the active column of largest remaining norm, norms recomputed
+ * exactly each step (R9), ties to the lowest index (R6).
+ *   Js  device int64[k] pivots;  R  NULL or k x n column-major (ldr >= k):
+ *   R(t, j) = row t of the triangular factor for ORIGINAL column j.
+ *   Requires 1 <= k <= min(l, n).  info as for sk_select_cols. */
+sk_status sk_select_cols_cpqr(sk_ctx* ctx, const double* X, int64_t l, int64_t n, int64_t ldx,
+                              int64_t k, int64_t* Js, double* R, int64_t ldr, int64_t* info);
+
+/* ---- S3: gather C = A(:, Js)  (eq:Js; columns in pivot order, R8) ---- */
+sk_status sk_gather_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
+                         const int64_t* Js, int64_t k, double* C, int64_t ldc);
+
+/* ---- S4: row skeletons by row-wise LUPP on C  (Alg. 2 line 4) ----
+ * Step t scans column t of C (m x k column-major, ldc >= m); outputs as for
+ * sk_select_cols with n -> m (Is = I_s of eq:Is).  Requires 1 <= k <= m. */
+sk_status sk_select_rows(sk_ctx* ctx, const double* C, int64_t m, int64_t k, int64_t ldc,
+                         int64_t* Is, double* Lf, int64_t ldlf, double* U, int64_t ldu,
+                         double* gaps, int64_t* info);
+
+/* ---- S5: ID coefficients  (eq:colID P:645-652; [I_k, R11^-1 R12] P:599; Thm 4.1) ----
+ * Z (k x n column-major, ldz >= k): Z(:, Js) = I_k exactly; the other columns
+ * T = X1^{-1} X2 = L1^{-T} L2^T with L1 = Lf(Js, :), L2 = Lf(rest, :) (R10).
+ *   Lf, Js  as produced by sk_select_cols (Lf non-NULL there).
+ *   eta     NULL or host double: sqrt(1 + ||T||_2^2) (Theorem 4.1 certificate);
+ *           non-NULL synchronises. */
+sk_status sk_id_coeffs(sk_ctx* ctx, const double* Lf, int64_t n, int64_t k, int64_t ldlf,
+                       const int64_t* Js, double* Z, int64_t ldz, double* eta);
+
+/* ---- S6: residual  (Remark 2.3 P:133-137; protocol P:554) ----
+ * res_fro (host) = ||A - approx||_F for `kind`, normA_fro (host, NULL-able) = ||A||_F.
+ * The m x n residual is never materialised.  Js (device int64[k]) is required
+ * for COL_ID, CUR, ID_COEFFS; Is (device int64[k]) for ROW_ID and CUR; Z
+ * (k x n, ldz >= k) for ID_COEFFS only.  Orthonormal bases are computed from
+ * the LUPP factor of the skeleton (range(C) = range(Lf_C))
+ * by two rounds of Cholesky QR.  Synchronises the stream. */
+sk_status sk_residual(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
+                      const int64_t* Js, const int64_t* Is, int64_t k, sk_residual_kind kind,
+                      const double* Z, int64_t ldz, double* res_fro, double* normA_fro);
+
+/* ---- Algorithm 2 end to end ---------------------------------
+ * Sketch (S0+S1) + column LUPP (S2) and, if Is != NULL, gather + row LUPP
+ * (S3+S4).  A may be a HOST pointer (a_on_host = 1): it is then copied to the
+ * context's workspace inside the call (pinned host memory gives full PCIe
+ * bandwidth).  Js / Is are HOST int64[k] outputs (Is NULL-able).  Synchronises.
+ * l, emb, zeta, seed as for sk_sketch; k as for sk_select_cols. */
+sk_status sk_rand_lupp(sk_ctx* ctx, const double* A, int a_on_host, int64_t m, int64_t n,
+                       int64_t lda, int64_t l, sk_embedding emb, int32_t zeta, uint64_t seed,
+                       int64_t k, int64_t* Js, int64_t* Is, int64_t* info);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKEL_H_ */

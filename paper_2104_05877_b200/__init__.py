@@ -1,0 +1,11 @@
+"""paper_2104_05877_b200 -- B200-native randomized LUPP skeleton selection.
+
+The hot path of Dong & Martinsson, arXiv 2104.05877 (sketch X = Gamma A, LUPP on X^T
+for the column skeletons J_s, LUPP on C = A(:, J_s) for the row skeletons I_s, the ID
+coefficients and the residual), as hand-written sm_100a kernels behind the C ABI in
+include/skel.h (libskel.so) with this thin ctypes binding on top.
+"""
+from .api import (  # noqa: F401
+    COL_ID, CUR, GAUSSIAN, ID_COEFFS, ROW_ID, SPARSE_SIGN, SkelError, context, fortran, gather_cols,
+    id_coeffs, launch_count, rand_lupp, residual, select_cols, select_cols_cpqr, select_rows, sketch,
+)

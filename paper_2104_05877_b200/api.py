@@ -1,0 +1,199 @@
+"""Thin Python binding over libskel.so: argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels; torch provides device
+memory and the current stream.  Names follow include/skel.h (and the paper:
+J_s, I_s, Z, eta).  Layout conventions:
+
+  A   (m, n) float64 CUDA tensor, COLUMN-major (A.stride() == (1, lda));
+      ``fortran(t)`` converts a row-major tensor.
+  X   (l, n) float64, row-major (the sketch, X^T column-major).
+  Lf  (n, k) float64, column-major.   Z (k, n) float64, column-major.
+  Js, Is  (k,) int64 CUDA tensors (0-based, pivot order).
+"""
+import ctypes
+
+import torch
+
+from . import _lib
+
+GAUSSIAN, SPARSE_SIGN = 0, 1
+COL_ID, ROW_ID, CUR, ID_COEFFS = 0, 1, 2, 3
+_EMB = {"gaussian": GAUSSIAN, "sparse_sign": SPARSE_SIGN, GAUSSIAN: GAUSSIAN, SPARSE_SIGN: SPARSE_SIGN}
+_KIND = {"col_id": COL_ID, "row_id": ROW_ID, "cur": CUR, "id_coeffs": ID_COEFFS,
+         COL_ID: COL_ID, ROW_ID: ROW_ID, CUR: CUR, ID_COEFFS: ID_COEFFS}
+
+
+class SkelError(RuntimeError):
+    def __init__(self, status, msg, info=0):
+        super().__init__(f"{_lib.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.info = info
+
+
+_ctxs = {}
+
+
+def lib():
+    return _lib.load()
+
+
+def context(device=None):
+    """The (cached) sk_ctx for the device, re-targeted to torch's current stream."""
+    L = lib()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    key = dev.index
+    if key not in _ctxs:
+        h = ctypes.c_void_p()
+        st = L.sk_create(ctypes.byref(h), dev.index, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+        if st != 0:
+            raise SkelError(st, "sk_create failed (is this a B200 / sm_100 device?)")
+        _ctxs[key] = h
+    h = _ctxs[key]
+    L.sk_set_stream(h, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    return h
+
+
+def launch_count(device=None):
+    return int(lib().sk_launch_count(context(device)))
+
+
+def _check(st, h, info=0):
+    if st != 0:
+        msg = lib().sk_last_error(h).decode()
+        raise SkelError(st, msg, info)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def fortran(t):
+    """Column-major copy of a 2-D tensor (same values, stride (1, rows))."""
+    return t.t().contiguous().t()
+
+
+def _colmajor(A, name):
+    if A.dim() != 2 or A.dtype != torch.float64 or not A.is_cuda:
+        raise ValueError(f"{name} must be a 2-D float64 CUDA tensor")
+    if A.stride(0) != 1 and A.shape[1] > 1:
+        raise ValueError(f"{name} must be column-major (use api.fortran)")
+    return max(A.stride(1), A.shape[0], 1)
+
+
+def sketch(A, l, embedding="gaussian", seed=0, zeta=8, out=None):
+    """X = Gamma A (Algorithm 2 lines 1-2)."""
+    lda = _colmajor(A, "A")
+    m, n = A.shape
+    X = out if out is not None else torch.empty((l, n), dtype=torch.float64, device=A.device)
+    h = context(A.device.index)
+    _check(lib().sk_sketch(h, _ptr(A), m, n, lda, l, _EMB[embedding], zeta, seed & (2**64 - 1), _ptr(X),
+                           max(X.stride(0), n)), h)
+    return X
+
+
+def select_cols(X, k, want_factors=True, want_gaps=False, check=True):
+    """Column LUPP on the sketch (eq:def_LUPP, Alg. 2 line 3). Returns (Js, Lf, U, gaps)."""
+    l, n = X.shape
+    if X.stride(1) != 1:
+        raise ValueError("X must be row-major")
+    dev = X.device
+    Js = torch.empty(k, dtype=torch.int64, device=dev)
+    Lf = torch.empty((k, n), dtype=torch.float64, device=dev).t() if want_factors else None
+    U = torch.empty((k, k), dtype=torch.float64, device=dev).t() if want_factors else None
+    gaps = torch.empty(k, dtype=torch.float64, device=dev) if want_gaps else None
+    info = ctypes.c_int64(0)
+    h = context(dev.index)
+    st = lib().sk_select_cols(h, _ptr(X), l, n, max(X.stride(0), n), k, _ptr(Js), _ptr(Lf), n, _ptr(U), k,
+                              _ptr(gaps), ctypes.byref(info) if check else None)
+    _check(st, h, info.value)
+    return Js, Lf, U, gaps
+
+
+def select_cols_cpqr(X, k, want_r=False, check=True):
+    """Column-pivoted QR on the sketch (eq:def_QRCP). Returns (Js, R)."""
+    l, n = X.shape
+    dev = X.device
+    Js = torch.empty(k, dtype=torch.int64, device=dev)
+    R = torch.empty((n, k), dtype=torch.float64, device=dev).t() if want_r else None
+    info = ctypes.c_int64(0)
+    h = context(dev.index)
+    st = lib().sk_select_cols_cpqr(h, _ptr(X), l, n, max(X.stride(0), n), k, _ptr(Js), _ptr(R), k,
+                                   ctypes.byref(info) if check else None)
+    _check(st, h, info.value)
+    return Js, R
+
+
+def gather_cols(A, Js):
+    """C = A(:, J_s) (eq:Js), column-major m x k."""
+    lda = _colmajor(A, "A")
+    m, n = A.shape
+    k = Js.numel()
+    C = torch.empty((k, m), dtype=torch.float64, device=A.device).t()
+    h = context(A.device.index)
+    _check(lib().sk_gather_cols(h, _ptr(A), m, n, lda, _ptr(Js), k, _ptr(C), m), h)
+    return C
+
+
+def select_rows(C, k=None, want_factors=True, want_gaps=False, check=True):
+    """Row LUPP on C (Alg. 2 line 4). Returns (Is, Lf, U, gaps)."""
+    ldc = _colmajor(C, "C")
+    m, kk = C.shape
+    k = kk if k is None else k
+    dev = C.device
+    Is = torch.empty(k, dtype=torch.int64, device=dev)
+    Lf = torch.empty((k, m), dtype=torch.float64, device=dev).t() if want_factors else None
+    U = torch.empty((k, k), dtype=torch.float64, device=dev).t() if want_factors else None
+    gaps = torch.empty(k, dtype=torch.float64, device=dev) if want_gaps else None
+    info = ctypes.c_int64(0)
+    h = context(dev.index)
+    st = lib().sk_select_rows(h, _ptr(C), m, k, ldc, _ptr(Is), _ptr(Lf), m, _ptr(U), k, _ptr(gaps),
+                              ctypes.byref(info) if check else None)
+    _check(st, h, info.value)
+    return Is, Lf, U, gaps
+
+
+def id_coeffs(Lf, Js, want_eta=False):
+    """Z with Z(:, J_s) = I and T = L1^{-T} L2^T elsewhere (Thm 4.1). Returns (Z, eta)."""
+    n, k = Lf.shape
+    ldlf = _colmajor(Lf, "Lf")
+    Z = torch.empty((n, k), dtype=torch.float64, device=Lf.device).t()
+    eta = ctypes.c_double(0.0)
+    h = context(Lf.device.index)
+    _check(lib().sk_id_coeffs(h, _ptr(Lf), n, k, ldlf, _ptr(Js), _ptr(Z), k,
+                              ctypes.byref(eta) if want_eta else None), h)
+    return Z, (eta.value if want_eta else None)
+
+
+def residual(A, Js=None, Is=None, kind="col_id", Z=None):
+    """(||A - approx||_F, ||A||_F) for kind in col_id / row_id / cur / id_coeffs."""
+    lda = _colmajor(A, "A")
+    m, n = A.shape
+    k = (Js if Js is not None else Is).numel()
+    res = ctypes.c_double(0.0)
+    nrm = ctypes.c_double(0.0)
+    ldz = Z.stride(1) if Z is not None else k
+    h = context(A.device.index)
+    _check(lib().sk_residual(h, _ptr(A), m, n, lda, _ptr(Js), _ptr(Is), k, _KIND[kind], _ptr(Z), ldz,
+                             ctypes.byref(res), ctypes.byref(nrm)), h)
+    return res.value, nrm.value
+
+
+def rand_lupp(A, k, l=None, embedding="gaussian", seed=0, zeta=8, rows=False, device=0):
+    """Algorithm 2 end to end.  A may be a CPU tensor (copied inside the call)
+    or a CUDA tensor; returns host int64 tensors (Js, Is or None)."""
+    on_host = not A.is_cuda
+    if A.dtype != torch.float64 or A.dim() != 2:
+        raise ValueError("A must be a 2-D float64 tensor")
+    if A.stride(0) != 1 and A.shape[1] > 1:
+        raise ValueError("A must be column-major")
+    m, n = A.shape
+    lda = max(A.stride(1), m)
+    l = k + 10 if l is None else l
+    Js = torch.empty(k, dtype=torch.int64)
+    Is = torch.empty(k, dtype=torch.int64) if rows else None
+    info = ctypes.c_int64(0)
+    h = context(device if on_host else A.device.index)
+    st = lib().sk_rand_lupp(h, _ptr(A), 1 if on_host else 0, m, n, lda, l, _EMB[embedding], zeta,
+                            seed & (2**64 - 1), k, _ptr(Js), _ptr(Is), ctypes.byref(info))
+    _check(st, h, info.value)
+    return Js, Is

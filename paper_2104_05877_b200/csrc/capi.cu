@@ -1,0 +1,269 @@
+// capi.cu -- the extern "C" entry points of libskel.so (include/skel.h).
+// Argument validation happens here, before anything is enqueued; the work is done by
+// the kernels in sketch.cu, lupp.cu, cpqr.cu, dense.cu, idcoef.cu, residual.cu.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+#include "internal.h"
+
+using namespace skel;
+
+namespace {
+
+// Copy n device int64/double values to host (pinned scratch) and synchronise.
+sk_status to_host(sk_ctx* c, void* dst, const void* src_dev, size_t bytes) {
+  if (bytes > 4096) {
+    SK_CUDA(c, cudaMemcpyAsync(dst, src_dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    return SK_OK;
+  }
+  SK_CUDA(c, cudaMemcpyAsync(c->host_scratch, src_dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+  SK_CUDA(c, cudaStreamSynchronize(c->stream));
+  std::memcpy(dst, c->host_scratch, bytes);
+  return SK_OK;
+}
+
+sk_status finish_info(sk_ctx* c, const int64_t* status_dev, int64_t* info, const char* what) {
+  if (!info) return SK_OK;
+  int64_t st = 0;
+  SK_TRY(to_host(c, &st, status_dev, sizeof(int64_t)));
+  *info = st;
+  if (st != 0)
+    return fail(c, SK_E_RANK, std::string(what) + ": rank deficiency at step " + std::to_string(st));
+  return SK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sk_status sk_create(sk_ctx** out, int device, void* stream) {
+  if (!out) return SK_E_ARG;
+  *out = nullptr;
+  sk_ctx* c = new (std::nothrow) sk_ctx();
+  if (!c) return SK_E_NOMEM;
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess)
+    e = cudaDeviceGetAttribute(&c->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e == cudaSuccess) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    if (major != 10 || minor != 0) {
+      c->err = "libskel.so is built for sm_100a (B200) only";
+      delete c;
+      return SK_E_CUDA;
+    }
+  }
+  if (e == cudaSuccess) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    e = cudaMemPoolCreate(&c->pool, &props);
+    if (e == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      e = cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  if (e == cudaSuccess) e = cudaMallocHost(&c->host_scratch, 4096);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (c->pool) cudaMemPoolDestroy(c->pool);
+    delete c;
+    return SK_E_CUDA;
+  }
+  *out = c;
+  return SK_OK;
+}
+
+sk_status sk_set_stream(sk_ctx* c, void* stream) {
+  if (!c) return SK_E_ARG;
+  c->stream = static_cast<cudaStream_t>(stream);
+  return SK_OK;
+}
+
+void sk_destroy(sk_ctx* c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->stream);
+  if (c->pool) cudaMemPoolDestroy(c->pool);
+  if (c->host_scratch) cudaFreeHost(c->host_scratch);
+  delete c;
+}
+
+const char* sk_last_error(const sk_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+const char* sk_version(void) { return "skel 0.1 sm_100a"; }
+
+int64_t sk_workspace_bytes(const sk_ctx* c) {
+  if (!c || !c->pool) return 0;
+  uint64_t v = 0;
+  cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrReservedMemCurrent, &v);
+  return (int64_t)v;
+}
+
+int64_t sk_launch_count(const sk_ctx* c) { return c ? c->launches : 0; }
+
+sk_status sk_sketch(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                    sk_embedding emb, int32_t zeta, uint64_t seed, double* X, int64_t ldx) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, A && X, "sk_sketch: NULL A or X");
+  SK_ARG(c, m >= 1 && n >= 0 && l >= 1 && l <= m, "sk_sketch: need 1 <= l <= m, n >= 0");
+  SK_ARG(c, lda >= m && ldx >= n, "sk_sketch: lda >= m and ldx >= n required");
+  SK_ARG(c, m < (1LL << 40) && l <= (1 << 20), "sk_sketch: size out of range");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  if (emb == SK_EMB_GAUSSIAN) return sketch_dense(c, A, m, n, lda, l, seed, X, ldx);
+  if (emb == SK_EMB_SPARSE_SIGN) {
+    SK_ARG(c, zeta >= 2 && zeta <= l && zeta <= 64, "sk_sketch: sparse sign needs 2 <= zeta <= min(l, 64)");
+    return sketch_sparse(c, A, m, n, lda, l, zeta, seed, X, ldx);
+  }
+  return fail(c, SK_E_ARG, "sk_sketch: unknown embedding");
+}
+
+sk_status sk_select_cols(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, int64_t k,
+                         int64_t* Js, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps,
+                         int64_t* info) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, X && Js, "sk_select_cols: NULL X or Js");
+  SK_ARG(c, k >= 1 && k <= l && k <= n && ldx >= n, "sk_select_cols: need 1 <= k <= min(l, n), ldx >= n");
+  SK_ARG(c, !Lf || ldlf >= n, "sk_select_cols: ldlf >= n required");
+  SK_ARG(c, !U || ldu >= k, "sk_select_cols: ldu >= k required");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf st;
+  SK_TRY(st.alloc(c, sizeof(int64_t)));
+  SK_TRY(lupp(c, X, true, n, k, ldx, Js, Lf, ldlf, U, ldu, gaps, st.as<int64_t>()));
+  return finish_info(c, st.as<int64_t>(), info, "sk_select_cols");
+}
+
+sk_status sk_select_cols_cpqr(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, int64_t k,
+                              int64_t* Js, double* R, int64_t ldr, int64_t* info) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, X && Js, "sk_select_cols_cpqr: NULL X or Js");
+  SK_ARG(c, k >= 1 && k <= l && k <= n && ldx >= n, "sk_select_cols_cpqr: need 1 <= k <= min(l, n)");
+  SK_ARG(c, !R || ldr >= k, "sk_select_cols_cpqr: ldr >= k required");
+  SK_ARG(c, l <= 8192, "sk_select_cols_cpqr: l <= 8192");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf st;
+  SK_TRY(st.alloc(c, sizeof(int64_t)));
+  SK_TRY(cpqr(c, X, l, n, ldx, k, Js, R, ldr, st.as<int64_t>()));
+  return finish_info(c, st.as<int64_t>(), info, "sk_select_cols_cpqr");
+}
+
+sk_status sk_gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* Js,
+                         int64_t k, double* C, int64_t ldc) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, A && Js && C, "sk_gather_cols: NULL pointer");
+  SK_ARG(c, m >= 0 && n >= 0 && k >= 0 && lda >= m && ldc >= m, "sk_gather_cols: bad sizes");
+  (void)n;
+  SK_CUDA(c, cudaSetDevice(c->device));
+  return gather_cols(c, A, m, lda, Js, k, C, ldc);
+}
+
+sk_status sk_select_rows(sk_ctx* c, const double* C, int64_t m, int64_t k, int64_t ldc, int64_t* Is,
+                         double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps, int64_t* info) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, C && Is, "sk_select_rows: NULL C or Is");
+  SK_ARG(c, k >= 1 && k <= m && ldc >= m, "sk_select_rows: need 1 <= k <= m, ldc >= m");
+  SK_ARG(c, !Lf || ldlf >= m, "sk_select_rows: ldlf >= m required");
+  SK_ARG(c, !U || ldu >= k, "sk_select_rows: ldu >= k required");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf st;
+  SK_TRY(st.alloc(c, sizeof(int64_t)));
+  SK_TRY(lupp(c, C, false, m, k, ldc, Is, Lf, ldlf, U, ldu, gaps, st.as<int64_t>()));
+  return finish_info(c, st.as<int64_t>(), info, "sk_select_rows");
+}
+
+sk_status sk_id_coeffs(sk_ctx* c, const double* Lf, int64_t n, int64_t k, int64_t ldlf, const int64_t* Js,
+                       double* Z, int64_t ldz, double* eta) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, Lf && Js && Z, "sk_id_coeffs: NULL pointer");
+  SK_ARG(c, k >= 1 && k <= n && ldlf >= n && ldz >= k, "sk_id_coeffs: bad sizes");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf e;
+  if (eta) SK_TRY(e.alloc(c, sizeof(double)));
+  SK_TRY(id_coeffs(c, Lf, n, k, ldlf, Js, Z, ldz, eta ? e.as<double>() : nullptr));
+  if (eta) SK_TRY(to_host(c, eta, e.p, sizeof(double)));
+  return SK_OK;
+}
+
+sk_status sk_residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* Js,
+                      const int64_t* Is, int64_t k, sk_residual_kind kind, const double* Z, int64_t ldz,
+                      double* res_fro, double* normA_fro) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, A && res_fro, "sk_residual: NULL A or res_fro");
+  SK_ARG(c, m >= 1 && n >= 1 && lda >= m && k >= 1 && k <= m && k <= n, "sk_residual: bad sizes");
+  SK_ARG(c, kind >= SK_RES_COL_ID && kind <= SK_RES_ID_COEFFS, "sk_residual: unknown kind");
+  const bool need_js = kind != SK_RES_ROW_ID, need_is = kind == SK_RES_ROW_ID || kind == SK_RES_CUR;
+  SK_ARG(c, !need_js || Js, "sk_residual: Js required");
+  SK_ARG(c, !need_is || Is, "sk_residual: Is required");
+  SK_ARG(c, kind != SK_RES_ID_COEFFS || (Z && ldz >= k), "sk_residual: Z (ldz >= k) required");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf sums, st;
+  SK_TRY(sums.alloc(c, 2 * sizeof(double)));
+  SK_TRY(st.alloc(c, sizeof(int64_t)));
+  SK_TRY(residual(c, A, m, n, lda, Js, Is, k, (int)kind, Z, ldz, sums.as<double>(), st.as<int64_t>()));
+  int64_t info = 0;
+  SK_TRY(finish_info(c, st.as<int64_t>(), &info, "sk_residual (basis of the skeleton)"));
+  double h[2];
+  SK_TRY(to_host(c, h, sums.p, sizeof(h)));
+  *res_fro = std::sqrt(h[0]);
+  if (normA_fro) *normA_fro = std::sqrt(h[1]);
+  return SK_OK;
+}
+
+sk_status sk_rand_lupp(sk_ctx* c, const double* A, int a_on_host, int64_t m, int64_t n, int64_t lda,
+                       int64_t l, sk_embedding emb, int32_t zeta, uint64_t seed, int64_t k, int64_t* Js,
+                       int64_t* Is, int64_t* info) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, A && Js, "sk_rand_lupp: NULL A or Js");
+  SK_ARG(c, m >= 1 && n >= 1 && lda >= m && l >= 1 && l <= m && k >= 1 && k <= l && k <= n,
+         "sk_rand_lupp: need 1 <= k <= l <= m, k <= n");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf Ad, Xd, Jd, Cd, Id, st;
+  const double* Adev = A;
+  int64_t ldad = lda;
+  if (a_on_host) {
+    SK_TRY(Ad.alloc(c, (size_t)m * n * sizeof(double)));
+    SK_CUDA(c, cudaMemcpy2DAsync(Ad.p, (size_t)m * sizeof(double), A, (size_t)lda * sizeof(double),
+                                 (size_t)m * sizeof(double), (size_t)n, cudaMemcpyHostToDevice, c->stream));
+    Adev = Ad.as<double>();
+    ldad = m;
+  }
+  SK_TRY(Xd.alloc(c, (size_t)l * n * sizeof(double)));
+  SK_TRY(Jd.alloc(c, (size_t)k * sizeof(int64_t)));
+  SK_TRY(st.alloc(c, sizeof(int64_t)));
+  SK_TRY(sk_sketch(c, Adev, m, n, ldad, l, emb, zeta, seed, Xd.as<double>(), n));
+  SK_TRY(lupp(c, Xd.as<double>(), true, n, k, n, Jd.as<int64_t>(), nullptr, 0, nullptr, 0, nullptr,
+              st.as<int64_t>()));
+  int64_t inf = 0;
+  SK_TRY(finish_info(c, st.as<int64_t>(), &inf, "sk_rand_lupp (columns)"));
+  if (info) *info = inf;
+  if (Is) {
+    SK_ARG(c, k <= m, "sk_rand_lupp: k <= m required for row skeletons");
+    SK_TRY(Cd.alloc(c, (size_t)m * k * sizeof(double)));
+    SK_TRY(Id.alloc(c, (size_t)k * sizeof(int64_t)));
+    SK_TRY(gather_cols(c, Adev, m, ldad, Jd.as<int64_t>(), k, Cd.as<double>(), m));
+    SK_TRY(lupp(c, Cd.as<double>(), false, m, k, m, Id.as<int64_t>(), nullptr, 0, nullptr, 0, nullptr,
+                st.as<int64_t>()));
+    SK_TRY(finish_info(c, st.as<int64_t>(), &inf, "sk_rand_lupp (rows)"));
+    if (info) *info = inf;
+    SK_TRY(to_host(c, Is, Id.p, (size_t)k * sizeof(int64_t)));
+  }
+  SK_TRY(to_host(c, Js, Jd.p, (size_t)k * sizeof(int64_t)));
+  return SK_OK;
+}
+
+}  // extern "C"

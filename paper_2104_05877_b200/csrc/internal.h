@@ -1,0 +1,70 @@
+// internal.h -- host-side drivers shared by the translation units of libskel.so.
+#pragma once
+#include "common.cuh"
+
+namespace skel {
+
+// ---------------------------------------------------------------- GEMM (gemm.cu)
+// C (M x N, col-major, ldc) = alpha * op(A) op(B) + beta * C, all FP64 column-major.
+// op(A) is M x K (A stored M x K if !ta, K x M if ta); op(B) is K x N.
+sk_status gemm(sk_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
+               const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+               int64_t ldc);
+// sums[0] += ||beta*C + alpha*op(A)op(B)||_F^2 and sums[1] += ||C||_F^2, C read only
+// (the fused residual reduction).  sums: device double[2], overwritten.
+sk_status gemm_sumsq(sk_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
+                     const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                     const double* C, int64_t ldc, double* sums);
+
+// ---------------------------------------------------------------- sketch (sketch.cu)
+sk_status sketch_dense(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                       uint64_t seed, double* X, int64_t ldx);
+sk_status sketch_sparse(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                        int zeta, uint64_t seed, double* X, int64_t ldx);
+
+// ---------------------------------------------------------------- LUPP (lupp.cu)
+// k-step swap-free LUPP on the rows of an n x k panel.  The panel is given either
+// as rows 0..k-1 of a row-major X (row_major = true, ld = ldx) or as a column-major
+// n x k matrix (row_major = false, ld = ldc).  Outputs device Js[k]; Lf (n x k, ldlf)
+// is required (workspace-backed if the caller passed NULL); U/gaps optional.
+// status_dev: device int64 written with 0 or the failing 1-based step.
+sk_status lupp(sk_ctx* c, const double* P, bool row_major, int64_t n, int64_t k, int64_t ld,
+               int64_t* Js, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps,
+               int64_t* status_dev);
+
+// ---------------------------------------------------------------- CPQR (cpqr.cu)
+sk_status cpqr(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, int64_t k,
+               int64_t* Js, double* R, int64_t ldr, int64_t* status_dev);
+
+// ---------------------------------------------------------------- small dense kernels (dense.cu)
+sk_status gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t lda, const int64_t* J,
+                      int64_t k, double* C, int64_t ldc);
+// R^T (n x k, col-major ld n) = A(I, :)^T
+sk_status gather_rows_t(sk_ctx* c, const double* A, int64_t n, int64_t lda, const int64_t* I,
+                        int64_t k, double* Rt, int64_t ldrt);
+// In-place blocked Cholesky of the SPD k x k matrix G (lower, col-major ld); status_dev = 0 or
+// 1-based failing column.
+sk_status potrf_lower(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t* status_dev);
+// X (rows x k, ldx) <- X * L^{-T} with L lower k x k non-unit (Cholesky factor).
+sk_status trsm_right_lt(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L,
+                        int64_t ldl);
+// X (rows x k, ldx) <- X * L^{-1} with L unit lower k x k.
+sk_status trsm_right_l_unit(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx,
+                            const double* L, int64_t ldl);
+// Q (m x k, ldq) := orthonormal basis of range(Q) by two Cholesky-QR passes.
+sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64_t* status_dev);
+// out[0] = sum of in[0..n) pairs etc: finishes per-CTA partial sums deterministically.
+sk_status reduce_pairs(sk_ctx* c, const double* partial, int64_t count, double* out);
+// largest eigenvalue of the SPD k x k matrix G by power iteration (device result).
+sk_status lambda_max(sk_ctx* c, const double* G, int64_t k, int64_t ld, double* out_dev);
+
+// ---------------------------------------------------------------- ID coefficients (idcoef.cu)
+sk_status id_coeffs(sk_ctx* c, const double* Lf, int64_t n, int64_t k, int64_t ldlf,
+                    const int64_t* Js, double* Z, int64_t ldz, double* eta_dev);
+
+// ---------------------------------------------------------------- residual (residual.cu)
+sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda,
+                   const int64_t* Js, const int64_t* Is, int64_t k, int kind, const double* Z,
+                   int64_t ldz, double* sums_dev, int64_t* status_dev);
+
+}  // namespace skel

@@ -1,0 +1,72 @@
+// residual.cu -- S6: Frobenius residual of the column ID, row ID, stable CUR and C*Z.
+//
+// Paper: CC^+A (eq:def_column_id), AR^+R (eq:def_row_id), stable CUR
+// Q_C (Q_C^T A Q_R) Q_R^T (Remark 2.3, eq:cur_stable; protocol P:554) and
+// A ~ C Z (eq:colID).  Frobenius norm (R12).
+//
+// ortho(C): the LUPP of C (row LUPP, the same kernel as S4) gives C = Lf_C U with
+// U invertible, so range(C) = range(Lf_C); Lf_C has |entries| <= 1 and a unit lower
+// triangular pivot block, hence is well conditioned even when C is not (cond(C) = 1.6e11
+// at C2 k=512), and two passes of Cholesky QR on Lf_C give an orthonormal basis to
+// working accuracy.  The residual A - Q (Q^T A) is never
+// materialised: the last GEMM squares and sums its tiles in the epilogue (EPI_SUMSQ).
+#include "common.cuh"
+#include "internal.h"
+
+namespace skel {
+
+static sk_status basis_from_cols(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q,
+                                 int64_t* status_dev) {
+  DBuf piv;
+  SK_TRY(piv.alloc(c, (size_t)k * sizeof(int64_t)));
+  SK_TRY(lupp(c, C, false, rows, k, rows, piv.as<int64_t>(), Q, rows, nullptr, 0, nullptr, status_dev));
+  return cholqr2(c, Q, rows, k, rows, status_dev);
+}
+
+sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* Js,
+                   const int64_t* Is, int64_t k, int kind, const double* Z, int64_t ldz, double* sums,
+                   int64_t* status_dev) {
+  SK_CUDA(c, cudaMemsetAsync(status_dev, 0, sizeof(int64_t), c->stream));
+  if (kind == SK_RES_ID_COEFFS) {
+    DBuf C;
+    SK_TRY(C.alloc(c, (size_t)m * k * sizeof(double)));
+    SK_TRY(gather_cols(c, A, m, lda, Js, k, C.as<double>(), m));
+    return gemm_sumsq(c, false, false, m, n, k, -1.0, C.as<double>(), m, Z, ldz, 1.0, A, lda, sums);
+  }
+  DBuf Qc, Qr, Cb, Rt, W;
+  if (kind == SK_RES_COL_ID || kind == SK_RES_CUR) {
+    SK_TRY(Cb.alloc(c, (size_t)m * k * sizeof(double)));
+    SK_TRY(Qc.alloc(c, (size_t)m * k * sizeof(double)));
+    SK_TRY(gather_cols(c, A, m, lda, Js, k, Cb.as<double>(), m));
+    SK_TRY(basis_from_cols(c, Cb.as<double>(), m, k, Qc.as<double>(), status_dev));
+    Cb.release();
+  }
+  if (kind == SK_RES_ROW_ID || kind == SK_RES_CUR) {
+    SK_TRY(Rt.alloc(c, (size_t)n * k * sizeof(double)));
+    SK_TRY(Qr.alloc(c, (size_t)n * k * sizeof(double)));
+    SK_TRY(gather_rows_t(c, A, n, lda, Is, k, Rt.as<double>(), n));
+    SK_TRY(basis_from_cols(c, Rt.as<double>(), n, k, Qr.as<double>(), status_dev));
+    Rt.release();
+  }
+  if (kind == SK_RES_COL_ID) {
+    SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
+    SK_TRY(gemm(c, true, false, k, n, m, 1.0, Qc.as<double>(), m, A, lda, 0.0, W.as<double>(), k));
+    return gemm_sumsq(c, false, false, m, n, k, -1.0, Qc.as<double>(), m, W.as<double>(), k, 1.0, A, lda, sums);
+  }
+  if (kind == SK_RES_ROW_ID) {
+    SK_TRY(W.alloc(c, (size_t)m * k * sizeof(double)));
+    SK_TRY(gemm(c, false, false, m, k, n, 1.0, A, lda, Qr.as<double>(), n, 0.0, W.as<double>(), m));
+    return gemm_sumsq(c, false, true, m, n, k, -1.0, W.as<double>(), m, Qr.as<double>(), n, 1.0, A, lda, sums);
+  }
+  // CUR: W = Qc^T A (k x n), Mid = W Qr (k x k), B = Qc Mid (m x k), residual A - B Qr^T
+  DBuf Mid, B;
+  SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
+  SK_TRY(Mid.alloc(c, (size_t)k * k * sizeof(double)));
+  SK_TRY(B.alloc(c, (size_t)m * k * sizeof(double)));
+  SK_TRY(gemm(c, true, false, k, n, m, 1.0, Qc.as<double>(), m, A, lda, 0.0, W.as<double>(), k));
+  SK_TRY(gemm(c, false, false, k, k, n, 1.0, W.as<double>(), k, Qr.as<double>(), n, 0.0, Mid.as<double>(), k));
+  SK_TRY(gemm(c, false, false, m, k, k, 1.0, Qc.as<double>(), m, Mid.as<double>(), k, 0.0, B.as<double>(), m));
+  return gemm_sumsq(c, false, true, m, n, k, -1.0, B.as<double>(), m, Qr.as<double>(), n, 1.0, A, lda, sums);
+}
+
+}  // namespace skel

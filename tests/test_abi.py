@@ -1,0 +1,49 @@
+"""CPU: libskel.so loads, exports every symbol include/skel.h declares, and rejects bad calls
+without touching a GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2104_05877_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "skel.h")
+
+
+def declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:sk_status|void|const char\*|int64_t)\s+(sk_\w+)\s*\(", txt, re.M)))
+
+
+def test_header_declares_the_boundary():
+    names = declared()
+    for n in ("sk_sketch", "sk_select_cols", "sk_select_rows", "sk_id_coeffs", "sk_residual",
+              "sk_select_cols_cpqr", "sk_gather_cols", "sk_rand_lupp", "sk_create", "sk_destroy"):
+        assert n in names
+    assert names == _lib.EXPORTS
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for n in declared():
+        assert hasattr(lib, n), n
+    assert lib.sk_version().decode().startswith("skel")
+
+
+def test_null_context_is_an_argument_error():
+    lib = _lib.load()
+    assert lib.sk_sketch(None, None, 1, 1, 1, 1, 0, 8, 0, None, 1) == _lib.SK_E_ARG
+    assert lib.sk_select_cols(None, None, 1, 1, 1, 1, None, None, 1, None, 1, None, None) == _lib.SK_E_ARG
+    assert lib.sk_last_error(None).decode() == "null context"
+    lib.sk_destroy(None)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    with pytest.raises(OSError):
+        _lib._lib = None
+        try:
+            _lib.load(str(tmp_path / "nope.so"))
+        finally:
+            _lib._lib = None

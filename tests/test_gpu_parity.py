@@ -1,0 +1,244 @@
+"""GPU parity: every C-ABI entry point against the oracle on the same seeded inputs.
+
+Tolerances: sketch 1e-12 relative Frobenius; skeleton sets identical
+except documented near-ties; Lf / Z 1e-10 relative; residuals 1e-9 relative + 4u||A||_F;
+integer work (pivots, identity block) bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2104_05877_b200 as sk
+from inputs import kahan_witness, make_c1, make_lowrank
+from oracle import cpqr as o_cpqr
+from oracle import idcoef as o_id
+from oracle import lupp as o_lupp
+from oracle import residual as o_res
+from oracle import sketch as o_sketch
+from tests.parity import lupp_parity, rel_fro
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+U = 2.0 ** -53
+
+
+def dev_f(a):
+    """numpy (any order) -> column-major CUDA float64 tensor."""
+    return sk.fortran(torch.from_numpy(np.ascontiguousarray(a)).to(DEV))
+
+
+def dev_rowmajor(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def rand_mat(m, n, seed, decay=0.97):
+    rng = np.random.default_rng(seed)
+    r = min(m, n)
+    return make_lowrank(m, n, decay ** np.arange(r), rng)
+
+
+# ------------------------------------------------------------------ S0+S1 dense sketch
+@pytest.mark.parametrize("m,n,l,seed", [
+    (256, 256, 40, 2001),        # C1 shape
+    (1000, 777, 37, 5),          # ragged tiles in every dimension, odd l
+    (4096, 300, 26, 2018),       # C2 k=16 shape (column-reduced)
+    (3000, 64, 200, 9),          # split-K path (small n)
+    (65, 3, 65, 1),              # l = m, tiny n
+])
+def test_sketch_dense_parity(m, n, l, seed):
+    A = rand_mat(m, n, seed)
+    X = sk.sketch(dev_f(A), l, "gaussian", seed).cpu().numpy()
+    ref = o_sketch.sketch(A, l, "gaussian", seed)
+    assert rel_fro(X, ref) <= 1e-12
+
+
+def test_sketch_dense_odd_lda():
+    m, n, l = 301, 50, 20
+    A = rand_mat(m, n, 3)
+    buf = torch.zeros((n, m + 3), dtype=torch.float64, device=DEV)
+    buf[:, :m] = torch.from_numpy(A.T.copy()).to(DEV)
+    Av = buf.t()[:m]                       # column-major view, lda = m + 3 (odd)
+    X = sk.sketch(Av, l, "gaussian", 11).cpu().numpy()
+    assert rel_fro(X, o_sketch.sketch(A, l, "gaussian", 11)) <= 1e-12
+
+
+# ------------------------------------------------------------------ S1' sparse sketch
+@pytest.mark.parametrize("m,n,l,zeta,seed", [
+    (1000, 100, 60, 8, 2003),
+    (300, 33, 16, 8, 1),
+    (517, 70, 510, 8, 4),
+    (129, 5, 40, 33, 6),
+])
+def test_sketch_sparse_parity(m, n, l, zeta, seed):
+    A = rand_mat(m, n, seed)
+    X = sk.sketch(dev_f(A), l, "sparse_sign", seed, zeta).cpu().numpy()
+    ref = o_sketch.sketch(A, l, "sparse_sign", seed, zeta)
+    assert rel_fro(X, ref) <= 1e-12
+
+
+# ------------------------------------------------------------------ S2 select_cols
+@pytest.mark.parametrize("n,l,k,seed", [
+    (256, 40, 20, 1),            # C1 shape
+    (1000, 74, 64, 2),           # one panel
+    (3000, 140, 130, 3),         # several panels + trailing GEMM
+    (777, 70, 70, 4),            # k = l, ragged n
+    (70, 70, 70, 5),             # k = n (square)
+])
+def test_select_cols_parity(n, l, k, seed):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((l, n))
+    Js, Lf, Ug, gaps = sk.select_cols(dev_rowmajor(X), k, want_gaps=True)
+    (piv, Lo, Uo, go), ties = lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(X, k, f))
+    Lg = Lf.cpu().numpy()
+    assert np.max(np.abs(Lg)) <= 1.0 + 1e-14
+    np.testing.assert_array_equal(Lg[Js.cpu().numpy(), np.arange(k)], 1.0)
+    if ties == 0:
+        assert rel_fro(Lg, Lo) <= 1e-10
+        assert rel_fro(Ug.cpu().numpy(), Uo) <= 1e-10
+        np.testing.assert_allclose(gaps.cpu().numpy(), go, atol=1e-9)
+
+
+def test_select_cols_kahan_all_ties():
+    # Lemma 2 witness: every step is an exact tie -> lowest index -> 0..l-1
+    l = 20
+    X = kahan_witness(l, l + 9)
+    Js, Lf, _, _ = sk.select_cols(dev_rowmajor(X), l)
+    assert Js.cpu().tolist() == list(range(l))
+    Z, eta = sk.id_coeffs(Lf, Js, want_eta=True)
+    T = Z.cpu().numpy()[:, l:]
+    assert np.max(np.abs(T)) == 2.0 ** (l - 1)
+    assert eta >= 2.0 ** (l - 1)
+
+
+def test_select_cols_ties_lowest_original_index():
+    X = np.array([[1.0, 1.0, 3.0], [5.0, -5.0, 0.0]])
+    Js, _, _, _ = sk.select_cols(dev_rowmajor(X), 2)
+    assert Js.cpu().tolist() == [2, 0]
+
+
+def test_select_cols_rank_failure():
+    rng = np.random.default_rng(8)
+    C = rng.standard_normal((30, 3)) @ rng.standard_normal((3, 4))
+    X = C.T.copy()                                   # 4 x 30 of rank 3
+    with pytest.raises(sk.SkelError) as e:
+        sk.select_cols(dev_rowmajor(X), 4)
+    assert e.value.status == 2 and e.value.info == 4
+
+
+def test_select_cols_bad_args():
+    X = dev_rowmajor(np.ones((4, 10)))
+    with pytest.raises(sk.SkelError) as e:
+        sk.select_cols(X, 5)                          # k > l
+    assert e.value.status == 1
+
+
+# ------------------------------------------------------------------ S4 select_rows
+@pytest.mark.parametrize("m,k,seed", [(500, 20, 1), (3000, 100, 2), (129, 129, 3), (20000, 12, 4)])
+def test_select_rows_parity(m, k, seed):
+    rng = np.random.default_rng(seed)
+    C = rng.standard_normal((m, k))
+    Is, Lf, _, _ = sk.select_rows(dev_f(C), k)
+    (piv, Lo, _, _), ties = lupp_parity(Is.cpu().numpy(), lambda f: o_lupp.select_rows(C, k, f))
+    if ties == 0:
+        assert rel_fro(Lf.cpu().numpy(), Lo) <= 1e-10
+
+
+def test_gather_cols_bitwise():
+    A = rand_mat(300, 50, 1)
+    J = torch.tensor([7, 3, 49, 0], dtype=torch.int64, device=DEV)
+    C = sk.gather_cols(dev_f(A), J).cpu().numpy()
+    np.testing.assert_array_equal(C, A[:, [7, 3, 49, 0]])
+
+
+# ------------------------------------------------------------------ S2' CPQR
+@pytest.mark.parametrize("l,n,k,seed", [(26, 400, 16, 1), (74, 1000, 64, 2), (30, 5000, 30, 3)])
+def test_cpqr_parity(l, n, k, seed):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((l, n))
+    Js, R = sk.select_cols_cpqr(dev_rowmajor(X), k, want_r=True)
+    piv, Ro = o_cpqr.select_cols_cpqr(X, k)
+    assert Js.cpu().tolist() == piv.tolist()
+    assert rel_fro(R.cpu().numpy(), Ro) <= 1e-10
+
+
+def test_cpqr_spec_case():
+    X = np.array([[3.0, 0.0, 0.0], [0.0, 4.0, 0.0]])
+    Js, _ = sk.select_cols_cpqr(dev_rowmajor(X), 2)
+    assert Js.cpu().tolist() == [1, 0]
+
+
+# ------------------------------------------------------------------ S5 id_coeffs
+@pytest.mark.parametrize("n,k,seed", [(300, 20, 1), (2000, 100, 2), (64, 64, 3)])
+def test_id_coeffs_parity(n, k, seed):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((k + 5, n))
+    Js, Lf, _, _ = sk.select_cols(dev_rowmajor(X), k)
+    Z, eta = sk.id_coeffs(Lf, Js, want_eta=True)
+    Zg = Z.cpu().numpy()
+    jg = Js.cpu().numpy()
+    np.testing.assert_array_equal(Zg[:, jg], np.eye(k))          # identity block, bitwise
+    Zo, _, eta_o = o_id.id_coeffs(Lf.cpu().numpy(), jg)          # same factor -> isolates S5
+    assert rel_fro(Zg, Zo) <= 1e-10
+    assert abs(eta - eta_o) <= 1e-8 * eta_o
+
+
+def test_id_coeffs_spec_eta():
+    X = np.array([[1.0, 0.0, 0.5], [0.0, 1.0, 0.5]])
+    Js, Lf, _, _ = sk.select_cols(dev_rowmajor(X), 2)
+    Z, eta = sk.id_coeffs(Lf, Js, want_eta=True)
+    np.testing.assert_allclose(Z.cpu().numpy()[:, 2], [0.5, 0.5], atol=1e-16)
+    assert abs(eta - math.sqrt(1.5)) < 1e-12
+
+
+# ------------------------------------------------------------------ S6 residual
+@pytest.mark.parametrize("kind", ["col_id", "row_id", "cur", "id_coeffs"])
+def test_residual_parity(kind):
+    A, sigma = make_c1(seed=1001)
+    k, l = 20, 40
+    Ad = dev_f(A)
+    X = sk.sketch(Ad, l, "gaussian", 2001)
+    Js, Lf, _, _ = sk.select_cols(X, k)
+    C = sk.gather_cols(Ad, Js)
+    Is, _, _, _ = sk.select_rows(C, k)
+    Z = sk.id_coeffs(Lf, Js)[0] if kind == "id_coeffs" else None
+    r, nA = sk.residual(Ad, Js, Is, kind, Z)
+    ro, nAo = o_res.residual(A, Js.cpu().numpy(), Is.cpu().numpy(), kind,
+                             Z.cpu().numpy() if Z is not None else None)
+    assert abs(r - ro) <= 1e-9 * ro + 4 * U * nAo
+    assert abs(nA - nAo) <= 1e-13 * nAo
+    assert r >= o_res.optimal_error(sigma, k) * (1 - 1e-12)
+
+
+def test_residual_exact_rank_is_zero():
+    rng = np.random.default_rng(4)
+    A = make_lowrank(400, 300, np.array([5.0, 3, 2, 1, 0.5, 0.25]), rng)
+    Ad = dev_f(A)
+    X = sk.sketch(Ad, 6, "gaussian", 1)
+    Js, _, _, _ = sk.select_cols(X, 6)
+    Is, _, _, _ = sk.select_rows(sk.gather_cols(Ad, Js), 6)
+    for kind in ("col_id", "row_id", "cur"):
+        r, nA = sk.residual(Ad, Js, Is, kind)
+        assert r <= 1e-12 * nA
+
+
+def test_residual_identity_closed_form():
+    n, k = 200, 17
+    Ad = dev_f(np.eye(n))
+    J = torch.arange(k, dtype=torch.int64, device=DEV)
+    r, nA = sk.residual(Ad, J, J, "col_id")
+    assert abs(r - math.sqrt(n - k)) < 1e-12 and abs(nA - math.sqrt(n)) < 1e-12
+
+
+# ------------------------------------------------------------------ Algorithm 2 end to end
+def test_rand_lupp_host_and_device_agree():
+    A = rand_mat(600, 500, 7, 0.95)
+    Af = np.asfortranarray(A)
+    Js_h, Is_h = sk.rand_lupp(torch.from_numpy(Af.T.copy()).t(), 30, 40, rows=True, seed=5)
+    Ad = dev_f(A)
+    X = sk.sketch(Ad, 40, "gaussian", 5)
+    Js, _, _, _ = sk.select_cols(X, 30)
+    Is, _, _, _ = sk.select_rows(sk.gather_cols(Ad, Js), 30)
+    assert Js_h.tolist() == Js.cpu().tolist()
+    assert Is_h.tolist() == Is.cpu().tolist()
