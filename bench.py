@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark of the randomized-LUPP skeleton-selection hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--k 512] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): A = U diag(10^(-i/50)) V^T, 4096 x 4096 FP64,
+Haar U, V (seed 1002); Gaussian Omega, k = 512, l = k + 10 = 522 (seed 2002 + k).
+One step = the whole hot path of SURVEY.md section 8(a) for C2:
+    S0+S1 sketch X = Omega A  ->  S2 select_cols (LUPP)  ->  S2' select_cols_cpqr (comparison)
+    ->  S5 id_coeffs  ->  S6 residual ||A - CC^+A||_F (gather S3 + LUPP-basis S4 inside).
+value = the BASELINE.json metric "skeleton-selection time (sketch+LUPP)" = S1 + S2 device time
+per step (ms, lower is better), max over ranks.  ms_per_step = the whole step.
+L2 policy: a 512 MiB buffer is overwritten between timed steps (untimed), so every step
+starts cold; per-step CUDA events on the library's stream.
+
+--impl reference times the plain CPU oracle (oracle/) on the same config on the host cores
+(the reference arm for this paper-only build).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.13   # measured DMMA issue ceiling on this pool's B200 (profiles/round1/fp64_peaks.txt)
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--k", type=int, default=512)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    from inputs import CONFIGS
+    cfg = CONFIGS[args.config]
+    k = args.k
+    l = cfg["l"](k)
+    seed = cfg["sk_seed"] + (k if args.config in ("C2", "C4") else 0)
+    desc = {
+        "C2": f"C2: A 4096x4096 FP64 = U diag(10^(-i/50)) V^T (Haar), Gaussian Omega, k={k}, l={l}",
+    }.get(args.config, f"{args.config} k={k} l={l}")
+    return cfg, k, l, seed, desc
+
+
+def make_input(args, cfg):
+    from inputs import make_config
+    A, sigma = make_config(args.config, seed=cfg["seed"])
+    return A, sigma
+
+
+def cpu_info():
+    cores = len(os.sched_getaffinity(0))
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cores, model
+
+
+def oracle_selection(A, k, l, seed, emb="gaussian"):
+    """The oracle's sketch + LUPP (test infrastructure; timed as the CPU baseline)."""
+    from oracle import lupp as o_lupp
+    from oracle import sketch as o_sketch
+    X = o_sketch.sketch(A, l, emb, seed)
+    piv, _, _, _ = o_lupp.select_cols(X, k)
+    return piv
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=5)
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        busy = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg, k, l, seed, desc = workload(args)
+    A, _ = make_input(args, cfg)
+    cores, model = cpu_info()
+    steps = max(1, min(args.steps, 3))
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        oracle_selection(A, k, l, seed)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle_selection(A, k, l, seed)
+        times.append((time.perf_counter() - t0) * 1e3)
+    v = statistics.mean(times)
+    line = {
+        "impl": "reference", "metric": "skeleton-selection time (sketch+LUPP)", "value": v, "unit": "ms",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": v, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "m": 4096, "n": 4096, "k": k, "l": l},
+        "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "oracle",
+                         "sample": f"full {args.config} selection (oracle sketch + LUPP) on {model}"},
+        "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_05877_b200 as sk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)
+
+    cfg, k, l, seed, desc = workload(args)
+    A_np, sigma = make_input(args, cfg)
+    m, n = A_np.shape
+    with torch.cuda.stream(stream):
+        A = sk.fortran(torch.from_numpy(np.ascontiguousarray(A_np)).to(dev))
+        flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize(dev)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(record):
+        """One pass of the hot path; record(name, start_event, end_event)."""
+        e = [ev() for _ in range(6)]
+        e[0].record(stream)
+        X = sk.sketch(A, l, "gaussian", seed)
+        e[1].record(stream)
+        Js, Lf, _, _ = sk.select_cols(X, k, check=False)
+        e[2].record(stream)
+        Jc, _ = sk.select_cols_cpqr(X, k, check=False)
+        e[3].record(stream)
+        Z, _ = sk.id_coeffs(Lf, Js)
+        e[4].record(stream)
+        res, nA = sk.residual(A, Js, None, "col_id")
+        e[5].record(stream)
+        record(e)
+        return Js, Jc, res, nA
+
+    stage_names = ["sketch", "select_cols_lupp", "select_cols_cpqr", "id_coeffs", "residual"]
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(lambda e: None)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        recs = []
+        launches0 = sk.launch_count(local)
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize(dev)
+            for _ in range(args.steps):
+                flush.fill_(1)                     # untimed L2 flush between steps
+                out = step(recs.append)
+            torch.cuda.synchronize(dev)
+        launches = sk.launch_count(local) - launches0
+        if world > 1:
+            dist.barrier()
+    stage_ms = {nm: [] for nm in stage_names}
+    step_ms = []
+    for e in recs:
+        for i, nm in enumerate(stage_names):
+            stage_ms[nm].append(e[i].elapsed_time(e[i + 1]))
+        step_ms.append(e[0].elapsed_time(e[5]))
+    sel = [a + b for a, b in zip(stage_ms["sketch"], stage_ms["select_cols_lupp"])]
+    value = statistics.mean(sel)
+    ms_step = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([value, ms_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        value, ms_step = float(t[0]), float(t[1])
+
+    Js, Jc, res, nA = out
+    from oracle.residual import optimal_error  # closed form sum_{i>k} sigma_i^2 (Eckart-Young)
+    opt = optimal_error(sigma, k)
+
+    # roofline of the dominant kernel: the dense DMMA sketch (one launch per call)
+    sk_ms = statistics.mean(stage_ms["sketch"])
+    flops = 2.0 * l * m * n
+    achieved = flops / (sk_ms * 1e-3) / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "round1", "sketch_dram_bytes.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"{args.config}_k{k}")
+        except Exception:
+            traffic = None
+    roofline = {"kernel": "k_sketch_dense", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "peak_source": "measured FP64 DMMA ceiling (tools/microbench/fp64_pipes.cu); "
+                               "MEASURED_PEAKS.json has no FP64 entry; cuBLAS DGEMM measured 35.5"}
+
+    # end to end through the public API with host buffers (Algorithm 2 entry point)
+    e2e = None
+    if not args.no_e2e:
+        A_host = torch.from_numpy(np.ascontiguousarray(A_np.T)).pin_memory().t()
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                sk.rand_lupp(A_host, k, l, seed=seed, device=local)
+            times = []
+            for _ in range(max(3, min(args.steps, 10))):
+                e0, e1 = ev(), ev()
+                e0.record(stream)
+                sk.rand_lupp(A_host, k, l, seed=seed, device=local)
+                e1.record(stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+        e2e_v = statistics.mean(times)
+        if world > 1:
+            t = torch.tensor([e2e_v], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_v = float(t[0])
+        e2e = {"value": e2e_v, "unit": "ms", "h2d_bytes_per_step": int(m * n * 8), "d2h_bytes_per_step": int(k * 8),
+               "api": "sk_rand_lupp (host A, pinned) -> Js on host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores, model = cpu_info()
+        t0 = time.perf_counter()
+        piv_o = oracle_selection(A_np, k, l, seed)
+        cpu_ms = (time.perf_counter() - t0) * 1e3
+        same = int(np.sum(piv_o == Js.cpu().numpy()))
+        cpu = {"value": cpu_ms, "unit": "ms", "cores": cores, "kind": "oracle",
+               "sample": f"one full {args.config} selection (sketch + LUPP), numpy/BLAS on {model}",
+               "pivots_equal_to_gpu": f"{same}/{k}"}
+
+    if rank == 0:
+        line = {
+            "metric": "skeleton-selection time (sketch+LUPP)", "value": value, "unit": "ms",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": False, "scaling": "weak" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "m": m, "n": n, "k": k, "l": l,
+                       "l2": "flushed: 512 MiB overwrite between timed steps (untimed)",
+                       "parallelism": "replicas" if world > 1 else "1 GPU"},
+            "stages_ms": {nm: statistics.mean(v) for nm, v in stage_ms.items()},
+            "sketch_tflops": achieved,
+            "residual": {"col_id_fro": res, "normA_fro": nA, "opt_fro": opt, "ratio": res / opt if opt > 0 else None},
+            "cpqr_overlap": int(len(set(Js.cpu().tolist()) & set(Jc.cpu().tolist()))),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
