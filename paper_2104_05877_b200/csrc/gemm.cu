@@ -116,7 +116,31 @@ __global__ void __launch_bounds__(NT) k_gemm(Params p) {
   }
   dev::cp_async_wait<0>();
 
-  if (MODE == EPI_STORE || MODE == EPI_PARTIAL) {
+  if (MODE == EPI_STORE) {
+    // issue every C load before the first store (the compiler cannot reorder them: aliasing)
+    double cv[4][4][2];
+    const bool rd = p.beta != 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int m = m0 + wm + i * 8 + g, n = n0 + wn + j * 8 + 2 * q + h;
+          cv[i][j][h] = (rd && m < p.M && n < p.N) ? p.C[m + (int64_t)n * p.ldc] : 0.0;
+        }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int m = m0 + wm + i * 8 + g, n = n0 + wn + j * 8 + 2 * q + h;
+          if (m < p.M && n < p.N)
+            p.C[m + (int64_t)n * p.ldc] = rd ? fma(p.beta, cv[i][j][h], p.alpha * acc[i][j][h])
+                                             : p.alpha * acc[i][j][h];
+        }
+  } else if (MODE == EPI_PARTIAL) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int m = m0 + wm + i * 8 + g;
@@ -127,13 +151,7 @@ __global__ void __launch_bounds__(NT) k_gemm(Params p) {
         for (int h = 0; h < 2; ++h) {
           const int n = n0 + wn + j * 8 + 2 * q + h;
           if (n >= p.N) continue;
-          if (MODE == EPI_PARTIAL) {
-            p.out[(int64_t)blockIdx.z * p.M * p.N + m + (int64_t)n * p.M] = acc[i][j][h];
-          } else {
-            double* cp = p.C + m + (int64_t)n * p.ldc;
-            const double v = p.alpha * acc[i][j][h];
-            *cp = (p.beta == 0.0) ? v : fma(p.beta, *cp, v);
-          }
+          p.out[(int64_t)blockIdx.z * p.M * p.N + m + (int64_t)n * p.M] = acc[i][j][h];
         }
     }
   } else {  // EPI_SUMSQ: e = alpha*acc + beta*Cin; accumulate e^2 and Cin^2 (never written)

@@ -8,21 +8,24 @@
 // rows 0..k-1 of X enter), R6 (ties -> lowest original index, no physical swaps),
 // R7 (rank failure when |pivot| <= 1e-14 max|M|).
 //
-// B200 design: the k-long chain of global argmaxes is the
-// critical path, so the pivot search runs inside ONE thread-block cluster (16 CTAs,
-// distributed shared memory) where an exchange costs a cluster barrier (~0.2 us)
-// instead of a grid-wide barrier (~3.7 us measured).  The panel is factored in column
-// blocks of width bp held in the cluster's shared memory; between blocks the whole GPU
-// applies the trailing update with the DMMA GEMM:
-//     per block [c0, c1):  k_panel  (cluster)  : bp pivot steps, L block, U(c0:c1, c0:c1)
-//                          k_u12    (grid)     : U(c0:c1, c1:k) = L11^{-1} M(piv, c1:k)
-//                          gemm     (grid)     : M(:, c1:k) -= Lf(:, c0:c1) U(c0:c1, c1:k)
-// The blocked and unblocked eliminations are the same algorithm; only rounding differs.
+// B200 design.  The k-long chain of global argmaxes is the
+// critical path.  The pivot search therefore runs inside ONE thread-block cluster
+// (16 CTAs on 16 SMs, distributed shared memory): an exchange costs one cluster
+// barrier instead of a grid-wide flag barrier (3.7 us measured, tools/microbench).
+// The panel is factored in column blocks of width bp held in the cluster's shared
+// memory (one thread per row), so a step is
+//     warp argmax -> CTA argmax -> DSMEM publish -> cluster barrier -> remote fetch of
+//     the winning row (<= bp doubles) -> update pass (which also yields the next argmax),
+// two CTA barriers and one cluster barrier per pivot.  Between column blocks:
+//     k_lupp_u12 (grid) : U(c0:c1, c1:k) = L11^{-1} M(piv, c1:k)   (forward substitution)
+//     gemm       (grid) : M(:, c1:k) -= Lf(:, c0:c1) U(c0:c1, c1:k) (DMMA)
+// Blocked and unblocked elimination are the same algorithm; only rounding differs.
 #include <cooperative_groups.h>
 
 #include <algorithm>
 
 #include "common.cuh"
+#include "dmma.cuh"
 #include "internal.h"
 
 namespace cg = cooperative_groups;
@@ -30,19 +33,22 @@ namespace cg = cooperative_groups;
 namespace skel {
 namespace {
 
-constexpr int PNT = 512;   // threads per panel CTA
+constexpr int PNT = 256;            // threads per panel CTA
+constexpr int PNW = PNT / 32;       // warps
+constexpr int MAXCS = 16;           // max cluster size
+constexpr int U12_BP = 64;          // max block width when there is a trailing update
 
-struct Slot {
-  double a1, a2;
-  long long idx;
-  long long pad;
+struct Slot {            // a warp's pivot candidate, published to every CTA of the cluster
+  unsigned long long key;  // bits(|v|) + 1 (0 = none): orders like |v|
+  long long idx;           // global row
+  unsigned long long sec;  // runner-up key (for the gap diagnostic)
+  double lp;               // the candidate row's multiplier of the previous step
 };
 
 struct PanelParams {
   double* W;  int64_t n;  int k;        // working panel, n x k col-major (ld n), trailing-updated
   int c0, bp;                            // this column block
   int R;                                 // rows per CTA
-  int pstride;                           // smem row stride (odd)
   int* rowstate;                         // global: -1 active, else step at which picked
   int64_t* Js; double* Lf; int64_t ldlf; double* Uw;   // Uw: k x k col-major (ld k)
   double* gaps;
@@ -67,143 +73,607 @@ __global__ void k_lupp_init(const double* P, bool row_major, int64_t n, int k, i
   if ((threadIdx.x & 31) == 0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(mx));
 }
 
+// Shared-memory layout of the panel kernel (bytes), shared by host and device.
+struct PanelSmem {
+  size_t P, urow, wrow, slots, ub, js, gp, state, mbar, total;
+  int stride, rs;
+  __host__ __device__ PanelSmem(int R, int bp) {
+    stride = ((bp + 1) | 3) - 1;            // = 2 mod 4 doubles: 16-byte row-per-lane access is conflict-free
+    if (stride < bp) stride += 4;
+    rs = (bp + 3) & ~1;                     // row buffers (even: 16-byte aligned)
+    P = 0;
+    size_t o = (size_t)R * stride * sizeof(double);
+    urow = o;  o += (size_t)2 * rs * sizeof(double);                // pivot rows U(s,:), U(s-1,:) (CTA)
+    wrow = o;  o += (size_t)2 * PNW * rs * sizeof(double);          // published candidate rows per warp
+    o = (o + 15) & ~(size_t)15;
+    slots = o; o += (size_t)2 * MAXCS * PNW * sizeof(Slot);
+    ub = o;    o += (size_t)bp * bp * sizeof(double);                  // U block (CTA 0)
+    js = o;    o += (size_t)bp * sizeof(long long);
+    gp = o;    o += (size_t)bp * sizeof(double);
+    state = o; o += (size_t)R * sizeof(int);
+    o = (o + 15) & ~(size_t)15;
+    mbar = o;  o += 2 * sizeof(unsigned long long);
+    total = o + 64;
+  }
+};
+
+// Warp argmax of (key, idx): largest key, ties -> lowest idx; plus the runner-up key.
+// REDUX-based (32-bit halves), no shuffles of doubles.
+__device__ __forceinline__ void warp_argmax(unsigned long long key, unsigned idx, unsigned long long sec,
+                                            unsigned long long& wkey, unsigned& widx,
+                                            unsigned long long& wsec, bool want_sec) {
+  const unsigned FULL = 0xffffffffu;
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mh = __reduce_max_sync(FULL, hi);
+  const unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
+  wkey = ((unsigned long long)mh << 32) | ml;
+  widx = __reduce_min_sync(FULL, (key == wkey && key != 0ull) ? idx : 0xffffffffu);
+  wsec = 0ull;
+  if (want_sec) {
+    const unsigned long long own = (key == wkey && idx == widx) ? sec : key;
+    const unsigned sh = __reduce_max_sync(FULL, (unsigned)(own >> 32));
+    const unsigned sl = __reduce_max_sync(FULL, (unsigned)(own >> 32) == sh ? (unsigned)own : 0u);
+    wsec = ((unsigned long long)sh << 32) | sl;
+  }
+}
+
+__device__ __forceinline__ void cand_push(unsigned long long k, long long i, unsigned long long& key, long long& idx,
+                                          unsigned long long& sec) {
+  if (k > key || (k == key && k != 0ull && i < idx)) {
+    sec = key > sec ? key : sec;
+    key = k; idx = i;
+  } else {
+    sec = k > sec ? k : sec;
+  }
+}
+
+__device__ __forceinline__ unsigned long long mag_key(double v) {
+  return (unsigned long long)__double_as_longlong(fabs(v)) + 1ull;
+}
+
+// ---- cluster mailbox: st.async into a peer CTA's shared memory, completing bytes on the
+// peer's mbarrier; the receiver waits on its own mbarrier (no cluster-wide barrier).
+__device__ __forceinline__ unsigned mapa(unsigned local_addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v2(unsigned raddr, unsigned long long a, unsigned long long b,
+                                            unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+               ::"r"(raddr), "l"(a), "l"(b), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned addr, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(unsigned addr, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(addr), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// One thread per row (RPT = ceil(R / PNT) rows per thread), the CTA's block of rows in
+// shared memory.  Pivot step s, per warp, with no CTA-wide barrier:
+//   A  wait on this CTA's mailbox (mbarrier) for the CS*PNW warp candidates of step s;
+//      reduce them (REDUX) to the winner -- identical in every warp of every CTA;
+//   F  fetch the winner's published row copy from its owner's shared memory (DSMEM) and
+//      apply the one update it lacks (step s-1 on columns >= s+1);
+//   B  critical part: multipliers L(i,s) and column s+1 of own rows -> warp argmax ->
+//      copy of the candidate row into this warp's publish buffer -> st.async of the
+//      candidate into every CTA's mailbox (completes bytes on that CTA's mbarrier);
+//   C  bulk Schur update of columns >= s+2, overlapping the exchange of step s+1.
+template <bool GAPS>
 __global__ void __launch_bounds__(PNT, 1) k_lupp_panel(PanelParams p) {
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
   const int csize = (int)cluster.num_blocks();
-  extern __shared__ __align__(16) double sm[];
-  double* P = sm;                                               // [R][pstride]
-  double* urow = P + (size_t)p.R * p.pstride;                   // [bp]
-  Slot* slots = reinterpret_cast<Slot*>(urow + ((p.bp + 1) & ~1));   // [2][csize]
-  dev::Cand* red = reinterpret_cast<dev::Cand*>(slots + 2 * csize);  // [33]
-  int* state = reinterpret_cast<int*>(red + 33);                 // [R]
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const PanelSmem L(p.R, p.bp);
+  double* P = reinterpret_cast<double*>(smraw + L.P);                 // [R][stride]
+  Slot* slots = reinterpret_cast<Slot*>(smraw + L.slots);             // [2][MAXCS*PNW]
+  double* ub = reinterpret_cast<double*>(smraw + L.ub);               // [bp][bp]
+  long long* js = reinterpret_cast<long long*>(smraw + L.js);         // [bp]
+  double* gp = reinterpret_cast<double*>(smraw + L.gp);               // [bp]
+  int* state = reinterpret_cast<int*>(smraw + L.state);               // [R]
+  const unsigned mbar0 = dev::smem_u32(smraw + L.mbar);                // 2 mbarriers (step parity)
+  const unsigned slots_u32 = dev::smem_u32(slots);
   __shared__ int s_stop;
 
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bp = p.bp, ps = L.stride, rs = L.rs;
+  double* urow0 = reinterpret_cast<double*>(smraw + L.urow);                           // + par*rs
+  double* wrow0 = reinterpret_cast<double*>(smraw + L.wrow) + (size_t)warp * rs;
+  const unsigned wrow_u32 = dev::smem_u32(smraw + L.wrow);
   const int64_t r0 = (int64_t)crank * p.R;
   const int Rc = (int)std::max<int64_t>(0, std::min<int64_t>(p.R, p.n - r0));
-  if (threadIdx.x == 0) s_stop = (*p.status != 0);
-  // load this CTA's rows of the column block (coalesced along rows)
-  for (int e = threadIdx.x; e < Rc * p.bp; e += PNT) {
-    const int li = e % Rc, s = e / Rc;
-    P[li * p.pstride + s] = p.W[(r0 + li) + (int64_t)(p.c0 + s) * p.n];
+  const int nslots = csize * PNW;
+
+  if (tid == 0) {
+    s_stop = (*p.status != 0);
+    mbar_init(mbar0, 1);
+    mbar_init(mbar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int li = threadIdx.x; li < Rc; li += PNT) state[li] = p.rowstate[r0 + li];
+  for (int e = tid; e < Rc * bp; e += PNT) {          // async copy, coalesced along rows
+    const int li = e % Rc, s = e / Rc;
+    dev::cp_async8(P + (size_t)li * ps + s, p.W + (r0 + li) + (int64_t)(p.c0 + s) * p.n, true);
+  }
+  dev::cp_async_commit();
+  for (int li = tid; li < Rc; li += PNT) state[li] = p.rowstate[r0 + li];
   const double tol = 1e-14 * __longlong_as_double((long long)*p.maxbits);
-  cluster.sync();
-  const bool stopped = s_stop;
+  dev::cp_async_wait<0>();
+  cluster.sync();    // rows staged, mbarriers initialised cluster-wide
+  const int s_end = s_stop ? 0 : bp;
 
-  // thread -> (row, column-lane) map for the Schur update
-  int tpr = 1;
-  while (tpr < 32 && Rc > 0 && tpr * 2 * Rc <= PNT) tpr *= 2;
-  const int rows_per_pass = PNT / tpr;
-  const int my_cj = threadIdx.x % tpr;
+  // publish this warp's candidate for step `sn`: rows' column sn, copy of the winning row
+  auto publish = [&](int sn, unsigned long long ckey, long long cidx, unsigned long long csec) {
+    const int par = sn & 1;
+    if (tid == 0) mbar_arm(mbar0 + 8 * par, (unsigned)(nslots * sizeof(Slot)));
+    __syncwarp();   // the lanes' row updates are visible to the lanes copying the candidate row
+    unsigned long long wk, ws;
+    unsigned wi;
+    warp_argmax(ckey, (unsigned)cidx, csec, wk, wi, ws, GAPS);
+    if (wk) {   // copy row wi, columns sn-1 .. bp-1 (multiplier of step sn-1 included)
+      const double* src = P + (size_t)wi * ps;
+      double* dst = wrow0 + (size_t)par * PNW * rs;
+      for (int j = max(sn - 1, 0) + lane; j < bp; j += 32) dst[j] = src[j];
+    }
+    __syncwarp();
+    const double lpc = (wk && sn > 0) ? P[(size_t)wi * ps + sn - 1] : 0.0;
+    if (lane < csize) {
+      const unsigned off = (unsigned)((par * (MAXCS * PNW) + crank * PNW + warp) * sizeof(Slot));
+      const unsigned ra = mapa(slots_u32 + off, (unsigned)lane);
+      const unsigned rb = mapa(mbar0 + 8 * par, (unsigned)lane);
+      const long long gi = wk ? (long long)(r0 + wi) : 0x7fffffffffffffffLL;
+      st_async_v2(ra, wk, (unsigned long long)gi, rb);
+      st_async_v2(ra + 16, ws, (unsigned long long)__double_as_longlong(lpc), rb);
+    }
+  };
 
-  int s_end = stopped ? 0 : p.bp;
+  if (s_end > 0) {   // candidate for step 0
+    unsigned long long ckey = 0ull, csec = 0ull;
+    long long cidx = 0x7fffffffffffffffLL;
+    for (int li = tid; li < Rc; li += PNT)
+      if (state[li] < 0) cand_push(mag_key(P[(size_t)li * ps]), li, ckey, cidx, csec);
+    publish(0, ckey, cidx, csec);
+  }
+  int s_done = s_end;
   for (int s = 0; s < s_end; ++s) {
-    const int t = p.c0 + s;
-    // (a) local candidate over active rows
-    dev::Cand c = dev::cand_none();
-    for (int li = threadIdx.x; li < Rc; li += PNT)
-      if (state[li] < 0) {
-        dev::Cand d{fabs(P[li * p.pstride + s]), -1.0, (long long)(r0 + li)};
-        c = dev::cand_merge(c, d);
-      }
-    c = dev::block_cand_reduce(c, red);
-    // (b) publish to every CTA of the cluster (distributed shared memory)
-    Slot* mine = slots + (s & 1) * csize + crank;
-    if (threadIdx.x < csize) {
-      Slot* dst = cluster.map_shared_rank(mine, (int)threadIdx.x);
-      *dst = Slot{c.a1, c.a2, c.i1, 0};
+    const int t = p.c0 + s, par = s & 1;
+    // (A) mailbox -> winner
+    mbar_wait(mbar0 + 8 * par, (unsigned)((s >> 1) & 1));
+    unsigned long long bk = 0ull, bs = 0ull;
+    long long bi = 0x7fffffffffffffffLL;
+    double blp = 0.0;
+    for (int e = lane; e < nslots; e += 32) {
+      const Slot sl = slots[par * (MAXCS * PNW) + e];
+      if (sl.key && (sl.key > bk || (sl.key == bk && sl.idx < bi))) blp = sl.lp;
+      if (sl.key) cand_push(sl.key, sl.idx, bk, bi, bs);
+      if (GAPS) bs = sl.sec > bs ? sl.sec : bs;
     }
-    cluster.sync();
-    // (c) identical reduction in every CTA
-    dev::Cand w = dev::cand_none();
-    for (int r = 0; r < csize; ++r) {
-      const Slot& sl = slots[(s & 1) * csize + r];
-      w = dev::cand_merge(w, dev::Cand{sl.a1, sl.a2, sl.idx});
-    }
-    if (!(w.a1 > tol)) {   // rank failure (R7): same decision in every CTA
-      if (crank == 0 && threadIdx.x == 0) {
+    unsigned long long wk, ws;
+    unsigned wi;
+    warp_argmax(bk, bk ? (unsigned)bi : 0xffffffffu, bs, wk, wi, ws, GAPS);
+    const double a1 = wk ? __longlong_as_double((long long)(wk - 1ull)) : -1.0;
+    if (!(a1 > tol)) {   // rank failure (R7): the same decision in every warp of every CTA
+      if (crank == 0 && tid == 0) {
         *p.status = t + 1;
         for (int tt = t; tt < p.k; ++tt) p.Js[tt] = -1;
       }
+      s_done = s;
       break;
     }
-    const int wr = (int)(w.i1 / p.R);
-    const int wl = (int)(w.i1 - (int64_t)wr * p.R);
-    // (d) fetch the pivot row's remaining block entries from its owner
+    const long long widx = (long long)wi;
+    const unsigned wlanes = __ballot_sync(0xffffffffu, bk == wk && bi == widx);
+    const double lp = __shfl_sync(0xffffffffu, blp, __ffs(wlanes) - 1);
+    // (F) the winner's published row copy (one remote load per thread, the CTA shares it),
+    //     fixed up with the step s-1 update it lacks
+    double* ucur = urow0 + (size_t)par * rs;
+    const double* uprev = urow0 + (size_t)(par ^ 1) * rs;
     {
-      const double* rp = cluster.map_shared_rank(P + (size_t)wl * p.pstride, wr);
-      for (int j = s + threadIdx.x; j < p.bp; j += PNT) urow[j] = rp[j];
-    }
-    __syncthreads();
-    if (crank == 0) {
-      if (threadIdx.x == 0) {
-        p.Js[t] = w.i1;
-        if (p.gaps) p.gaps[t] = (w.a1 - fmax(w.a2, 0.0)) / w.a1;
+      const int wr = (int)(widx / p.R);
+      const int wl = (int)(widx - (int64_t)wr * p.R);
+      const int ww = (wl % PNT) >> 5;
+      const unsigned src = mapa(wrow_u32 + (unsigned)(((size_t)par * PNW + ww) * rs * sizeof(double)), (unsigned)wr);
+      for (int j = s + tid; j < bp; j += PNT) {
+        double v;
+        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(src + 8u * j));
+        ucur[j] = (s > 0 && j > s) ? fma(-lp, uprev[j], v) : v;
       }
-      for (int j = s + threadIdx.x; j < p.bp; j += PNT) p.Uw[t + (int64_t)(p.c0 + j) * p.k] = urow[j];
+      asm volatile("bar.sync 1, %0;" ::"n"(PNT) : "memory");
     }
-    if (wr == crank && threadIdx.x == 0) state[wl] = t;
-    __syncthreads();
-    // (e) Schur-complement update of the active rows (columns s..bp-1 of the block)
-    const double piv = urow[s];
-    for (int base = 0; base < Rc; base += rows_per_pass) {
-      const int li = base + threadIdx.x / tpr;
-      double L = 0.0;
-      const bool act = li < Rc && state[li] < 0;
-      if (act) L = P[li * p.pstride + s] / piv;
-      __syncwarp();
-      if (act) {
-        double* row = P + (size_t)li * p.pstride;
-        for (int j = s + 1 + my_cj; j < p.bp; j += tpr) row[j] = fma(-L, urow[j], row[j]);
+    if (crank == 0 && warp == 0) {
+      if (lane == 0) {
+        js[s] = widx;
+        if (GAPS) {
+          const double a2 = ws ? __longlong_as_double((long long)(ws - 1ull)) : 0.0;
+          gp[s] = (a1 - a2) / a1;
+        }
       }
-      __syncthreads();
-      if (act && my_cj == 0) P[li * p.pstride + s] = L;
+      for (int j = s + lane; j < bp; j += 32) ub[s * bp + j] = ucur[j];
     }
-    __syncthreads();
+    // (B) multipliers and column s+1 of own rows; candidate for step s+1
+    const double piv = ucur[s];
+    const bool more = s + 1 < bp;
+    const double u1 = more ? ucur[s + 1] : 0.0;
+    unsigned long long ckey = 0ull, csec = 0ull;
+    long long cidx = 0x7fffffffffffffffLL;
+    for (int li = tid; li < Rc; li += PNT) {
+      if (state[li] >= 0) continue;
+      if (r0 + li == widx) { state[li] = t; continue; }
+      double* row = P + (size_t)li * ps;
+      const double Lm = row[s] / piv;
+      row[s] = Lm;
+      if (more) {
+        const double v = fma(-Lm, u1, row[s + 1]);
+        row[s + 1] = v;
+        cand_push(mag_key(v), li, ckey, cidx, csec);
+      }
+    }
+    if (more) publish(s + 1, ckey, cidx, csec);
+    // (C) bulk update of columns >= s+2 (off the pivot chain's critical path)
+    if (s + 2 < bp) {
+      for (int li = tid; li < Rc; li += PNT) {
+        if (state[li] != -1) continue;
+        double* row = P + (size_t)li * ps;
+        const double Lm = row[s];
+        int j = s + 2;
+        if (j & 1) { row[j] = fma(-Lm, ucur[j], row[j]); ++j; }
+        for (; j + 3 < bp; j += 4) {
+          double2 x0 = *reinterpret_cast<double2*>(row + j);
+          double2 x1 = *reinterpret_cast<double2*>(row + j + 2);
+          const double2 y0 = *reinterpret_cast<const double2*>(ucur + j);
+          const double2 y1 = *reinterpret_cast<const double2*>(ucur + j + 2);
+          x0.x = fma(-Lm, y0.x, x0.x); x0.y = fma(-Lm, y0.y, x0.y);
+          x1.x = fma(-Lm, y1.x, x1.x); x1.y = fma(-Lm, y1.y, x1.y);
+          *reinterpret_cast<double2*>(row + j) = x0;
+          *reinterpret_cast<double2*>(row + j + 2) = x1;
+        }
+        for (; j < bp; ++j) row[j] = fma(-Lm, ucur[j], row[j]);
+      }
+    }
   }
-  // write the L block and the row states back
-  for (int e = threadIdx.x; e < Rc * p.bp; e += PNT) {
-    const int li = e % Rc, s = e / Rc;
-    const int st = state[li], t = p.c0 + s;
-    double v;
-    if (st < 0 || st > t) v = P[li * p.pstride + s];
-    else v = (st == t) ? 1.0 : 0.0;
+  __syncthreads();
+  // outputs of the block: pivots, gaps, U rows (CTA 0); the L block and row states (all)
+  if (crank == 0) {
+    for (int s = tid; s < s_done; s += PNT) {
+      p.Js[p.c0 + s] = js[s];
+      if (GAPS) p.gaps[p.c0 + s] = gp[s];
+    }
+    for (int e = tid; e < s_done * bp; e += PNT) {
+      const int s = e / bp, j = e % bp;
+      if (j >= s) p.Uw[(p.c0 + s) + (int64_t)(p.c0 + j) * p.k] = ub[s * bp + j];
+    }
+  }
+  for (int e = tid; e < Rc * bp; e += PNT) {        // coalesced along rows
+    const int li = e % Rc, j = e / Rc;
+    const int st = state[li], t = p.c0 + j;
+    const double v = (st < 0 || st > t) ? P[(size_t)li * ps + j] : (st == t ? 1.0 : 0.0);
     p.Lf[(r0 + li) + (int64_t)t * p.ldlf] = v;
   }
-  for (int li = threadIdx.x; li < Rc; li += PNT) p.rowstate[r0 + li] = state[li];
+  for (int li = tid; li < Rc; li += PNT) p.rowstate[r0 + li] = state[li];
   cluster.sync();   // no CTA leaves while a peer may still read its shared memory
 }
 
-// U(c0+s, j) = M(piv_s, j) - sum_{s'<s} L11(s, s') U(c0+s', j), j in [c1, k).  One warp per column.
-__global__ void k_lupp_u12(const double* W, int64_t n, int k, int c0, int bp, const int64_t* Js,
-                           const double* Lf, int64_t ldlf, double* Uw, const int64_t* status) {
-  if (*status != 0) return;
-  extern __shared__ double L11[];   // bp x bp, row s holds L11(s, 0..s-1)
-  for (int e = threadIdx.x; e < bp * bp; e += blockDim.x) {
-    const int s = e / bp, sp = e % bp;
-    L11[e] = sp < s ? Lf[Js[c0 + s] + (int64_t)(c0 + sp) * ldlf] : 0.0;
+// Register-resident variant of k_lupp_panel: each thread keeps its RPT rows of the block
+// (NB columns, RPT*NB = 64 doubles) in registers, so the bulk Schur update is pure DFMA
+// with no shared-memory traffic.  The step loop is unrolled in chunks of 8 pivots so every
+// register index is static; after a chunk the register window slides left by 8 columns.
+// The shared-memory "mirror" P keeps, per row, the multipliers L(i, s) (written every step)
+// and a snapshot of the remaining columns taken once per chunk (just before the candidate
+// of the chunk's first step is published).  A CTA reconstructs the winning row from the
+// owner's mirror and the U rows of the current chunk (k_ring):
+//     U(s, j) = mirror(p, j) - sum_{s' = cb-1}^{s-1} L(p, s') U(s', j)      (j >= s)
+// so no per-step row copy is needed on the publishing side.
+constexpr int KRING = 64;   // U rows of the block (bp <= 64 for the register kernel)
+
+__host__ __device__ inline size_t reg_smem_bytes(int R, int bp, int nb, int stride) {
+  size_t o = (((size_t)R * stride + 1) & ~(size_t)1) * sizeof(double);   // mirror
+  o += (size_t)KRING * ((bp + nb + 3) & ~1) * sizeof(double);   // U-row ring (+ zero tail), as in the kernel
+  o += (size_t)(bp + 2) * sizeof(double);                 // fetched raw row
+  o = (o + 15) & ~(size_t)15;
+  o += (size_t)2 * MAXCS * PNW * sizeof(Slot);
+  o += (size_t)bp * sizeof(long long) + (size_t)bp * sizeof(double);
+  o += (size_t)R * sizeof(int);                           // row states
+  o = (o + 15) & ~(size_t)15;
+  return o + 2 * sizeof(unsigned long long) + 64;
+}
+
+template <bool GAPS, int RPT, int NB>
+__global__ void __launch_bounds__(PNT, 1) k_lupp_panel_reg(PanelParams p) {
+  static_assert(NB % 8 == 0 && NB >= 16, "chunked window");
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int csize = (int)cluster.num_blocks();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int bp = p.bp;
+  const int ps = ((bp + 1) | 1);                              // odd stride: per-row lane access
+  const int urs = (bp + NB + 3) & ~1;                         // ring row stride (even)
+  double* P = reinterpret_cast<double*>(smraw);               // mirror [R][ps]
+  double* ring = P + (((size_t)p.R * ps + 1) & ~(size_t)1);    // [KRING][urs], 16-byte aligned
+  double* xraw = ring + (size_t)KRING * urs;                  // [bp + 2]
+  unsigned char* q8 = reinterpret_cast<unsigned char*>(xraw + bp + 2);
+  q8 = reinterpret_cast<unsigned char*>(((uintptr_t)q8 + 15) & ~(uintptr_t)15);
+  Slot* slots = reinterpret_cast<Slot*>(q8);                  // [2][MAXCS*PNW]
+  long long* js = reinterpret_cast<long long*>(slots + 2 * MAXCS * PNW);   // [bp]
+  double* gp = reinterpret_cast<double*>(js + bp);                        // [bp]
+  int* state = reinterpret_cast<int*>(gp + bp);                           // [R]
+  unsigned char* mb = reinterpret_cast<unsigned char*>(state + p.R);
+  mb = reinterpret_cast<unsigned char*>(((uintptr_t)mb + 15) & ~(uintptr_t)15);
+  const unsigned mbar0 = dev::smem_u32(mb);
+  const unsigned slots_u32 = dev::smem_u32(slots);
+  const unsigned P_u32 = dev::smem_u32(P);
+  __shared__ int s_stop;
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = tid >> 5;
+  const int64_t r0 = (int64_t)crank * p.R;
+  const int Rc = (int)std::max<int64_t>(0, std::min<int64_t>(p.R, p.n - r0));
+  const int nslots = csize * PNW;
+
+  if (tid == 0) {
+    s_stop = (*p.status != 0);
+    mbar_init(mbar0, 1);
+    mbar_init(mbar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int e = tid; e < KRING * urs; e += PNT) ring[e] = 0.0;   // zero tails stay zero
+  for (int e = tid; e < Rc * bp; e += PNT) {
+    const int li = e % Rc, s = e / Rc;
+    dev::cp_async8(P + (size_t)li * ps + s, p.W + (r0 + li) + (int64_t)(p.c0 + s) * p.n, true);
+  }
+  dev::cp_async_commit();
+  const double tol = 1e-14 * __longlong_as_double((long long)*p.maxbits);
+  dev::cp_async_wait<0>();
+  __syncthreads();
+  (void)state;
+  double v[RPT][NB];
+  int st[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int li = tid + PNT * r;
+    st[r] = li < Rc ? p.rowstate[r0 + li] : -2;
+#pragma unroll
+    for (int q = 0; q < NB; ++q) v[r][q] = (li < Rc && q < bp) ? P[(size_t)li * ps + q] : 0.0;
+  }
+  cluster.sync();
+  const int s_end = s_stop ? 0 : bp;
+
+  auto publish = [&](int sn, unsigned long long ckey, long long cidx, unsigned long long csec) {
+    const int par = sn & 1;
+    if (tid == 0) mbar_arm(mbar0 + 8 * par, (unsigned)(nslots * sizeof(Slot)));
+    unsigned long long wk, ws;
+    unsigned wi;
+    warp_argmax(ckey, (unsigned)cidx, csec, wk, wi, ws, GAPS);
+    __syncwarp();   // mirror writes of the lanes precede the release of the st.async below
+    if (lane < csize) {
+      const unsigned off = (unsigned)((par * (MAXCS * PNW) + crank * PNW + warp) * sizeof(Slot));
+      const unsigned ra = mapa(slots_u32 + off, (unsigned)lane);
+      const unsigned rb = mapa(mbar0 + 8 * par, (unsigned)lane);
+      const long long gi = wk ? (long long)(r0 + wi) : 0x7fffffffffffffffLL;
+      st_async_v2(ra, wk, (unsigned long long)gi, rb);
+      st_async_v2(ra + 16, ws, 0ull, rb);
+    }
+  };
+
+  if (s_end > 0) {
+    unsigned long long ckey = 0ull, csec = 0ull;
+    long long cidx = 0x7fffffffffffffffLL;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+      if (st[r] == -1) cand_push(mag_key(v[r][0]), tid + PNT * r, ckey, cidx, csec);
+    publish(0, ckey, cidx, csec);
+  }
+  int s_done = s_end;
+  bool stop = false;
+  for (int cb = 0; cb < s_end && !stop; cb += 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int s = cb + i;
+      if (s >= s_end) break;
+      const int t = p.c0 + s, par = s & 1;
+      // (A) mailbox -> winner
+      mbar_wait(mbar0 + 8 * par, (unsigned)((s >> 1) & 1));
+      unsigned long long bk = 0ull, bs = 0ull;
+      long long bi = 0x7fffffffffffffffLL;
+      for (int e = lane; e < nslots; e += 32) {
+        const Slot sl = slots[par * (MAXCS * PNW) + e];
+        if (sl.key) cand_push(sl.key, sl.idx, bk, bi, bs);
+        if (GAPS) bs = sl.sec > bs ? sl.sec : bs;
+      }
+      unsigned long long wk, ws;
+      unsigned wi;
+      warp_argmax(bk, bk ? (unsigned)bi : 0xffffffffu, bs, wk, wi, ws, GAPS);
+      const double a1 = wk ? __longlong_as_double((long long)(wk - 1ull)) : -1.0;
+      if (!(a1 > tol)) {
+        if (crank == 0 && tid == 0) {
+          *p.status = t + 1;
+          for (int tt = t; tt < p.k; ++tt) p.Js[tt] = -1;
+        }
+        s_done = s;
+        stop = true;
+        break;
+      }
+      const long long widx = (long long)wi;
+      // (F) the winning row: the owner's mirror (remote) corrected by this chunk's pivots
+      const int s0 = cb > 0 ? cb - 1 : 0;          // first step whose update the mirror lacks
+      {
+        const int wr = (int)(widx / p.R);
+        const int wl = (int)(widx - (int64_t)wr * p.R);
+        const unsigned src = mapa(P_u32 + (unsigned)((size_t)wl * ps * sizeof(double)), (unsigned)wr);
+        for (int j = s0 + tid; j < bp; j += PNT) {
+          double x;
+          asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(x) : "r"(src + 8u * j));
+          xraw[j] = x;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(PNT) : "memory");
+        double* ucur = ring + (size_t)s * urs;
+        for (int j = s + tid; j < bp; j += PNT) {
+          double u = xraw[j];
+          for (int sp = s0; sp < s; ++sp)
+            if (!(sp == cb - 1 && j == cb)) u = fma(-xraw[sp], ring[(size_t)sp * urs + j], u);
+          ucur[j] = u;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(PNT) : "memory");
+      }
+      const double* ucur = ring + (size_t)s * urs;
+      if (crank == 0 && tid == 0) {
+        js[s] = widx;
+        if (GAPS) {
+          const double a2 = ws ? __longlong_as_double((long long)(ws - 1ull)) : 0.0;
+          gp[s] = (a1 - a2) / a1;
+        }
+      }
+      // (B) multipliers (also into the mirror), column s+1, candidate for step s+1
+      const double piv = ucur[s];
+      const bool more = s + 1 < bp;
+      const double u1 = ucur[s + 1];
+      unsigned long long ckey = 0ull, csec = 0ull;
+      long long cidx = 0x7fffffffffffffffLL;
+      double Lm[RPT];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        Lm[r] = 0.0;
+        const int li = tid + PNT * r;
+        if (st[r] == -1) {
+          if (r0 + li == widx) {
+            st[r] = t;
+          } else {
+            Lm[r] = v[r][i] / piv;
+            v[r][i] = Lm[r];
+            P[(size_t)li * ps + s] = Lm[r];
+            v[r][i + 1] = fma(-Lm[r], u1, v[r][i + 1]);
+            if (more) cand_push(mag_key(v[r][i + 1]), li, ckey, cidx, csec);
+          }
+        }
+      }
+      if (i == 7 && more) {   // snapshot of columns >= cb+8 for the next chunk's reconstruction
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int li = tid + PNT * r;
+          if (li < Rc) {
+#pragma unroll
+            for (int q = 8; q < NB; ++q)
+              if (cb + q < bp) P[(size_t)li * ps + cb + q] = v[r][q];
+          }
+        }
+      }
+      if (more) publish(s + 1, ckey, cidx, csec);
+      // (C) bulk update of columns >= s+2 in registers (zero tail of U beyond bp)
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const double lm = Lm[r];
+        if (lm != 0.0) {
+          if ((i + 2) & 1) v[r][i + 2] = fma(-lm, ucur[cb + i + 2], v[r][i + 2]);
+#pragma unroll
+          for (int q = ((i + 3) & ~1); q < NB; q += 2) {
+            const double2 u = *reinterpret_cast<const double2*>(ucur + cb + q);
+            v[r][q] = fma(-lm, u.x, v[r][q]);
+            v[r][q + 1] = fma(-lm, u.y, v[r][q + 1]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int q = 0; q < NB; ++q) v[r][q] = (q + 8 < NB) ? v[r][q + 8] : 0.0;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int warps = blockDim.x >> 5;
-  const int c1 = c0 + bp;
-  for (int j = c1 + blockIdx.x * warps + (threadIdx.x >> 5); j < k; j += gridDim.x * warps) {
-    double u0 = 0.0, u1 = 0.0;   // u[lane], u[lane + 32]
-    for (int s = 0; s < bp; ++s) {
-      double part = 0.0;
-      if (lane < s) part = L11[s * bp + lane] * u0;
-      if (lane + 32 < s) part = fma(L11[s * bp + lane + 32], u1, part);
-      part = dev::warp_sum(part);
-      const double v = W[Js[c0 + s] + (int64_t)j * n] - part;
-      if (s == lane) u0 = v;
-      if (s == lane + 32) u1 = v;
+  if (crank == 0) {
+    for (int s = tid; s < s_done; s += PNT) {
+      p.Js[p.c0 + s] = js[s];
+      if (GAPS) p.gaps[p.c0 + s] = gp[s];
     }
-    if (lane < bp) Uw[(c0 + lane) + (int64_t)j * k] = u0;
-    if (lane + 32 < bp) Uw[(c0 + lane + 32) + (int64_t)j * k] = u1;
+    for (int e = tid; e < s_done * bp; e += PNT) {
+      const int s = e / bp, j = e % bp;
+      if (j >= s) p.Uw[(p.c0 + s) + (int64_t)(p.c0 + j) * p.k] = ring[(size_t)s * urs + j];
+    }
   }
+  // L block (multipliers kept in the mirror) and row states
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int li = tid + PNT * r;
+    if (li < Rc) {
+      state[li] = st[r];
+      p.rowstate[r0 + li] = st[r];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < Rc * bp; e += PNT) {
+    const int li = e % Rc, j = e / Rc;
+    const int sr = state[li], t = p.c0 + j;
+    const double val = (sr < 0 || sr > t) ? P[(size_t)li * ps + j] : (sr == t ? 1.0 : 0.0);
+    p.Lf[(r0 + li) + (int64_t)t * p.ldlf] = val;
+  }
+  __syncthreads();
+  cluster.sync();
 }
+
+// U(c0+s, j) = M(piv_s, j) - sum_{s'<s} L11(s, s') U(c0+s', j), j in [c1, k).
+// One thread per column, the column of U in registers (bp <= U12_BP), L11 broadcast from smem.
+__global__ void __launch_bounds__(256) k_lupp_u12(const double* W, int64_t n, int k, int c0, int bp,
+                                                  const int64_t* Js, const double* Lf, int64_t ldlf,
+                                                  double* Uw, const int64_t* status) {
+  if (*status != 0) return;
+  extern __shared__ __align__(16) double u12sm[];
+  double (*L11)[U12_BP + 1] = reinterpret_cast<double (*)[U12_BP + 1]>(u12sm);
+  double (*Wv)[33] = reinterpret_cast<double (*)[33]>(u12sm + U12_BP * (U12_BP + 1));
+  int64_t* piv = reinterpret_cast<int64_t*>(u12sm + U12_BP * (U12_BP + 1) + U12_BP * 33);
+  const int j0 = c0 + bp + blockIdx.x * 32;
+  for (int s = threadIdx.x; s < bp; s += blockDim.x) piv[s] = Js[c0 + s];
+  __syncthreads();
+  for (int e = threadIdx.x; e < bp * bp; e += blockDim.x) {      // async gathers: all in flight
+    const int s = e % bp, sp = e / bp;
+    if (sp < s) dev::cp_async8(&L11[s][sp], Lf + piv[s] + (int64_t)(c0 + sp) * ldlf, true);
+  }
+  for (int e = threadIdx.x; e < bp * 32; e += blockDim.x) {
+    const int s = e % bp, cc = e / bp;
+    const int j = j0 + cc;
+    dev::cp_async8(&Wv[s][cc], j < k ? W + piv[s] + (int64_t)j * n : W, j < k);
+  }
+  dev::cp_async_commit();
+  dev::cp_async_wait<0>();
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int j = j0 + threadIdx.x;
+  if (j >= k) return;
+  double u[U12_BP];
+#pragma unroll
+  for (int s = 0; s < U12_BP; ++s) u[s] = s < bp ? Wv[s][threadIdx.x] : 0.0;
+#pragma unroll
+  for (int s = 1; s < U12_BP; ++s) {
+    if (s < bp) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+      for (int sp = 0; sp + 3 < s; sp += 4) {
+        a0 = fma(L11[s][sp], u[sp], a0);
+        a1 = fma(L11[s][sp + 1], u[sp + 1], a1);
+        a2 = fma(L11[s][sp + 2], u[sp + 2], a2);
+        a3 = fma(L11[s][sp + 3], u[sp + 3], a3);
+      }
+#pragma unroll
+      for (int sp = (s / 4) * 4; sp < s; ++sp) a0 = fma(L11[s][sp], u[sp], a0);
+      u[s] -= (a0 + a1) + (a2 + a3);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < U12_BP; ++s)
+    if (s < bp) Uw[(c0 + s) + (int64_t)j * k] = u[s];
+}
+
+constexpr size_t kU12Smem = sizeof(double) * (U12_BP * (U12_BP + 1) + U12_BP * 33 + U12_BP);
 
 __global__ void k_copy_u(const double* Uw, int k, double* U, int64_t ldu) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
@@ -212,6 +682,8 @@ __global__ void k_copy_u(const double* Uw, int k, double* U, int64_t ldu) {
     U[i + j * ldu] = i <= j ? Uw[e] : 0.0;
   }
 }
+
+using PanelFn = void (*)(PanelParams);
 
 struct ClusterCfg {
   int cs = 0;
@@ -226,11 +698,15 @@ ClusterCfg pick_cluster(sk_ctx* c) {
   if (done) return cfg;
   done = true;
   cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, k_lupp_panel);
-  cfg.max_dyn = c->max_smem_optin - (int)fa.sharedSizeBytes;
-  cudaFuncSetAttribute(k_lupp_panel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  const cudaError_t ea = cudaFuncSetAttribute(k_lupp_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.max_dyn);
-  if (ea != cudaSuccess) cfg.why += std::string("smem attribute: ") + cudaGetErrorString(ea) + "; ";
+  cudaFuncGetAttributes(&fa, k_lupp_panel<true>);
+  cfg.max_dyn = c->max_smem_optin - (int)fa.sharedSizeBytes - 64;
+  for (PanelFn fn : {k_lupp_panel<true>, k_lupp_panel<false>, k_lupp_panel_reg<true, 1, 64>,
+                     k_lupp_panel_reg<false, 1, 64>, k_lupp_panel_reg<true, 2, 32>, k_lupp_panel_reg<false, 2, 32>,
+                     k_lupp_panel_reg<true, 4, 16>, k_lupp_panel_reg<false, 4, 16>}) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.max_dyn);
+  }
+  cudaFuncSetAttribute(k_lupp_u12, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kU12Smem);
   for (int cs : {16, 8, 4, 2, 1}) {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(cs);
@@ -241,7 +717,7 @@ ClusterCfg pick_cluster(sk_ctx* c) {
     at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     lc.attrs = at; lc.numAttrs = 1;
     int nclusters = 0;
-    const cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, k_lupp_panel, &lc);
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, k_lupp_panel<true>, &lc);
     if (e == cudaSuccess && nclusters > 0) {
       cfg.cs = cs; cfg.ok = true;
       break;
@@ -261,16 +737,29 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   if (!cfg.ok) return fail(c, SK_E_CUDA, "no thread-block cluster configuration for the LUPP panel: " + cfg.why);
   const int cs = cfg.cs;
   const int64_t R = cdiv(n, cs);
-  const size_t fixed = 2 * cs * sizeof(Slot) + 33 * sizeof(dev::Cand) + (size_t)R * sizeof(int) +
-                       (64 + 2) * sizeof(double) + 1024;
-  const int64_t budget = (int64_t)cfg.max_dyn - (int64_t)fixed;
-  int64_t bp = budget / (R * 8) - 1;
-  bp = std::min<int64_t>(bp, 64);
-  bp = std::min<int64_t>(bp, k);
-  if (bp < 1) return fail(c, SK_E_ARG, "LUPP panel too tall for one cluster (n too large)");
-  // odd smem stride (bank-conflict-free row-per-thread access)
-  auto stride_of = [](int64_t b) { return (b % 2 == 0) ? b + 1 : b; };
-  while (bp > 1 && R * stride_of(bp) * 8 > budget) --bp;
+  if (R > 16 * PNT) return fail(c, SK_E_ARG, "LUPP panel too tall for one cluster (n too large)");
+  // register-resident kernel when a thread's rows x block fit 64 doubles, else the
+  // shared-memory kernel with the widest block whose rows fit the cluster's shared memory
+  PanelFn fn = nullptr;
+  int64_t bp = 0;
+  size_t smem_bytes = 0;
+  const int rpt = (int)cdiv(R, PNT);
+  if (rpt <= 4) {
+    const int nb = rpt == 1 ? 64 : rpt == 2 ? 32 : 16;
+    const int rv = rpt == 1 ? 1 : rpt == 2 ? 2 : 4;
+    bp = std::min<int64_t>(k, nb);
+    smem_bytes = reg_smem_bytes((int)R, (int)bp, nb, (int)((bp + 1) | 1));
+    if (rv == 1) fn = gaps ? k_lupp_panel_reg<true, 1, 64> : k_lupp_panel_reg<false, 1, 64>;
+    if (rv == 2) fn = gaps ? k_lupp_panel_reg<true, 2, 32> : k_lupp_panel_reg<false, 2, 32>;
+    if (rv == 4) fn = gaps ? k_lupp_panel_reg<true, 4, 16> : k_lupp_panel_reg<false, 4, 16>;
+  } else {
+    bp = std::min<int64_t>(k, 1024);
+    while (bp > 1 && (int64_t)PanelSmem((int)R, (int)bp).total > cfg.max_dyn) bp = (bp > 64) ? bp / 2 : bp - 1;
+    if (bp < k) bp = std::min<int64_t>(bp, U12_BP);
+    fn = gaps ? k_lupp_panel<true> : k_lupp_panel<false>;
+    smem_bytes = PanelSmem((int)R, (int)bp).total;
+  }
+  if ((int64_t)smem_bytes > cfg.max_dyn) return fail(c, SK_E_ARG, "LUPP panel staging exceeds shared memory");
 
   DBuf Wb, Ub, stateb, maxb, Lfb;
   SK_TRY(Wb.alloc(c, (size_t)n * k * sizeof(double)));
@@ -294,30 +783,25 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     const int b = (int)std::min<int64_t>(bp, k - c0);
     PanelParams pp{};
     pp.W = Wb.as<double>(); pp.n = n; pp.k = (int)k;
-    pp.c0 = (int)c0; pp.bp = b; pp.R = (int)R; pp.pstride = (int)stride_of(b);
+    pp.c0 = (int)c0; pp.bp = b; pp.R = (int)R;
     pp.rowstate = stateb.as<int>();
     pp.Js = Js; pp.Lf = Lf; pp.ldlf = ldlf; pp.Uw = Ub.as<double>(); pp.gaps = gaps;
     pp.maxbits = maxb.as<unsigned long long>(); pp.status = status_dev;
-    const size_t smem = (size_t)R * pp.pstride * 8 + (size_t)((b + 1) & ~1) * 8 + 2 * cs * sizeof(Slot) +
-                        33 * sizeof(dev::Cand) + (size_t)R * sizeof(int);
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(cs);
     lc.blockDim = dim3(PNT);
-    lc.dynamicSmemBytes = smem;
+    lc.dynamicSmemBytes = smem_bytes;
     lc.stream = c->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     lc.attrs = at; lc.numAttrs = 1;
-    SK_CUDA(c, cudaLaunchKernelEx(&lc, k_lupp_panel, pp));
+    SK_CUDA(c, cudaLaunchKernelEx(&lc, fn, pp));
     SK_TRY(launched(c));
     const int64_t c1 = c0 + b;
     if (c1 < k) {
-      const int warps = 8;
-      const int blocks = (int)std::min<int64_t>(cdiv(k - c1, warps), 4LL * c->num_sms);
-      const size_t s2 = (size_t)b * b * sizeof(double);
-      k_lupp_u12<<<blocks, warps * 32, s2, c->stream>>>(Wb.as<double>(), n, (int)k, (int)c0, b, Js, Lf,
-                                                       ldlf, Ub.as<double>(), status_dev);
+      k_lupp_u12<<<(unsigned)cdiv(k - c1, 32), 256, kU12Smem, c->stream>>>(Wb.as<double>(), n, (int)k, (int)c0, b, Js,
+                                                                  Lf, ldlf, Ub.as<double>(), status_dev);
       SK_TRY(launched(c));
       SK_TRY(gemm(c, false, false, n, k - c1, b, -1.0, Lf + c0 * ldlf, ldlf, Ub.as<double>() + c0 + c1 * k,
                   k, 1.0, Wb.as<double>() + c1 * n, n));
