@@ -2,6 +2,7 @@
 // Argument validation happens here, before anything is enqueued; the work is done by
 // the kernels in sketch.cu, lupp.cu, cpqr.cu, dense.cu, idcoef.cu, residual.cu.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -46,6 +47,7 @@ sk_status sk_create(sk_ctx** out, int device, void* stream) {
   if (!c) return SK_E_NOMEM;
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
+  if (const char* v = std::getenv("SKEL_SKETCH_LEGACY")) c->force_legacy_sketch = v[0] == '1';
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess)

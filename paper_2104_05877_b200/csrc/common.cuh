@@ -23,6 +23,9 @@ struct sk_ctx {
   int64_t ws_hwm = 0;       // high-water mark of pooled bytes
   // pinned host scratch for small device->host results (info, scalars)
   void* host_scratch = nullptr;
+  // A/B switch (env SKEL_SKETCH_LEGACY=1 at sk_create): use the cp.async sketch kernel
+  // instead of the TMA + cluster-shared-Omega one.
+  bool force_legacy_sketch = false;
 };
 
 namespace skel {
