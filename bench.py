@@ -253,7 +253,7 @@ def main():
             traffic = json.load(open(tf)).get(f"{args.config}_k{k}")
         except Exception:
             traffic = None
-    roofline = {"kernel": "k_sketch_dense", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+    roofline = {"kernel": "k_sketch_tma", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "peak_source": "measured FP64 DMMA ceiling (tools/microbench/fp64_pipes.cu); "
                                "MEASURED_PEAKS.json has no FP64 entry; cuBLAS DGEMM measured 35.5"}

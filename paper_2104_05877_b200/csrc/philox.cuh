@@ -36,11 +36,13 @@ __host__ __device__ __forceinline__ uint2 seed_key(uint64_t seed) {
   return make_uint2((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
 }
 
-// (w_hi >> 5) * 2^26 + (w_lo >> 6) is an exact integer < 2^53; + 0.5 then * 2^-53.
+// U53 (R2): u = (N + 0.5) * 2^-53 with N = (w_hi >> 5) * 2^26 + (w_lo >> 6) < 2^53,
+// the sum N + 0.5 rounded to nearest-even in double.  Computed as RN(2N + 1) * 2^-54: the
+// integer 2N+1 (< 2^54) is formed exactly on the integer pipe and converted once, which
+// rounds identically (same real value, same 53-bit RN), and the power-of-two scale is exact.
 __device__ __forceinline__ double u53(uint32_t w_hi, uint32_t w_lo) {
-  const double a = (double)(w_hi >> 5), b = (double)(w_lo >> 6);
-  const double t = __dadd_rn(__dmul_rn(a, 67108864.0), b);   // exact
-  return __dmul_rn(__dadd_rn(t, 0.5), 1.0 / 9007199254740992.0);
+  const uint64_t N = ((uint64_t)(w_hi >> 5) << 26) | (uint64_t)(w_lo >> 6);
+  return __dmul_rn(__ull2double_rn(2ull * N + 1ull), 1.0 / 18014398509481984.0);
 }
 
 // Standard normals z_{2p}, z_{2p+1} of column i (before the 1/sqrt(l) scale).

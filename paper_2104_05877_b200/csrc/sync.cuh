@@ -35,6 +35,12 @@ __device__ __forceinline__ void mbar_arm(unsigned addr, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive_cluster(unsigned cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Arrive (count 1) on an mbarrier of a peer CTA with CTA-scope release semantics -- the
+// consumer-release idiom of a multicast pipeline: it only orders this thread's prior shared
+// memory reads before the peer's producer overwrites the buffer (no GPU-scope fence).
+__device__ __forceinline__ void mbar_arrive_remote(unsigned cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // Spin until the phase with the given parity has completed (CTA-scope acquire).
 __device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
   unsigned done = 0;
@@ -47,6 +53,18 @@ __device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
         : "r"(addr), "r"(parity)
         : "memory");
   } while (!done);
+}
+// Non-blocking probe: has the phase with the given parity completed?
+__device__ __forceinline__ bool mbar_test(unsigned addr, unsigned parity) {
+  unsigned done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return done != 0;
 }
 // Same, with cluster-scope acquire (the phase was completed by peers' releases).
 __device__ __forceinline__ void mbar_wait_cluster(unsigned addr, unsigned parity) {
