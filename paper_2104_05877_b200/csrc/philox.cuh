@@ -36,22 +36,109 @@ __host__ __device__ __forceinline__ uint2 seed_key(uint64_t seed) {
   return make_uint2((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
 }
 
-// U53 (R2): u = (N + 0.5) * 2^-53 with N = (w_hi >> 5) * 2^26 + (w_lo >> 6) < 2^53,
-// the sum N + 0.5 rounded to nearest-even in double.  Computed as RN(2N + 1) * 2^-54: the
-// integer 2N+1 (< 2^54) is formed exactly on the integer pipe and converted once, which
-// rounds identically (same real value, same 53-bit RN), and the power-of-two scale is exact.
+// U53 (R2): u = RN(N + 0.5) * 2^-53 with N = (w_hi >> 5) * 2^26 + (w_lo >> 6) < 2^53.
+// Built without an int->double conversion (the conversion unit is slow next to the DMMA-bound
+// sketch): for N < 2^52, N + 0.5 is exact and equals as_double(0x4330...0 + N) - (2^52 - 0.5);
+// for N >= 2^52 the spacing is 1 and round-half-even gives K = N + (N & 1) (even, <= 2^53),
+// = 2 * (as_double(0x4330...0 + K/2) - 2^52).  Every DADD/DMUL below is exact.
 __device__ __forceinline__ double u53(uint32_t w_hi, uint32_t w_lo) {
   const uint64_t N = ((uint64_t)(w_hi >> 5) << 26) | (uint64_t)(w_lo >> 6);
-  return __dmul_rn(__ull2double_rn(2ull * N + 1ull), 1.0 / 18014398509481984.0);
+  const bool big = (N >> 52) != 0;
+  const uint64_t K = big ? (N + (N & 1ull)) >> 1 : N;
+  const double off = big ? 4503599627370496.0 : 4503599627370495.5;
+  const double scale = big ? 1.0 / 4503599627370496.0 : 1.0 / 9007199254740992.0;
+  return __dmul_rn(__dsub_rn(__longlong_as_double((long long)(0x4330000000000000ull + K)), off), scale);
 }
 
-// Standard normals z_{2p}, z_{2p+1} of column i (before the 1/sqrt(l) scale).
+// ---- branch-free FP64 elementary functions for Box-Muller -------------------------------
+// CUDA's log / sqrt / sincospi contain divergent slow paths (BSSY/BSYNC regions), which keeps
+// the compiler from interleaving independent Box-Muller chains; the sketch's producer warps
+// run several chains per thread, so these straight-line versions (restated textbook
+// algorithms, accurate to a few ulp on the ranges used) are what lets them overlap.
+
+// log(u) for u in [2^-54, 1] (normal, positive): fdlibm's reduction u = 2^e m,
+// m in (sqrt2/2, sqrt2], f = m - 1, s = f / (2 + f), log m = 2 atanh s with the
+// Remez polynomial R(s^2) of fdlibm's e_log.c (|error| < 2^-58.45 on the reduced range).
+__device__ __forceinline__ double bm_log(double u) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(u);
+  int e = (int)(bits >> 52) - 1023;
+  double m = __longlong_as_double((long long)((bits & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+  const bool big = m > 1.4142135623730951;
+  m = big ? 0.5 * m : m;
+  e = big ? e + 1 : e;
+  const double f = m - 1.0;                       // exact
+  const double d = 2.0 + f;
+  float rf;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)d));
+  double r = (double)rf;                          // 1/d to ~2^-23, then two Newton steps
+  r = fma(r, fma(-d, r, 1.0), r);
+  r = fma(r, fma(-d, r, 1.0), r);
+  double sq = f * r;
+  sq = fma(fma(-d, sq, f), r, sq);                // s = f / d to ~0.5 ulp
+  const double z = sq * sq, w = z * z;
+  const double t1 = w * (3.999999999940941908e-01 + w * (2.222219843214978396e-01 + w * 1.531383769920937332e-01));
+  const double t2 = z * (6.666666666666735130e-01 +
+                         w * (2.857142874366239149e-01 + w * (1.818357216161805012e-01 + w * 1.479819860511658591e-01)));
+  const double R = t2 + t1;
+  const double hfsq = 0.5 * f * f;
+  const double de = (double)e;
+  return de * 6.93147180369123816490e-01 - ((hfsq - (sq * (hfsq + R) + de * 1.90821492927058770002e-10)) - f);
+}
+
+// sqrt(x) for x in [0, 80]: float rsqrt seed, two Newton steps, one Markstein correction.
+__device__ __forceinline__ double bm_sqrt(double x) {
+  const double xs = fmax(x, 1e-300);
+  float yf;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"((float)xs));
+  double y = (double)yf;
+  y = fma(0.5 * y, fma(-xs * y, y, 1.0), y);
+  y = fma(0.5 * y, fma(-xs * y, y, 1.0), y);
+  double s = xs * y;
+  s = fma(0.5 * y, fma(-s, s, xs), s);
+  return x > 0.0 ? s : 0.0;
+}
+
+// sin(pi t), cos(pi t) for t in [0, 2]: t = n/2 + r exactly (|r| <= 1/4), x = pi r with a
+// two-term pi, Taylor polynomials of sin to x^17 and cos to x^16 (truncation < 1e-17 for
+// |x| <= pi/4), quadrant n mod 4 by selects.
+__device__ __forceinline__ void bm_sincospi(double t, double& sn, double& cs) {
+  const double n = rint(2.0 * t);
+  const double r = fma(n, -0.5, t);               // exact
+  const double x = fma(r, 3.141592653589793116, r * 1.2246467991473532e-16);
+  const double z = x * x;
+  double ps = 2.8114572543455206e-15;             // 1/17!
+  ps = fma(z, ps, -7.6471637318198164e-13);       // -1/15!
+  ps = fma(z, ps, 1.6059043836821613e-10);        // 1/13!
+  ps = fma(z, ps, -2.5052108385441720e-08);       // -1/11!
+  ps = fma(z, ps, 2.7557319223985893e-06);        // 1/9!
+  ps = fma(z, ps, -1.9841269841269841e-04);       // -1/7!
+  ps = fma(z, ps, 8.3333333333333332e-03);        // 1/5!
+  ps = fma(z, ps, -1.6666666666666666e-01);       // -1/3!
+  const double s = fma(x * z, ps, x);
+  double pc = 4.7794773323873853e-14;             // 1/16!
+  pc = fma(z, pc, -1.1470745597729725e-11);       // -1/14!
+  pc = fma(z, pc, 2.0876756987868100e-09);        // 1/12!
+  pc = fma(z, pc, -2.7557319223985888e-07);       // -1/10!
+  pc = fma(z, pc, 2.4801587301587302e-05);        // 1/8!
+  pc = fma(z, pc, -1.3888888888888889e-03);       // -1/6!
+  pc = fma(z, pc, 4.1666666666666664e-02);        // 1/4!
+  pc = fma(z, pc, -0.5);                          // -1/2!
+  const double c = fma(z, pc, 1.0);
+  const int q = (int)n & 3;                       // quadrant: (s, c) -> (c, -s) -> (-s, -c) -> (-c, s)
+  const bool odd = (q & 1) != 0;
+  const double a = odd ? c : s, b = odd ? s : c;
+  const unsigned long long sa = (unsigned long long)(q & 2) << 62, sb = (unsigned long long)((q + 1) & 2) << 62;
+  sn = __longlong_as_double(__double_as_longlong(a) ^ (long long)sa);
+  cs = __longlong_as_double(__double_as_longlong(b) ^ (long long)sb);
+}
+
+// Standard normals z_{2p}, z_{2p+1} of column i (before the 1/sqrt(l) scale), Box-Muller (R2).
 __device__ __forceinline__ void gauss_pair(uint64_t i, uint32_t p, uint2 key, double& z0, double& z1) {
   const uint4 w = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), p, kTagGauss), key);
   const double u1 = u53(w.x, w.y), u2 = u53(w.z, w.w);
-  const double rad = sqrt(-2.0 * log(u1));
+  const double rad = bm_sqrt(-2.0 * bm_log(u1));
   double s, c;
-  sincospi(2.0 * u2, &s, &c);
+  bm_sincospi(2.0 * u2, s, c);
   z0 = rad * c;
   z1 = rad * s;
 }
