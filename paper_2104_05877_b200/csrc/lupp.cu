@@ -23,6 +23,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <vector>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "dmma.cuh"
@@ -54,6 +57,7 @@ struct PanelParams {
   double* gaps;
   const unsigned long long* maxbits;     // max |M| (bit pattern)
   int64_t* status;                       // 0 or 1-based failing step
+  long long* tprobe;                     // experiments only (env SKEL_LUPP_PROBE): per-step clock64 marks
 };
 
 __global__ void k_lupp_init(const double* P, bool row_major, int64_t n, int k, int64_t ld, double* W,
@@ -621,6 +625,249 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_reg(PanelParams p) {
   cluster.sync();
 }
 
+// ------------------------------------------------------------------------------------------
+// v2 panel: CTA-reduced candidates + a row-carrying all-to-all.
+// Per pivot step s (measured primitives, profiles/round1/mailbox_lat.txt: a 16-CTA all-to-all
+// of 34 x 16 B messages completes in ~890 cycles, a DSMEM load round trip ~265 cycles):
+//   (A) every warp: REDUX argmax of column s over its active rows; the owner lane copies its
+//       row (block coordinates) to the warp's smem slot; one CTA barrier;
+//   (B) every warp reduces the 8 warp candidates to the CTA candidate; warp w st.async's the
+//       CTA candidate + its row to CTAs w and w + 8 (one message per CTA pair per step);
+//   (C) the deferred bulk Schur update of step s-1 (columns >= s+1) overlaps the exchange;
+//   (D) wait for the CS messages; every warp picks the same winner (REDUX, ties -> lowest
+//       global index); the winner's row is local; its columns > s lack only the step s-1
+//       update (taken before (C) ran on the owner), which is applied on read:
+//       U(s, c) = row(c) - row(s-1) * U(s-1, c);
+//   (E) multipliers and column s+1 of the own rows (the next step's search column).
+// One CTA barrier and one cluster exchange per pivot; no remote loads.
+template <int RPT, int NB, bool GAPS>
+__global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
+  static_assert(NB % 8 == 0 && RPT * NB <= 64, "register window");
+  constexpr int MSGD = 4 + NB;                       // doubles per message: key, idx, sec, L(s-1), row[NB]
+  constexpr int MSG = MSGD / 2;                      // 16-byte chunks
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int csize = (int)cluster.num_blocks();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double* ub = reinterpret_cast<double*>(smraw);                         // [NB][NB]
+  double* wrow = ub + NB * NB;                                           // [2][PNW][NB]
+  unsigned long long* wck = reinterpret_cast<unsigned long long*>(wrow + 2 * PNW * NB);   // [2][PNW]
+  long long* wci = reinterpret_cast<long long*>(wck + 2 * PNW);          // [2][PNW]
+  unsigned long long* wcs = reinterpret_cast<unsigned long long*>(wci + 2 * PNW);         // [2][PNW]
+  double* wlp = reinterpret_cast<double*>(wcs + 2 * PNW);                // [2][PNW] candidate's L(s-1)
+  double* mbox = reinterpret_cast<double*>(wlp + 2 * PNW);               // [2][MAXCS][MSGD]
+  long long* js = reinterpret_cast<long long*>(mbox + 2 * MAXCS * MSGD); // [NB]
+  double* gp = reinterpret_cast<double*>(js + NB);                       // [NB]
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(gp + NB);   // [2]
+  const unsigned mbar0 = dev::smem_u32(mbar);
+  const unsigned mbox_u = dev::smem_u32(mbox);
+  __shared__ int s_stop;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bp = p.bp;
+  const int64_t r0 = (int64_t)crank * p.R;
+  const int Rc = (int)std::max<int64_t>(0, std::min<int64_t>(p.R, p.n - r0));
+
+  if (tid == 0) {
+    s_stop = (*p.status != 0);
+    mbar_init(mbar0, 1);
+    mbar_init(mbar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double v[RPT][NB];
+  int st[RPT];
+  double lprev[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int li = tid + PNT * r;
+    const bool in = li < Rc;
+    st[r] = in ? p.rowstate[r0 + li] : -2;
+    lprev[r] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+      v[r][q] = (in && q < bp) ? p.W[(r0 + li) + (int64_t)(p.c0 + q) * p.n] : 0.0;   // coalesced along rows
+  }
+  const double tol = 1e-14 * __longlong_as_double((long long)*p.maxbits);
+  __syncthreads();
+  cluster.sync();    // mbarriers initialised cluster-wide before any message
+  const int s_end = s_stop ? 0 : bp;
+  int s_done = s_end;
+  bool stop = false;
+
+  // Steps run in chunks of 8 with the chunk unrolled, so the register window (v[r][q] =
+  // block column cb + q) is indexed statically; the window slides by 8 after each chunk.
+  // (A per-step slide with a rolled loop was measured 1.5x slower: predicated full-width
+  // updates and longer dependency chains, profiles/round1/lupp_probe.txt.)
+  for (int cb = 0; cb < s_end && !stop; cb += 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int s = cb + i;
+      if (s >= s_end) break;
+      const int t = p.c0 + s, par = s & 1;
+      const bool probe = p.tprobe != nullptr && crank == 0 && tid == 0;
+      if (probe) p.tprobe[(int64_t)t * 8 + 0] = clock64();
+      // (A) local candidate of column s, owner copies its row (block coordinates)
+      unsigned long long ckey = 0ull, csec = 0ull;
+      long long cidx = 0x7fffffffffffffffLL;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+        if (st[r] == -1) cand_push(mag_key(v[r][i]), tid + PNT * r, ckey, cidx, csec);
+      unsigned long long wk, ws;
+      unsigned wi;
+      warp_argmax(ckey, (unsigned)cidx, csec, wk, wi, ws, GAPS);
+      if (wk && (int)(wi & 31u) == lane) {
+        double* dst = wrow + (size_t)(par * PNW + warp) * NB + cb;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+          if ((int)wi == tid + PNT * r) {
+            wlp[par * PNW + warp] = lprev[r];
+#pragma unroll
+            for (int q = i; q < NB; ++q)
+              if (cb + q < NB) dst[q] = v[r][q];
+          }
+      }
+      if (lane == 0) {
+        wck[par * PNW + warp] = wk;
+        wci[par * PNW + warp] = wk ? (long long)(r0 + wi) : 0x7fffffffffffffffLL;
+        wcs[par * PNW + warp] = ws;
+      }
+      if (tid == 0) mbar_arm(mbar0 + 8 * par, (unsigned)(csize * MSG * 16));
+      if (probe) p.tprobe[(int64_t)t * 8 + 1] = clock64();
+      asm volatile("bar.sync 1, %0;" ::"n"(PNT) : "memory");
+      if (probe) p.tprobe[(int64_t)t * 8 + 2] = clock64();
+      // (B) CTA candidate -> every CTA of the cluster
+      {
+        const unsigned long long k8 = lane < PNW ? wck[par * PNW + lane] : 0ull;
+        const long long i8 = lane < PNW ? wci[par * PNW + lane] : 0x7fffffffffffffffLL;
+        const unsigned long long s8 = lane < PNW ? wcs[par * PNW + lane] : 0ull;
+        unsigned long long bk, bs;
+        unsigned bl;
+        warp_argmax(k8, k8 ? (unsigned)(i8 - r0) : 0xffffffffu, s8, bk, bl, bs, GAPS);
+        const unsigned wl = __ballot_sync(0xffffffffu, k8 == bk && k8 != 0ull && (unsigned)(i8 - r0) == bl);
+        const int cw = wl ? __ffs(wl) - 1 : 0;
+        const long long gidx = bk ? r0 + (long long)bl : 0x7fffffffffffffffLL;
+        const double* src = wrow + (size_t)(par * PNW + cw) * NB;
+        const unsigned slot = mbox_u + (unsigned)(((par * MAXCS) + crank) * MSGD * 8);
+        for (int d = warp; d < csize; d += PNW) {
+          const unsigned rslot = mapa(slot, (unsigned)d);
+          const unsigned rbar = mapa(mbar0 + 8 * par, (unsigned)d);
+          for (int j = lane; j < MSG; j += 32) {
+            unsigned long long x, y;
+            if (j == 0) { x = bk; y = (unsigned long long)gidx; }
+            else if (j == 1) { x = bs; y = (unsigned long long)__double_as_longlong(wlp[par * PNW + cw]); }
+            else {
+              x = (unsigned long long)__double_as_longlong(src[2 * (j - 2)]);
+              y = (unsigned long long)__double_as_longlong(src[2 * (j - 2) + 1]);
+            }
+            st_async_v2(rslot + 16u * j, x, y, rbar);
+          }
+        }
+      }
+      if (probe) p.tprobe[(int64_t)t * 8 + 3] = clock64();
+      // (C) deferred bulk update of step s-1: columns >= s+1 (window q with cb+q >= s+1)
+      if (s > 0) {
+        const double* uprev = ub + (size_t)(s - 1) * NB + cb;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const double lm = lprev[r];
+          if (lm != 0.0) {
+#pragma unroll
+            for (int q = i + 1; q < NB; ++q)
+              if (cb + q < NB) v[r][q] = fma(-lm, uprev[q], v[r][q]);
+          }
+        }
+      }
+      if (probe) p.tprobe[(int64_t)t * 8 + 4] = clock64();
+      // (D) the cluster's winner and its row
+      mbar_wait(mbar0 + 8 * par, (unsigned)((s >> 1) & 1));
+      if (probe) p.tprobe[(int64_t)t * 8 + 5] = clock64();
+      const double* box = mbox + (size_t)par * MAXCS * MSGD;
+      const unsigned long long gk = lane < csize ? __double_as_longlong(box[lane * MSGD]) : 0ull;
+      const long long gi8 = lane < csize ? __double_as_longlong(box[lane * MSGD + 1]) : 0x7fffffffffffffffLL;
+      const unsigned long long gs8 = lane < csize ? __double_as_longlong(box[lane * MSGD + 2]) : 0ull;
+      // ties -> lowest global index: CTA row ranges are ordered by rank, so the lowest lane
+      unsigned long long wkey, wsec;
+      unsigned wlane;
+      warp_argmax(gk, gk ? (unsigned)lane : 0xffffffffu, gs8, wkey, wlane, wsec, GAPS);
+      const double a1 = wkey ? __longlong_as_double((long long)(wkey - 1ull)) : -1.0;
+      if (!(a1 > tol)) {
+        if (crank == 0 && tid == 0) {
+          *p.status = t + 1;
+          for (int tt = t; tt < p.k; ++tt) p.Js[tt] = -1;
+        }
+        s_done = s;
+        stop = true;
+        break;
+      }
+      const long long widx = __shfl_sync(0xffffffffu, gi8, (int)wlane);
+      const double* row = box + (size_t)wlane * MSGD + 4;
+      const double* uprev = ub + (size_t)(s > 0 ? s - 1 : 0) * NB;
+      const double lp = s > 0 ? box[(size_t)wlane * MSGD + 3] : 0.0;
+      const double piv = row[s];
+      const double u1 = s + 1 < bp ? (s > 0 ? fma(-lp, uprev[s + 1], row[s + 1]) : row[s + 1]) : 0.0;
+      if (warp == PNW - 1) {   // U(s, :) for the bulk update of the next step, fix-ups and the output
+        double* ucur = ub + (size_t)s * NB;
+        for (int c = s + lane; c < bp; c += 32) ucur[c] = (s > 0 && c > s) ? fma(-lp, uprev[c], row[c]) : row[c];
+      }
+      if (crank == 0 && tid == 0) {
+        js[s] = widx;
+        if (GAPS) {
+          const double a2 = wsec ? __longlong_as_double((long long)(wsec - 1ull)) : 0.0;
+          gp[s] = (a1 - a2) / a1;
+        }
+      }
+      if (probe) p.tprobe[(int64_t)t * 8 + 6] = clock64();
+      // (E) multipliers, the next search column, the L column of step s
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int li = tid + PNT * r;
+        double lout = 0.0;
+        lprev[r] = 0.0;
+        if (st[r] == -1) {
+          if (r0 + li == widx) {
+            st[r] = t;
+            lout = 1.0;
+          } else {
+            const double lm = v[r][i] / piv;
+            v[r][i] = lm;
+            if (i + 1 < NB) v[r][i + 1] = fma(-lm, u1, v[r][i + 1]);
+            lprev[r] = lm;
+            lout = lm;
+          }
+        }
+        if (li < Rc) p.Lf[(r0 + li) + (int64_t)t * p.ldlf] = lout;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int q = 0; q < NB; ++q) v[r][q] = (q + 8 < NB) ? v[r][q + 8] : 0.0;
+  }
+  __syncthreads();
+  if (crank == 0) {
+    for (int s = tid; s < s_done; s += PNT) {
+      p.Js[p.c0 + s] = js[s];
+      if (GAPS) p.gaps[p.c0 + s] = gp[s];
+    }
+    for (int e = tid; e < s_done * bp; e += PNT) {
+      const int s = e / bp, j = e % bp;
+      if (j >= s) p.Uw[(p.c0 + s) + (int64_t)(p.c0 + j) * p.k] = ub[(size_t)s * NB + j];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int li = tid + PNT * r;
+    if (li < Rc) p.rowstate[r0 + li] = st[r];
+  }
+  cluster.sync();
+}
+
+template <int NB>
+constexpr size_t v2_smem_bytes() {
+  return sizeof(double) * ((size_t)NB * NB + 2 * PNW * NB) + 4 * 2 * PNW * 8 +
+         sizeof(double) * 2 * MAXCS * (4 + NB) + NB * 8 + NB * 8 + 16 + 64;
+}
+
 // U(c0+s, j) = M(piv_s, j) - sum_{s'<s} L11(s, s') U(c0+s', j), j in [c1, k).
 // One thread per column, the column of U in registers (bp <= U12_BP), L11 broadcast from smem.
 __global__ void __launch_bounds__(256) k_lupp_u12(const double* W, int64_t n, int k, int c0, int bp,
@@ -706,6 +953,11 @@ ClusterCfg pick_cluster(sk_ctx* c) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.max_dyn);
   }
+  for (PanelFn fn : {k_lupp_panel_v2<1, 64, true>, k_lupp_panel_v2<1, 64, false>, k_lupp_panel_v2<2, 32, true>,
+                     k_lupp_panel_v2<2, 32, false>, k_lupp_panel_v2<4, 16, true>, k_lupp_panel_v2<4, 16, false>}) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem_bytes<64>());
+  }
   cudaFuncSetAttribute(k_lupp_u12, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kU12Smem);
   for (int cs : {16, 8, 4, 2, 1}) {
     cudaLaunchConfig_t lc{};
@@ -744,7 +996,14 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   int64_t bp = 0;
   size_t smem_bytes = 0;
   const int rpt = (int)cdiv(R, PNT);
-  if (rpt <= 4) {
+  static const bool force_v1 = [] { const char* e = std::getenv("SKEL_LUPP_V1"); return e && e[0] == '1'; }();
+  if (rpt <= 4 && !force_v1) {
+    const int nb = rpt == 1 ? 64 : rpt == 2 ? 32 : 16;
+    bp = std::min<int64_t>(k, nb);
+    if (rpt == 1) { fn = gaps ? k_lupp_panel_v2<1, 64, true> : k_lupp_panel_v2<1, 64, false>; smem_bytes = v2_smem_bytes<64>(); }
+    else if (rpt == 2) { fn = gaps ? k_lupp_panel_v2<2, 32, true> : k_lupp_panel_v2<2, 32, false>; smem_bytes = v2_smem_bytes<32>(); }
+    else { fn = gaps ? k_lupp_panel_v2<4, 16, true> : k_lupp_panel_v2<4, 16, false>; smem_bytes = v2_smem_bytes<16>(); }
+  } else if (rpt <= 4) {
     const int nb = rpt == 1 ? 64 : rpt == 2 ? 32 : 16;
     const int rv = rpt == 1 ? 1 : rpt == 2 ? 2 : 4;
     bp = std::min<int64_t>(k, nb);
@@ -761,7 +1020,12 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   }
   if ((int64_t)smem_bytes > cfg.max_dyn) return fail(c, SK_E_ARG, "LUPP panel staging exceeds shared memory");
 
-  DBuf Wb, Ub, stateb, maxb, Lfb;
+  DBuf Wb, Ub, stateb, maxb, Lfb, probeb;
+  static const bool want_probe = [] { const char* e = std::getenv("SKEL_LUPP_PROBE"); return e && e[0] == '1'; }();
+  if (want_probe) {
+    SK_TRY(probeb.alloc(c, (size_t)k * 8 * sizeof(long long)));
+    SK_CUDA(c, cudaMemsetAsync(probeb.p, 0, (size_t)k * 8 * sizeof(long long), c->stream));
+  }
   SK_TRY(Wb.alloc(c, (size_t)n * k * sizeof(double)));
   SK_TRY(Ub.alloc(c, (size_t)k * k * sizeof(double)));
   SK_TRY(stateb.alloc(c, (size_t)n * sizeof(int)));
@@ -787,6 +1051,7 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     pp.rowstate = stateb.as<int>();
     pp.Js = Js; pp.Lf = Lf; pp.ldlf = ldlf; pp.Uw = Ub.as<double>(); pp.gaps = gaps;
     pp.maxbits = maxb.as<unsigned long long>(); pp.status = status_dev;
+    pp.tprobe = want_probe ? probeb.as<long long>() : nullptr;
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(cs);
     lc.blockDim = dim3(PNT);
@@ -806,6 +1071,25 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
       SK_TRY(gemm(c, false, false, n, k - c1, b, -1.0, Lf + c0 * ldlf, ldlf, Ub.as<double>() + c0 + c1 * k,
                   k, 1.0, Wb.as<double>() + c1 * n, n));
     }
+  }
+  if (want_probe) {   // experiments: per-step phase durations (cycles) of CTA 0, thread 0, to stderr
+    std::vector<long long> h((size_t)k * 8);
+    SK_CUDA(c, cudaMemcpyAsync(h.data(), probeb.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    int cnt = 0;
+    for (int64_t t = 1; t + 1 < k; ++t) {
+      const long long* a = &h[(size_t)t * 8];
+      const long long* b = &h[(size_t)(t + 1) * 8];
+      if (!a[0] || !b[0] || b[0] < a[0]) continue;
+      for (int j = 0; j < 6; ++j) acc[j] += (double)(a[j + 1] - a[j]);
+      acc[6] += (double)(b[0] - a[6]);
+      ++cnt;
+    }
+    if (cnt)
+      std::fprintf(stderr, "[lupp probe] n=%lld k=%lld steps=%d  A %.0f | bar %.0f | send %.0f | bulk %.0f | wait %.0f | reduce+U %.0f | E+next %.0f cycles\n",
+                   (long long)n, (long long)k, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
+                   acc[5] / cnt, acc[6] / cnt);
   }
   if (U) {
     const int blocks = (int)std::min<int64_t>(cdiv(k * k, 256), 4LL * c->num_sms);
