@@ -160,10 +160,130 @@ def run_reference(args):
     return 0
 
 
+def main_dist(args, world, rank, local):
+    """N > 1 GPUs (torchrun): the column-sharded path of SURVEY 8(e), weak scaling.
+
+    Rank r holds a 4096 x 4096 C2-type block (own Haar factors, seed 1002 + r), so the global A is
+    4096 x 4096N.  One step = sketch of the local block (Omega regenerated from the seed, no
+    communication) -> all-gather of the k LUPP-visible sketch rows -> column LUPP on the full panel
+    (replicated, identical J_s on every rank) -> C = A(:, J_s) by a sum all-reduce -> column-ID
+    residual (local squared sums + all-reduce).  value = sketch + selection time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_05877_b200 as sk
+    from inputs import make_c2
+    from paper_2104_05877_b200.dist import _all_gather_cols
+
+    dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)
+    k = args.k
+    l = k + 10
+    seed = 2002 + k
+    A_np, _ = make_c2(seed=1002 + rank)
+    m, nloc = A_np.shape
+    n_global = nloc * world
+    col0 = rank * nloc
+    with torch.cuda.stream(stream):
+        A = sk.fortran(torch.from_numpy(np.ascontiguousarray(A_np)).to(dev))
+        flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(record):
+        e = [ev() for _ in range(5)]
+        e[0].record(stream)
+        X = sk.sketch(A, l, "gaussian", seed)
+        e[1].record(stream)
+        Xk = _all_gather_cols(X[:k], n_global, None, world)
+        Js, _, _, _ = sk.select_cols(Xk, k, check=False)
+        e[2].record(stream)
+        C = sk.gather_cols_shard(A, Js, col0)
+        Ct = C.t().contiguous()
+        dist.all_reduce(Ct)
+        e[3].record(stream)
+        r2, a2 = sk.residual_cols(A, Ct.t())
+        sums = torch.tensor([r2, a2], dtype=torch.float64, device=dev)
+        dist.all_reduce(sums)
+        e[4].record(stream)
+        record(e)
+        return Js, sums
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(lambda e: None)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        recs = []
+        launches0 = sk.launch_count(local)
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize(dev)
+            for _ in range(args.steps):
+                flush.fill_(1)
+                out = step(recs.append)
+            torch.cuda.synchronize(dev)
+        launches = sk.launch_count(local) - launches0
+        dist.barrier()
+    sk_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in recs)
+    sel_ms = statistics.mean(e[0].elapsed_time(e[2]) for e in recs)
+    step_ms = statistics.mean(e[0].elapsed_time(e[4]) for e in recs)
+    t = torch.tensor([sel_ms, step_ms, sk_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sel_ms, step_ms, sk_ms_max = float(t[0]), float(t[1]), float(t[2])
+    Js, sums = out
+    achieved = 2.0 * l * m * nloc / (sk_ms * 1e-3) / 1e12
+    # end to end: pinned host block -> device (inside the timed region) -> sketch -> selection -> J_s on host
+    e2e = None
+    if not args.no_e2e:
+        A_host = torch.from_numpy(np.ascontiguousarray(A_np.T)).pin_memory()      # rows = columns of A
+        A_dev = torch.empty_like(A_host, device=dev)
+        times = []
+        with torch.cuda.stream(stream):
+            for it in range(2 + max(3, min(args.steps, 10))):
+                e0, e1 = ev(), ev()
+                e0.record(stream)
+                A_dev.copy_(A_host, non_blocking=True)
+                Ad = A_dev.t()
+                X = sk.sketch(Ad, l, "gaussian", seed)
+                Xk = _all_gather_cols(X[:k], n_global, None, world)
+                Js_d, _, _, _ = sk.select_cols(Xk, k, check=False)
+                Js_h = Js_d.cpu()
+                e1.record(stream)
+                e1.synchronize()
+                if it >= 2:
+                    times.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(t[0]), "unit": "ms", "h2d_bytes_per_step": int(m * nloc * 8),
+               "d2h_bytes_per_step": int(k * 8), "api": "dist path (torch.distributed + libskel.so), host A block per rank"}
+    if rank == 0:
+        line = {
+            "metric": "skeleton-selection time (sketch+LUPP)", "value": sel_ms, "unit": "ms",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2-type blocks: A 4096 x {n_global} FP64 column-sharded, 4096 x 4096 "
+                                   f"U diag(10^(-i/50)) V^T per rank, Gaussian Omega, k={k}, l={l}",
+                       "m": m, "n": n_global, "k": k, "l": l, "parallelism": f"column-sharded x{world}",
+                       "l2": "flushed: 512 MiB overwrite between timed steps (untimed)"},
+            "residual": {"col_id_fro": math.sqrt(max(float(sums[0]), 0.0)), "normA_fro": math.sqrt(float(sums[1]))},
+            "roofline": {"kernel": "k_sketch_tma", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None},
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return main_dist(args, int(os.environ["WORLD_SIZE"]), int(os.environ.get("RANK", "0")),
+                         int(os.environ.get("LOCAL_RANK", "0")))
 
     import torch
     import torch.distributed as dist

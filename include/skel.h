@@ -136,6 +136,13 @@ sk_status sk_select_cols_cpqr(sk_ctx* ctx, const double* X, int64_t l, int64_t n
 sk_status sk_gather_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
                          const int64_t* Js, int64_t k, double* C, int64_t ldc);
 
+/* ---- S3 on a column-sharded A ----
+ * A is this rank's column block (m x ncols, columns col0 .. col0+ncols-1 of the global A).
+ * C(:, t) = A(:, Js[t] - col0) for the skeletons this rank owns and 0 for the others, so a
+ * sum-all-reduce over ranks assembles C = A_global(:, Js) exactly (x + 0 = x). */
+sk_status sk_gather_cols_shard(sk_ctx* ctx, const double* A, int64_t m, int64_t ncols, int64_t lda, int64_t col0,
+                               const int64_t* Js, int64_t k, double* C, int64_t ldc);
+
 /* ---- S4: row skeletons by row-wise LUPP on C  (Alg. 2 line 4) ----
  * Step t scans column t of C (m x k column-major, ldc >= m); outputs as for
  * sk_select_cols with n -> m (Is = I_s of eq:Is).  Requires 1 <= k <= m. */
@@ -162,6 +169,15 @@ sk_status sk_id_coeffs(sk_ctx* ctx, const double* Lf, int64_t n, int64_t k, int6
 sk_status sk_residual(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
                       const int64_t* Js, const int64_t* Is, int64_t k, sk_residual_kind kind,
                       const double* Z, int64_t ldz, double* res_fro, double* normA_fro);
+
+/* ---- S6 for a given skeleton matrix (column-sharded residual) ----
+ * sums (host double[2]): sums[0] = ||A - Q Q^T A||_F^2, sums[1] = ||A||_F^2 with Q = ortho(C)
+ * (eq:def_column_id, Frobenius R12), for A m x n column-major and C m x k column-major
+ * (ldc >= m) supplied by the caller (e.g. assembled across ranks).  Squared sums, so the column
+ * blocks of a sharded A add up: ||A - CC^+A||_F^2 = sum over ranks.  Synchronises.  SK_E_RANK if
+ * C is numerically rank deficient. */
+sk_status sk_residual_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* C,
+                           int64_t k, int64_t ldc, double* sums);
 
 /* ---- Algorithm 2 end to end ---------------------------------
  * Sketch (S0+S1) + column LUPP (S2) and, if Is != NULL, gather + row LUPP

@@ -22,6 +22,8 @@ _SIGS = {
                        ctypes.POINTER(c_i64)],
     "sk_select_cols_cpqr": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, ctypes.POINTER(c_i64)],
     "sk_gather_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64],
+    "sk_gather_cols_shard": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64],
+    "sk_residual_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_i64, c_i64, ctypes.POINTER(ctypes.c_double)],
     "sk_select_rows": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, c_dp, c_i64, c_dp,
                        ctypes.POINTER(c_i64)],
     "sk_id_coeffs": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, ctypes.POINTER(ctypes.c_double)],

@@ -134,6 +134,30 @@ def gather_cols(A, Js):
     return C
 
 
+def gather_cols_shard(A_local, Js, col0, m=None):
+    """C(:, t) = A_global(:, J_s[t]) for the skeletons in this rank's column block
+    [col0, col0 + ncols), zero columns for the others (sum over ranks = C)."""
+    lda = _colmajor(A_local, "A")
+    m, ncols = A_local.shape
+    k = Js.numel()
+    C = torch.empty((k, m), dtype=torch.float64, device=A_local.device).t()
+    h = context(A_local.device.index)
+    _check(lib().sk_gather_cols_shard(h, _ptr(A_local), m, ncols, lda, col0, _ptr(Js), k, _ptr(C), m), h)
+    return C
+
+
+def residual_cols(A, C):
+    """(||A - Q Q^T A||_F^2, ||A||_F^2) with Q = ortho(C), C given (column-sharded residual)."""
+    lda = _colmajor(A, "A")
+    ldc = _colmajor(C, "C")
+    m, n = A.shape
+    k = C.shape[1]
+    sums = (ctypes.c_double * 2)()
+    h = context(A.device.index)
+    _check(lib().sk_residual_cols(h, _ptr(A), m, n, lda, _ptr(C), k, ldc, sums), h)
+    return float(sums[0]), float(sums[1])
+
+
 def select_rows(C, k=None, want_factors=True, want_gaps=False, check=True):
     """Row LUPP on C (Alg. 2 line 4). Returns (Is, Lf, U, gaps)."""
     ldc = _colmajor(C, "C")

@@ -170,6 +170,32 @@ sk_status sk_gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64
   return gather_cols(c, A, m, lda, Js, k, C, ldc);
 }
 
+sk_status sk_gather_cols_shard(sk_ctx* c, const double* A, int64_t m, int64_t ncols, int64_t lda, int64_t col0,
+                               const int64_t* Js, int64_t k, double* C, int64_t ldc) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, Js && C && (A || ncols == 0), "sk_gather_cols_shard: NULL pointer");
+  SK_ARG(c, m >= 0 && ncols >= 0 && k >= 0 && col0 >= 0 && lda >= m && ldc >= m, "sk_gather_cols_shard: bad sizes");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  return gather_cols_shard(c, A, m, lda, col0, ncols, Js, k, C, ldc);
+}
+
+sk_status sk_residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* C, int64_t k,
+                           int64_t ldc, double* sums) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, A && C && sums, "sk_residual_cols: NULL pointer");
+  SK_ARG(c, m >= 1 && n >= 1 && k >= 1 && k <= m && lda >= m && ldc >= m, "sk_residual_cols: bad sizes");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf d, st;
+  SK_TRY(d.alloc(c, 2 * sizeof(double)));
+  SK_TRY(st.alloc(c, sizeof(int64_t)));
+  SK_TRY(residual_cols(c, A, m, n, lda, C, k, ldc, d.as<double>(), st.as<int64_t>()));
+  int64_t info = 0;
+  SK_TRY(finish_info(c, st.as<int64_t>(), &info, "sk_residual_cols (basis of C)"));
+  return to_host(c, sums, d.p, 2 * sizeof(double));
+}
+
 sk_status sk_select_rows(sk_ctx* c, const double* C, int64_t m, int64_t k, int64_t ldc, int64_t* Is,
                          double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps, int64_t* info) {
   if (!c) return SK_E_ARG;

@@ -14,14 +14,17 @@ namespace {
 
 constexpr int TB = 32;   // diagonal block size
 
+// C(:, t) = A(:, J[t] - col0) when col0 <= J[t] < col0 + ncols (this rank's column block), else 0.
+// Unsharded use: col0 = 0, ncols = n.
 __global__ void k_gather_cols(const double* A, int64_t m, int64_t lda, const int64_t* J, int64_t k,
-                              double* C, int64_t ldc) {
+                              int64_t col0, int64_t ncols, double* C, int64_t ldc) {
   const int64_t t = blockIdx.y;
-  const int64_t j = J[t];
-  const double* src = A + j * lda;
+  const int64_t j = J[t] - col0;
+  const bool own = j >= 0 && j < ncols;
+  const double* src = A + (own ? j : 0) * lda;
   double* dst = C + t * ldc;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = src[i];
+    dst[i] = own ? src[i] : 0.0;
 }
 
 // Rt(:, t) = A(I[t], :)^T  (row gather; reads are strided by lda, writes coalesced)
@@ -174,9 +177,14 @@ __global__ void k_fill_ones(double* x, int64_t k) {
 
 sk_status gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t lda, const int64_t* J, int64_t k,
                       double* C, int64_t ldc) {
-  if (k == 0 || m == 0) return SK_OK;
-  const int bx = (int)std::min<int64_t>(cdiv(m, 256), 64);
-  k_gather_cols<<<dim3(bx, (unsigned)k), 256, 0, c->stream>>>(A, m, lda, J, k, C, ldc);
+  return gather_cols_shard(c, A, m, lda, 0, INT64_MAX, J, k, C, ldc);
+}
+
+sk_status gather_cols_shard(sk_ctx* c, const double* A, int64_t m, int64_t lda, int64_t col0, int64_t ncols,
+                            const int64_t* J, int64_t k, double* C, int64_t ldc) {
+  if (m == 0 || k == 0) return SK_OK;
+  const unsigned bx = (unsigned)std::min<int64_t>(cdiv(m, 256), 64);
+  k_gather_cols<<<dim3(bx, (unsigned)k), 256, 0, c->stream>>>(A, m, lda, J, k, col0, ncols, C, ldc);
   return launched(c);
 }
 

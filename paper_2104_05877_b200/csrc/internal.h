@@ -39,6 +39,9 @@ sk_status cpqr(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, in
 // ---------------------------------------------------------------- small dense kernels (dense.cu)
 sk_status gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t lda, const int64_t* J,
                       int64_t k, double* C, int64_t ldc);
+// Shard-aware gather: C(:, t) = A(:, J[t] - col0) if the column is in [col0, col0 + ncols), else 0.
+sk_status gather_cols_shard(sk_ctx* c, const double* A, int64_t m, int64_t lda, int64_t col0, int64_t ncols,
+                            const int64_t* J, int64_t k, double* C, int64_t ldc);
 // R^T (n x k, col-major ld n) = A(I, :)^T
 sk_status gather_rows_t(sk_ctx* c, const double* A, int64_t n, int64_t lda, const int64_t* I,
                         int64_t k, double* Rt, int64_t ldrt);
@@ -66,5 +69,10 @@ sk_status id_coeffs(sk_ctx* c, const double* Lf, int64_t n, int64_t k, int64_t l
 sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda,
                    const int64_t* Js, const int64_t* Is, int64_t k, int kind, const double* Z,
                    int64_t ldz, double* sums_dev, int64_t* status_dev);
+
+// sums[0] = ||A - Q Q^T A||_F^2, sums[1] = ||A||_F^2 with Q = ortho(C) (C m x k given explicitly;
+// the distributed column-ID residual, where C is assembled across ranks).
+sk_status residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* C, int64_t k,
+                        int64_t ldc, double* sums_dev, int64_t* status_dev);
 
 }  // namespace skel

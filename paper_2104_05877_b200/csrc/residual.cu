@@ -69,4 +69,19 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
   return gemm_sumsq(c, false, true, m, n, k, -1.0, B.as<double>(), m, Qr.as<double>(), n, 1.0, A, lda, sums);
 }
 
+sk_status residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* C, int64_t k,
+                        int64_t ldc, double* sums, int64_t* status_dev) {
+  SK_CUDA(c, cudaMemsetAsync(status_dev, 0, sizeof(int64_t), c->stream));
+  DBuf Cc, Qc, W;
+  SK_TRY(Cc.alloc(c, (size_t)m * k * sizeof(double)));
+  SK_TRY(Qc.alloc(c, (size_t)m * k * sizeof(double)));
+  SK_CUDA(c, cudaMemcpy2DAsync(Cc.p, (size_t)m * sizeof(double), C, (size_t)ldc * sizeof(double), (size_t)m * sizeof(double),
+                               (size_t)k, cudaMemcpyDeviceToDevice, c->stream));
+  SK_TRY(basis_from_cols(c, Cc.as<double>(), m, k, Qc.as<double>(), status_dev));
+  Cc.release();
+  SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
+  SK_TRY(gemm(c, true, false, k, n, m, 1.0, Qc.as<double>(), m, A, lda, 0.0, W.as<double>(), k));
+  return gemm_sumsq(c, false, false, m, n, k, -1.0, Qc.as<double>(), m, W.as<double>(), k, 1.0, A, lda, sums);
+}
+
 }  // namespace skel

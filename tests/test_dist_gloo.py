@@ -1,0 +1,139 @@
+"""The column-sharded path on CPU: the merge rule and the rank protocol.
+
+* oracle.dist (per-step exchange with the lowest-global-index merge rule) == single-process LUPP,
+  pivots and factors bit for bit, including exact ties that straddle a shard boundary.
+* paper_2104_05877_b200.dist.dist_rand_lupp over a world-size-2 gloo group, with a host backend
+  built from the oracle standing in for the CUDA kernels, reproduces the unsharded oracle path:
+  J_s, C = A(:, J_s), I_s and the column-ID residual.
+"""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from inputs import kahan_witness, make_c1
+from oracle import dist as o_dist
+from oracle import lupp as o_lupp
+from oracle import residual as o_res
+from oracle import sketch as o_sketch
+from paper_2104_05877_b200.dist import dist_rand_lupp, shard
+
+
+@pytest.mark.parametrize("n,world", [(10, 3), (4096, 8), (7, 7), (5, 1), (1000, 6)])
+def test_shard_partitions_columns(n, world):
+    blocks = [shard(n, world, r) for r in range(world)]
+    assert blocks[0][0] == 0
+    for (c0, nc), (c1, _) in zip(blocks, blocks[1:]):
+        assert c0 + nc == c1
+    assert sum(nc for _, nc in blocks) == n
+    assert max(nc for _, nc in blocks) - min(nc for _, nc in blocks) <= 1
+
+
+@pytest.mark.parametrize("splits", [[40], [13, 27], [10, 10, 10, 10], [1, 38, 1]])
+def test_sharded_merge_rule_equals_single_lupp(splits):
+    rng = np.random.default_rng(len(splits))
+    X = rng.standard_normal((12, sum(splits)))
+    blocks = np.split(X, np.cumsum(splits)[:-1], axis=1)
+    piv_d, Lf_d, U_d = o_dist.select_cols_sharded(blocks, 10)
+    piv, Lf, U, _ = o_lupp.select_cols(X, 10)
+    assert piv.tolist() == piv_d.tolist()
+    np.testing.assert_array_equal(Lf, Lf_d)
+    np.testing.assert_array_equal(U, U_d)
+
+
+def test_sharded_ties_go_to_lowest_global_index():
+    # Kahan witness: every step is an exact tie; shards split the tied columns, so a
+    # rank-local "first maximum" rule would pick a later global index at a shard boundary.
+    l = 8
+    X = kahan_witness(l, 20)
+    perm = np.r_[np.arange(l, 20), np.arange(l)]           # tied columns moved to the last shard
+    Xp = X[:, perm]
+    for splits in ([12, 8], [5, 7, 8], [19, 1]):
+        blocks = np.split(Xp, np.cumsum(splits)[:-1], axis=1)
+        piv_d, _, _ = o_dist.select_cols_sharded(blocks, l)
+        piv, _, _, _ = o_lupp.select_cols(Xp, l)
+        assert piv_d.tolist() == piv.tolist()
+
+
+class HostBackend:
+    """Test stand-in for the CUDA kernels (the oracle, on CPU tensors)."""
+
+    def sketch(self, A_local, l, embedding, seed, zeta):
+        return torch.from_numpy(o_sketch.sketch(A_local.numpy(), l, embedding, seed, zeta))
+
+    def select_cols(self, Xk, k):
+        piv, Lf, _, _ = o_lupp.select_cols(Xk.numpy(), k)
+        return torch.from_numpy(piv), torch.from_numpy(Lf)
+
+    def select_rows(self, C, k):
+        piv, _, _, _ = o_lupp.select_rows(C.numpy(), k)
+        return torch.from_numpy(piv)
+
+    def gather_cols_shard(self, A_local, Js, col0):
+        m, nc = A_local.shape
+        C = torch.zeros((Js.numel(), m), dtype=torch.float64).t()
+        for t, j in enumerate(Js.tolist()):
+            if col0 <= j < col0 + nc:
+                C[:, t] = A_local[:, j - col0]
+        return C
+
+    def residual_cols(self, A_local, C):
+        A = A_local.numpy()
+        Q = o_res.ortho(C.numpy())
+        E = A - Q @ (Q.T @ A)
+        return float(np.sum(E * E)), float(np.sum(A * A))
+
+
+def _worker(rank, world, port, A, k, l, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = A.shape[1]
+        c0, nc = shard(n, world, rank)
+        A_local = torch.from_numpy(np.asfortranarray(A[:, c0:c0 + nc]))
+        out = dist_rand_lupp(A_local, n, k, l, "gaussian", seed, rows=True, residual=True, backend=HostBackend())
+        q.put((rank, out["Js"].tolist(), out["Is"].tolist(), out["C"].numpy().copy(), out["residual"], out["normA"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dist_rand_lupp_gloo_matches_unsharded_oracle(world):
+    A, _ = make_c1(seed=1001)
+    A = A[:, :251]                                           # ragged shards
+    k, l, seed = 20, 40, 2001
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, A, k, l, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    X = o_sketch.sketch(A, l, "gaussian", seed)
+    piv, _, _, _ = o_lupp.select_cols(X, k)
+    ipiv, _, _, _ = o_lupp.select_rows(A[:, piv], k)
+    r_or, n_or = o_res.residual(A, piv, kind="col_id")
+    for rank, Js, Is, C, r, nA in res:
+        assert Js == piv.tolist(), rank
+        np.testing.assert_array_equal(C, A[:, piv])          # assembled exactly by the sum all-reduce
+        assert Is == ipiv.tolist()
+        assert abs(r - r_or) <= 1e-12 * r_or + 4 * 2.0 ** -53 * n_or
+        assert abs(nA - n_or) <= 1e-14 * n_or
+    assert math.isfinite(res[0][4])

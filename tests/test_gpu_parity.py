@@ -242,3 +242,53 @@ def test_rand_lupp_host_and_device_agree():
     Is, _, _, _ = sk.select_rows(sk.gather_cols(Ad, Js), 30)
     assert Js_h.tolist() == Js.cpu().tolist()
     assert Is_h.tolist() == Is.cpu().tolist()
+
+
+# ------------------------------------------------------------------ column-sharded entry points (8(e))
+def test_gather_cols_shard_bitwise():
+    A = rand_mat(300, 50, 2)
+    Ad = dev_f(A)
+    J = torch.tensor([7, 3, 49, 0, 20, 21], dtype=torch.int64, device=DEV)
+    col0, nc = 20, 25                                    # this "rank" owns columns 20..44
+    C = sk.gather_cols_shard(Ad[:, col0:col0 + nc], J, col0).cpu().numpy()
+    ref = np.zeros((300, 6))
+    for t, j in enumerate([7, 3, 49, 0, 20, 21]):
+        if col0 <= j < col0 + nc:
+            ref[:, t] = A[:, j]
+    np.testing.assert_array_equal(C, ref)
+
+
+def test_residual_cols_matches_oracle_and_adds_over_shards():
+    A, _ = make_c1(seed=1001)
+    k = 20
+    Ad = dev_f(A)
+    X = sk.sketch(Ad, 40, "gaussian", 2001)
+    Js, _, _, _ = sk.select_cols(X, k)
+    C = sk.gather_cols(Ad, Js)
+    r2a, a2a = sk.residual_cols(Ad[:, :100], C)
+    r2b, a2b = sk.residual_cols(Ad[:, 100:], C)
+    ro, nAo = o_res.residual(A, Js.cpu().numpy(), kind="col_id")
+    r = math.sqrt(r2a + r2b)
+    assert abs(r - ro) <= 1e-9 * ro + 4 * U * nAo
+    assert abs(math.sqrt(a2a + a2b) - nAo) <= 1e-13 * nAo
+
+
+def test_dist_rand_lupp_nccl_world1():
+    import torch.distributed as tdist
+    from paper_2104_05877_b200.dist import dist_rand_lupp
+    os_env = __import__("os").environ
+    os_env.setdefault("MASTER_ADDR", "127.0.0.1")
+    os_env.setdefault("MASTER_PORT", "29517")
+    tdist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        A, _ = make_c1(seed=1001)
+        out = dist_rand_lupp(dev_f(A), A.shape[1], 20, 40, "gaussian", 2001, rows=True, residual=True)
+        X = o_sketch.sketch(A, 40, "gaussian", 2001)
+        piv, _, _, _ = o_lupp.select_cols(X, 20)
+        assert out["Js"].cpu().tolist() == piv.tolist()
+        ipiv, _, _, _ = o_lupp.select_rows(A[:, piv], 20)
+        assert out["Is"].cpu().tolist() == ipiv.tolist()
+        ro, nAo = o_res.residual(A, piv, kind="col_id")
+        assert abs(out["residual"] - ro) <= 1e-9 * ro + 4 * U * nAo
+    finally:
+        tdist.destroy_process_group()
