@@ -163,5 +163,29 @@ __device__ __forceinline__ uint64_t sparse_col(uint64_t i, int l, int zeta, uint
   return (uint64_t)sw.x | ((uint64_t)sw.y << 32);   // bit j of word (j/32) -> bit j
 }
 
+// Register-resident variant of sparse_col for zeta <= 8 (identical draws; unrolled so rows[]
+// stays in registers).
+__device__ __forceinline__ uint64_t sparse_col8(uint64_t i, int l, int zeta, uint2 key, int (&rows)[8]) {
+  const uint32_t ilo = (uint32_t)i, ihi = (uint32_t)(i >> 32);
+  const int nrc = (zeta + 3) >> 2;
+  const uint4 sw = philox4x32_10(make_uint4(ilo, ihi, (uint32_t)nrc, kTagSparse), key);
+  const uint4 w0 = philox4x32_10(make_uint4(ilo, ihi, 0u, kTagSparse), key);
+  const uint4 w1 = zeta > 4 ? philox4x32_10(make_uint4(ilo, ihi, 1u, kTagSparse), key) : make_uint4(0, 0, 0, 0);
+  const uint32_t words[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    rows[j] = -1;
+    if (j < zeta) {
+      const uint32_t nrange = (uint32_t)(l - zeta + j + 1);
+      int t = (int)(((uint64_t)words[j] * nrange) >> 32);
+      bool taken = false;
+#pragma unroll
+      for (int q = 0; q < j; ++q) taken |= (rows[q] == t);
+      rows[j] = taken ? (int)nrange - 1 : t;
+    }
+  }
+  return (uint64_t)sw.x | ((uint64_t)sw.y << 32);
+}
+
 }  // namespace dev
 }  // namespace skel

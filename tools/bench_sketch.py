@@ -29,10 +29,13 @@ SHAPES = [  # (name, m, n, l, embedding)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--only", default="", help="substring filter on the shape name")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     flush = torch.empty(512 << 18, dtype=torch.int32, device=dev)
     for name, m, n, l, emb in SHAPES:
+        if a.only and a.only not in name:
+            continue
         A = sk.fortran(torch.randn(m, n, dtype=torch.float64, device=dev))
         X = torch.empty((l, n), dtype=torch.float64, device=dev)
         for _ in range(3):
