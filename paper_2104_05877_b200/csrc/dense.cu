@@ -36,104 +36,8 @@ __global__ void k_gather_rows_t(const double* A, int64_t n, int64_t lda, const i
     Rt[j + t * ldrt] = A[i + j * lda];
 }
 
-// Unblocked Cholesky of one jb x jb diagonal block (lower, in place), jb <= TB.
-__global__ void k_potrf_diag(double* G, int64_t ld, int jb, int64_t col0, int64_t* status) {
-  if (*status != 0) return;
-  __shared__ double a[TB][TB + 1];
-  __shared__ int bad;
-  const int tid = threadIdx.x;
-  if (tid == 0) bad = 0;
-  for (int e = tid; e < jb * jb; e += blockDim.x) {
-    const int i = e % jb, j = e / jb;
-    a[i][j] = G[i + j * ld];
-  }
-  __syncthreads();
-  for (int c = 0; c < jb; ++c) {
-    if (tid == 0) {
-      const double d = a[c][c];
-      if (!(d > 0.0)) {
-        bad = c + 1;
-      } else {
-        a[c][c] = sqrt(d);
-      }
-    }
-    __syncthreads();
-    if (bad) break;
-    const double d = a[c][c];
-    for (int i = c + 1 + tid; i < jb; i += blockDim.x) a[i][c] /= d;
-    __syncthreads();
-    for (int e = tid; e < (jb - c - 1) * (jb - c - 1); e += blockDim.x) {
-      const int i = c + 1 + e % (jb - c - 1), j = c + 1 + e / (jb - c - 1);
-      if (j <= i) a[i][j] = fma(-a[i][c], a[j][c], a[i][j]);
-    }
-    __syncthreads();
-  }
-  if (bad) {
-    if (tid == 0) *status = col0 + bad;
-    return;
-  }
-  for (int e = tid; e < jb * jb; e += blockDim.x) {
-    const int i = e % jb, j = e / jb;
-    G[i + j * ld] = j <= i ? a[i][j] : 0.0;
-  }
-}
 
-// X(rows x jb) <- X * Ljj^{-T}, Ljj lower non-unit (jb <= TB).  One thread per row.
-__global__ void k_trsm_diag_lt(double* X, int64_t rows, int64_t ldx, int jb, const double* L,
-                               int64_t ldl, const int64_t* status) {
-  if (status && *status != 0) return;
-  __shared__ double l[TB][TB + 1];
-  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) {
-    const int i = e % jb, j = e / jb;
-    l[i][j] = L[i + j * ldl];
-  }
-  __syncthreads();
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    double x[TB];
-#pragma unroll
-    for (int c = 0; c < TB; ++c) {
-      if (c < jb) {
-        double s = X[r + c * ldx];
-#pragma unroll
-        for (int cp = 0; cp < TB; ++cp)
-          if (cp < c) s = fma(-x[cp], l[c][cp], s);
-        x[c] = s / l[c][c];
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < TB; ++c)
-      if (c < jb) X[r + c * ldx] = x[c];
-  }
-}
 
-// X(rows x jb) <- X * Ljj^{-1}, Ljj unit lower (jb <= TB): x[c] = y[c] - sum_{c'>c} x[c'] L[c'][c].
-__global__ void k_trsm_diag_l_unit(double* X, int64_t rows, int64_t ldx, int jb, const double* L,
-                                   int64_t ldl) {
-  __shared__ double l[TB][TB + 1];
-  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) {
-    const int i = e % jb, j = e / jb;
-    l[i][j] = L[i + j * ldl];
-  }
-  __syncthreads();
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    double x[TB];
-#pragma unroll
-    for (int c = TB - 1; c >= 0; --c) {
-      if (c < jb) {
-        double s = X[r + c * ldx];
-#pragma unroll
-        for (int cp = TB - 1; cp > 0; --cp)
-          if (cp > c && cp < jb) s = fma(-x[cp], l[cp][c], s);
-        x[c] = s;
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < TB; ++c)
-      if (c < jb) X[r + c * ldx] = x[c];
-  }
-}
 
 // One power-iteration step: y = G x / ||x||; done early when converged (flag).
 __global__ void k_power_step(const double* G, int64_t k, int64_t ld, const double* x, double* y,
@@ -173,6 +77,159 @@ __global__ void k_fill_ones(double* x, int64_t k) {
     x[i] = 1.0 + 1e-3 * (double)((i * 2654435761LL) % 1000) / 1000.0;
 }
 
+
+// ---- 64-wide diagonal blocks: factor / invert in one CTA, apply by an in-place row kernel ----
+constexpr int TB2 = 64;
+
+// MODE 0: G (jb x jb SPD, ld) -> its Cholesky factor L (lower, upper zeroed, in place) and
+//         W = L^{-1} (lower, ldw).  MODE 1: G holds a unit lower L (read only) -> W = L^{-1}.
+// status: 1-based failing column (+ col0) on a non-positive pivot (MODE 0).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_diag_inv(double* G, int64_t ld, int jb, double* W, int64_t ldw,
+                                                  int64_t col0, int64_t* status) {
+  if (status && *status != 0) return;
+  extern __shared__ double dinv_sm[];
+  double (*a)[TB2 + 1] = reinterpret_cast<double (*)[TB2 + 1]>(dinv_sm);
+  double (*w)[TB2 + 1] = reinterpret_cast<double (*)[TB2 + 1]>(dinv_sm + TB2 * (TB2 + 1));
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < TB2 * TB2; e += 256) {
+    const int i = e & (TB2 - 1), j = e >> 6;
+    a[i][j] = (i < jb && j < jb) ? G[i + j * ld] : (i == j ? 1.0 : 0.0);
+    w[i][j] = 0.0;
+  }
+  __syncthreads();
+  if (MODE == 0) {   // (MODE 2: a non-unit lower factor is given; MODE 1: unit lower)
+    // right-looking Cholesky, one barrier per column: every thread recomputes 1/sqrt of the pivot
+    // from shared memory (no serial thread-0 step), scales its column entries and updates its
+    // 16 x 16-grid share of the trailing triangle with independent FMAs.
+    for (int c = 0; c < jb; ++c) {
+      const double d = a[c][c];
+      if (!(d > 0.0)) {
+        if (tid == 0) *status = col0 + c + 1;
+        return;
+      }
+      const double rs = 1.0 / sqrt(d);
+      const int i0 = c + 1 + (tid >> 4), j0 = c + 1 + (tid & 15);
+      double li[4], lj[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        li[q] = (i0 + 16 * q < jb) ? a[i0 + 16 * q][c] * rs : 0.0;
+        lj[q] = (j0 + 16 * q < jb) ? a[j0 + 16 * q][c] * rs : 0.0;
+      }
+      __syncthreads();                     // everyone has read column c before it is rewritten
+      if (tid == 0) a[c][c] = d * rs;      // sqrt(d)
+      if ((tid & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i0 + 16 * q < jb) a[i0 + 16 * q][c] = li[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + 16 * q;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int j = j0 + 16 * r;
+          if (i < jb && j <= i) a[i][j] = fma(-li[q], lj[r], a[i][j]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // W = L^{-1} by elimination on [L | I]: step t scales row t of W by 1/L(t,t) and removes
+  // L(i,t) * W(t,:) from every row i > t -- a rank-1 update per step, 16 x 16 thread grid
+  for (int e = tid; e < TB2; e += 256) w[e][e] = 1.0;
+  __syncthreads();
+  for (int t = 0; t < jb; ++t) {
+    // row t of W is final once scaled; rows i > t drop L(i,t)/L(t,t) * W(t,:)
+    const double inv = MODE == 1 ? 1.0 : 1.0 / a[t][t];
+    const int i0 = t + 1 + (tid >> 4), j0 = tid & 15;
+    double wt[4], li[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      wt[q] = (j0 + 16 * q <= t) ? w[t][j0 + 16 * q] * inv : 0.0;
+      li[q] = (i0 + 16 * q < jb) ? a[i0 + 16 * q][t] : 0.0;
+    }
+    __syncthreads();
+    if (tid < 16 && MODE != 1) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (j0 + 16 * q <= t) w[t][j0 + 16 * q] = wt[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + 16 * q;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (i < jb && j0 + 16 * r <= t) w[i][j0 + 16 * r] = fma(-li[q], wt[r], w[i][j0 + 16 * r]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < TB2 * TB2; e += 256) {
+    const int i = e & (TB2 - 1), jj = e >> 6;
+    if (i < jb && jj < jb) {
+      W[i + jj * ldw] = jj <= i ? w[i][jj] : 0.0;
+      if (MODE == 0) G[i + jj * ld] = jj <= i ? a[i][jj] : 0.0;
+    }
+  }
+}
+
+// X (rows x jb, ldx) <- X * M in place, M = W^T (TRANS) or W, W jb x jb (ldw).  A CTA owns 32 whole
+// rows, so reading and writing X never race.
+template <bool TRANS>
+__global__ void __launch_bounds__(256) k_right_tri_mul(double* X, int64_t rows, int64_t ldx, const double* W,
+                                                       int64_t ldw, int jb) {
+  extern __shared__ double rtm_sm[];
+  double (*m)[TB2 + 1] = reinterpret_cast<double (*)[TB2 + 1]>(rtm_sm);              // m[t][c] = M(t, c)
+  double (*x)[TB2 + 1] = reinterpret_cast<double (*)[TB2 + 1]>(rtm_sm + TB2 * (TB2 + 1));
+  for (int e = threadIdx.x; e < TB2 * TB2; e += 256) {   // coalesced along W's leading dimension
+    const int f = e % TB2, g = e / TB2;
+    const double v = (f < jb && g < jb) ? W[f + (int64_t)g * ldw] : 0.0;   // W(f, g)
+    if (TRANS) m[g][f] = v;                                               // M(t, c) = W(c, t)
+    else m[f][g] = v;                                                     // M(t, c) = W(t, c)
+  }
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  for (int e = threadIdx.x; e < 32 * TB2; e += 256) {
+    const int rr = e % 32, t = e / 32;
+    const int64_t r = r0 + rr;
+    x[rr][t] = (r < rows && t < jb) ? X[r + t * ldx] : 0.0;
+  }
+  __syncthreads();
+  // thread: row rr = tid % 32, columns c = tid / 32 + 8 q (8 per thread)
+  const int rr = threadIdx.x & 31, cb = threadIdx.x >> 5;
+  double o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[q] = 0.0;
+  for (int t = 0; t < jb; ++t) {
+    const double xv = x[rr][t];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = fma(xv, m[t][cb + 8 * q], o[q]);
+  }
+  const int64_t r = r0 + rr;
+  if (r < rows) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = cb + 8 * q;
+      if (c < jb) X[r + c * ldx] = o[q];
+    }
+  }
+}
+constexpr size_t kDiagInvSmem = 2 * TB2 * (TB2 + 1) * sizeof(double);
+constexpr size_t kRtmSmem = (TB2 + 32) * (TB2 + 1) * sizeof(double);
+
+sk_status dense_attrs(sk_ctx* c) {
+  static bool done = false;
+  if (done) return SK_OK;
+  SK_CUDA(c, cudaFuncSetAttribute(k_diag_inv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagInvSmem));
+  SK_CUDA(c, cudaFuncSetAttribute(k_diag_inv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagInvSmem));
+  SK_CUDA(c, cudaFuncSetAttribute(k_diag_inv<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagInvSmem));
+  SK_CUDA(c, cudaFuncSetAttribute(k_right_tri_mul<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtmSmem));
+  SK_CUDA(c, cudaFuncSetAttribute(k_right_tri_mul<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtmSmem));
+  done = true;
+  return SK_OK;
+}
+
 }  // namespace
 
 sk_status gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t lda, const int64_t* J, int64_t k,
@@ -197,16 +254,21 @@ sk_status gather_rows_t(sk_ctx* c, const double* A, int64_t n, int64_t lda, cons
 }
 
 sk_status potrf_lower(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t* status_dev) {
-  for (int64_t j0 = 0; j0 < k; j0 += TB) {
-    const int jb = (int)std::min<int64_t>(TB, k - j0);
-    k_potrf_diag<<<1, 256, 0, c->stream>>>(G + j0 + j0 * ld, ld, jb, j0, status_dev);
+  SK_TRY(dense_attrs(c));
+  // right-looking, 64-wide blocks: L_jj and W_jj = L_jj^{-1} in one CTA, panel L_rj = G_rj W_jj^T
+  // in place, trailing update by DMMA GEMM.  The W_jj blocks are kept (diagonal of c->tri_w) for
+  // the triangular solve that follows.
+  DBuf Wd;
+  SK_TRY(Wd.alloc(c, (size_t)k * TB2 * sizeof(double)));
+  for (int64_t j0 = 0; j0 < k; j0 += TB2) {
+    const int jb = (int)std::min<int64_t>(TB2, k - j0);
+    k_diag_inv<0><<<1, 256, kDiagInvSmem, c->stream>>>(G + j0 + j0 * ld, ld, jb, Wd.as<double>() + j0, k, j0, status_dev);
     SK_TRY(launched(c));
     const int64_t j1 = j0 + jb;
     if (j1 < k) {
       const int64_t rows = k - j1;
-      const int blocks = (int)std::min<int64_t>(cdiv(rows, 128), 4LL * c->num_sms);
-      k_trsm_diag_lt<<<blocks, 128, 0, c->stream>>>(G + j1 + j0 * ld, rows, ld, jb, G + j0 + j0 * ld, ld,
-                                                     status_dev);
+      k_right_tri_mul<true><<<(unsigned)cdiv(rows, 32), 256, kRtmSmem, c->stream>>>(G + j1 + j0 * ld, rows, ld,
+                                                                             Wd.as<double>() + j0, k, jb);
       SK_TRY(launched(c));
       SK_TRY(gemm(c, false, true, rows, rows, jb, -1.0, G + j1 + j0 * ld, ld, G + j1 + j0 * ld, ld, 1.0,
                   G + j1 + j1 * ld, ld));
@@ -217,13 +279,23 @@ sk_status potrf_lower(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t* stat
 
 sk_status trsm_right_lt(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L,
                         int64_t ldl) {
-  for (int64_t j0 = 0; j0 < k; j0 += TB) {
-    const int jb = (int)std::min<int64_t>(TB, k - j0);
+  SK_TRY(dense_attrs(c));
+  // X_j <- (X_j - X_<j L_j,<j^T) L_jj^{-T}, 64-wide blocks; L_jj^{-1} re-formed per block (cheap)
+  DBuf Wd;
+  SK_TRY(Wd.alloc(c, (size_t)TB2 * TB2 * sizeof(double)));
+  DBuf Lc;
+  SK_TRY(Lc.alloc(c, (size_t)TB2 * TB2 * sizeof(double)));
+  for (int64_t j0 = 0; j0 < k; j0 += TB2) {
+    const int jb = (int)std::min<int64_t>(TB2, k - j0);
     if (j0 > 0)
       SK_TRY(gemm(c, false, true, rows, jb, j0, -1.0, X, ldx, L + j0, ldl, 1.0, X + j0 * ldx, ldx));
-    const int blocks = (int)std::min<int64_t>(cdiv(rows, 128), 8LL * c->num_sms);
-    k_trsm_diag_lt<<<blocks, 128, 0, c->stream>>>(X + j0 * ldx, rows, ldx, jb, L + j0 + j0 * ldl, ldl,
-                                                   nullptr);
+    // W = L_jj^{-1}: L_jj is already a Cholesky factor; invert it as a (non-unit) lower matrix
+    SK_CUDA(c, cudaMemcpy2DAsync(Lc.p, TB2 * sizeof(double), L + j0 + j0 * ldl, ldl * sizeof(double),
+                                 jb * sizeof(double), jb, cudaMemcpyDeviceToDevice, c->stream));
+    k_diag_inv<2><<<1, 256, kDiagInvSmem, c->stream>>>(Lc.as<double>(), TB2, jb, Wd.as<double>(), TB2, 0, nullptr);
+    SK_TRY(launched(c));
+    k_right_tri_mul<true><<<(unsigned)cdiv(rows, 32), 256, kRtmSmem, c->stream>>>(X + j0 * ldx, rows, ldx, Wd.as<double>(),
+                                                                           TB2, jb);
     SK_TRY(launched(c));
   }
   return SK_OK;
@@ -231,16 +303,25 @@ sk_status trsm_right_lt(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t l
 
 sk_status trsm_right_l_unit(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L,
                             int64_t ldl) {
-  const int64_t nblk = cdiv(k, TB);
+  SK_TRY(dense_attrs(c));
+  // X_j <- (X_j - X_>j L_>j,j) L_jj^{-1} (unit lower), 64-wide blocks from the last
+  DBuf Wd, Lc;
+  SK_TRY(Wd.alloc(c, (size_t)TB2 * TB2 * sizeof(double)));
+  SK_TRY(Lc.alloc(c, (size_t)TB2 * TB2 * sizeof(double)));
+  const int64_t nblk = cdiv(k, TB2);
   for (int64_t b = nblk - 1; b >= 0; --b) {
-    const int64_t j0 = b * TB;
-    const int jb = (int)std::min<int64_t>(TB, k - j0);
+    const int64_t j0 = b * TB2;
+    const int jb = (int)std::min<int64_t>(TB2, k - j0);
     const int64_t j1 = j0 + jb;
     if (j1 < k)
       SK_TRY(gemm(c, false, false, rows, jb, k - j1, -1.0, X + j1 * ldx, ldx, L + j1 + j0 * ldl, ldl, 1.0,
                   X + j0 * ldx, ldx));
-    const int blocks = (int)std::min<int64_t>(cdiv(rows, 128), 8LL * c->num_sms);
-    k_trsm_diag_l_unit<<<blocks, 128, 0, c->stream>>>(X + j0 * ldx, rows, ldx, jb, L + j0 + j0 * ldl, ldl);
+    SK_CUDA(c, cudaMemcpy2DAsync(Lc.p, TB2 * sizeof(double), L + j0 + j0 * ldl, ldl * sizeof(double),
+                                 jb * sizeof(double), jb, cudaMemcpyDeviceToDevice, c->stream));
+    k_diag_inv<1><<<1, 256, kDiagInvSmem, c->stream>>>(Lc.as<double>(), TB2, jb, Wd.as<double>(), TB2, 0, nullptr);
+    SK_TRY(launched(c));
+    k_right_tri_mul<false><<<(unsigned)cdiv(rows, 32), 256, kRtmSmem, c->stream>>>(X + j0 * ldx, rows, ldx,
+                                                                            Wd.as<double>(), TB2, jb);
     SK_TRY(launched(c));
   }
   return SK_OK;
