@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       if (s >= s_end) break;
       const int t = p.c0 + s, par = s & 1;
       const bool probe = p.tprobe != nullptr && crank == 0 && tid == 0;
-      if (probe) p.tprobe[(int64_t)t * 8 + 0] = clock64();
+      if (probe) p.tprobe[(int64_t)t * 16 + 0] = clock64();
       // (A) local candidate of column s, owner copies its row (block coordinates)
       unsigned long long ckey = 0ull, csec = 0ull;
       long long cidx = 0x7fffffffffffffffLL;
@@ -715,6 +715,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       unsigned long long wk, ws;
       unsigned wi;
       warp_argmax(ckey, (unsigned)cidx, csec, wk, wi, ws, GAPS);
+      if (probe) p.tprobe[(int64_t)t * 16 + 8] = clock64();
       if (wk && (int)(wi & 31u) == lane) {
         double* dst = wrow + (size_t)(par * PNW + warp) * NB + cb;
 #pragma unroll
@@ -722,8 +723,8 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
           if ((int)wi == tid + PNT * r) {
             wlp[par * PNW + warp] = lprev[r];
 #pragma unroll
-            for (int q = i; q < NB; ++q)
-              if (cb + q < NB) dst[q] = v[r][q];
+            for (int q = (i & ~1); q + 1 < NB; q += 2)   // live columns, 16-byte stores (column i-1 rides along)
+              if (cb + q + 1 < NB) *reinterpret_cast<double2*>(dst + q) = make_double2(v[r][q], v[r][q + 1]);
           }
       }
       if (lane == 0) {
@@ -731,10 +732,13 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
         wci[par * PNW + warp] = wk ? (long long)(r0 + wi) : 0x7fffffffffffffffLL;
         wcs[par * PNW + warp] = ws;
       }
-      if (tid == 0) mbar_arm(mbar0 + 8 * par, (unsigned)(csize * MSG * 16));
-      if (probe) p.tprobe[(int64_t)t * 8 + 1] = clock64();
+      // message = header (2 chunks) + the row's live chunks (columns >= s, rounded to pairs)
+      const int jrow0 = 2 + (s >> 1);
+      const int nchunk = 2 + (MSG - jrow0);
+      if (tid == 0) mbar_arm(mbar0 + 8 * par, (unsigned)(csize * nchunk * 16));
+      if (probe) p.tprobe[(int64_t)t * 16 + 1] = clock64();
       asm volatile("bar.sync 1, %0;" ::"n"(PNT) : "memory");
-      if (probe) p.tprobe[(int64_t)t * 8 + 2] = clock64();
+      if (probe) p.tprobe[(int64_t)t * 16 + 2] = clock64();
       // (B) CTA candidate -> every CTA of the cluster
       {
         const unsigned long long k8 = lane < PNW ? wck[par * PNW + lane] : 0ull;
@@ -748,10 +752,12 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
         const long long gidx = bk ? r0 + (long long)bl : 0x7fffffffffffffffLL;
         const double* src = wrow + (size_t)(par * PNW + cw) * NB;
         const unsigned slot = mbox_u + (unsigned)(((par * MAXCS) + crank) * MSGD * 8);
+        if (probe) p.tprobe[(int64_t)t * 16 + 9] = clock64();
         for (int d = warp; d < csize; d += PNW) {
           const unsigned rslot = mapa(slot, (unsigned)d);
           const unsigned rbar = mapa(mbar0 + 8 * par, (unsigned)d);
-          for (int j = lane; j < MSG; j += 32) {
+          for (int jj = lane; jj < nchunk; jj += 32) {
+            const int j = jj < 2 ? jj : jrow0 + (jj - 2);
             unsigned long long x, y;
             if (j == 0) { x = bk; y = (unsigned long long)gidx; }
             else if (j == 1) { x = bs; y = (unsigned long long)__double_as_longlong(wlp[par * PNW + cw]); }
@@ -763,7 +769,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
           }
         }
       }
-      if (probe) p.tprobe[(int64_t)t * 8 + 3] = clock64();
+      if (probe) p.tprobe[(int64_t)t * 16 + 3] = clock64();
       // (C) deferred bulk update of step s-1: columns >= s+1 (window q with cb+q >= s+1)
       if (s > 0) {
         const double* uprev = ub + (size_t)(s - 1) * NB + cb;
@@ -771,16 +777,23 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
         for (int r = 0; r < RPT; ++r) {
           const double lm = lprev[r];
           if (lm != 0.0) {
+            if ((i + 1) & 1) {   // odd start column, then 16-byte pairs of U(s-1, :)
+              if (cb + i + 1 < NB) v[r][i + 1] = fma(-lm, uprev[i + 1], v[r][i + 1]);
+            }
 #pragma unroll
-            for (int q = i + 1; q < NB; ++q)
-              if (cb + q < NB) v[r][q] = fma(-lm, uprev[q], v[r][q]);
+            for (int q = (i + 2) & ~1; q + 1 < NB; q += 2)
+              if (cb + q + 1 < NB) {
+                const double2 u2 = *reinterpret_cast<const double2*>(uprev + q);
+                v[r][q] = fma(-lm, u2.x, v[r][q]);
+                v[r][q + 1] = fma(-lm, u2.y, v[r][q + 1]);
+              }
           }
         }
       }
-      if (probe) p.tprobe[(int64_t)t * 8 + 4] = clock64();
+      if (probe) p.tprobe[(int64_t)t * 16 + 4] = clock64();
       // (D) the cluster's winner and its row
       mbar_wait(mbar0 + 8 * par, (unsigned)((s >> 1) & 1));
-      if (probe) p.tprobe[(int64_t)t * 8 + 5] = clock64();
+      if (probe) p.tprobe[(int64_t)t * 16 + 5] = clock64();
       const double* box = mbox + (size_t)par * MAXCS * MSGD;
       const unsigned long long gk = lane < csize ? __double_as_longlong(box[lane * MSGD]) : 0ull;
       const long long gi8 = lane < csize ? __double_as_longlong(box[lane * MSGD + 1]) : 0x7fffffffffffffffLL;
@@ -816,7 +829,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
           gp[s] = (a1 - a2) / a1;
         }
       }
-      if (probe) p.tprobe[(int64_t)t * 8 + 6] = clock64();
+      if (probe) p.tprobe[(int64_t)t * 16 + 6] = clock64();
       // (E) multipliers, the next search column, the L column of step s
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
@@ -1023,8 +1036,8 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   DBuf Wb, Ub, stateb, maxb, Lfb, probeb;
   static const bool want_probe = [] { const char* e = std::getenv("SKEL_LUPP_PROBE"); return e && e[0] == '1'; }();
   if (want_probe) {
-    SK_TRY(probeb.alloc(c, (size_t)k * 8 * sizeof(long long)));
-    SK_CUDA(c, cudaMemsetAsync(probeb.p, 0, (size_t)k * 8 * sizeof(long long), c->stream));
+    SK_TRY(probeb.alloc(c, (size_t)k * 16 * sizeof(long long)));
+    SK_CUDA(c, cudaMemsetAsync(probeb.p, 0, (size_t)k * 16 * sizeof(long long), c->stream));
   }
   SK_TRY(Wb.alloc(c, (size_t)n * k * sizeof(double)));
   SK_TRY(Ub.alloc(c, (size_t)k * k * sizeof(double)));
@@ -1073,23 +1086,28 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     }
   }
   if (want_probe) {   // experiments: per-step phase durations (cycles) of CTA 0, thread 0, to stderr
-    std::vector<long long> h((size_t)k * 8);
+    std::vector<long long> h((size_t)k * 16);
     SK_CUDA(c, cudaMemcpyAsync(h.data(), probeb.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     SK_CUDA(c, cudaStreamSynchronize(c->stream));
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    // marks: 0 start, 8 warp argmax, 1 row copy+slot write, 2 CTA barrier, 9 CTA reduce, 3 sends,
+    // 4 bulk, 5 wait, 6 reduce+U, next 0
+    const int order[] = {0, 8, 1, 2, 9, 3, 4, 5, 6};
+    const char* names[] = {"argmax", "copy", "bar", "ctared", "send", "bulk", "wait", "red+U", "E+next"};
+    double acc[9] = {0};
     int cnt = 0;
     for (int64_t t = 1; t + 1 < k; ++t) {
-      const long long* a = &h[(size_t)t * 8];
-      const long long* b = &h[(size_t)(t + 1) * 8];
+      const long long* a = &h[(size_t)t * 16];
+      const long long* b = &h[(size_t)(t + 1) * 16];
       if (!a[0] || !b[0] || b[0] < a[0]) continue;
-      for (int j = 0; j < 6; ++j) acc[j] += (double)(a[j + 1] - a[j]);
-      acc[6] += (double)(b[0] - a[6]);
+      for (int j = 0; j < 8; ++j) acc[j] += (double)(a[order[j + 1]] - a[order[j]]);
+      acc[8] += (double)(b[0] - a[6]);
       ++cnt;
     }
-    if (cnt)
-      std::fprintf(stderr, "[lupp probe] n=%lld k=%lld steps=%d  A %.0f | bar %.0f | send %.0f | bulk %.0f | wait %.0f | reduce+U %.0f | E+next %.0f cycles\n",
-                   (long long)n, (long long)k, cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
-                   acc[5] / cnt, acc[6] / cnt);
+    if (cnt) {
+      std::fprintf(stderr, "[lupp probe] n=%lld k=%lld steps=%d ", (long long)n, (long long)k, cnt);
+      for (int j = 0; j < 9; ++j) std::fprintf(stderr, " %s %.0f", names[j], acc[j] / cnt);
+      std::fprintf(stderr, " cycles\n");
+    }
   }
   if (U) {
     const int blocks = (int)std::min<int64_t>(cdiv(k * k, 256), 4LL * c->num_sms);
