@@ -101,6 +101,17 @@ sk_status sk_sketch(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t 
                     int64_t l, sk_embedding emb, int32_t zeta, uint64_t seed,
                     double* X, int64_t ldx);
 
+/* ---- S1 with power iterations (Rand-LUPP-1piter) ----
+ * X = Omega (A^T A)^q, the plain power-iteration row-space approximator of eq:def_power_iter
+ * with Omega an l x n embedding drawn exactly like sk_sketch's Gamma but over the
+ * column index of A (R1: Omega(r, j) from (seed, r, j)).  q = 0 is sk_sketch (X = Gamma A,
+ * Gamma l x m).  Computed as T = Omega A^T, then X = T A, q - 1 times T = X A^T, X = T A
+ * (2q passes over A).  A m x n column-major; X l x n row-major (ldx >= n).  Requires 1 <= l <= n
+ * for q >= 1, 0 <= q <= 64.  Not orthogonalised: the paper notes the plain form is unstable for
+ * ill-conditioned A and q > 1. */
+sk_status sk_sketch_power(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                          sk_embedding emb, int32_t zeta, uint64_t seed, int32_t q, double* X, int64_t ldx);
+
 /* ---- S2: column skeletons by LUPP on the sketch  (eq:def_LUPP; Alg. 2 line 3) ----
  * k-step LU with partial pivoting on the n x k panel X^T(:, 0:k) = rows 0..k-1
  * of X (R5: only those rows can influence the first k pivots).  Step t picks

@@ -23,3 +23,22 @@ def sketch(A, l, kind="gaussian", seed=0, zeta=8):
 def sketch_columns(A_cols, l, kind="gaussian", seed=0, zeta=8):
     """X[:, J] for a sample of columns A[:, J] (same Gamma; used for full-size spot checks)."""
     return sketch(A_cols, l, kind, seed, zeta)
+
+
+def sketch_power(A, l, kind="gaussian", seed=0, q=1, zeta=8):
+    """Row-space approximator with q plain power iterations, eq:def_power_iter:
+
+        X = Omega (A^T A)^q,   Omega l x n drawn like Gamma (oracle.omega) over the n index.
+
+    q = 0 is the row sketch X = Gamma A (Gamma l x m).  Written out literally: form the
+    Gram matrix A^T A and apply it q times (the paper's O(T_s + (2q-1) nnz(A) l) evaluation
+    order is the GPU's business; the value is the same)."""
+    A = np.asarray(A, dtype=np.float64)
+    if q == 0:
+        return sketch(A, l, kind, seed, zeta)
+    n = A.shape[1]
+    X = omega.embedding(kind, seed, l, n, zeta)
+    G = A.T @ A
+    for _ in range(q):
+        X = X @ G
+    return X

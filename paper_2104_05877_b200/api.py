@@ -91,6 +91,17 @@ def sketch(A, l, embedding="gaussian", seed=0, zeta=8, out=None):
     return X
 
 
+def sketch_power(A, l, embedding="gaussian", seed=0, q=1, zeta=8, out=None):
+    """X = Omega (A^T A)^q (eq:def_power_iter; Rand-LUPP-1piter for q = 1)."""
+    lda = _colmajor(A, "A")
+    m, n = A.shape
+    X = out if out is not None else torch.empty((l, n), dtype=torch.float64, device=A.device)
+    h = context(A.device.index)
+    _check(lib().sk_sketch_power(h, _ptr(A), m, n, lda, l, _EMB[embedding], zeta, seed & (2**64 - 1), q, _ptr(X),
+                                 max(X.stride(0), n)), h)
+    return X
+
+
 def select_cols(X, k, want_factors=True, want_gaps=False, check=True):
     """Column LUPP on the sketch (eq:def_LUPP, Alg. 2 line 3). Returns (Js, Lf, U, gaps)."""
     l, n = X.shape

@@ -128,6 +128,20 @@ sk_status sk_sketch(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t ld
   return fail(c, SK_E_ARG, "sk_sketch: unknown embedding");
 }
 
+sk_status sk_sketch_power(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                          sk_embedding emb, int32_t zeta, uint64_t seed, int32_t q, double* X, int64_t ldx) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, A && X, "sk_sketch_power: NULL A or X");
+  SK_ARG(c, q >= 0 && q <= 64, "sk_sketch_power: 0 <= q <= 64");
+  if (q == 0) return sk_sketch(c, A, m, n, lda, l, emb, zeta, seed, X, ldx);
+  SK_ARG(c, m >= 1 && n >= 1 && l >= 1 && l <= n, "sk_sketch_power: need 1 <= l <= n, m >= 1");
+  SK_ARG(c, lda >= m && ldx >= n, "sk_sketch_power: lda >= m and ldx >= n required");
+  SK_ARG(c, emb == SK_EMB_GAUSSIAN || (zeta >= 2 && zeta <= l && zeta <= 64), "sk_sketch_power: bad zeta");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  return sketch_power(c, A, m, n, lda, l, (int)emb, zeta, seed, q, X, ldx);
+}
+
 sk_status sk_select_cols(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, int64_t k,
                          int64_t* Js, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps,
                          int64_t* info) {

@@ -215,6 +215,22 @@ __global__ void __launch_bounds__(256) k_right_tri_mul(double* X, int64_t rows, 
     }
   }
 }
+// Out (cols x rows, ldout) = In^T for In rows x cols (ldin), both column-major; 32 x 32 tiles.
+__global__ void k_transpose_any(const double* In, int64_t rows, int64_t cols, int64_t ldin, double* Out,
+                                int64_t ldout) {
+  __shared__ double tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x, j = j0 + r;
+    if (i < rows && j < cols) tile[r][threadIdx.x] = In[i + j * ldin];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t j = j0 + threadIdx.x, i = i0 + r;
+    if (i < rows && j < cols) Out[j + i * ldout] = tile[threadIdx.x][r];
+  }
+}
+
 constexpr size_t kDiagInvSmem = 2 * TB2 * (TB2 + 1) * sizeof(double);
 constexpr size_t kRtmSmem = (TB2 + 32) * (TB2 + 1) * sizeof(double);
 
@@ -235,6 +251,15 @@ sk_status dense_attrs(sk_ctx* c) {
 sk_status gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t lda, const int64_t* J, int64_t k,
                       double* C, int64_t ldc) {
   return gather_cols_shard(c, A, m, lda, 0, INT64_MAX, J, k, C, ldc);
+}
+
+sk_status transpose(sk_ctx* c, const double* In, int64_t rows, int64_t cols, int64_t ldin, double* Out,
+                    int64_t ldout) {
+  if (rows == 0 || cols == 0) return SK_OK;
+  const dim3 g((unsigned)cdiv(rows, 32), (unsigned)cdiv(cols, 32));
+  if (g.y > 65535) return fail(c, SK_E_ARG, "transpose: too many columns");
+  k_transpose_any<<<g, dim3(32, 8), 0, c->stream>>>(In, rows, cols, ldin, Out, ldout);
+  return launched(c);
 }
 
 sk_status gather_cols_shard(sk_ctx* c, const double* A, int64_t m, int64_t lda, int64_t col0, int64_t ncols,

@@ -22,6 +22,11 @@ sk_status sketch_dense(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t
 sk_status sketch_sparse(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
                         int zeta, uint64_t seed, double* X, int64_t ldx);
 
+// X = Omega (A^T A)^q (eq:def_power_iter), Omega l x n drawn like the sketch's Gamma
+// over the n index; q >= 1.  X l x n row-major (ldx >= n).
+sk_status sketch_power(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
+                       int zeta, uint64_t seed, int q, double* X, int64_t ldx);
+
 // ---------------------------------------------------------------- LUPP (lupp.cu)
 // k-step swap-free LUPP on the rows of an n x k panel.  The panel is given either
 // as rows 0..k-1 of a row-major X (row_major = true, ld = ldx) or as a column-major
@@ -39,6 +44,9 @@ sk_status cpqr(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, in
 // ---------------------------------------------------------------- small dense kernels (dense.cu)
 sk_status gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t lda, const int64_t* J,
                       int64_t k, double* C, int64_t ldc);
+// Out (cols x rows, ldout) = In^T, In rows x cols (ldin), column-major.
+sk_status transpose(sk_ctx* c, const double* In, int64_t rows, int64_t cols, int64_t ldin, double* Out,
+                    int64_t ldout);
 // Shard-aware gather: C(:, t) = A(:, J[t] - col0) if the column is in [col0, col0 + ncols), else 0.
 sk_status gather_cols_shard(sk_ctx* c, const double* A, int64_t m, int64_t lda, int64_t col0, int64_t ncols,
                             const int64_t* J, int64_t k, double* C, int64_t ldc);

@@ -64,6 +64,30 @@ def test_sketch_dense_odd_lda():
     assert rel_fro(X, o_sketch.sketch(A, l, "gaussian", 11)) <= 1e-12
 
 
+# ------------------------------------------------------------------ S1 with power iterations (8(f))
+@pytest.mark.parametrize("m,n,l,q,seed", [(256, 256, 40, 1, 2001), (700, 333, 37, 1, 5), (300, 200, 26, 2, 9)])
+def test_sketch_power_parity(m, n, l, q, seed):
+    A = rand_mat(m, n, seed, 0.9)
+    X = sk.sketch_power(dev_f(A), l, "gaussian", seed, q).cpu().numpy()
+    ref = o_sketch.sketch_power(A, l, "gaussian", seed, q)
+    assert rel_fro(X, ref) <= 1e-12
+
+
+def test_rand_lupp_1piter_c1():
+    """Rand-LUPP-1piter on C1: pivots identical to the oracle, residual within tolerance."""
+    A, sigma = make_c1(seed=1001)
+    Ad = dev_f(A)
+    k, l = 20, 40
+    X = sk.sketch_power(Ad, l, "gaussian", 2001, 1)
+    Js, _, _, _ = sk.select_cols(X, k)
+    Xo = o_sketch.sketch_power(A, l, "gaussian", 2001, 1)
+    (piv, _, _, _), _ = lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(Xo, k, f))
+    r, nA = sk.residual(Ad, Js, None, "col_id")
+    ro, nAo = o_res.residual(A, piv, kind="col_id")
+    assert abs(r - ro) <= 1e-9 * ro + 4 * U * nAo
+    assert r >= o_res.optimal_error(sigma, k) * (1 - 1e-12)
+
+
 # ------------------------------------------------------------------ S1' sparse sketch
 @pytest.mark.parametrize("m,n,l,zeta,seed", [
     (1000, 100, 60, 8, 2003),

@@ -62,6 +62,25 @@ def test_sparse_sketch_is_signed_row_sums():
     np.testing.assert_allclose(sketch.sketch(A, l, "sparse_sign", 3, z), X, atol=1e-13)
 
 
+def test_power_sketch_closed_forms():
+    # eq:def_power_iter: X = Omega (A^T A)^q.  (a) A with orthonormal columns scaled by s:
+    # A^T A = diag(s^2) exactly -> X = Omega diag(s^(2q)) column-wise; (b) A = I -> X = Omega;
+    # (c) q = 0 is the row sketch; (d) rank-r A -> rank-r X.
+    rng = np.random.default_rng(11)
+    m, n, l = 40, 12, 5
+    Q, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    s = np.linspace(0.5, 2.0, n)
+    A = Q * s
+    Om = omega.gaussian(7, l, n)
+    for q in (1, 2):
+        np.testing.assert_allclose(sketch.sketch_power(A, l, "gaussian", 7, q), Om * s ** (2 * q), rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(sketch.sketch_power(np.eye(n), l, "gaussian", 7, 1), Om, rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(sketch.sketch_power(A, l, "gaussian", 7, 0), sketch.sketch(A, l, "gaussian", 7))
+    Ar = make_lowrank(m, n, np.array([3.0, 1.0, 0.2]), rng)
+    sv = np.linalg.svd(sketch.sketch_power(Ar, 6, "gaussian", 3, 1), compute_uv=False)
+    assert sv[3] < 1e-12 * sv[0] and sv[2] > 1e-6 * sv[0]
+
+
 # ----------------------------------------------------------------------------- LUPP
 def test_lupp_spec_2x2_case():
     # X = [[4,2],[1,3]] -> pivots [1,2] (1-based), L_l = [[4,0],[1,2.5]], R = [[1,.5],[0,1]].
