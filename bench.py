@@ -34,13 +34,22 @@ FP64_PEAK_TFLOPS = 37.13   # measured DMMA issue ceiling on this pool's B200 (pr
 L2_FLUSH_BYTES = 512 << 20
 
 
+def hbm_peak_gbs():
+    """(GB/s, source): MEASURED_PEAKS.json's copy bandwidth, else the profiling guide's fallback."""
+    try:
+        v = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--k", type=int, default=512)
+    ap.add_argument("--k", type=int, default=None, help="default: C1 20, C2 512, C3 500, C4 200, C5 1000")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -51,11 +60,15 @@ def parse():
 def workload(args):
     from inputs import CONFIGS
     cfg = CONFIGS[args.config]
+    if args.k is None:
+        args.k = {"C1": 20, "C2": 512, "C3": 500, "C4": 200, "C5": 1000}[args.config]
     k = args.k
     l = cfg["l"](k)
     seed = cfg["sk_seed"] + (k if args.config in ("C2", "C4") else 0)
     desc = {
         "C2": f"C2: A 4096x4096 FP64 = U diag(10^(-i/50)) V^T (Haar), Gaussian Omega, k={k}, l={l}",
+        "C5": f"C5: A 131072x65536 FP64 (68.7 GB) = U diag(i^-1.5) V^T, U,V products of 64 Householder "
+              f"reflectors, built on the device; Gaussian Omega, k={k}, l={l}",
     }.get(args.config, f"{args.config} k={k} l={l}")
     if getattr(args, "piter", 0):
         desc += f", {args.piter} plain power iteration(s) X = Omega (A^T A)^q (Rand-LUPP-{args.piter}piter)"
@@ -303,10 +316,17 @@ def main():
     stream = torch.cuda.Stream(dev)
 
     cfg, k, l, seed, desc = workload(args)
-    A_np, sigma = make_input(args, cfg)
-    m, n = A_np.shape
+    emb = cfg["emb"]
     with torch.cuda.stream(stream):
-        A = sk.fortran(torch.from_numpy(np.ascontiguousarray(A_np)).to(dev))
+        if args.config == "C5":          # 68.7 GB: built on the device (inputs/c5.py), no host copy
+            from inputs.c5 import build_on_device
+            A, sigma = build_on_device(dev)
+            A_np = None
+            m, n = A.shape
+        else:
+            A_np, sigma = make_input(args, cfg)
+            m, n = A_np.shape
+            A = sk.fortran(torch.from_numpy(np.ascontiguousarray(A_np)).to(dev))
         flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     torch.cuda.synchronize(dev)
 
@@ -316,7 +336,8 @@ def main():
         """One pass of the hot path; record(name, start_event, end_event)."""
         e = [ev() for _ in range(6)]
         e[0].record(stream)
-        X = sk.sketch(A, l, "gaussian", seed) if args.piter == 0 else sk.sketch_power(A, l, "gaussian", seed, args.piter)
+        X = (sk.sketch(A, l, emb, seed, cfg.get("zeta", 8)) if args.piter == 0
+             else sk.sketch_power(A, l, emb, seed, args.piter, cfg.get("zeta", 8)))
         e[1].record(stream)
         Js, Lf, _, _ = sk.select_cols(X, k, check=False)
         e[2].record(stream)
@@ -367,10 +388,8 @@ def main():
     from oracle.residual import optimal_error  # closed form sum_{i>k} sigma_i^2 (Eckart-Young)
     opt = optimal_error(sigma, k)
 
-    # roofline of the dominant kernel: the dense DMMA sketch (one launch per call)
+    # roofline of the dominant kernel of the selection: the sketch (one launch per call)
     sk_ms = statistics.mean(stage_ms["sketch"])
-    flops = 2.0 * l * m * n * max(1, 2 * args.piter)   # q = 0: one pass; q >= 1: 2q passes (Omega A^T, then A)
-    achieved = flops / (sk_ms * 1e-3) / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", "round1", "sketch_dram_bytes.json")
     if os.path.exists(tf):
@@ -378,14 +397,25 @@ def main():
             traffic = json.load(open(tf)).get(f"{args.config}_k{k}")
         except Exception:
             traffic = None
-    roofline = {"kernel": "k_sketch_tma", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "peak_source": "measured FP64 DMMA ceiling (tools/microbench/fp64_pipes.cu); "
-                               "MEASURED_PEAKS.json has no FP64 entry; cuBLAS DGEMM measured 35.5"}
+    if emb == "sparse_sign":
+        # HBM bound: A read once + X written (Omega generated, 0 bytes), SURVEY 8(d)
+        nbytes = 8.0 * (m * n + l * n)
+        achieved = nbytes / (sk_ms * 1e-3) / 1e9
+        peak = hbm_peak_gbs()
+        roofline = {"kernel": "k_sketch_sparse3", "bound": "hbm", "achieved": achieved, "peak": peak[0],
+                    "unit": "GB/s", "frac": achieved / peak[0], "traffic": traffic, "peak_source": peak[1]}
+    else:
+        flops = 2.0 * l * m * n * max(1, 2 * args.piter)   # q = 0: one pass; q >= 1: 2q passes (Omega A^T, then A)
+        achieved = flops / (sk_ms * 1e-3) / 1e12
+        roofline = {"kernel": "k_sketch_tma", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                    "peak_source": "measured FP64 DMMA ceiling (tools/microbench/fp64_pipes.cu, "
+                                   "profiles/round1/fp64_pipes.txt); MEASURED_PEAKS.json has no FP64 entry; "
+                                   "cuBLAS DGEMM measured 35.5"}
 
     # end to end through the public API with host buffers (Algorithm 2 entry point)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and A_np is not None:
         A_host = torch.from_numpy(np.ascontiguousarray(A_np.T)).pin_memory().t()
         with torch.cuda.stream(stream):
             for _ in range(2):
@@ -407,7 +437,7 @@ def main():
                "api": "sk_rand_lupp (host A, pinned) -> Js on host"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and A_np is not None:
         cores, model = cpu_info()
         t0 = time.perf_counter()
         piv_o = oracle_selection(A_np, k, l, seed)
@@ -427,7 +457,7 @@ def main():
                        "l2": "flushed: 512 MiB overwrite between timed steps (untimed)",
                        "parallelism": "replicas" if world > 1 else "1 GPU"},
             "stages_ms": {nm: statistics.mean(v) for nm, v in stage_ms.items()},
-            "sketch_tflops": achieved,
+            "sketch_rate": {"value": achieved, "unit": roofline["unit"]},
             "residual": {"col_id_fro": res, "normA_fro": nA, "opt_fro": opt, "ratio": res / opt if opt > 0 else None},
             "cpqr_overlap": int(len(set(Js.cpu().tolist()) & set(Jc.cpu().tolist()))),
             "roofline": roofline,

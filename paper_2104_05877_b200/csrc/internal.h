@@ -37,6 +37,9 @@ sk_status lupp(sk_ctx* c, const double* P, bool row_major, int64_t n, int64_t k,
                int64_t* Js, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps,
                int64_t* status_dev);
 
+// Tallest panel the cluster LUPP handles (rows).
+int64_t lupp_max_rows(sk_ctx* c);
+
 // ---------------------------------------------------------------- CPQR (cpqr.cu)
 sk_status cpqr(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, int64_t k,
                int64_t* Js, double* R, int64_t ldr, int64_t* status_dev);

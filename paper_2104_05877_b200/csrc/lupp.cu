@@ -995,6 +995,11 @@ ClusterCfg pick_cluster(sk_ctx* c) {
 
 }  // namespace
 
+int64_t lupp_max_rows(sk_ctx* c) {
+  const ClusterCfg cfg = pick_cluster(c);
+  return cfg.ok ? (int64_t)cfg.cs * 16 * PNT : 0;
+}
+
 sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t k, int64_t ld,
                int64_t* Js, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps,
                int64_t* status_dev) {

@@ -15,8 +15,35 @@
 
 namespace skel {
 
+// G <- G + s I with s = 11 (rows k + k (k + 1)) u trace(G)  (the shift of shifted CholeskyQR3,
+// Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020: makes the first Cholesky succeed for
+// cond(C) up to ~u^-1, after which CholeskyQR2 restores orthogonality).
+__global__ void k_add_shift(double* G, int64_t k, int64_t ld, int64_t rows) {
+  __shared__ double red[34];
+  double t = 0.0;
+  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) t += G[i + i * ld];
+  t = dev::block_sum(t, red);
+  const double s = 11.0 * ((double)rows * (double)k + (double)k * (double)(k + 1)) * 1.1102230246251565e-16 * t;
+  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) G[i + i * ld] += s;
+}
+
+// Columns of C whose row LUPP does not fit one cluster (rows > 16 x 256): shifted CholeskyQR3.
+static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q,
+                                       int64_t* status_dev) {
+  SK_CUDA(c, cudaMemcpyAsync(Q, C, (size_t)rows * k * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  DBuf G;
+  SK_TRY(G.alloc(c, (size_t)k * k * sizeof(double)));
+  SK_TRY(gemm(c, true, false, k, k, rows, 1.0, Q, rows, Q, rows, 0.0, G.as<double>(), k));
+  k_add_shift<<<1, 1024, 0, c->stream>>>(G.as<double>(), k, k, rows);
+  SK_TRY(launched(c));
+  SK_TRY(potrf_lower(c, G.as<double>(), k, k, status_dev));
+  SK_TRY(trsm_right_lt(c, Q, rows, k, rows, G.as<double>(), k));
+  return cholqr2(c, Q, rows, k, rows, status_dev);
+}
+
 static sk_status basis_from_cols(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q,
                                  int64_t* status_dev) {
+  if (rows > lupp_max_rows(c)) return basis_shifted_cholqr3(c, C, rows, k, Q, status_dev);
   DBuf piv;
   SK_TRY(piv.alloc(c, (size_t)k * sizeof(int64_t)));
   SK_TRY(lupp(c, C, false, rows, k, rows, piv.as<int64_t>(), Q, rows, nullptr, 0, nullptr, status_dev));

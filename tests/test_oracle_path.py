@@ -316,6 +316,19 @@ def test_brute_force_subset_bounds():
         assert residual.residual(A, piv, kind="col_id")[0] >= best * (1 - 1e-12)
 
 
+def test_c5_generator_wy_equals_reflectors_small():
+    # C5's compact-WY construction (the GPU build path) equals the reflector-by-reflector
+    # definition, and the spectrum is exactly sigma (small instance of the same code).
+    from inputs import c5
+    Y, Yp, s = c5.factors(7, 300, 200, 8)
+    W, Z = c5.wy_operands(Y, Yp, s)
+    A = -(Y @ W) - Z @ Yp.T
+    A[np.arange(200), np.arange(200)] += s
+    cols = np.stack([c5.column_by_reflectors(j, Y, Yp, s) for j in range(200)], 1)
+    np.testing.assert_allclose(A, cols, atol=1e-14)
+    np.testing.assert_allclose(np.linalg.svd(A, compute_uv=False), s, atol=1e-14)
+
+
 def test_generators_spectra():
     A, sigma = make_c1(seed=3, m=64, n=64)
     s = np.linalg.svd(A, compute_uv=False)
