@@ -101,6 +101,15 @@ sk_status sk_sketch(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t 
                     int64_t l, sk_embedding emb, int32_t zeta, uint64_t seed,
                     double* X, int64_t ldx);
 
+/* ---- column sketch for streaming two-sided selection (Algorithm 3) ----
+ * Y = A Omega^T with Omega an l x n embedding drawn like sk_sketch's Gamma over the column index
+ * of A (an independent draw from X = Gamma A when the seed differs, Alg. 3 line 1).  Row-wise
+ * LUPP on Y (sk_select_rows) gives I_s without forming C (Alg. 3 line 4).  A m x n column-major;
+ * Y m x l column-major (ldy >= m).  Requires 1 <= l <= n.  (Computed as the row sketch of A^T:
+ * one transpose pass plus one sketch pass; the fused single-pass dual sketch is future work.) */
+sk_status sk_sketch_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                         sk_embedding emb, int32_t zeta, uint64_t seed, double* Y, int64_t ldy);
+
 /* ---- S1 with power iterations (Rand-LUPP-1piter) ----
  * X = Omega (A^T A)^q, the plain power-iteration row-space approximator of eq:def_power_iter
  * with Omega an l x n embedding drawn exactly like sk_sketch's Gamma but over the

@@ -42,3 +42,11 @@ def sketch_power(A, l, kind="gaussian", seed=0, q=1, zeta=8):
     for _ in range(q):
         X = X @ G
     return X
+
+
+def sketch_cols(A, l, kind="gaussian", seed=0, zeta=8):
+    """Column sketch Y = A Omega^T of Algorithm 3 line 2, Omega l x n drawn like Gamma
+    (oracle.omega) over the column index of A."""
+    A = np.asarray(A, dtype=np.float64)
+    Om = omega.embedding(kind, seed, l, A.shape[1], zeta)
+    return A @ Om.T

@@ -18,6 +18,7 @@ _SIGS = {
     "sk_create": [ctypes.POINTER(c_dp), c_int, c_dp],
     "sk_set_stream": [c_dp, c_dp],
     "sk_sketch": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64, c_dp, c_i64],
+    "sk_sketch_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64, c_dp, c_i64],
     "sk_sketch_power": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64,
                         ctypes.c_int32, c_dp, c_i64],
     "sk_select_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, c_dp, c_i64, c_dp,

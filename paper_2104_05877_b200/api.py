@@ -91,6 +91,27 @@ def sketch(A, l, embedding="gaussian", seed=0, zeta=8, out=None):
     return X
 
 
+def sketch_cols(A, l, embedding="gaussian", seed=0, zeta=8):
+    """Y = A Omega^T (m x l, column-major), the column sketch of Algorithm 3."""
+    lda = _colmajor(A, "A")
+    m, n = A.shape
+    Y = torch.empty((l, m), dtype=torch.float64, device=A.device).t()
+    h = context(A.device.index)
+    _check(lib().sk_sketch_cols(h, _ptr(A), m, n, lda, l, _EMB[embedding], zeta, seed & (2**64 - 1), _ptr(Y), m), h)
+    return Y
+
+
+def stream_select(A, k, l=None, embedding="gaussian", seed_x=0, seed_y=1, zeta=8):
+    """Algorithm 3 (streaming two-sided selection): X = Gamma A and Y = A Omega^T from
+    independent embeddings, column LUPP on X -> J_s, row LUPP on Y -> I_s.  Returns (Js, Is)."""
+    l = k + 10 if l is None else l
+    X = sketch(A, l, embedding, seed_x, zeta)
+    Y = sketch_cols(A, l, embedding, seed_y, zeta)
+    Js, _, _, _ = select_cols(X, k, want_factors=False)
+    Is, _, _, _ = select_rows(Y, k, want_factors=False)
+    return Js, Is
+
+
 def sketch_power(A, l, embedding="gaussian", seed=0, q=1, zeta=8, out=None):
     """X = Omega (A^T A)^q (eq:def_power_iter; Rand-LUPP-1piter for q = 1)."""
     lda = _colmajor(A, "A")

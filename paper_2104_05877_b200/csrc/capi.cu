@@ -128,6 +128,18 @@ sk_status sk_sketch(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t ld
   return fail(c, SK_E_ARG, "sk_sketch: unknown embedding");
 }
 
+sk_status sk_sketch_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                         sk_embedding emb, int32_t zeta, uint64_t seed, double* Y, int64_t ldy) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, A && Y, "sk_sketch_cols: NULL A or Y");
+  SK_ARG(c, m >= 1 && n >= 1 && l >= 1 && l <= n, "sk_sketch_cols: need 1 <= l <= n, m >= 1");
+  SK_ARG(c, lda >= m && ldy >= m, "sk_sketch_cols: lda >= m and ldy >= m required");
+  SK_ARG(c, emb == SK_EMB_GAUSSIAN || (zeta >= 2 && zeta <= l && zeta <= 64), "sk_sketch_cols: bad zeta");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  return sketch_cols(c, A, m, n, lda, l, (int)emb, zeta, seed, Y, ldy);
+}
+
 sk_status sk_sketch_power(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
                           sk_embedding emb, int32_t zeta, uint64_t seed, int32_t q, double* X, int64_t ldx) {
   if (!c) return SK_E_ARG;

@@ -22,6 +22,9 @@ sk_status sketch_dense(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t
 sk_status sketch_sparse(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
                         int zeta, uint64_t seed, double* X, int64_t ldx);
 
+// Y = A Omega^T (m x l col-major, ldy >= m), Omega l x n (Alg. 3 column sketch).
+sk_status sketch_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
+                      int zeta, uint64_t seed, double* Y, int64_t ldy);
 // X = Omega (A^T A)^q (eq:def_power_iter), Omega l x n drawn like the sketch's Gamma
 // over the n index; q >= 1.  X l x n row-major (ldx >= n).
 sk_status sketch_power(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,

@@ -88,6 +88,27 @@ def test_rand_lupp_1piter_c1():
     assert r >= o_res.optimal_error(sigma, k) * (1 - 1e-12)
 
 
+# ------------------------------------------------------------------ Algorithm 3 (streaming two-sided selection, 8(f))
+@pytest.mark.parametrize("m,n,l,emb,seed", [(256, 256, 40, "gaussian", 3), (600, 333, 37, "gaussian", 4),
+                                             (500, 300, 30, "sparse_sign", 5)])
+def test_sketch_cols_parity(m, n, l, emb, seed):
+    A = rand_mat(m, n, seed)
+    Y = sk.sketch_cols(dev_f(A), l, emb, seed).cpu().numpy()
+    assert rel_fro(Y, o_sketch.sketch_cols(A, l, emb, seed)) <= 1e-12
+
+
+def test_stream_select_alg3_c1():
+    A, sigma = make_c1(seed=1001)
+    k, l = 20, 40
+    Js, Is = sk.stream_select(dev_f(A), k, l, seed_x=2001, seed_y=3001)
+    Xo = o_sketch.sketch(A, l, "gaussian", 2001)
+    Yo = o_sketch.sketch_cols(A, l, "gaussian", 3001)
+    lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(Xo, k, f))
+    lupp_parity(Is.cpu().numpy(), lambda f: o_lupp.select_rows(Yo, k, f))
+    r, nA = sk.residual(dev_f(A), Js, Is, "cur")
+    assert r >= o_res.optimal_error(sigma, k) * (1 - 1e-12)
+
+
 # ------------------------------------------------------------------ S1' sparse sketch
 @pytest.mark.parametrize("m,n,l,zeta,seed", [
     (1000, 100, 60, 8, 2003),

@@ -81,6 +81,23 @@ def test_power_sketch_closed_forms():
     assert sv[3] < 1e-12 * sv[0] and sv[2] > 1e-6 * sv[0]
 
 
+def test_streaming_alg3_closed_forms_and_exact_rank_cur():
+    # Alg. 3: Y = A Omega^T.  A = I -> Y = Omega^T.  On an exact rank-k A, column LUPP on
+    # X = Gamma A and row LUPP on Y = A Omega^T (independent draws, one pass) give skeletons whose
+    # stable CUR reproduces A (residual at rounding level): both sketches capture range and co-range.
+    Om = omega.gaussian(5, 6, 9)
+    np.testing.assert_array_equal(sketch.sketch_cols(np.eye(9), 6, "gaussian", 5), Om.T)
+    rng = np.random.default_rng(3)
+    A = make_lowrank(120, 90, np.array([4.0, 2.0, 1.0, 0.5, 0.1]), rng)
+    k, l = 5, 9
+    X = sketch.sketch(A, l, "gaussian", 11)
+    Y = sketch.sketch_cols(A, l, "gaussian", 12)
+    piv, _, _, _ = lupp.select_cols(X, k)
+    ipiv, _, _, _ = lupp.select_rows(Y, k)
+    r, nA = residual.residual(A, piv, ipiv, kind="cur")
+    assert r <= 1e-12 * nA
+
+
 # ----------------------------------------------------------------------------- LUPP
 def test_lupp_spec_2x2_case():
     # X = [[4,2],[1,3]] -> pivots [1,2] (1-based), L_l = [[4,0],[1,2.5]], R = [[1,.5],[0,1]].
