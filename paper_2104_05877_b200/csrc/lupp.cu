@@ -716,17 +716,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       unsigned wi;
       warp_argmax(ckey, (unsigned)cidx, csec, wk, wi, ws, GAPS);
       if (probe) p.tprobe[(int64_t)t * 16 + 8] = clock64();
-      if (wk && (int)(wi & 31u) == lane) {
-        double* dst = wrow + (size_t)(par * PNW + warp) * NB + cb;
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-          if ((int)wi == tid + PNT * r) {
-            wlp[par * PNW + warp] = lprev[r];
-#pragma unroll
-            for (int q = (i & ~1); q + 1 < NB; q += 2)   // live columns, 16-byte stores (column i-1 rides along)
-              if (cb + q + 1 < NB) *reinterpret_cast<double2*>(dst + q) = make_double2(v[r][q], v[r][q + 1]);
-          }
-      }
+      if (probe) p.tprobe[(int64_t)t * 16 + 10] = clock64();
       if (lane == 0) {
         wck[par * PNW + warp] = wk;
         wci[par * PNW + warp] = wk ? (long long)(r0 + wi) : 0x7fffffffffffffffLL;
@@ -750,9 +740,24 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
         const unsigned wl = __ballot_sync(0xffffffffu, k8 == bk && k8 != 0ull && (unsigned)(i8 - r0) == bl);
         const int cw = wl ? __ffs(wl) - 1 : 0;
         const long long gidx = bk ? r0 + (long long)bl : 0x7fffffffffffffffLL;
+        if (probe) p.tprobe[(int64_t)t * 16 + 9] = clock64();
+        // only the CTA-winning warp's owner lane copies its row (one warp's 16-byte stores instead
+        // of all 8 warps'), then every warp sends to its 2 destination CTAs
+        if (warp == cw && bk && (int)(bl & 31u) == lane) {
+          double* dst = wrow + (size_t)(par * PNW + cw) * NB + cb;
+#pragma unroll
+          for (int r = 0; r < RPT; ++r)
+            if ((int)bl == tid + PNT * r) {
+              wlp[par * PNW + cw] = lprev[r];
+#pragma unroll
+              for (int q = (i & ~1); q + 1 < NB; q += 2)   // live columns, 16-byte stores
+                if (cb + q + 1 < NB) *reinterpret_cast<double2*>(dst + q) = make_double2(v[r][q], v[r][q + 1]);
+            }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(PNT) : "memory");
         const double* src = wrow + (size_t)(par * PNW + cw) * NB;
         const unsigned slot = mbox_u + (unsigned)(((par * MAXCS) + crank) * MSGD * 8);
-        if (probe) p.tprobe[(int64_t)t * 16 + 9] = clock64();
+        const double lpw = wlp[par * PNW + cw];
         for (int d = warp; d < csize; d += PNW) {
           const unsigned rslot = mapa(slot, (unsigned)d);
           const unsigned rbar = mapa(mbar0 + 8 * par, (unsigned)d);
@@ -760,7 +765,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
             const int j = jj < 2 ? jj : jrow0 + (jj - 2);
             unsigned long long x, y;
             if (j == 0) { x = bk; y = (unsigned long long)gidx; }
-            else if (j == 1) { x = bs; y = (unsigned long long)__double_as_longlong(wlp[par * PNW + cw]); }
+            else if (j == 1) { x = bs; y = (unsigned long long)__double_as_longlong(lpw); }
             else {
               x = (unsigned long long)__double_as_longlong(src[2 * (j - 2)]);
               y = (unsigned long long)__double_as_longlong(src[2 * (j - 2) + 1]);
@@ -1096,21 +1101,21 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     SK_CUDA(c, cudaStreamSynchronize(c->stream));
     // marks: 0 start, 8 warp argmax, 1 row copy+slot write, 2 CTA barrier, 9 CTA reduce, 3 sends,
     // 4 bulk, 5 wait, 6 reduce+U, next 0
-    const int order[] = {0, 8, 1, 2, 9, 3, 4, 5, 6};
-    const char* names[] = {"argmax", "copy", "bar", "ctared", "send", "bulk", "wait", "red+U", "E+next"};
-    double acc[9] = {0};
+    const int order[] = {0, 8, 10, 1, 2, 9, 3, 4, 5, 6};
+    const char* names[] = {"argmax", "copy", "slots", "bar", "ctared", "send", "bulk", "wait", "red+U", "E+next"};
+    double acc[10] = {0};
     int cnt = 0;
     for (int64_t t = 1; t + 1 < k; ++t) {
       const long long* a = &h[(size_t)t * 16];
       const long long* b = &h[(size_t)(t + 1) * 16];
       if (!a[0] || !b[0] || b[0] < a[0]) continue;
-      for (int j = 0; j < 8; ++j) acc[j] += (double)(a[order[j + 1]] - a[order[j]]);
-      acc[8] += (double)(b[0] - a[6]);
+      for (int j = 0; j < 9; ++j) acc[j] += (double)(a[order[j + 1]] - a[order[j]]);
+      acc[9] += (double)(b[0] - a[6]);
       ++cnt;
     }
     if (cnt) {
       std::fprintf(stderr, "[lupp probe] n=%lld k=%lld steps=%d ", (long long)n, (long long)k, cnt);
-      for (int j = 0; j < 9; ++j) std::fprintf(stderr, " %s %.0f", names[j], acc[j] / cnt);
+      for (int j = 0; j < 10; ++j) std::fprintf(stderr, " %s %.0f", names[j], acc[j] / cnt);
       std::fprintf(stderr, " cycles\n");
     }
   }
