@@ -57,8 +57,11 @@ typedef enum {
  * (R3).  Sparse sign: zeta nonzeros +-1/sqrt(zeta) per column at
  * uniformly random distinct rows (R4); zeta = min(l, 8) in practice
  * (P:185).  Both are regenerated on the fly from (seed, row, column) with
- * Philox4x32-10 (R1, R2) and never stored in HBM. */
-typedef enum { SK_EMB_GAUSSIAN = 0, SK_EMB_SPARSE_SIGN = 1 } sk_embedding;
+ * Philox4x32-10 (R1, R2) and never stored in HBM.  SRTT:
+ * sqrt(m/l) Pi_{m->l} T Phi Pi_{m->m} with T the unitary discrete Hartley transform, the random
+ * permutation / selection as keyed Feistel bijections and the signs from Philox (R18); applied by
+ * a per-column radix-2 FFT in shared memory, m a power of two <= 16384 (R19), SK_E_ARG otherwise. */
+typedef enum { SK_EMB_GAUSSIAN = 0, SK_EMB_SPARSE_SIGN = 1, SK_EMB_SRTT = 2 } sk_embedding;
 
 /* Which approximation sk_residual measures (Frobenius norm, R12).
  *   COL_ID    ||A - C C^+ A||              eq:def_column_id

@@ -107,4 +107,68 @@ def embedding(kind, seed, l, m, zeta=8):
         return gaussian(seed, l, m)
     if kind in ("sparse_sign", 1):
         return sparse_sign(seed, l, m, zeta)
+    if kind in ("srtt", 2):
+        return srtt(seed, l, m)
     raise ValueError(kind)
+
+
+# ----------------------------------------------------------------------------------- SRTT
+# Subsampled randomized trigonometric transform (Table 1):
+#     Gamma = sqrt(m/l) Pi_{m->l} T Phi Pi_{m->m},
+# T the unitary discrete Hartley transform T(k, i) = cas(2 pi i k / m) / sqrt(m), cas = cos + sin.
+# Readings (R18): the random choices are counter-based so both sides can draw them
+# independently -- Pi_{m->m} and Pi_{m->l} are keyed 4-round Feistel bijections on the b = log2(m)
+# bit indices (XOR of each half with a Philox word of the other half), Phi(i) = -1 iff bit 0 of a
+# Philox word of i is 1.  R19: m must be a power of two (the fast transform's radix-2 length).
+TAG_PERM, TAG_SUBS, TAG_SIGN = 0x5045524D, 0x53554253, 0x5349474E
+
+
+def feistel(x, b, tag, seed):
+    """Keyed bijection of [0, 2^b) (4 rounds; round r XORs one half with a Philox word of the other)."""
+    k0, k1 = _seed_key(seed)
+    x = np.asarray(x, dtype=np.uint64)
+    hb = b // 2
+    lb = b - hb
+    lo = x & np.uint64((1 << lb) - 1)
+    hi = x >> np.uint64(lb)
+    for r in range(4):
+        if r % 2 == 0:
+            w = philox4x32_10(lo, r, 0, tag, k0, k1)[0]
+            hi = hi ^ (w & np.uint64((1 << hb) - 1))
+        else:
+            w = philox4x32_10(hi, r, 0, tag, k0, k1)[0]
+            lo = lo ^ (w & np.uint64((1 << lb) - 1))
+    return ((hi << np.uint64(lb)) | lo).astype(np.int64)
+
+
+def srtt_parts(seed, l, m):
+    """(perm, signs, sel): y_i = signs_i x_{perm_i}; output row r takes transform index sel_r."""
+    b = int(m).bit_length() - 1
+    if m < 2 or (1 << b) != m:
+        raise ValueError("SRTT needs m a power of two (R19)")
+    if not (1 <= l <= m):
+        raise ValueError("1 <= l <= m")
+    idx = np.arange(m, dtype=np.uint64)
+    perm = feistel(idx, b, TAG_PERM, seed)
+    k0, k1 = _seed_key(seed)
+    w = philox4x32_10(idx, 0, 0, TAG_SIGN, k0, k1)[0]
+    signs = np.where((w & np.uint64(1)) == 1, -1.0, 1.0)
+    sel = feistel(np.arange(l, dtype=np.uint64), b, TAG_SUBS, seed)
+    return perm, signs, sel
+
+
+def hartley(m):
+    """The unitary DHT matrix, by definition."""
+    i = np.arange(m)
+    th = 2.0 * np.pi * (np.outer(i, i) % m) / m       # reduce i k mod m first (exact integers)
+    return (np.cos(th) + np.sin(th)) / math.sqrt(m)
+
+
+def srtt(seed, l, m):
+    """Dense SRTT embedding Gamma (l x m), formed literally: sqrt(m/l) Pi_{m->l} T Phi Pi_{m->m}."""
+    perm, signs, sel = srtt_parts(seed, l, m)
+    Pmm = np.zeros((m, m))
+    Pmm[np.arange(m), perm] = 1.0                    # (Pi x)_i = x_{perm_i}
+    Pml = np.zeros((l, m))
+    Pml[np.arange(l), sel] = 1.0
+    return math.sqrt(m / l) * Pml @ hartley(m) @ np.diag(signs) @ Pmm

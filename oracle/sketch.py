@@ -20,6 +20,18 @@ def sketch(A, l, kind="gaussian", seed=0, zeta=8):
     return G @ A
 
 
+def sketch_srtt_fft(A, l, seed=0):
+    """SRTT sketch for larger m with the library FFT as the transform step (DHT = Re F - Im F of
+    the DFT F, F(k) = sum_i y_i e^{-2 pi i ik/m}); otherwise the same formula as omega.srtt."""
+    A = np.asarray(A, dtype=np.float64)
+    m = A.shape[0]
+    perm, signs, sel = omega.srtt_parts(seed, l, m)
+    Y = signs[:, None] * A[perm]
+    F = np.fft.fft(Y, axis=0)
+    H = (F.real - F.imag) / np.sqrt(m)
+    return np.sqrt(m / l) * H[sel]
+
+
 def sketch_columns(A_cols, l, kind="gaussian", seed=0, zeta=8):
     """X[:, J] for a sample of columns A[:, J] (same Gamma; used for full-size spot checks)."""
     return sketch(A_cols, l, kind, seed, zeta)

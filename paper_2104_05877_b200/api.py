@@ -16,9 +16,10 @@ import torch
 
 from . import _lib
 
-GAUSSIAN, SPARSE_SIGN = 0, 1
+GAUSSIAN, SPARSE_SIGN, SRTT = 0, 1, 2
 COL_ID, ROW_ID, CUR, ID_COEFFS = 0, 1, 2, 3
-_EMB = {"gaussian": GAUSSIAN, "sparse_sign": SPARSE_SIGN, GAUSSIAN: GAUSSIAN, SPARSE_SIGN: SPARSE_SIGN}
+_EMB = {"gaussian": GAUSSIAN, "sparse_sign": SPARSE_SIGN, "srtt": SRTT, GAUSSIAN: GAUSSIAN, SPARSE_SIGN: SPARSE_SIGN,
+        SRTT: SRTT}
 _KIND = {"col_id": COL_ID, "row_id": ROW_ID, "cur": CUR, "id_coeffs": ID_COEFFS,
          COL_ID: COL_ID, ROW_ID: ROW_ID, CUR: CUR, ID_COEFFS: ID_COEFFS}
 

@@ -125,6 +125,7 @@ sk_status sk_sketch(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t ld
     SK_ARG(c, zeta >= 2 && zeta <= l && zeta <= 64, "sk_sketch: sparse sign needs 2 <= zeta <= min(l, 64)");
     return sketch_sparse(c, A, m, n, lda, l, zeta, seed, X, ldx);
   }
+  if (emb == SK_EMB_SRTT) return sketch_srtt(c, A, m, n, lda, l, seed, X, ldx);
   return fail(c, SK_E_ARG, "sk_sketch: unknown embedding");
 }
 
@@ -135,7 +136,8 @@ sk_status sk_sketch_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64
   SK_ARG(c, A && Y, "sk_sketch_cols: NULL A or Y");
   SK_ARG(c, m >= 1 && n >= 1 && l >= 1 && l <= n, "sk_sketch_cols: need 1 <= l <= n, m >= 1");
   SK_ARG(c, lda >= m && ldy >= m, "sk_sketch_cols: lda >= m and ldy >= m required");
-  SK_ARG(c, emb == SK_EMB_GAUSSIAN || (zeta >= 2 && zeta <= l && zeta <= 64), "sk_sketch_cols: bad zeta");
+  SK_ARG(c, emb >= SK_EMB_GAUSSIAN && emb <= SK_EMB_SRTT, "sk_sketch_cols: unknown embedding");
+  SK_ARG(c, emb != SK_EMB_SPARSE_SIGN || (zeta >= 2 && zeta <= l && zeta <= 64), "sk_sketch_cols: bad zeta");
   SK_CUDA(c, cudaSetDevice(c->device));
   return sketch_cols(c, A, m, n, lda, l, (int)emb, zeta, seed, Y, ldy);
 }
@@ -149,7 +151,8 @@ sk_status sk_sketch_power(sk_ctx* c, const double* A, int64_t m, int64_t n, int6
   if (q == 0) return sk_sketch(c, A, m, n, lda, l, emb, zeta, seed, X, ldx);
   SK_ARG(c, m >= 1 && n >= 1 && l >= 1 && l <= n, "sk_sketch_power: need 1 <= l <= n, m >= 1");
   SK_ARG(c, lda >= m && ldx >= n, "sk_sketch_power: lda >= m and ldx >= n required");
-  SK_ARG(c, emb == SK_EMB_GAUSSIAN || (zeta >= 2 && zeta <= l && zeta <= 64), "sk_sketch_power: bad zeta");
+  SK_ARG(c, emb >= SK_EMB_GAUSSIAN && emb <= SK_EMB_SRTT, "sk_sketch_power: unknown embedding");
+  SK_ARG(c, emb != SK_EMB_SPARSE_SIGN || (zeta >= 2 && zeta <= l && zeta <= 64), "sk_sketch_power: bad zeta");
   SK_CUDA(c, cudaSetDevice(c->device));
   return sketch_power(c, A, m, n, lda, l, (int)emb, zeta, seed, q, X, ldx);
 }

@@ -17,6 +17,9 @@ namespace dev {
 
 constexpr uint32_t kTagGauss = 0x47415553u;   // "GAUS"
 constexpr uint32_t kTagSparse = 0x53504152u;  // "SPAR"
+constexpr uint32_t kTagPerm = 0x5045524Du;    // "PERM"  SRTT Pi_{m->m}
+constexpr uint32_t kTagSubs = 0x53554253u;    // "SUBS"  SRTT Pi_{m->l}
+constexpr uint32_t kTagSign = 0x5349474Eu;    // "SIGN"  SRTT Phi
 
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 #pragma unroll
@@ -161,6 +164,29 @@ __device__ __forceinline__ uint64_t sparse_col(uint64_t i, int l, int zeta, uint
     rows[j] = t;
   }
   return (uint64_t)sw.x | ((uint64_t)sw.y << 32);   // bit j of word (j/32) -> bit j
+}
+
+// SRTT (R18): keyed 4-round Feistel bijection of [0, 2^b); round r XORs one half with
+// the first Philox word of (other half, r, 0, tag).  feistel_inv runs the rounds backwards.
+__device__ __forceinline__ uint32_t feistel(uint32_t x, int b, uint32_t tag, uint2 key) {
+  const int hb = b >> 1, lb = b - hb;
+  uint32_t lo = x & ((1u << lb) - 1u), hi = x >> lb;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if ((r & 1) == 0) hi ^= philox4x32_10(make_uint4(lo, (uint32_t)r, 0u, tag), key).x & ((1u << hb) - 1u);
+    else lo ^= philox4x32_10(make_uint4(hi, (uint32_t)r, 0u, tag), key).x & ((1u << lb) - 1u);
+  }
+  return (hi << lb) | lo;
+}
+__device__ __forceinline__ uint32_t feistel_inv(uint32_t x, int b, uint32_t tag, uint2 key) {
+  const int hb = b >> 1, lb = b - hb;
+  uint32_t lo = x & ((1u << lb) - 1u), hi = x >> lb;
+#pragma unroll
+  for (int r = 3; r >= 0; --r) {
+    if ((r & 1) == 0) hi ^= philox4x32_10(make_uint4(lo, (uint32_t)r, 0u, tag), key).x & ((1u << hb) - 1u);
+    else lo ^= philox4x32_10(make_uint4(hi, (uint32_t)r, 0u, tag), key).x & ((1u << lb) - 1u);
+  }
+  return (hi << lb) | lo;
 }
 
 // Register-resident variant of sparse_col for zeta <= 8 (identical draws; unrolled so rows[]

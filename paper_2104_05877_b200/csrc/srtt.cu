@@ -1,0 +1,162 @@
+// srtt.cu -- SRTT embedding: X = Gamma A with
+//     Gamma = sqrt(m/l) Pi_{m->l} T Phi Pi_{m->m}           (Table 1)
+// T the unitary discrete Hartley transform, T(k, i) = cas(2 pi i k / m) / sqrt(m).
+// Readings (R18, R19): Pi_{m->m}, Pi_{m->l} are keyed Feistel bijections of the
+// b = log2(m)-bit indices and Phi(i) = -1 iff bit 0 of Philox(i, 0, 0, 'SIGN') is set
+// (philox.cuh); m must be a power of two.  Nothing of Gamma is stored in HBM.
+//
+// One CTA per column at a time (grid-stride over columns; 1 CTA per SM, shared memory bound):
+//   1. y = Phi Pi x: x = A(:, j) is read coalesced and scattered into shared memory at the
+//      inverse-permuted position q = Pi^{-1}(i) with sign Phi(q) (inverse permutation and signs
+//      are tabulated once per CTA), packed as N = m/2 complex z_n = y_2n + i y_2n+1 in
+//      bit-reversed order;
+//   2. radix-2 DIT FFT of length N in shared memory (twiddle table per CTA);
+//   3. for the l selected indices k = Pi_{m->l}(r): the real-input DFT
+//      Y_k = E_k + e^{-2 pi i k/m} O_k with E = (Z_k + conj Z_{N-k})/2, O = (Z_k - conj Z_{N-k})/(2i),
+//      then the Hartley value H_k = Re Y_k - Im Y_k and X(r, j) = H_k / sqrt(l)
+//      (sqrt(m/l) * 1/sqrt(m)).
+// Work O(m log m) per column; the bound is reading A once (8mn bytes).
+#include <cmath>
+
+#include "common.cuh"
+#include "internal.h"
+#include "philox.cuh"
+
+namespace skel {
+namespace {
+
+constexpr int RNT = 512;
+
+struct SrttParams {
+  const double* A; int64_t lda;
+  int64_t m, n; int l; int b;     // m = 2^b
+  uint2 key;
+  double* X; int64_t ldx;
+};
+
+__host__ __device__ inline size_t srtt_smem(int64_t m, int l) {
+  const int64_t N = m / 2;
+  return (size_t)N * 16 /* z */ + (size_t)(64 + (N / 128 + 1)) * 16 /* two-level twiddles */ + (size_t)m * 2 /* inv perm */ +
+         (size_t)((m + 31) / 32) * 4 /* sign bits */ + (size_t)l * 2 /* selection */;
+}
+
+__device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }
+
+__global__ void __launch_bounds__(RNT, 1) k_sketch_srtt(SrttParams p) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  const int64_t m = p.m, N = m / 2;
+  const int lgN = p.b - 1;
+  double2* z = reinterpret_cast<double2*>(rsm);                               // [N]
+  // twiddle e^{-2 pi i t/N} = twA[t & 63] * twB[t >> 6]: two small tables, no bank-conflicting
+  // strided lookups (a single table indexed by pos * (N >> s) is a 32-way conflict mid-transform)
+  double2* twA = z + N;                                                        // [64]
+  double2* twB = twA + 64;                                                     // [N/128 + 1]
+  uint16_t* pinv = reinterpret_cast<uint16_t*>(twB + (N / 128 + 1));          // [m]   (m <= 65536)
+  uint32_t* sgn = reinterpret_cast<uint32_t*>(pinv + m);                       // [m/32]
+  uint16_t* sel = reinterpret_cast<uint16_t*>(sgn + (m + 31) / 32);           // [l]
+  const int tid = threadIdx.x;
+  // ---- per-CTA tables (Gamma's structure, regenerated, never in HBM)
+  for (int64_t t = tid; t < 64 + N / 128 + 1; t += RNT) {
+    const double ang = t < 64 ? 2.0 * (double)t / (double)N : 2.0 * (double)((t - 64) * 64) / (double)N;
+    double s, c;
+    dev::bm_sincospi(ang, s, c);
+    twA[t] = make_double2(c, -s);                       // (twB follows twA contiguously)
+  }
+  for (int64_t i = tid; i < m; i += RNT) pinv[i] = (uint16_t)dev::feistel_inv((uint32_t)i, p.b, dev::kTagPerm, p.key);
+  for (int64_t w = tid; w < (m + 31) / 32; w += RNT) {
+    uint32_t bits = 0u;
+    for (int q = 0; q < 32 && w * 32 + q < m; ++q) {
+      const uint32_t i = (uint32_t)(w * 32 + q);
+      bits |= (dev::philox4x32_10(make_uint4(i, 0u, 0u, dev::kTagSign), p.key).x & 1u) << q;
+    }
+    sgn[w] = bits;
+  }
+  for (int r = tid; r < p.l; r += RNT) sel[r] = (uint16_t)dev::feistel((uint32_t)r, p.b, dev::kTagSubs, p.key);
+  __syncthreads();
+  const double inv_sqrt_l = 1.0 / sqrt((double)p.l);
+
+  // the column is held in registers (m / RNT <= 32 per thread) and the next column's loads are
+  // issued before the current column's FFT, so HBM latency overlaps the transform
+  constexpr int XPT = 32;
+  double xv[XPT];
+  auto load_col = [&](int64_t j) {
+    const double* col = p.A + j * p.lda;
+#pragma unroll
+    for (int q = 0; q < XPT; ++q) {
+      const int64_t i = tid + (int64_t)q * RNT;
+      xv[q] = (j < p.n && i < m) ? __ldcs(col + i) : 0.0;
+    }
+  };
+  load_col(blockIdx.x);
+  for (int64_t j = blockIdx.x; j < p.n; j += gridDim.x) {
+    // 1. scatter y_q = Phi(q) x_{Pi(q)} into bit-reversed complex slots
+#pragma unroll
+    for (int qq = 0; qq < XPT; ++qq) {
+      const int64_t i = tid + (int64_t)qq * RNT;
+      if (i < m) {
+        const uint32_t q = pinv[i];
+        const double x = xv[qq];
+        const double y = ((sgn[q >> 5] >> (q & 31)) & 1u) ? -x : x;
+        double* zd = reinterpret_cast<double*>(z + bitrev(q >> 1, lgN));
+        zd[q & 1u] = y;
+      }
+    }
+    __syncthreads();
+    load_col(j + gridDim.x);
+    // 2. radix-2 DIT FFT of length N
+    for (int s = 1; s <= lgN; ++s) {
+      const int64_t half = 1ll << (s - 1);
+      const int64_t tstride = N >> s;                 // twiddle index step
+      for (int64_t bfly = tid; bfly < N / 2; bfly += RNT) {
+        const int64_t g = bfly >> (s - 1), pos = bfly & (half - 1);
+        const int64_t i0 = (g << s) + pos, i1 = i0 + half;
+        const int64_t ti = pos * tstride;                 // < N/2
+        const double2 wa = twA[ti & 63], wb = twB[ti >> 6];
+        const double2 w = make_double2(wa.x * wb.x - wa.y * wb.y, wa.x * wb.y + wa.y * wb.x);
+        const double2 u = z[i0], v = z[i1];
+        const double2 vw = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+        z[i0] = make_double2(u.x + vw.x, u.y + vw.y);
+        z[i1] = make_double2(u.x - vw.x, u.y - vw.y);
+      }
+      __syncthreads();
+    }
+    // 3. selected Hartley outputs
+    for (int r = tid; r < p.l; r += RNT) {
+      const int64_t k = sel[r];
+      const int64_t k1 = k & (N - 1), k2 = (N - k1) & (N - 1);
+      const double2 Zk = z[k1], Zc = make_double2(z[k2].x, -z[k2].y);
+      const double2 E = make_double2(0.5 * (Zk.x + Zc.x), 0.5 * (Zk.y + Zc.y));
+      const double2 D = make_double2(0.5 * (Zk.x - Zc.x), 0.5 * (Zk.y - Zc.y));
+      const double2 O = make_double2(D.y, -D.x);                      // D / i
+      double s, c;
+      dev::bm_sincospi(2.0 * (double)k / (double)m, s, c);            // e^{-2 pi i k/m} = c - i s
+      const double yr = E.x + (O.x * c + O.y * s);
+      const double yi = E.y + (O.y * c - O.x * s);
+      p.X[(int64_t)r * p.ldx + j] = (yr - yi) * inv_sqrt_l;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+sk_status sketch_srtt(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, uint64_t seed,
+                      double* X, int64_t ldx) {
+  if (n == 0) return SK_OK;
+  int b = 0;
+  while ((1ll << b) < m) ++b;
+  if ((1ll << b) != m || m < 8) return fail(c, SK_E_ARG, "sk_sketch: SRTT needs m a power of two >= 8 (R19)");
+  const size_t smem = srtt_smem(m, (int)l);
+  if (m > 32 * RNT || smem > (size_t)c->max_smem_optin)
+    return fail(c, SK_E_ARG, "sk_sketch: SRTT column transform exceeds shared memory (m <= 16384)");
+  SrttParams p{};
+  p.A = A; p.lda = lda; p.m = m; p.n = n; p.l = (int)l; p.b = b;
+  p.key = dev::seed_key(seed);
+  p.X = X; p.ldx = ldx;
+  SK_CUDA(c, cudaFuncSetAttribute(k_sketch_srtt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)std::min<int64_t>(n, c->num_sms);
+  k_sketch_srtt<<<grid, RNT, smem, c->stream>>>(p);
+  return launched(c);
+}
+
+}  // namespace skel

@@ -109,6 +109,29 @@ def test_stream_select_alg3_c1():
     assert r >= o_res.optimal_error(sigma, k) * (1 - 1e-12)
 
 
+# ------------------------------------------------------------------ SRTT embedding (8(f) rank 3)
+@pytest.mark.parametrize("m,n,l,seed", [(8, 5, 3, 1), (256, 256, 40, 2001), (4096, 333, 266, 7), (16384, 70, 510, 3)])
+def test_sketch_srtt_parity(m, n, l, seed):
+    A = rand_mat(m, n, seed)
+    X = sk.sketch(dev_f(A), l, "srtt", seed).cpu().numpy()
+    assert rel_fro(X, o_sketch.sketch_srtt_fft(A, l, seed)) <= 1e-12
+
+
+def test_srtt_rand_lupp_c1():
+    A, sigma = make_c1(seed=1001)
+    k, l = 20, 40
+    X = sk.sketch(dev_f(A), l, "srtt", 2001)
+    Js, _, _, _ = sk.select_cols(X, k)
+    Xo = o_sketch.sketch_srtt_fft(A, l, 2001)
+    lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(Xo, k, f))
+
+
+def test_sketch_srtt_rejects_non_power_of_two():
+    with pytest.raises(sk.SkelError) as e:
+        sk.sketch(dev_f(rand_mat(100, 10, 1)), 8, "srtt", 1)
+    assert e.value.status == 1
+
+
 # ------------------------------------------------------------------ S1' sparse sketch
 @pytest.mark.parametrize("m,n,l,zeta,seed", [
     (1000, 100, 60, 8, 2003),

@@ -110,3 +110,33 @@ def test_sparse_sign_norm_preservation():
         g = omega.sparse_sign(s, 16, 4, 8)
         vals.append(np.sum(g[:, 0] ** 2))
     assert abs(np.mean(vals) - 1.0) < 0.1
+
+
+# ------------------------------------------------------------------ SRTT (R18, R19)
+@pytest.mark.parametrize("b", [3, 8, 12, 17])
+def test_srtt_feistel_is_a_bijection(b):
+    x = np.arange(2 ** b, dtype=np.uint64)
+    for tag in (omega.TAG_PERM, omega.TAG_SUBS):
+        y = omega.feistel(x, b, tag, 99)
+        assert np.array_equal(np.sort(y), np.arange(2 ** b))
+
+
+def test_srtt_closed_forms():
+    m, l = 64, 20
+    T = omega.hartley(m)
+    np.testing.assert_allclose(T @ T, np.eye(m), atol=1e-13)          # the unitary DHT is an involution
+    np.testing.assert_allclose(T, T.T, atol=0)                         # and symmetric
+    G = omega.srtt(5, l, m)
+    np.testing.assert_allclose(G @ G.T, (m / l) * np.eye(l), atol=1e-12)   # rows of a scaled unitary
+    perm, signs, sel = omega.srtt_parts(5, l, m)
+    assert set(np.unique(signs)) <= {-1.0, 1.0} and len(set(sel.tolist())) == l
+
+
+def test_srtt_fft_route_equals_definition_and_preserves_norms():
+    from oracle import sketch as o_sketch
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((128, 9))
+    np.testing.assert_allclose(o_sketch.sketch(A, 30, "srtt", 7), o_sketch.sketch_srtt_fft(A, 30, 7), atol=1e-12)
+    x = rng.standard_normal(256)
+    ratios = [np.sum(o_sketch.sketch_srtt_fft(x[:, None], 64, s) ** 2) / np.sum(x * x) for s in range(200)]
+    assert abs(np.mean(ratios) - 1.0) < 0.05                          # E ||Gamma x||^2 = ||x||^2

@@ -23,6 +23,8 @@ SHAPES = [  # (name, m, n, l, embedding)
     ("C4 k=100", 65536, 784, 200, "gaussian"),
     ("C4 k=200", 65536, 784, 400, "gaussian"),
     ("C3 sparse", 16384, 16384, 510, "sparse_sign"),
+    ("C2 srtt k=512", 4096, 4096, 522, "srtt"),
+    ("C3 srtt", 16384, 16384, 510, "srtt"),
 ]
 
 
@@ -53,7 +55,7 @@ def main():
         if emb == "gaussian":
             tf = 2.0 * l * m * n / (ms * 1e-3) / 1e12
             print(f"{name:12s} m={m:6d} n={n:6d} l={l:4d}  {ms:8.4f} ms  {tf:6.2f} TF/s  {tf / PEAK:5.1%} of DMMA peak")
-        else:
+        else:   # sparse sign / SRTT: HBM bound (A once + X)
             gbs = 8.0 * (m * n + l * n) / (ms * 1e-3) / 1e9
             print(f"{name:12s} m={m:6d} n={n:6d} l={l:4d}  {ms:8.4f} ms  {gbs:7.1f} GB/s  {gbs / 6439.8:5.1%} of HBM")
         del A, X
