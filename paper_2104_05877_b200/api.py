@@ -76,9 +76,9 @@ def fortran(t):
 def _colmajor(A, name):
     if A.dim() != 2 or A.dtype != torch.float64 or not A.is_cuda:
         raise ValueError(f"{name} must be a 2-D float64 CUDA tensor")
-    if A.stride(0) != 1 and A.shape[1] > 1:
+    if A.stride(0) != 1 and A.shape[0] > 1 and A.shape[1] > 1:
         raise ValueError(f"{name} must be column-major (use api.fortran)")
-    return max(A.stride(1), A.shape[0], 1)
+    return max(A.stride(1) if A.shape[1] > 1 else A.shape[0], A.shape[0], 1)
 
 
 def sketch(A, l, embedding="gaussian", seed=0, zeta=8, out=None):

@@ -115,7 +115,7 @@ sk_status sk_sketch(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t ld
                     sk_embedding emb, int32_t zeta, uint64_t seed, double* X, int64_t ldx) {
   if (!c) return SK_E_ARG;
   c->err.clear();
-  SK_ARG(c, A && X, "sk_sketch: NULL A or X");
+  SK_ARG(c, n == 0 || (A && X), "sk_sketch: NULL A or X");
   SK_ARG(c, m >= 1 && n >= 0 && l >= 1 && l <= m, "sk_sketch: need 1 <= l <= m, n >= 0");
   SK_ARG(c, lda >= m && ldx >= n, "sk_sketch: lda >= m and ldx >= n required");
   SK_ARG(c, m < (1LL << 40) && l <= (1 << 20), "sk_sketch: size out of range");

@@ -1,0 +1,115 @@
+"""GPU edge cases through the C ABI: empty and degenerate sizes, single rows/columns, k = 1,
+l = m, ties, zero matrices, lda padding, argument errors -- each against the oracle or a closed form."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2104_05877_b200 as sk
+from oracle import lupp as o_lupp
+from oracle import residual as o_res
+from oracle import sketch as o_sketch
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def dev_f(a):
+    return sk.fortran(torch.from_numpy(np.ascontiguousarray(a)).to(DEV))
+
+
+def test_sketch_empty_n():
+    A = torch.empty((50, 0), dtype=torch.float64, device=DEV)
+    X = sk.sketch(A, 10, "gaussian", 1)
+    assert X.shape == (10, 0)
+
+
+@pytest.mark.parametrize("emb", ["gaussian", "sparse_sign"])
+def test_sketch_single_row_and_column(emb):
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((64, 1))
+    l = 8
+    X = sk.sketch(dev_f(A), l, emb, 5, 2 if emb == "sparse_sign" else 8).cpu().numpy()
+    ref = o_sketch.sketch(A, l, emb, 5, 2 if emb == "sparse_sign" else 8)
+    assert np.linalg.norm(X - ref) <= 1e-12 * np.linalg.norm(ref)
+    A1 = rng.standard_normal((1, 7))                     # m = l = 1
+    X1 = sk.sketch(dev_f(A1), 1, "gaussian", 5).cpu().numpy()
+    np.testing.assert_allclose(X1, o_sketch.sketch(A1, 1, "gaussian", 5), rtol=1e-14)
+
+
+def test_sketch_zero_matrix_is_zero():
+    X = sk.sketch(dev_f(np.zeros((300, 40))), 20, "gaussian", 3).cpu().numpy()
+    assert np.count_nonzero(X) == 0
+
+
+def test_select_cols_k1_is_argmax_first_row():
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((3, 500))
+    Js, Lf, U, _ = sk.select_cols(torch.from_numpy(X).to(DEV), 1)
+    assert Js.item() == int(np.argmax(np.abs(X[0])))
+    np.testing.assert_allclose(Lf.cpu().numpy()[:, 0], X[0] / X[0, Js.item()], rtol=1e-15)
+
+
+def test_select_rows_single_column_and_k_equals_m():
+    rng = np.random.default_rng(2)
+    C = rng.standard_normal((40, 1))
+    Is, _, _, _ = sk.select_rows(dev_f(C), 1)
+    assert Is.item() == int(np.argmax(np.abs(C[:, 0])))
+    Cs = rng.standard_normal((12, 12))
+    Is, _, _, _ = sk.select_rows(dev_f(Cs), 12)
+    piv, _, _, _ = o_lupp.select_rows(Cs, 12)
+    assert Is.cpu().tolist() == piv.tolist()
+
+
+def test_select_cols_all_zero_is_rank_failure_at_step_1():
+    with pytest.raises(sk.SkelError) as e:
+        sk.select_cols(torch.zeros((4, 100), dtype=torch.float64, device=DEV), 3)
+    assert e.value.status == 2 and e.value.info == 1
+
+
+def test_select_cols_exact_ties_everywhere():
+    # every entry of the first row equal: the lowest index wins each tie (R6)
+    X = np.ones((2, 64))
+    X[1] = np.arange(64)
+    Js, _, _, _ = sk.select_cols(torch.from_numpy(X).to(DEV), 2)
+    piv, _, _, _ = o_lupp.select_cols(X, 2)
+    assert Js.cpu().tolist() == piv.tolist() == [0, 63]
+
+
+def test_residual_full_rank_skeleton_is_zero_and_k_equals_n():
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((80, 30))
+    J = torch.arange(30, dtype=torch.int64, device=DEV)
+    r, nA = sk.residual(dev_f(A), J, None, "col_id")       # C = A: the projector is exact
+    assert r <= 1e-12 * nA
+
+
+def test_padded_lda_everywhere():
+    rng = np.random.default_rng(4)
+    m, n, l, k = 200, 90, 24, 12
+    A = rng.standard_normal((m, n))
+    buf = torch.zeros((n, m + 5), dtype=torch.float64, device=DEV)
+    buf[:, :m] = torch.from_numpy(A.T.copy()).to(DEV)
+    Av = buf.t()[:m]                                       # lda = m + 5
+    X = sk.sketch(Av, l, "gaussian", 9)
+    Js, _, _, _ = sk.select_cols(X, k)
+    r, nA = sk.residual(Av, Js, None, "col_id")
+    ro, nAo = o_res.residual(A, Js.cpu().numpy(), kind="col_id")
+    assert abs(r - ro) <= 1e-9 * ro + 4 * 2.0 ** -53 * nAo
+
+
+@pytest.mark.parametrize("call", ["l_gt_m", "k_gt_l", "zeta_bad", "bad_kind"])
+def test_argument_errors_are_reported(call):
+    A = dev_f(np.ones((10, 10)))
+    with pytest.raises((sk.SkelError, KeyError)) as e:
+        if call == "l_gt_m":
+            sk.sketch(A, 11, "gaussian", 1)
+        elif call == "k_gt_l":
+            sk.select_cols(torch.ones((3, 10), dtype=torch.float64, device=DEV), 4)
+        elif call == "zeta_bad":
+            sk.sketch(A, 5, "sparse_sign", 1, 9)
+        else:
+            sk.residual(A, torch.zeros(2, dtype=torch.int64, device=DEV), None, "nope")
+    if isinstance(e.value, sk.SkelError):
+        assert e.value.status == 1
