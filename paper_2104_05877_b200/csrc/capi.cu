@@ -93,6 +93,9 @@ sk_status sk_set_stream(sk_ctx* c, void* stream) {
 void sk_destroy(sk_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
+  if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
   if (c->pool) cudaMemPoolDestroy(c->pool);
   if (c->host_scratch) cudaFreeHost(c->host_scratch);
   delete c;

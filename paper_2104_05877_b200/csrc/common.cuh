@@ -26,6 +26,9 @@ struct sk_ctx {
   // A/B switch (env SKEL_SKETCH_LEGACY=1 at sk_create): use the cp.async sketch kernel
   // instead of the TMA + cluster-shared-Omega one.
   bool force_legacy_sketch = false;
+  // lowest-priority helper stream + events for look-ahead overlap (LUPP trailing updates)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
 };
 
 namespace skel {

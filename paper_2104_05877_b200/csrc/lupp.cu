@@ -1066,6 +1066,16 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
                                                stateb.as<int>(), maxb.as<unsigned long long>());
     SK_TRY(launched(c));
   }
+  static const bool no_lookahead = [] { const char* e = std::getenv("SKEL_LUPP_NO_LOOKAHEAD"); return e && e[0] == '1'; }();
+  const bool lookahead = !no_lookahead && bp < k;
+  if (lookahead && !c->aux) {
+    int lo = 0, hi = 0;
+    SK_CUDA(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SK_CUDA(c, cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo));   // lo = least priority
+    SK_CUDA(c, cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming));
+    SK_CUDA(c, cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming));
+  }
+  bool rest_pending = false;
   for (int64_t c0 = 0; c0 < k; c0 += bp) {
     const int b = (int)std::min<int64_t>(bp, k - c0);
     PanelParams pp{};
@@ -1088,13 +1098,31 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     SK_TRY(launched(c));
     const int64_t c1 = c0 + b;
     if (c1 < k) {
+      // look-ahead: the next block's columns are updated on the main stream; the rest of the
+      // trailing update runs on the low-priority aux stream, overlapping the next panel
+      if (rest_pending) SK_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_b, 0));   // before u12 reads W(piv, c1:)
+      rest_pending = false;
       k_lupp_u12<<<(unsigned)cdiv(k - c1, 32), 256, kU12Smem, c->stream>>>(Wb.as<double>(), n, (int)k, (int)c0, b, Js,
                                                                   Lf, ldlf, Ub.as<double>(), status_dev);
       SK_TRY(launched(c));
-      SK_TRY(gemm(c, false, false, n, k - c1, b, -1.0, Lf + c0 * ldlf, ldlf, Ub.as<double>() + c0 + c1 * k,
+      const int64_t nn = lookahead ? std::min<int64_t>(bp, k - c1) : k - c1;
+      SK_TRY(gemm(c, false, false, n, nn, b, -1.0, Lf + c0 * ldlf, ldlf, Ub.as<double>() + c0 + c1 * k,
                   k, 1.0, Wb.as<double>() + c1 * n, n));
+      if (c1 + nn < k) {
+        SK_CUDA(c, cudaEventRecord(c->ev_a, c->stream));
+        SK_CUDA(c, cudaStreamWaitEvent(c->aux, c->ev_a, 0));
+        cudaStream_t main_stream = c->stream;
+        c->stream = c->aux;
+        const sk_status st = gemm(c, false, false, n, k - c1 - nn, b, -1.0, Lf + c0 * ldlf, ldlf,
+                                  Ub.as<double>() + c0 + (c1 + nn) * k, k, 1.0, Wb.as<double>() + (c1 + nn) * n, n);
+        c->stream = main_stream;
+        SK_TRY(st);
+        SK_CUDA(c, cudaEventRecord(c->ev_b, c->aux));
+        rest_pending = true;
+      }
     }
   }
+  if (rest_pending) SK_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_b, 0));
   if (want_probe) {   // experiments: per-step phase durations (cycles) of CTA 0, thread 0, to stderr
     std::vector<long long> h((size_t)k * 16);
     SK_CUDA(c, cudaMemcpyAsync(h.data(), probeb.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));

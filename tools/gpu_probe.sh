@@ -4,3 +4,4 @@ timeout 600 python -m pytest tests -m gpu -x -q -k "select or lupp or full or re
 SKEL_LUPP_PROBE=1 timeout 300 python tools/bench_lupp.py --reps 1 > gpurun_out/probe.log 2>&1
 timeout 300 python tools/bench_lupp.py > gpurun_out/bench_lupp.log 2>&1
 echo done
+SKEL_LUPP_NO_LOOKAHEAD=1 timeout 300 python tools/bench_lupp.py > gpurun_out/bench_lupp_nola.log 2>&1
