@@ -155,6 +155,15 @@ sk_status sk_select_cols(sk_ctx* ctx, const double* X, int64_t l, int64_t n, int
 sk_status sk_select_cols_cpqr(sk_ctx* ctx, const double* X, int64_t l, int64_t n, int64_t ldx,
                               int64_t k, int64_t* Js, double* R, int64_t ldr, int64_t* info);
 
+/* ---- RSVD-DEIM column skeletons (comparator of Sec. 5) ----
+ * Q_X = ortho(X^T) (n x l), [U, S, V~] = svd(A Q_X, 'econ'), V^ = Q_X V~ (eq:rsvd_procedures,
+ * P:237-243), then DEIM = column-wise LUPP on V^(:, 0:k)^T.  A m x n column-major,
+ * X = Gamma A the l x n row-major sketch (ldx >= n).  Js device int64[k] in pivot order.
+ * Requires 1 <= k <= l <= min(m, n).  The l x l SVD step is cuSOLVER's (geqrf + gesvd on the
+ * triangular factor); everything else runs in this library's kernels.  info as sk_select_cols. */
+sk_status sk_select_cols_deim(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* X,
+                              int64_t l, int64_t ldx, int64_t k, int64_t* Js, int64_t* info);
+
 /* ---- S3: gather C = A(:, Js)  (eq:Js; columns in pivot order, R8) ---- */
 sk_status sk_gather_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
                          const int64_t* Js, int64_t k, double* C, int64_t ldc);

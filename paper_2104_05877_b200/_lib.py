@@ -24,6 +24,7 @@ _SIGS = {
     "sk_select_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, c_dp, c_i64, c_dp,
                        ctypes.POINTER(c_i64)],
     "sk_select_cols_cpqr": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, ctypes.POINTER(c_i64)],
+    "sk_select_cols_deim": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_i64, c_i64, c_i64, c_dp, ctypes.POINTER(c_i64)],
     "sk_gather_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64],
     "sk_gather_cols_shard": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64],
     "sk_residual_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_i64, c_i64, ctypes.POINTER(ctypes.c_double)],

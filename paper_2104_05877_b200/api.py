@@ -156,6 +156,20 @@ def select_cols_cpqr(X, k, want_r=False, check=True):
     return Js, R
 
 
+def select_cols_deim(A, X, k, check=True):
+    """RSVD-DEIM column skeletons (eq:rsvd_procedures + DEIM) from A and its sketch X."""
+    lda = _colmajor(A, "A")
+    m, n = A.shape
+    l = X.shape[0]
+    Js = torch.empty(k, dtype=torch.int64, device=A.device)
+    info = ctypes.c_int64(0)
+    h = context(A.device.index)
+    st = lib().sk_select_cols_deim(h, _ptr(A), m, n, lda, _ptr(X), l, max(X.stride(0), n), k, _ptr(Js),
+                                   ctypes.byref(info) if check else None)
+    _check(st, h, info.value)
+    return Js
+
+
 def gather_cols(A, Js):
     """C = A(:, J_s) (eq:Js), column-major m x k."""
     lda = _colmajor(A, "A")

@@ -191,6 +191,21 @@ sk_status sk_select_cols_cpqr(sk_ctx* c, const double* X, int64_t l, int64_t n, 
   return finish_info(c, st.as<int64_t>(), info, "sk_select_cols_cpqr");
 }
 
+sk_status sk_select_cols_deim(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* X,
+                              int64_t l, int64_t ldx, int64_t k, int64_t* Js, int64_t* info) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, A && X && Js, "sk_select_cols_deim: NULL pointer");
+  SK_ARG(c, k >= 1 && k <= l && l <= m && l <= n && lda >= m && ldx >= n,
+         "sk_select_cols_deim: need 1 <= k <= l <= min(m, n), lda >= m, ldx >= n");
+  SK_ARG(c, m < (1LL << 31) && n < (1LL << 31), "sk_select_cols_deim: size out of range");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf st;
+  SK_TRY(st.alloc(c, sizeof(int64_t)));
+  SK_TRY(select_cols_deim(c, A, m, n, lda, X, l, ldx, k, Js, st.as<int64_t>()));
+  return finish_info(c, st.as<int64_t>(), info, "sk_select_cols_deim");
+}
+
 sk_status sk_gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* Js,
                          int64_t k, double* C, int64_t ldc) {
   if (!c) return SK_E_ARG;

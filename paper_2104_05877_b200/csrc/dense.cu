@@ -231,6 +231,13 @@ __global__ void k_transpose_any(const double* In, int64_t rows, int64_t cols, in
   }
 }
 
+__global__ void k_upper_triangle(const double* B, int64_t ldb, int64_t n, double* R, int64_t ldr) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    R[i + j * ldr] = i <= j ? B[i + j * ldb] : 0.0;
+  }
+}
+
 constexpr size_t kDiagInvSmem = 2 * TB2 * (TB2 + 1) * sizeof(double);
 constexpr size_t kRtmSmem = (TB2 + 32) * (TB2 + 1) * sizeof(double);
 
@@ -251,6 +258,13 @@ sk_status dense_attrs(sk_ctx* c) {
 sk_status gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t lda, const int64_t* J, int64_t k,
                       double* C, int64_t ldc) {
   return gather_cols_shard(c, A, m, lda, 0, INT64_MAX, J, k, C, ldc);
+}
+
+sk_status upper_triangle(sk_ctx* c, const double* B, int64_t ldb, int64_t n, double* R, int64_t ldr) {
+  if (n == 0) return SK_OK;
+  const int blocks = (int)std::min<int64_t>(cdiv(n * n, 256), 4LL * c->num_sms);
+  k_upper_triangle<<<blocks, 256, 0, c->stream>>>(B, ldb, n, R, ldr);
+  return launched(c);
 }
 
 sk_status transpose(sk_ctx* c, const double* In, int64_t rows, int64_t cols, int64_t ldin, double* Out,

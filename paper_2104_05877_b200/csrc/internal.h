@@ -43,6 +43,14 @@ sk_status lupp(sk_ctx* c, const double* P, bool row_major, int64_t n, int64_t k,
                int64_t* Js, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps,
                int64_t* status_dev);
 
+// Q (rows x k, ld rows) = an orthonormal basis of range(C) (C rows x k, ld rows): LUPP basis +
+// CholeskyQR2, or shifted CholeskyQR3 for panels taller than one cluster's LUPP (residual.cu).
+sk_status orthonormal_basis(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q, int64_t* status_dev);
+// R (n x n, ldr) = upper triangle of B (first n columns, ldb), zeros below (dense.cu).
+sk_status upper_triangle(sk_ctx* c, const double* B, int64_t ldb, int64_t n, double* R, int64_t ldr);
+// RSVD-DEIM column skeletons from A and its row sketch X (deim.cu).
+sk_status select_cols_deim(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t l,
+                           int64_t ldx, int64_t k, int64_t* Js, int64_t* status_dev);
 // Tallest panel the cluster LUPP handles (rows).
 int64_t lupp_max_rows(sk_ctx* c);
 

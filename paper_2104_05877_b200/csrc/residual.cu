@@ -41,8 +41,7 @@ static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows,
   return cholqr2(c, Q, rows, k, rows, status_dev);
 }
 
-static sk_status basis_from_cols(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q,
-                                 int64_t* status_dev) {
+sk_status orthonormal_basis(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q, int64_t* status_dev) {
   if (rows > lupp_max_rows(c)) return basis_shifted_cholqr3(c, C, rows, k, Q, status_dev);
   DBuf piv;
   SK_TRY(piv.alloc(c, (size_t)k * sizeof(int64_t)));
@@ -65,14 +64,14 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
     SK_TRY(Cb.alloc(c, (size_t)m * k * sizeof(double)));
     SK_TRY(Qc.alloc(c, (size_t)m * k * sizeof(double)));
     SK_TRY(gather_cols(c, A, m, lda, Js, k, Cb.as<double>(), m));
-    SK_TRY(basis_from_cols(c, Cb.as<double>(), m, k, Qc.as<double>(), status_dev));
+    SK_TRY(orthonormal_basis(c, Cb.as<double>(), m, k, Qc.as<double>(), status_dev));
     Cb.release();
   }
   if (kind == SK_RES_ROW_ID || kind == SK_RES_CUR) {
     SK_TRY(Rt.alloc(c, (size_t)n * k * sizeof(double)));
     SK_TRY(Qr.alloc(c, (size_t)n * k * sizeof(double)));
     SK_TRY(gather_rows_t(c, A, n, lda, Is, k, Rt.as<double>(), n));
-    SK_TRY(basis_from_cols(c, Rt.as<double>(), n, k, Qr.as<double>(), status_dev));
+    SK_TRY(orthonormal_basis(c, Rt.as<double>(), n, k, Qr.as<double>(), status_dev));
     Rt.release();
   }
   if (kind == SK_RES_COL_ID) {
@@ -104,7 +103,7 @@ sk_status residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_
   SK_TRY(Qc.alloc(c, (size_t)m * k * sizeof(double)));
   SK_CUDA(c, cudaMemcpy2DAsync(Cc.p, (size_t)m * sizeof(double), C, (size_t)ldc * sizeof(double), (size_t)m * sizeof(double),
                                (size_t)k, cudaMemcpyDeviceToDevice, c->stream));
-  SK_TRY(basis_from_cols(c, Cc.as<double>(), m, k, Qc.as<double>(), status_dev));
+  SK_TRY(orthonormal_basis(c, Cc.as<double>(), m, k, Qc.as<double>(), status_dev));
   Cc.release();
   SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
   SK_TRY(gemm(c, true, false, k, n, m, 1.0, Qc.as<double>(), m, A, lda, 0.0, W.as<double>(), k));

@@ -132,6 +132,20 @@ def test_sketch_srtt_rejects_non_power_of_two():
     assert e.value.status == 1
 
 
+# ------------------------------------------------------------------ RSVD-DEIM (8(f) rank 4)
+@pytest.mark.parametrize("k,l", [(20, 40), (10, 30)])
+def test_select_cols_deim_c1(k, l):
+    from oracle import deim as o_deim
+    A, sigma = make_c1(seed=1001)
+    Ad = dev_f(A)
+    X = sk.sketch(Ad, l, "gaussian", 2001)
+    Js = sk.select_cols_deim(Ad, X, k)
+    Xo = o_sketch.sketch(A, l, "gaussian", 2001)
+    assert Js.cpu().tolist() == o_deim.select_cols_deim(A, Xo, k).tolist()
+    r, nA = sk.residual(Ad, Js, None, "col_id")
+    assert r >= o_res.optimal_error(sigma, k) * (1 - 1e-12)
+
+
 # ------------------------------------------------------------------ S1' sparse sketch
 @pytest.mark.parametrize("m,n,l,zeta,seed", [
     (1000, 100, 60, 8, 2003),

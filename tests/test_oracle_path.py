@@ -98,6 +98,25 @@ def test_streaming_alg3_closed_forms_and_exact_rank_cur():
     assert r <= 1e-12 * nA
 
 
+def test_rsvd_deim_exact_rank_recovers_true_singular_vectors():
+    # eq:rsvd_procedures: when rank(A) = l the sketch's row space is row(A), so V^ equals A's right
+    # singular vectors up to sign (closed form from the construction), and DEIM on V^ equals LUPP
+    # on those true vectors.
+    from oracle import deim
+    rng = np.random.default_rng(8)
+    m, n, l = 60, 40, 6
+    U, _ = np.linalg.qr(rng.standard_normal((m, l)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, l)))
+    s = np.array([6.0, 4.0, 3.0, 2.0, 1.5, 1.0])
+    A = (U * s) @ V.T
+    X = sketch.sketch(A, l, "gaussian", 4)
+    Vh = deim.rsvd_vectors(A, X)
+    np.testing.assert_allclose(np.abs(np.sum(Vh * V, axis=0)), np.ones(l), atol=1e-10)
+    piv = deim.select_cols_deim(A, X, 4)
+    piv_true, _, _, _ = lupp.lupp_panel(V[:, :4], 4)
+    assert piv.tolist() == piv_true.tolist()
+
+
 # ----------------------------------------------------------------------------- LUPP
 def test_lupp_spec_2x2_case():
     # X = [[4,2],[1,3]] -> pivots [1,2] (1-based), L_l = [[4,0],[1,2.5]], R = [[1,.5],[0,1]].
