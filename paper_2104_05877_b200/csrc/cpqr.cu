@@ -148,8 +148,9 @@ __global__ void __launch_bounds__(QNT, 1) k_cpqr(QParams p) {
     for (int i = t + threadIdx.x; i < l; i += QNT) v[i] = *(volatile const double*)&wcol[i];
     __syncthreads();
     if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int i = t; i < l; ++i) s = fma(v[i], v[i], s);   // fixed order
+      // the winner's remaining squared norm is the value every CTA just reduced (computed once by
+      // its owner in a fixed order), so no serial O(l) pass on the critical path
+      const double s = s_alpha;
       const double nx = sqrt(s);
       const double alpha = v[t] >= 0.0 ? -nx : nx;
       const double vt = v[t] - alpha;
