@@ -386,7 +386,7 @@ def main():
 
     Js, Jc, res, nA = out
     from oracle.residual import optimal_error  # closed form sum_{i>k} sigma_i^2 (Eckart-Young)
-    opt = optimal_error(sigma, k)
+    opt = optimal_error(sigma, k) if sigma is not None else None   # C4 has no closed-form spectrum
 
     # roofline of the dominant kernel of the selection: the sketch (one launch per call)
     sk_ms = statistics.mean(stage_ms["sketch"])
@@ -458,7 +458,7 @@ def main():
                        "parallelism": "replicas" if world > 1 else "1 GPU"},
             "stages_ms": {nm: statistics.mean(v) for nm, v in stage_ms.items()},
             "sketch_rate": {"value": achieved, "unit": roofline["unit"]},
-            "residual": {"col_id_fro": res, "normA_fro": nA, "opt_fro": opt, "ratio": res / opt if opt > 0 else None},
+            "residual": {"col_id_fro": res, "normA_fro": nA, "opt_fro": opt, "ratio": res / opt if opt else None},
             "cpqr_overlap": int(len(set(Js.cpu().tolist()) & set(Jc.cpu().tolist()))),
             "roofline": roofline,
             "cpu_baseline": cpu,
