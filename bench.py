@@ -156,18 +156,18 @@ def run_reference(args):
     steps = max(1, min(args.steps, 3))
     warm = min(args.warmup, 1)
     for _ in range(warm):
-        oracle_selection(A, k, l, seed)
+        oracle_selection(A, k, l, seed, cfg["emb"])
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        oracle_selection(A, k, l, seed)
+        oracle_selection(A, k, l, seed, cfg["emb"])
         times.append((time.perf_counter() - t0) * 1e3)
     v = statistics.mean(times)
     line = {
         "impl": "reference", "metric": "skeleton-selection time (sketch+LUPP)", "value": v, "unit": "ms",
         "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": v, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "m": 4096, "n": 4096, "k": k, "l": l},
+        "config": {"workload": desc, "m": int(A.shape[0]), "n": int(A.shape[1]), "k": k, "l": l},
         "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "oracle",
                          "sample": f"full {args.config} selection (oracle sketch + LUPP) on {model}"},
         "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -440,7 +440,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and A_np is not None:
         cores, model = cpu_info()
         t0 = time.perf_counter()
-        piv_o = oracle_selection(A_np, k, l, seed)
+        piv_o = oracle_selection(A_np, k, l, seed, emb)
         cpu_ms = (time.perf_counter() - t0) * 1e3
         same = int(np.sum(piv_o == Js.cpu().numpy()))
         cpu = {"value": cpu_ms, "unit": "ms", "cores": cores, "kind": "oracle",
