@@ -145,6 +145,37 @@ sk_status sk_select_cols(sk_ctx* ctx, const double* X, int64_t l, int64_t n, int
                          int64_t k, int64_t* Js, double* Lf, int64_t ldlf, double* U,
                          int64_t ldu, double* gaps, int64_t* info);
 
+/* ---- S2 on a column-sharded sketch, one exchange per pivot step ----
+ * The same k-step LUPP as sk_select_cols (eq:def_LUPP; R5-R7), with the n x k panel
+ * M = X(0:k, :)^T split by rows over P ranks: rank r owns global rows col0 .. col0 + nloc - 1
+ * (the sketch columns of its block of A).  Per step every rank proposes its best active row as a
+ * RECORD of SK_LUPP_DIST_REC(k) doubles; the caller all-gathers the P records (any order) into
+ * `gathered` (P x REC, contiguous) and calls sk_lupp_dist_step, which applies the merged decision
+ * (max |value|, ties to the lowest GLOBAL index; rank failure below 1e-14 max|panel| over all
+ * ranks) to this rank's rows and writes the next proposal.  Pivots, Lf and U equal
+ * sk_select_cols on the unsharded panel.  No call synchronises or allocates, so the k-step
+ * sequence (steps interleaved with the collective) can be captured in a CUDA graph.
+ *   state   device buffer of sk_lupp_dist_state_bytes(nloc, k) bytes, caller-owned, holds the
+ *           local panel copy; one per concurrent selection.
+ *   X       rows 0..k-1 of this rank's l x nloc row-major sketch block (ldx >= nloc); read by
+ *           sk_lupp_dist_begin only.  nloc may be 0 (a rank with no columns).
+ *   cand    device double[REC]: this rank's proposal, written by begin (step 0) and by
+ *           sk_lupp_dist_step(t) for t < k.
+ *   Js      device int64[k] (replicated on every rank), written at t = 1..k; -1 from the failing
+ *           step on after a rank failure.
+ *   Lf      NULL or nloc x k column-major (ldlf >= nloc): this rank's rows of sk_select_cols' Lf.
+ *   U       NULL or k x k column-major (ldu >= k), replicated.
+ * Call begin, then for t = 1..k: all-gather(cand -> gathered), sk_lupp_dist_step(t).  Then
+ * sk_lupp_dist_info (synchronises) returns SK_E_RANK with *info = the failing 1-based step. */
+#define SK_LUPP_DIST_REC(k) ((k) + 4)
+size_t sk_lupp_dist_state_bytes(int64_t nloc, int64_t k);
+sk_status sk_lupp_dist_begin(sk_ctx* ctx, const double* X, int64_t nloc, int64_t ldx, int64_t k, int64_t col0,
+                             void* state, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand);
+sk_status sk_lupp_dist_step(sk_ctx* ctx, void* state, int64_t nloc, int64_t k, int64_t col0, int64_t t,
+                            const double* gathered, int32_t world, int64_t* Js, double* Lf, int64_t ldlf,
+                            double* U, int64_t ldu, double* cand);
+sk_status sk_lupp_dist_info(sk_ctx* ctx, const void* state, int64_t* info);
+
 /* ---- S2': column skeletons by CPQR on the sketch (eq:def_QRCP; Sec. 5 "Rand-CPQR") ----
  * k steps of Householder QR with column pivoting on all l rows of X; the pivot
  * is the active column of largest remaining norm, norms recomputed

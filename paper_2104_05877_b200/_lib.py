@@ -33,6 +33,10 @@ _SIGS = {
     "sk_id_coeffs": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, ctypes.POINTER(ctypes.c_double)],
     "sk_residual": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, c_int, c_dp, c_i64,
                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
+    "sk_lupp_dist_begin": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, c_dp, c_i64, c_dp],
+    "sk_lupp_dist_step": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, ctypes.c_int32, c_dp, c_dp, c_i64, c_dp,
+                          c_i64, c_dp],
+    "sk_lupp_dist_info": [c_dp, c_dp, ctypes.POINTER(c_i64)],
     "sk_rand_lupp": [c_dp, c_dp, c_int, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64,
                      c_i64, c_dp, c_dp, ctypes.POINTER(c_i64)],
 }
@@ -42,6 +46,7 @@ _OTHER = {
     "sk_version": ([], ctypes.c_char_p),
     "sk_workspace_bytes": ([c_dp], c_i64),
     "sk_launch_count": ([c_dp], c_i64),
+    "sk_lupp_dist_state_bytes": ([c_i64, c_i64], ctypes.c_size_t),
 }
 
 # every symbol include/skel.h declares

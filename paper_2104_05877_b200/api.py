@@ -268,3 +268,49 @@ def rand_lupp(A, k, l=None, embedding="gaussian", seed=0, zeta=8, rows=False, de
                             seed & (2**64 - 1), k, _ptr(Js), _ptr(Is), ctypes.byref(info))
     _check(st, h, info.value)
     return Js, Is
+
+
+class LuppDist:
+    """Per-step-exchange column LUPP on this rank's sketch block (sk_lupp_dist_*).
+
+    ``begin(X_local)`` copies rows 0..k-1 of the l x nloc row-major block and writes the step-0
+    proposal into ``cand``; then, for t = 1..k, the caller all-gathers ``cand`` into ``gathered``
+    (world x rec) and calls ``step(t)``.  Buffers are allocated once here, so the sequence can be
+    captured in a CUDA graph.  Js (replicated), Lf (this rank's rows) and U are the results."""
+
+    def __init__(self, nloc, k, col0, world, device=None, want_factors=True):
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.nloc, self.k, self.col0, self.world, self.device = nloc, k, col0, world, dev
+        self.rec = k + 4
+        nbytes = int(lib().sk_lupp_dist_state_bytes(nloc, k))
+        self.state = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.cand = torch.empty(self.rec, dtype=torch.float64, device=dev)
+        self.gathered = torch.empty(world * self.rec, dtype=torch.float64, device=dev)
+        self.Js = torch.empty(k, dtype=torch.int64, device=dev)
+        self.Lf = torch.empty((k, max(nloc, 1)), dtype=torch.float64, device=dev).t() if want_factors else None
+        self.U = torch.empty((k, k), dtype=torch.float64, device=dev).t() if want_factors else None
+
+    def begin(self, X_local):
+        if X_local.dtype != torch.float64 or not X_local.is_cuda or X_local.dim() != 2:
+            raise ValueError("X_local must be a 2-D float64 CUDA tensor")
+        if X_local.shape[1] != self.nloc or X_local.shape[0] < self.k:
+            raise ValueError("X_local must be l x nloc with l >= k")
+        if self.nloc > 1 and X_local.stride(1) != 1:
+            raise ValueError("X_local must be row-major")
+        ldx = max(X_local.stride(0), self.nloc) if X_local.shape[0] > 1 else max(self.nloc, 1)
+        h = context(self.device.index)
+        _check(lib().sk_lupp_dist_begin(h, _ptr(X_local), self.nloc, ldx, self.k, self.col0, _ptr(self.state),
+                                        _ptr(self.Lf), max(self.nloc, 1), _ptr(self.U), self.k, _ptr(self.cand)), h)
+
+    def step(self, t):
+        h = context(self.device.index)
+        _check(lib().sk_lupp_dist_step(h, _ptr(self.state), self.nloc, self.k, self.col0, t, _ptr(self.gathered),
+                                       self.world, _ptr(self.Js), _ptr(self.Lf), max(self.nloc, 1), _ptr(self.U),
+                                       self.k, _ptr(self.cand)), h)
+
+    def info(self):
+        """Synchronises; raises SkelError(SK_E_RANK) with .info = the failing 1-based step."""
+        info = ctypes.c_int64(0)
+        h = context(self.device.index)
+        _check(lib().sk_lupp_dist_info(h, _ptr(self.state), ctypes.byref(info)), h, info.value)
+        return 0

@@ -227,6 +227,46 @@ sk_status sk_gather_cols_shard(sk_ctx* c, const double* A, int64_t m, int64_t nc
   return gather_cols_shard(c, A, m, lda, col0, ncols, Js, k, C, ldc);
 }
 
+size_t sk_lupp_dist_state_bytes(int64_t nloc, int64_t k) {
+  if (nloc < 0 || k < 1) return 0;
+  return lupp_dist_state_bytes(nloc, k);
+}
+
+sk_status sk_lupp_dist_begin(sk_ctx* c, const double* X, int64_t nloc, int64_t ldx, int64_t k, int64_t col0,
+                             void* state, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, state && cand && (X || nloc == 0), "sk_lupp_dist_begin: NULL pointer");
+  SK_ARG(c, nloc >= 0 && k >= 1 && col0 >= 0 && ldx >= nloc, "sk_lupp_dist_begin: bad sizes");
+  SK_ARG(c, !Lf || ldlf >= nloc, "sk_lupp_dist_begin: ldlf >= nloc required");
+  SK_ARG(c, !U || ldu >= k, "sk_lupp_dist_begin: ldu >= k required");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  return lupp_dist_begin(c, X, nloc, ldx, k, col0, state, Lf, ldlf, U, ldu, cand);
+}
+
+sk_status sk_lupp_dist_step(sk_ctx* c, void* state, int64_t nloc, int64_t k, int64_t col0, int64_t t,
+                            const double* gathered, int32_t world, int64_t* Js, double* Lf, int64_t ldlf, double* U,
+                            int64_t ldu, double* cand) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, state && gathered && Js && cand, "sk_lupp_dist_step: NULL pointer");
+  SK_ARG(c, nloc >= 0 && k >= 1 && t >= 1 && t <= k && world >= 1 && col0 >= 0, "sk_lupp_dist_step: bad sizes");
+  SK_ARG(c, !Lf || ldlf >= nloc, "sk_lupp_dist_step: ldlf >= nloc required");
+  SK_ARG(c, !U || ldu >= k, "sk_lupp_dist_step: ldu >= k required");
+  return lupp_dist_step(c, state, nloc, k, col0, t, gathered, world, Js, Lf, ldlf, U, ldu, cand);
+}
+
+sk_status sk_lupp_dist_info(sk_ctx* c, const void* state, int64_t* info) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, state && info, "sk_lupp_dist_info: NULL pointer");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf st;
+  SK_TRY(st.alloc(c, sizeof(int64_t)));
+  SK_TRY(lupp_dist_status(c, state, st.as<int64_t>()));
+  return finish_info(c, st.as<int64_t>(), info, "sk_lupp_dist");
+}
+
 sk_status sk_residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* C, int64_t k,
                            int64_t ldc, double* sums) {
   if (!c) return SK_E_ARG;

@@ -54,6 +54,16 @@ sk_status select_cols_deim(sk_ctx* c, const double* A, int64_t m, int64_t n, int
 // Tallest panel the cluster LUPP handles (rows).
 int64_t lupp_max_rows(sk_ctx* c);
 
+// ---------------------------------------------------------------- distributed LUPP (lupp_dist.cu)
+// Per-step-exchange column LUPP on a column-sharded panel; see include/skel.h.
+size_t lupp_dist_state_bytes(int64_t nloc, int64_t k);
+sk_status lupp_dist_begin(sk_ctx* c, const double* X, int64_t nloc, int64_t ldx, int64_t k, int64_t col0, void* state,
+                          double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand);
+sk_status lupp_dist_step(sk_ctx* c, void* state, int64_t nloc, int64_t k, int64_t col0, int64_t t,
+                         const double* gathered, int world, int64_t* Js, double* Lf, int64_t ldlf, double* U,
+                         int64_t ldu, double* cand);
+sk_status lupp_dist_status(sk_ctx* c, const void* state, int64_t* status_dev_out);
+
 // ---------------------------------------------------------------- CPQR (cpqr.cu)
 sk_status cpqr(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, int64_t k,
                int64_t* Js, double* R, int64_t ldr, int64_t* status_dev);

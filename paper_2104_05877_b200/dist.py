@@ -6,11 +6,16 @@ One process per GPU.  A (m x n) is split into contiguous column blocks, rank r o
   sketch      X_r = Gamma A_r on every rank, no communication: Gamma(r, i) depends only on the
               seed and the row index i of A (R1), which is not sharded, so every rank
               regenerates the same Gamma and X = [X_0, X_1, ...] column-wise (Alg. 2 line 2).
-  select_cols the k sketch rows that column LUPP can read (R5) are all-gathered
-              (k x n doubles, one collective) and every rank runs the same deterministic
-              cluster LUPP kernel on identical bytes -> identical J_s on every rank
-              ("gather-then-replicate", SURVEY 8(e) variant ii).  Ties go to the lowest GLOBAL
-              index (R6), so the result equals single-GPU LUPP on the unsharded sketch.
+  select_cols two exchange patterns, both equal to single-GPU LUPP on the unsharded sketch
+              (ties to the lowest GLOBAL index, R6):
+              "step" (the per-step design): the panel stays sharded; at each of the
+              k pivot steps every rank proposes its best active row as one record (value,
+              global index, the row) and ONE all-gather of P records lets every rank apply the
+              same decision to its own rows (sk_lupp_dist_*; ``select_cols_stepwise``;
+              ``CapturedStepwise`` replays the k steps as one CUDA graph).
+              "replicate" (variant ii): the k sketch rows that column LUPP can read (R5) are
+              all-gathered once (k x n doubles) and every rank runs the single-GPU cluster
+              LUPP kernel on identical bytes.
   gather C    each rank writes the skeleton columns it owns (zeros elsewhere,
               sk_gather_cols_shard) and a sum all-reduce assembles C = A(:, J_s) exactly.
   select_rows row LUPP on the replicated C, identical on every rank (Alg. 2 line 4).
@@ -52,6 +57,9 @@ class CudaBackend:
         Js, Lf, U, _ = self.api.select_cols(Xk, k)
         return Js, Lf
 
+    def lupp_dist(self, nloc, k, col0, world, device=None):
+        return self.api.LuppDist(nloc, k, col0, world, device)
+
     def select_rows(self, C, k):
         Is, _, _, _ = self.api.select_rows(C, k)
         return Is
@@ -78,8 +86,62 @@ def _all_gather_cols(local, n_global, group, world):
     return torch.cat(cols, dim=1).contiguous()
 
 
+def _stepwise_loop(sel, k, group):
+    for t in range(1, k + 1):
+        dist.all_gather_into_tensor(sel.gathered, sel.cand, group=group)
+        sel.step(t)
+
+
+def select_cols_stepwise(X_local, n_global, k, group=None, backend=None):
+    """Column LUPP with one all-gather of P records per pivot step.
+    X_local: this rank's l x ncols sketch block (row-major).  Returns (Js replicated, Lf rows of
+    this rank's block, U replicated); raises on a rank failure (R7)."""
+    backend = backend or CudaBackend()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    col0, nloc = shard(n_global, world, rank)
+    if X_local.shape[1] != nloc:
+        raise ValueError(f"rank {rank}: X_local has {X_local.shape[1]} columns, shard() expects {nloc}")
+    if not (1 <= k <= X_local.shape[0]) or k > n_global:
+        raise ValueError("need 1 <= k <= l and k <= n")
+    sel = backend.lupp_dist(nloc, k, col0, world, X_local.device.index if X_local.is_cuda else None)
+    sel.begin(X_local)
+    _stepwise_loop(sel, k, group)
+    sel.info()
+    return sel.Js, sel.Lf, sel.U
+
+
+class CapturedStepwise:
+    """select_cols_stepwise with begin + the k (all-gather, step) pairs captured once in a CUDA
+    graph over fixed buffers (NCCL collectives are graph-capturable): ``run()`` replays it with
+    no per-step host work.  ``X_local`` is read at every replay (update it in place)."""
+
+    def __init__(self, X_local, n_global, k, group=None):
+        from . import api
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        col0, nloc = shard(n_global, world, rank)
+        self.k, self.group, self.X = k, group, X_local
+        self.sel = api.LuppDist(nloc, k, col0, world, X_local.device.index)
+        self._eager()                                   # warm-up: NCCL communicator, library context
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.sel.begin(self.X)
+            _stepwise_loop(self.sel, k, group)
+
+    def _eager(self):
+        self.sel.begin(self.X)
+        _stepwise_loop(self.sel, self.k, self.group)
+        self.sel.info()
+
+    def run(self):
+        self.graph.replay()
+        return self.sel.Js, self.sel.Lf, self.sel.U
+
+
 def dist_rand_lupp(A_local, n_global, k, l, embedding="gaussian", seed=0, zeta=8, rows=False,
-                   residual=False, group=None, backend=None):
+                   residual=False, group=None, backend=None, exchange="replicate"):
     """Algorithm 2 on a column-sharded A.  A_local: this rank's block (m x ncols, column-major).
 
     Returns a dict with J_s (global column indices, replicated), I_s (if rows), the skeleton
@@ -96,8 +158,13 @@ def dist_rand_lupp(A_local, n_global, k, l, embedding="gaussian", seed=0, zeta=8
         raise ValueError("need 1 <= k <= l <= m and k <= n")
     out = {"col0": col0, "ncols": ncols}
     X_local = backend.sketch(A_local, l, embedding, seed, zeta)               # l x ncols
-    Xk = _all_gather_cols(X_local[:k], n_global, group, world)                # k x n (rows 0..k-1)
-    Js, Lf = backend.select_cols(Xk, k)
+    if exchange == "step":
+        Js, Lf, _ = select_cols_stepwise(X_local, n_global, k, group, backend)  # Lf: this rank's rows
+    elif exchange == "replicate":
+        Xk = _all_gather_cols(X_local[:k], n_global, group, world)            # k x n (rows 0..k-1)
+        Js, Lf = backend.select_cols(Xk, k)
+    else:
+        raise ValueError("exchange must be 'step' or 'replicate'")
     out["Js"] = Js
     out["Lf"] = Lf
     if rows or residual:

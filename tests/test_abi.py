@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "skel.h")
 
 def declared():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:sk_status|void|const char\*|int64_t)\s+(sk_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:sk_status|void|const char\*|int64_t|size_t)\s+(sk_\w+)\s*\(", txt, re.M)))
 
 
 def test_header_declares_the_boundary():

@@ -137,3 +137,130 @@ def test_dist_rand_lupp_gloo_matches_unsharded_oracle(world):
         assert abs(r - r_or) <= 1e-12 * r_or + 4 * 2.0 ** -53 * n_or
         assert abs(nA - n_or) <= 1e-14 * n_or
     assert math.isfinite(res[0][4])
+
+
+# ---------------------------------------------------------------- per-step exchange
+class HostLuppDist:
+    """Test stand-in for api.LuppDist (the sk_lupp_dist_* kernels): the same record protocol --
+    [|value| or -1, global index or -1, local max|panel|, 0, row] -- in numpy, so the per-step
+    all-gather of dist.select_cols_stepwise runs over gloo on CPU."""
+
+    def __init__(self, nloc, k, col0, world, device=None):
+        self.nloc, self.k, self.col0, self.world = nloc, k, col0, world
+        self.rec = k + 4
+        self.cand = torch.zeros(self.rec, dtype=torch.float64)
+        self.gathered = torch.zeros(world * self.rec, dtype=torch.float64)
+        self.Js = torch.full((k,), -1, dtype=torch.int64)
+        self.Lf = torch.zeros((nloc, k), dtype=torch.float64)
+        self.U = torch.zeros((k, k), dtype=torch.float64)
+        self.status = 0
+
+    def begin(self, X_local):
+        self.M = X_local[:self.k].numpy().T.copy()
+        self.act = np.ones(self.nloc, dtype=bool)
+        self.lmax = float(np.max(np.abs(self.M))) if self.M.size else 0.0
+        self.status = 0
+        self._propose(0)
+
+    def _propose(self, t):
+        c = np.zeros(self.rec)
+        c[:3] = (-1.0, -1.0, self.lmax)
+        if self.act.any():
+            a = np.where(self.act, np.abs(self.M[:, t]), -1.0)
+            i = int(np.argmax(a))
+            c[0], c[1], c[4:] = a[i], self.col0 + i, self.M[i]
+        self.cand.copy_(torch.from_numpy(c))
+
+    def step(self, t):
+        if self.status:
+            return
+        G = self.gathered.view(self.world, self.rec).numpy()
+        gmax = float(G[:, 2].max())
+        best = None
+        for w in range(self.world):
+            if G[w, 1] >= 0 and (best is None or G[w, 0] > G[best, 0] or
+                                 (G[w, 0] == G[best, 0] and G[w, 1] < G[best, 1])):
+                best = w
+        if best is None or not (G[best, 0] > 1e-14 * gmax):
+            self.status = t
+            self.Js[t - 1:] = -1
+            return
+        g, row = int(G[best, 1]), G[best, 4:].copy()
+        self.Js[t - 1] = g
+        self.U[t - 1, t - 1:] = torch.from_numpy(row[t - 1:])
+        Lf = self.Lf.numpy()
+        if self.col0 <= g < self.col0 + self.nloc:
+            self.act[g - self.col0] = False
+            Lf[g - self.col0, t - 1] = 1.0
+        rows = np.nonzero(self.act)[0]
+        mult = self.M[rows, t - 1] / row[t - 1]
+        Lf[rows, t - 1] = mult
+        self.M[rows, t:] -= np.outer(mult, row[t:])
+        if t < self.k:
+            self._propose(t)
+
+    def info(self):
+        if self.status:
+            raise o_lupp.RankError(self.status)
+        return 0
+
+
+class HostStepBackend(HostBackend):
+    def lupp_dist(self, nloc, k, col0, world, device=None):
+        return HostLuppDist(nloc, k, col0, world)
+
+
+def _step_worker(rank, world, port, X, k, q):
+    from paper_2104_05877_b200.dist import select_cols_stepwise
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = X.shape[1]
+        c0, nc = shard(n, world, rank)
+        Xl = torch.from_numpy(np.ascontiguousarray(X[:, c0:c0 + nc]))
+        try:
+            Js, Lf, U = select_cols_stepwise(Xl, n, k, backend=HostStepBackend())
+            q.put((rank, "ok", Js.tolist(), Lf.numpy().copy(), U.numpy().copy()))
+        except o_lupp.RankError as e:
+            q.put((rank, "rank", e.step, None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_step(X, k, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, world, port, X, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("n,k,world", [(251, 20, 2), (100, 12, 3), (2, 2, 3)])
+def test_stepwise_gloo_equals_single_lupp(n, k, world):
+    # ragged shards; (2, 2, 3) leaves rank 2 with no columns (it proposes "none" every step)
+    X = np.random.default_rng(n + world).standard_normal((k + 3, n))
+    res = _run_step(X, k, world)
+    piv, Lf, U, _ = o_lupp.select_cols(X, k)
+    for rank, kind, Js, _, Ur in res:
+        assert kind == "ok" and Js == piv.tolist(), rank
+        np.testing.assert_array_equal(Ur, U)
+    np.testing.assert_array_equal(np.vstack([r[3] for r in res]), Lf)    # rank blocks stack to Lf
+
+
+def test_stepwise_gloo_ties_and_rank_failure():
+    l = 6
+    X = kahan_witness(l, 14)[:, np.r_[np.arange(l, 14), np.arange(l)]]   # tied columns in the last shard
+    res = _run_step(X, l, 3)
+    piv, _, _, _ = o_lupp.select_cols(X, l)
+    assert all(r[2] == piv.tolist() for r in res)
+    Z = np.zeros((4, 9))
+    Z[0, 3] = 1.0                                                       # rank 1 after step 1
+    res = _run_step(Z, 3, 2)
+    assert all(r[1] == "rank" and r[2] == 2 for r in res)

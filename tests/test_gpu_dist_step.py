@@ -1,0 +1,150 @@
+"""GPU parity of the per-step-exchange column LUPP (sk_lupp_dist_*).
+
+The P ranks of the column-sharded path are emulated in ONE process on one GPU: P LuppDist
+states over the P column blocks of the sketch, and the all-gather of their records done as a
+device copy between steps.  No kernel waits on another rank, so this is the exact per-step
+protocol without a multi-GPU launch.  The update rounds like the oracle (no FMA contraction), so
+pivots, U and the stacked Lf are compared BIT FOR BIT with oracle.lupp.select_cols on the
+unsharded sketch.  The NCCL tests run the real collective at world size 1 (eager and captured
+in a CUDA graph).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2104_05877_b200 as sk
+from inputs import kahan_witness, make_c2
+from oracle import lupp as o_lupp
+from oracle import sketch as o_sketch
+from paper_2104_05877_b200.dist import shard
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def emulate(X, k, world):
+    """Run the P-rank protocol in one process. Returns (Js, Lf stacked, U, info)."""
+    n = X.shape[1]
+    sels, blocks = [], []
+    for r in range(world):
+        c0, nc = shard(n, world, r)
+        sels.append(sk.LuppDist(nc, k, c0, world, 0))
+        blocks.append(torch.from_numpy(np.ascontiguousarray(X[:, c0:c0 + nc])).to(DEV))
+    for s, b in zip(sels, blocks):
+        s.begin(b)
+    for t in range(1, k + 1):
+        g = torch.cat([s.cand for s in sels])
+        for s in sels:
+            s.gathered.copy_(g)
+            s.step(t)
+    infos = []
+    for s in sels:
+        try:
+            infos.append(s.info())
+        except sk.SkelError as e:
+            infos.append(e.info)
+    Js = [s.Js.cpu().numpy() for s in sels]
+    for j in Js[1:]:
+        np.testing.assert_array_equal(j, Js[0])                       # replicated
+    Us = [s.U.cpu().numpy() for s in sels]
+    for u in Us[1:]:
+        np.testing.assert_array_equal(u, Us[0])
+    Lf = np.vstack([s.Lf.cpu().numpy()[:s.nloc] for s in sels])
+    return Js[0], Lf, Us[0], infos
+
+
+@pytest.mark.parametrize("n,k,world", [(251, 20, 1), (251, 20, 3), (1000, 64, 8), (300, 40, 7), (5, 5, 8)])
+def test_stepwise_bitwise_equals_oracle(n, k, world):
+    # (5, 5, 8): three ranks own no column; (300, 40, 7): ragged blocks spanning several CTAs
+    X = np.random.default_rng(7 * n + k).standard_normal((k + 5, n))
+    Js, Lf, U, infos = emulate(X, k, world)
+    piv, Lfo, Uo, _ = o_lupp.select_cols(X, k)
+    assert infos == [0] * world
+    np.testing.assert_array_equal(Js, piv)
+    np.testing.assert_array_equal(U, Uo)
+    np.testing.assert_array_equal(Lf, Lfo)
+
+
+def test_stepwise_c2_k512_full_size():
+    """C2 at the bench configuration: the oracle sketch (l = 522) of the 4096^2 input, 4 shards."""
+    A, _ = make_c2(seed=1002)
+    X = o_sketch.sketch(A, 522, "gaussian", 2002 + 512)
+    Js, Lf, U, infos = emulate(X, 512, 4)
+    piv, Lfo, Uo, _ = o_lupp.select_cols(X, 512)
+    assert infos == [0] * 4
+    np.testing.assert_array_equal(Js, piv)
+    np.testing.assert_array_equal(U, Uo)
+    np.testing.assert_array_equal(Lf, Lfo)
+
+
+def test_stepwise_ties_straddle_shards():
+    l = 10
+    X = kahan_witness(l, 40)[:, np.r_[np.arange(l, 40), np.arange(l)]]
+    for world in (2, 3, 5):
+        Js, _, U, infos = emulate(X, l, world)
+        piv, _, Uo, _ = o_lupp.select_cols(X, l)
+        np.testing.assert_array_equal(Js, piv)
+        np.testing.assert_array_equal(U, Uo)
+        assert infos == [0] * world
+
+
+def test_stepwise_rank_failure():
+    Z = np.zeros((6, 50))
+    Z[0, 31] = 3.0
+    Z[1, 7] = 1e-20                                                    # below 1e-14 max|panel|
+    Js, _, _, infos = emulate(Z, 4, 3)
+    assert infos == [2, 2, 2]
+    assert Js[0] == 31 and (Js[1:] == -1).all()
+
+
+def _nccl_world1(port):
+    import torch.distributed as tdist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
+    return tdist
+
+
+def test_stepwise_nccl_world1_eager_and_graph():
+    from paper_2104_05877_b200.dist import CapturedStepwise, select_cols_stepwise
+    tdist = _nccl_world1(29541)
+    try:
+        X = np.random.default_rng(5).standard_normal((70, 700))
+        piv, Lfo, Uo, _ = o_lupp.select_cols(X, 64)
+        Xd = torch.from_numpy(X).to(DEV)
+        Js, Lf, U = select_cols_stepwise(Xd, 700, 64)
+        np.testing.assert_array_equal(Js.cpu().numpy(), piv)
+        np.testing.assert_array_equal(Lf.cpu().numpy(), Lfo)
+        cap = CapturedStepwise(Xd, 700, 64)
+        for _ in range(2):
+            cap.sel.Js.fill_(-7)
+            Js, Lf, U = cap.run()
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(Js.cpu().numpy(), piv)
+            np.testing.assert_array_equal(U.cpu().numpy(), Uo)
+        X2 = np.random.default_rng(6).standard_normal((70, 700))        # new data, same graph
+        Xd.copy_(torch.from_numpy(X2))
+        Js, _, _ = cap.run()
+        piv2, _, _, _ = o_lupp.select_cols(X2, 64)
+        np.testing.assert_array_equal(Js.cpu().numpy(), piv2)
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_dist_rand_lupp_step_exchange_nccl_world1():
+    from inputs import make_c1
+    from paper_2104_05877_b200.dist import dist_rand_lupp
+    tdist = _nccl_world1(29543)
+    try:
+        A, _ = make_c1(seed=1001)
+        Ad = sk.fortran(torch.from_numpy(A).to(DEV))
+        out = dist_rand_lupp(Ad, 256, 20, 40, "gaussian", 2001, rows=True, exchange="step")
+        X = o_sketch.sketch(A, 40, "gaussian", 2001)
+        piv, _, _, _ = o_lupp.select_cols(X, 20)
+        assert out["Js"].cpu().tolist() == piv.tolist()
+        ipiv, _, _, _ = o_lupp.select_rows(A[:, piv], 20)
+        assert out["Is"].cpu().tolist() == ipiv.tolist()
+    finally:
+        tdist.destroy_process_group()
