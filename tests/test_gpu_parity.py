@@ -152,12 +152,18 @@ def test_select_cols_deim_c1(k, l):
     (300, 33, 16, 8, 1),
     (517, 70, 510, 8, 4),
     (129, 5, 40, 33, 6),
+    (1300, 4000, 700, 8, 7),     # 48 rows per warp, ragged last chunk and column tile, one i-half per CTA
+    (2048, 9000, 510, 8, 8),     # C3's l, whole chunks, full waves (no i-split)
+    (300, 70, 8, 4, 9),          # zeta < 8
 ])
 def test_sketch_sparse_parity(m, n, l, zeta, seed):
     A = rand_mat(m, n, seed)
-    X = sk.sketch(dev_f(A), l, "sparse_sign", seed, zeta).cpu().numpy()
+    Ad = dev_f(A)
+    X = sk.sketch(Ad, l, "sparse_sign", seed, zeta).cpu().numpy()
     ref = o_sketch.sketch(A, l, "sparse_sign", seed, zeta)
     assert rel_fro(X, ref) <= 1e-12
+    X2 = sk.sketch(Ad, l, "sparse_sign", seed, zeta).cpu().numpy()
+    np.testing.assert_array_equal(X, X2)                     # fixed summation order: deterministic
 
 
 # ------------------------------------------------------------------ S2 select_cols
