@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--piter", type=int, default=0, help="plain power iterations (Rand-LUPP-qpiter, P:527)")
+    ap.add_argument("--dist-exchange", default="replicate", choices=["replicate", "step"],
+                    help="N > 1: column-LUPP exchange -- one k x n all-gather then replicated LUPP, or one "
+                         "all-gather of P records per pivot step (CUDA graph)")
     return ap.parse_args()
 
 
@@ -195,7 +198,7 @@ def main_dist(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(dev)
-    k = args.k
+    k = args.k if args.k is not None else 512              # C2's bench k
     l = k + 10
     seed = 2002 + k
     A_np, _ = make_c2(seed=1002 + rank)
@@ -205,16 +208,24 @@ def main_dist(args, world, rank, local):
     with torch.cuda.stream(stream):
         A = sk.fortran(torch.from_numpy(np.ascontiguousarray(A_np)).to(dev))
         flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+        Xbuf = torch.empty((l, nloc), dtype=torch.float64, device=dev)
     torch.cuda.synchronize(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    cap = []
 
     def step(record):
         e = [ev() for _ in range(5)]
         e[0].record(stream)
-        X = sk.sketch(A, l, "gaussian", seed)
+        X = sk.sketch(A, l, "gaussian", seed, out=Xbuf)
         e[1].record(stream)
-        Xk = _all_gather_cols(X[:k], n_global, None, world)
-        Js, _, _, _ = sk.select_cols(Xk, k, check=False)
+        if args.dist_exchange == "step":
+            if not cap:
+                from paper_2104_05877_b200.dist import CapturedStepwise
+                cap.append(CapturedStepwise(Xbuf, n_global, k))
+            Js, _, _ = cap[0].run()
+        else:
+            Xk = _all_gather_cols(X[:k], n_global, None, world)
+            Js, _, _, _ = sk.select_cols(Xk, k, check=False)
         e[2].record(stream)
         C = sk.gather_cols_shard(A, Js, col0)
         Ct = C.t().contiguous()
@@ -281,7 +292,7 @@ def main_dist(args, world, rank, local):
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"C2-type blocks: A 4096 x {n_global} FP64 column-sharded, 4096 x 4096 "
                                    f"U diag(10^(-i/50)) V^T per rank, Gaussian Omega, k={k}, l={l}",
-                       "m": m, "n": n_global, "k": k, "l": l, "parallelism": f"column-sharded x{world}",
+                       "m": m, "n": n_global, "k": k, "l": l, "parallelism": f"column-sharded x{world}", "lupp_exchange": args.dist_exchange,
                        "l2": "flushed: 512 MiB overwrite between timed steps (untimed)"},
             "residual": {"col_id_fro": math.sqrt(max(float(sums[0]), 0.0)), "normA_fro": math.sqrt(float(sums[1]))},
             "roofline": {"kernel": "k_sketch_tma", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
@@ -297,8 +308,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        return main_dist(args, int(os.environ["WORLD_SIZE"]), int(os.environ.get("RANK", "0")),
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or os.environ.get("SKEL_BENCH_DIST") == "1":
+        return main_dist(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
                          int(os.environ.get("LOCAL_RANK", "0")))
 
     import torch
