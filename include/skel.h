@@ -165,7 +165,7 @@ sk_status sk_select_cols(sk_ctx* ctx, const double* X, int64_t l, int64_t n, int
  *           step on after a rank failure.
  *   Lf      NULL or nloc x k column-major (ldlf >= nloc): this rank's rows of sk_select_cols' Lf.
  *   U       NULL or k x k column-major (ldu >= k), replicated.
- * Call begin, then for t = 1..k: all-gather(cand -> gathered), sk_lupp_dist_step(t).  Then
+ * Call begin, then for t = 1..k: all-gather(cand -> gathered), sk_lupp_dist_step(t) (world <= 64).  Then
  * sk_lupp_dist_info (synchronises) returns SK_E_RANK with *info = the failing 1-based step. */
 #define SK_LUPP_DIST_REC(k) ((k) + 4)
 size_t sk_lupp_dist_state_bytes(int64_t nloc, int64_t k);

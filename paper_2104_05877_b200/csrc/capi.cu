@@ -250,7 +250,7 @@ sk_status sk_lupp_dist_step(sk_ctx* c, void* state, int64_t nloc, int64_t k, int
   if (!c) return SK_E_ARG;
   c->err.clear();
   SK_ARG(c, state && gathered && Js && cand, "sk_lupp_dist_step: NULL pointer");
-  SK_ARG(c, nloc >= 0 && k >= 1 && t >= 1 && t <= k && world >= 1 && col0 >= 0, "sk_lupp_dist_step: bad sizes");
+  SK_ARG(c, nloc >= 0 && k >= 1 && t >= 1 && t <= k && world >= 1 && world <= 64 && col0 >= 0, "sk_lupp_dist_step: bad sizes (world <= 64)");
   SK_ARG(c, !Lf || ldlf >= nloc, "sk_lupp_dist_step: ldlf >= nloc required");
   SK_ARG(c, !U || ldu >= k, "sk_lupp_dist_step: ldu >= k required");
   return lupp_dist_step(c, state, nloc, k, col0, t, gathered, world, Js, Lf, ldlf, U, ldu, cand);

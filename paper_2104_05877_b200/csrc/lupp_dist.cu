@@ -106,23 +106,53 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
   const int64_t REC = k + 4;
   if (*(volatile long long*)&L.hdr->status != 0) return;           // failure latched in an earlier step
   const bool corner = blockIdx.x == 0 && blockIdx.y == 0;
+  if (a.world > 64) return;                                          // checked on the host
 
-  // ---- decide step t - 1 from the gathered records (identical on every rank)
+  const int64_t c0 = t + (int64_t)blockIdx.y * DCW;                  // this CTA's first updated column
+  const int64_t i = (int64_t)blockIdx.x * DT + tid;
+  const bool in = i < nloc;
+  // prefetch this thread's row data (independent of the decision, overlaps its latency)
+  double mv[DCW];
+  double mprev = 0.0;
+  int fl = 0;
+  if (in) {
+    fl = L.flags[i];
+    if (t > 0) {
+      mprev = L.M[i + (t - 1) * nloc];
+#pragma unroll
+      for (int j = 0; j < DCW; ++j) mv[j] = c0 + j < k ? L.M[i + (c0 + j) * nloc] : 0.0;
+    } else {
+      mv[0] = L.M[i];
+    }
+  }
+
+  // ---- decide step t - 1 from the gathered records (identical on every rank): warp 0 reads the
+  //      records in parallel (lane w <- record w) and reduces max |value|, ties -> lowest index
   long long pl = -1;               // local index of the pivot row if this rank owns it
   const double* rec = nullptr;
   if (t > 0) {
-    if (tid == 0) {
-      double gmax = 0.0, best = -1.0;
-      long long bi = LLONG_MAX;
-      int bw = -1;
-      for (int w = 0; w < a.world; ++w) {
+    if (tid < 32) {
+      double gmax = 0.0;
+      dev::Cand cd = dev::cand_none();
+      for (int w = tid; w < a.world; w += 32) {
         const double* r = a.gathered + (int64_t)w * REC;
         gmax = fmax(gmax, r[2]);
         const long long idx = (long long)r[1];
-        if (idx >= 0 && dev::beats(r[0], idx, best, bi)) { best = r[0]; bi = idx; bw = w; }
+        if (idx >= 0) {
+          dev::Cand x = dev::cand_none();
+          x.a1 = r[0];
+          x.i1 = idx * 64 + w;                      // rank index rides in the low bits (world <= 64)
+          cd = dev::cand_merge(cd, x);
+        }
       }
-      s_bw = (bw >= 0 && best > 1e-14 * gmax) ? bw : -1;
-      s_g = bi;
+      cd = dev::warp_cand_reduce(cd);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+      if (tid == 0) {
+        const bool ok = cd.i1 != LLONG_MAX && cd.a1 > 1e-14 * gmax;
+        s_bw = ok ? (int)(cd.i1 & 63) : -1;
+        s_g = ok ? cd.i1 >> 6 : -1;
+      }
     }
     __syncthreads();
     if (s_bw < 0) {                                                   // R7: rank failure at step t
@@ -140,19 +170,14 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
       if (a.U)
         for (int64_t c = t - 1 + tid; c < k; c += DT) a.U[(t - 1) + c * a.ldu] = rec[4 + c];
     }
-  }
-  const int64_t c0 = t + (int64_t)blockIdx.y * DCW;                  // this CTA's first updated column
-  if (t > 0) {
     if (tid < DCW) su[tid] = c0 + tid < k ? rec[4 + c0 + tid] : 0.0;
     __syncthreads();
   }
-  const int64_t i = (int64_t)blockIdx.x * DT + tid;
-  const bool in = i < nloc;
-  bool act = in && L.flags[i] < 0 && i != pl;
+  bool act = in && fl < 0 && i != pl;
   double mt = 0.0;                                                    // M(i, t) after the update
   if (t > 0) {
     const double piv = rec[4 + t - 1];
-    const double li = act ? __ddiv_rn(L.M[i + (t - 1) * nloc], piv) : 0.0;
+    const double li = act ? __ddiv_rn(mprev, piv) : 0.0;
     if (blockIdx.y == 0 && in) {
       if (act) {
         if (a.Lf) a.Lf[i + (t - 1) * a.ldlf] = li;
@@ -163,17 +188,18 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
     }
     if (act) {
       double* Mi = L.M + i;
-#pragma unroll 8
+#pragma unroll
       for (int j = 0; j < DCW; ++j) {
         const int64_t c = c0 + j;
-        if (c >= k) break;
-        const double v = __dsub_rn(Mi[c * nloc], __dmul_rn(li, su[j]));
-        Mi[c * nloc] = v;
-        if (j == 0) mt = v;
+        if (c < k) {
+          const double v = __dsub_rn(mv[j], __dmul_rn(li, su[j]));
+          Mi[c * nloc] = v;
+          if (j == 0) mt = v;
+        }
       }
     }
   } else if (act) {
-    mt = L.M[i];
+    mt = mv[0];
   }
   if (t >= k) return;                                                  // last step: decision only
 
