@@ -246,7 +246,9 @@ sk_status sk_residual_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, i
  * Sketch (S0+S1) + column LUPP (S2) and, if Is != NULL, gather + row LUPP
  * (S3+S4).  A may be a HOST pointer (a_on_host = 1): it is then copied to the
  * context's workspace inside the call (pinned host memory gives full PCIe
- * bandwidth).  Js / Is are HOST int64[k] outputs (Is NULL-able).  Synchronises.
+ * bandwidth) in up to 8 column blocks on the context's helper stream, each block
+ * sketched as soon as it lands (X = Gamma A is column-separable), so the copy
+ * overlaps the sketch.  Js / Is are HOST int64[k] outputs (Is NULL-able).  Synchronises.
  * l, emb, zeta, seed as for sk_sketch; k as for sk_select_cols. */
 sk_status sk_rand_lupp(sk_ctx* ctx, const double* A, int a_on_host, int64_t m, int64_t n,
                        int64_t lda, int64_t l, sk_embedding emb, int32_t zeta, uint64_t seed,

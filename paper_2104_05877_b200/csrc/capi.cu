@@ -350,17 +350,47 @@ sk_status sk_rand_lupp(sk_ctx* c, const double* A, int a_on_host, int64_t m, int
   DBuf Ad, Xd, Jd, Cd, Id, st;
   const double* Adev = A;
   int64_t ldad = lda;
-  if (a_on_host) {
-    SK_TRY(Ad.alloc(c, (size_t)m * n * sizeof(double)));
-    SK_CUDA(c, cudaMemcpy2DAsync(Ad.p, (size_t)m * sizeof(double), A, (size_t)lda * sizeof(double),
-                                 (size_t)m * sizeof(double), (size_t)n, cudaMemcpyHostToDevice, c->stream));
-    Adev = Ad.as<double>();
-    ldad = m;
-  }
   SK_TRY(Xd.alloc(c, (size_t)l * n * sizeof(double)));
   SK_TRY(Jd.alloc(c, (size_t)k * sizeof(int64_t)));
   SK_TRY(st.alloc(c, sizeof(int64_t)));
-  SK_TRY(sk_sketch(c, Adev, m, n, ldad, l, emb, zeta, seed, Xd.as<double>(), n));
+  if (a_on_host) {
+    // X = Gamma A is column-separable: the host->device copy of column block b+1 (on the aux
+    // stream) overlaps the sketch of block b (on the context stream).
+    SK_TRY(Ad.alloc(c, (size_t)m * n * sizeof(double)));
+    SK_TRY(ensure_aux(c));
+    Adev = Ad.as<double>();
+    ldad = m;
+    const int64_t nb = ((double)m * n * 8 >= 64.0 * (1 << 20) && n >= 1024) ? std::min<int64_t>(8, n / 256) : 1;
+    const int64_t W = cdiv(cdiv(n, nb), 128) * 128;
+    cudaEvent_t ev[9];
+    int nev = 0;
+    sk_status rs = SK_OK;
+    auto mk = [&](cudaStream_t s) -> cudaEvent_t {
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+      ev[nev++] = e;
+      cudaEventRecord(e, s);
+      return e;
+    };
+    cudaEvent_t e0 = mk(c->stream);                        // Ad's allocation is ordered on the context stream
+    if (!e0 || cudaStreamWaitEvent(c->aux, e0, 0) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event");
+    for (int64_t j0 = 0; j0 < n && rs == SK_OK; j0 += W) {
+      const int64_t jw = std::min(W, n - j0);
+      if (cudaMemcpy2DAsync(Ad.as<double>() + j0 * m, (size_t)m * sizeof(double), A + j0 * lda,
+                            (size_t)lda * sizeof(double), (size_t)m * sizeof(double), (size_t)jw,
+                            cudaMemcpyHostToDevice, c->aux) != cudaSuccess) {
+        rs = fail(c, SK_E_CUDA, "sk_rand_lupp: host-to-device copy");
+        break;
+      }
+      cudaEvent_t eb = mk(c->aux);
+      if (!eb || cudaStreamWaitEvent(c->stream, eb, 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event"); break; }
+      rs = sk_sketch(c, Adev + j0 * m, m, jw, m, l, emb, zeta, seed, Xd.as<double>() + j0, n);
+    }
+    for (int e = 0; e < nev; ++e) cudaEventDestroy(ev[e]);
+    SK_TRY(rs);
+  } else {
+    SK_TRY(sk_sketch(c, Adev, m, n, ldad, l, emb, zeta, seed, Xd.as<double>(), n));
+  }
   SK_TRY(lupp(c, Xd.as<double>(), true, n, k, n, Jd.as<int64_t>(), nullptr, 0, nullptr, 0, nullptr,
               st.as<int64_t>()));
   int64_t inf = 0;

@@ -51,6 +51,8 @@ sk_status upper_triangle(sk_ctx* c, const double* B, int64_t ldb, int64_t n, dou
 // RSVD-DEIM column skeletons from A and its row sketch X (deim.cu).
 sk_status select_cols_deim(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t l,
                            int64_t ldx, int64_t k, int64_t* Js, int64_t* status_dev);
+// The context's lowest-priority helper stream and its two events, created on first use.
+sk_status ensure_aux(sk_ctx* c);
 // Tallest panel the cluster LUPP handles (rows).
 int64_t lupp_max_rows(sk_ctx* c);
 

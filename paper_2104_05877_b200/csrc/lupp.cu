@@ -1005,6 +1005,16 @@ int64_t lupp_max_rows(sk_ctx* c) {
   return cfg.ok ? (int64_t)cfg.cs * 16 * PNT : 0;
 }
 
+sk_status ensure_aux(sk_ctx* c) {
+  if (c->aux) return SK_OK;
+  int lo = 0, hi = 0;
+  SK_CUDA(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  SK_CUDA(c, cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo));   // lo = least priority
+  SK_CUDA(c, cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming));
+  SK_CUDA(c, cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming));
+  return SK_OK;
+}
+
 sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t k, int64_t ld,
                int64_t* Js, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps,
                int64_t* status_dev) {
@@ -1068,13 +1078,7 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   }
   static const bool no_lookahead = [] { const char* e = std::getenv("SKEL_LUPP_NO_LOOKAHEAD"); return e && e[0] == '1'; }();
   const bool lookahead = !no_lookahead && bp < k;
-  if (lookahead && !c->aux) {
-    int lo = 0, hi = 0;
-    SK_CUDA(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    SK_CUDA(c, cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo));   // lo = least priority
-    SK_CUDA(c, cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming));
-    SK_CUDA(c, cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming));
-  }
+  if (lookahead) SK_TRY(ensure_aux(c));
   bool rest_pending = false;
   for (int64_t c0 = 0; c0 < k; c0 += bp) {
     const int b = (int)std::min<int64_t>(bp, k - c0);

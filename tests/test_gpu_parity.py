@@ -380,3 +380,20 @@ def test_dist_rand_lupp_nccl_world1():
         assert abs(out["residual"] - ro) <= 1e-9 * ro + 4 * U * nAo
     finally:
         tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("emb", ["gaussian", "sparse_sign"])
+def test_rand_lupp_host_pipelined(emb):
+    """sk_rand_lupp with a HOST A large enough (64 MB) for the pipelined path: the copy of column
+    block b+1 overlaps the sketch of block b (8 blocks of 256 columns).  J_s and I_s equal the
+    oracle's (near-tie rule) and the device-A path's."""
+    m, n, k, l, seed = 4096, 2048, 64, 74, 31
+    A = rand_mat(m, n, seed, 0.995)
+    Ah = torch.from_numpy(np.asfortranarray(A)).t().contiguous().t()          # column-major host tensor
+    assert Ah.stride() == (1, m)
+    Js, Is = sk.rand_lupp(Ah.pin_memory() if emb == "gaussian" else Ah, k, l, emb, seed, rows=True)
+    Jd, Id = sk.rand_lupp(dev_f(A), k, l, emb, seed, rows=True)
+    X = o_sketch.sketch(A, l, emb, seed)
+    lupp_parity(Js.numpy(), lambda f: o_lupp.select_cols(X, k, f))
+    assert Js.tolist() == Jd.tolist() and Is.tolist() == Id.tolist()
+    lupp_parity(Is.numpy(), lambda f: o_lupp.select_rows(A[:, Js.numpy()], k, f))
