@@ -413,12 +413,13 @@ def main():
         nbytes = 8.0 * (m * n + l * n)
         achieved = nbytes / (sk_ms * 1e-3) / 1e9
         peak = hbm_peak_gbs()
-        roofline = {"kernel": "k_sketch_sparse3", "bound": "hbm", "achieved": achieved, "peak": peak[0],
+        roofline = {"kernel": "sk_sketch sparse sign = k_sparse_csr + k_sketch_sparse4", "bound": "hbm", "achieved": achieved, "peak": peak[0],
                     "unit": "GB/s", "frac": achieved / peak[0], "traffic": traffic, "peak_source": peak[1]}
     else:
         flops = 2.0 * l * m * n * max(1, 2 * args.piter)   # q = 0: one pass; q >= 1: 2q passes (Omega A^T, then A)
         achieved = flops / (sk_ms * 1e-3) / 1e12
-        roofline = {"kernel": "k_sketch_tma", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+        roofline = {"kernel": "sk_sketch Gaussian = k_omega_image + k_sketch_pre (+ split-K reduce)",
+                    "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                     "peak_source": "measured FP64 DMMA ceiling (tools/microbench/fp64_pipes.cu, "
                                    "profiles/round1/fp64_pipes.txt); MEASURED_PEAKS.json has no FP64 entry; "

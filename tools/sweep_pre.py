@@ -1,0 +1,52 @@
+"""Sweep SKEL_PRE_PLAN (bm, nw, splits) for the dense sketch shapes (plan_pre reads the variable
+on every call, so one process serves all plans).  usage: python tools/sweep_pre.py"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2104_05877_b200 as sk  # noqa: E402
+
+SHAPES = [("C2 k=16", 4096, 4096, 26), ("C2 k=64", 4096, 4096, 74), ("C2 k=256", 4096, 4096, 266),
+          ("C2 k=512", 4096, 4096, 522), ("C4 k=50", 65536, 784, 100), ("C4 k=100", 65536, 784, 200),
+          ("C4 k=200", 65536, 784, 400), ("C5 block", 131072, 8192, 1100)]
+PLANS = [(64, 8), (48, 10), (32, 8), (64, 6), (32, 10), (48, 8)]
+
+
+def timed(fn, reps=5):
+    flush = torch.empty(512 << 18, dtype=torch.int32, device="cuda")
+    fn()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return sorted(ts)[len(ts) // 2]
+
+
+for name, m, n, l in SHAPES:
+    A = sk.fortran(torch.randn(m, n, dtype=torch.float64, device="cuda"))
+    X = torch.empty((l, n), dtype=torch.float64, device="cuda")
+    os.environ.pop("SKEL_PRE_PLAN", None)
+    ms = timed(lambda: sk.sketch(A, l, "gaussian", 7, out=X))
+    ref = X.clone()
+    print(f"{name:10s} default plan {ms:8.4f} ms {2 * l * m * n / ms / 1e9 / 37.13:6.1%}", flush=True)
+    res = []
+    for bm, nw in PLANS:
+        for sp in (1, 2, 4, 8, 16, 32):
+            if sp > 1 and m // sp < 1024:
+                break
+            os.environ["SKEL_PRE_PLAN"] = f"{bm},{nw},{sp}"
+            ms = timed(lambda: sk.sketch(A, l, "gaussian", 7, out=X))
+            err = float((X - ref).norm() / ref.norm())
+            res.append((ms, bm, nw, sp, err))
+    res.sort()
+    for ms, bm, nw, sp, err in res[:6]:
+        print(f"    {bm:3d} {nw:3d} {sp:3d}  {ms:8.4f} ms {2 * l * m * n / ms / 1e9 / 37.13:6.1%}  rel {err:.1e}", flush=True)
+    del A, X
+    os.environ.pop("SKEL_PRE_PLAN", None)
