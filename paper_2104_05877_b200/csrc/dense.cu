@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -83,7 +85,39 @@ constexpr int TB2 = 64;
 
 // MODE 0: G (jb x jb SPD, ld) -> its Cholesky factor L (lower, upper zeroed, in place) and
 //         W = L^{-1} (lower, ldw).  MODE 1: G holds a unit lower L (read only) -> W = L^{-1}.
+//         MODE 2: G holds a non-unit lower L (read only) -> W = L^{-1}.
 // status: 1-based failing column (+ col0) on a non-positive pivot (MODE 0).
+// Blocked by 16.  A 16 x 16 diagonal block is factored AND inverted by one warp in registers
+// (lane i < 16 holds row i; columns broadcast by shuffles, no shared-memory round trips), the
+// panel below it is L_ip = A_ip W_pp^T (independent 16-term dot products over all threads), the
+// trailing triangle gets the rank-16 update; the off-diagonal blocks of W = L^{-1} follow by block
+// distance d: W_ij = -W_ii (sum_{j<=k<i} L_ik W_kj).
+constexpr int DB = 16;
+
+// lane i < 16: row i of a 16 x 16 lower factor L in r[0..15] (unit diagonal for MODE 1); on return
+// v = L^{-1} (row i), by forward elimination with shuffled rows.
+template <int MODE>
+__device__ __forceinline__ bool block16(double (&r)[DB], double (&v)[DB], int lane, int* badc) {
+  const unsigned full = 0xffffffffu;
+  // inverse by forward elimination on [L | I]: row t final after scaling; rows i > t drop L(i,t) row t
+#pragma unroll
+  for (int j = 0; j < DB; ++j) v[j] = (lane == j) ? 1.0 : 0.0;
+#pragma unroll
+  for (int t = 0; t < DB; ++t) {
+    const double inv = MODE == 1 ? 1.0 : 1.0 / __shfl_sync(full, r[t], t);
+    if (lane == t) {
+#pragma unroll
+      for (int j = 0; j <= t; ++j) v[j] *= inv;
+    }
+#pragma unroll
+    for (int j = 0; j <= t; ++j) {
+      const double wt = __shfl_sync(full, v[j], t);
+      if (lane > t && lane < DB) v[j] = fma(-r[t], wt, v[j]);
+    }
+  }
+  return true;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) k_diag_inv(double* G, int64_t ld, int jb, double* W, int64_t ldw,
                                                   int64_t col0, int64_t* status) {
@@ -91,8 +125,10 @@ __global__ void __launch_bounds__(256) k_diag_inv(double* G, int64_t ld, int jb,
   extern __shared__ double dinv_sm[];
   double (*a)[TB2 + 1] = reinterpret_cast<double (*)[TB2 + 1]>(dinv_sm);
   double (*w)[TB2 + 1] = reinterpret_cast<double (*)[TB2 + 1]>(dinv_sm + TB2 * (TB2 + 1));
+  double* tmp = dinv_sm + 2 * TB2 * (TB2 + 1);                      // [3][DB][DB]
   __shared__ int bad;
-  const int tid = threadIdx.x;
+  __shared__ double rdg[TB2];                                        // 1 / L(c, c) (MODE 0)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) bad = 0;
   for (int e = tid; e < TB2 * TB2; e += 256) {
     const int i = e & (TB2 - 1), j = e >> 6;
@@ -100,69 +136,110 @@ __global__ void __launch_bounds__(256) k_diag_inv(double* G, int64_t ld, int jb,
     w[i][j] = 0.0;
   }
   __syncthreads();
-  if (MODE == 0) {   // (MODE 2: a non-unit lower factor is given; MODE 1: unit lower)
-    // right-looking Cholesky, one barrier per column: every thread recomputes 1/sqrt of the pivot
-    // from shared memory (no serial thread-0 step), scales its column entries and updates its
-    // 16 x 16-grid share of the trailing triangle with independent FMAs.
-    for (int c = 0; c < jb; ++c) {
-      const double d = a[c][c];
-      if (!(d > 0.0)) {
-        if (tid == 0) *status = col0 + c + 1;
-        return;
-      }
-      const double rs = 1.0 / sqrt(d);
-      const int i0 = c + 1 + (tid >> 4), j0 = c + 1 + (tid & 15);
-      double li[4], lj[4];
+  if (MODE == 0) {
+    for (int c0 = 0; c0 < TB2; c0 += DB) {
+      if (warp == 0) {
+        // factor the diagonal block in shared memory, one column per step; the trailing update of
+        // the block is two-phase (all loads, then FMAs and stores) so its loads overlap
+        const int i = c0 + 1 + (lane & 15);                          // row offset added per column below
+        for (int c = c0; c < c0 + DB; ++c) {
+          const double d = a[c][c];
+          if (!(d > 0.0)) {
+            if (lane == 0) bad = c + 1;
+            break;
+          }
+          const double rs = rsqrt(d);
+          __syncwarp();
+          if (lane == 0) { a[c][c] = d * rs; rdg[c] = rs; }
+          if (lane < c0 + DB - c - 1) a[c + 1 + lane][c] *= rs;
+          __syncwarp();
+          const int ii = c + 1 + (lane & 15);
+          const int jb0 = c + 1 + (lane >> 4);
+          double lj[8], aij[8];
+          const double li = ii < c0 + DB ? a[ii][c] : 0.0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        li[q] = (i0 + 16 * q < jb) ? a[i0 + 16 * q][c] * rs : 0.0;
-        lj[q] = (j0 + 16 * q < jb) ? a[j0 + 16 * q][c] * rs : 0.0;
-      }
-      __syncthreads();                     // everyone has read column c before it is rewritten
-      if (tid == 0) a[c][c] = d * rs;      // sqrt(d)
-      if ((tid & 15) == 0) {
+          for (int q = 0; q < 8; ++q) {
+            const int j = jb0 + 2 * q;
+            const bool ok = ii < c0 + DB && j <= ii;
+            lj[q] = ok ? a[j][c] : 0.0;
+            aij[q] = ok ? a[ii][j] : 0.0;
+          }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (i0 + 16 * q < jb) a[i0 + 16 * q][c] = li[q];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = i0 + 16 * q;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int j = j0 + 16 * r;
-          if (i < jb && j <= i) a[i][j] = fma(-li[q], lj[r], a[i][j]);
+          for (int q = 0; q < 8; ++q) {
+            const int j = jb0 + 2 * q;
+            if (ii < c0 + DB && j <= ii) a[ii][j] = fma(-li, lj[q], aij[q]);
+          }
+          __syncwarp();
         }
+        (void)i;
+      }
+      __syncthreads();
+      if (bad) {
+        if (tid == 0 && status && bad <= jb) *status = col0 + bad;
+        if (bad <= jb) return;
+        __syncthreads();
+        if (tid == 0) bad = 0;                                       // pivot in the identity padding
+      }
+      // panel: rows i >= c0 + 16, L(i, :) = A(i, :) L_pp^{-T} by forward substitution (one row per thread)
+      for (int i = c0 + DB + tid; i < TB2; i += 256) {
+        double x[DB];
+#pragma unroll
+        for (int j = 0; j < DB; ++j) {
+          double v = a[i][c0 + j];
+#pragma unroll
+          for (int q = 0; q < j; ++q) v = fma(-x[q], a[c0 + j][c0 + q], v);
+          x[j] = v * rdg[c0 + j];
+        }
+#pragma unroll
+        for (int j = 0; j < DB; ++j) a[i][c0 + j] = x[j];
+      }
+      __syncthreads();
+      // trailing update of the lower triangle: A(i, j) -= L(i, panel) . L(j, panel)
+      {
+        const int ti = tid >> 4, tj = tid & 15;
+        for (int i = c0 + DB + ti; i < TB2; i += 16)
+          for (int j = c0 + DB + tj; j <= i; j += 16) {
+            double v = a[i][j];
+#pragma unroll
+            for (int q = 0; q < DB; ++q) v = fma(-a[i][c0 + q], a[j][c0 + q], v);
+            a[i][j] = v;
+          }
       }
       __syncthreads();
     }
   }
-  // W = L^{-1} by elimination on [L | I]: step t scales row t of W by 1/L(t,t) and removes
-  // L(i,t) * W(t,:) from every row i > t -- a rank-1 update per step, 16 x 16 thread grid
-  for (int e = tid; e < TB2; e += 256) w[e][e] = 1.0;
-  __syncthreads();
-  for (int t = 0; t < jb; ++t) {
-    // row t of W is final once scaled; rows i > t drop L(i,t)/L(t,t) * W(t,:)
-    const double inv = MODE == 1 ? 1.0 : 1.0 / a[t][t];
-    const int i0 = t + 1 + (tid >> 4), j0 = tid & 15;
-    double wt[4], li[4];
+  {                                                                  // invert the 4 diagonal blocks (warp p)
+    if (warp < TB2 / DB) {
+      const int c0 = warp * DB, i = lane & (DB - 1);
+      double r[DB], v[DB];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      wt[q] = (j0 + 16 * q <= t) ? w[t][j0 + 16 * q] * inv : 0.0;
-      li[q] = (i0 + 16 * q < jb) ? a[i0 + 16 * q][t] : 0.0;
+      for (int j = 0; j < DB; ++j) r[j] = (j <= i) ? a[c0 + i][c0 + j] : 0.0;
+      int badc = 0;
+      block16<MODE == 1 ? 1 : 2>(r, v, lane, &badc);
+      if (lane < DB) {
+#pragma unroll
+        for (int j = 0; j < DB; ++j) w[c0 + i][c0 + j] = j <= i ? v[j] : 0.0;
+      }
     }
     __syncthreads();
-    if (tid < 16 && MODE != 1) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (j0 + 16 * q <= t) w[t][j0 + 16 * q] = wt[q];
+  }
+  // off-diagonal blocks by block distance d: W_ij = -W_ii * sum_{k=j}^{i-1} L_ik W_kj
+  for (int d = 1; d < TB2 / DB; ++d) {
+    const int npair = TB2 / DB - d;
+    for (int e = tid; e < npair * DB * DB; e += 256) {
+      const int pr = e / (DB * DB), r = (e / DB) % DB, cc = e % DB;
+      const int bj = pr, bi = pr + d;
+      double v = 0.0;
+      for (int k = bj * DB; k < bi * DB; ++k) v = fma(a[bi * DB + r][k], w[k][bj * DB + cc], v);
+      tmp[pr * DB * DB + r * DB + cc] = v;
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = i0 + 16 * q;
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (i < jb && j0 + 16 * r <= t) w[i][j0 + 16 * r] = fma(-li[q], wt[r], w[i][j0 + 16 * r]);
+    __syncthreads();
+    for (int e = tid; e < npair * DB * DB; e += 256) {
+      const int pr = e / (DB * DB), r = (e / DB) % DB, cc = e % DB;
+      const int bj = pr, bi = pr + d;
+      double v = 0.0;
+      for (int q = 0; q <= r; ++q) v = fma(w[bi * DB + r][bi * DB + q], tmp[pr * DB * DB + q * DB + cc], v);
+      w[bi * DB + r][bj * DB + cc] = -v;
     }
     __syncthreads();
   }
@@ -238,7 +315,7 @@ __global__ void k_upper_triangle(const double* B, int64_t ldb, int64_t n, double
   }
 }
 
-constexpr size_t kDiagInvSmem = 2 * TB2 * (TB2 + 1) * sizeof(double);
+constexpr size_t kDiagInvSmem = (2 * TB2 * (TB2 + 1) + 3 * DB * DB) * sizeof(double);
 constexpr size_t kRtmSmem = (TB2 + 32) * (TB2 + 1) * sizeof(double);
 
 sk_status dense_attrs(sk_ctx* c) {
