@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(QNT, 1) k_cpqr(QParams p) {
   __shared__ double sred[34];
   __shared__ double s_beta, s_alpha;
   __shared__ long long s_piv;
+  __shared__ double sca[QNT], scf[QNT];                 // per-CTA candidates of this step (G <= QNT)
+  __shared__ long long sci[QNT];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = QNT / 32;
 
   // load own columns (X row-major: consecutive threads -> consecutive columns)
@@ -106,20 +108,25 @@ __global__ void __launch_bounds__(QNT, 1) k_cpqr(QParams p) {
       __threadfence();
       flag_release(p.flags + (size_t)gid * 16, p.epoch0 + t + 1);
     }
-    // (4) wait for every CTA, then reduce the candidates in a fixed order
-    for (int r = threadIdx.x; r < G; r += QNT)
+    // (4) wait for every CTA; the thread that saw CTA r's flag also fetches its candidate (one L2
+    //     round trip fewer on the critical path), then warp 0 reduces them in a fixed order
+    for (int r = threadIdx.x; r < G; r += QNT) {
       while (flag_acquire(p.flags + (size_t)r * 16) < p.epoch0 + t + 1) {
       }
+      const double* cr = p.cand + ((size_t)par * G + r) * 4;
+      const double2 c01 = __ldcg(reinterpret_cast<const double2*>(cr));
+      sca[r] = c01.x;
+      sci[r] = __double_as_longlong(c01.y);
+      if (t == 0) scf[r] = __ldcg(cr + 2);
+    }
     __syncthreads();
     if (warp == 0) {
       dev::Cand w = dev::cand_none();
       double f2 = 0.0;
       for (int r = lane; r < G; r += 32) {
-        const double* cr = p.cand + ((size_t)par * G + r) * 4;
-        const double a = *(volatile const double*)&cr[0];
-        const long long ix = __double_as_longlong(*(volatile const double*)&cr[1]);
-        if (a >= 0.0) w = dev::cand_merge(w, dev::Cand{a, -1.0, ix});
-        if (t == 0) f2 += *(volatile const double*)&cr[2];
+        const double a = sca[r];
+        if (a >= 0.0) w = dev::cand_merge(w, dev::Cand{a, -1.0, sci[r]});
+        if (t == 0) f2 += scf[r];
       }
       w = dev::warp_cand_reduce(w);
       if (t == 0) {
@@ -193,7 +200,7 @@ __global__ void __launch_bounds__(QNT, 1) k_cpqr(QParams p) {
 
 sk_status cpqr(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, int64_t k, int64_t* Js,
                double* R, int64_t ldr, int64_t* status_dev) {
-  int G = (int)std::min<int64_t>(c->num_sms, n);
+  int G = (int)std::min<int64_t>(std::min<int64_t>(c->num_sms, QNT), n);
   const int NC = (int)cdiv(n, G);
   G = (int)cdiv(n, NC);
   const size_t small = (size_t)l * 8 + (size_t)NC * 12 + 256;
