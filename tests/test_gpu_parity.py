@@ -397,3 +397,21 @@ def test_rand_lupp_host_pipelined(emb):
     lupp_parity(Js.numpy(), lambda f: o_lupp.select_cols(X, k, f))
     assert Js.tolist() == Jd.tolist() and Is.tolist() == Id.tolist()
     lupp_parity(Is.numpy(), lambda f: o_lupp.select_rows(A[:, Js.numpy()], k, f))
+
+
+@pytest.mark.parametrize("plan", ["48,8,1,0", "64,8,1,0", "32,8,1,0", "48,8,4,0", "48,8,4,1", "64,8,2,1", "32,8,8,1",
+                                  "fused"])
+def test_sketch_dense_plans(plan, monkeypatch):
+    """Every dense-sketch kernel configuration against the oracle: the pre-generated-Omega GEMM at
+    each tile height, K-splits through HBM partials (cl 0) and through cluster DSMEM (cl 1), and the
+    fused-generation kernel (SKEL_SKETCH_FUSED).  Ragged l, m and n span several tiles."""
+    m, n, l = 1000, 700, 61
+    A = rand_mat(m, n, 41)
+    if plan == "fused":
+        monkeypatch.setenv("SKEL_SKETCH_FUSED", "1")
+    else:
+        monkeypatch.setenv("SKEL_PRE_PLAN", plan)
+    X = sk.sketch(dev_f(A), l, "gaussian", 77).cpu().numpy()
+    monkeypatch.delenv("SKEL_PRE_PLAN", raising=False)
+    monkeypatch.delenv("SKEL_SKETCH_FUSED", raising=False)
+    assert rel_fro(X, o_sketch.sketch(A, l, "gaussian", 77)) <= 1e-12
