@@ -25,6 +25,10 @@ sk_status sketch_sparse(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_
 // X = Gamma A with the SRTT embedding (srtt.cu); m a power of two <= 16384.
 sk_status sketch_srtt(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, uint64_t seed,
                       double* X, int64_t ldx);
+// X (l x n row-major, ldx >= n; == X^T column-major) = Q^T A for a given Q (m x l column-major, ldq):
+// the sketch's TMA + DMMA GEMM with Omega = Q^T packed into its image (falls back to gemm()).
+sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int64_t m, int64_t n, int64_t lda,
+                   int64_t l, double* X, int64_t ldx);
 // Y = A Omega^T (m x l col-major, ldy >= m), Omega l x n (Alg. 3 column sketch).
 sk_status sketch_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
                       int zeta, uint64_t seed, double* Y, int64_t ldy);

@@ -75,9 +75,10 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
     Rt.release();
   }
   if (kind == SK_RES_COL_ID) {
+    // W^T (n x k col-major) = (Qc^T A)^T by the sketch's TMA + DMMA GEMM (Omega = Qc^T)
     SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
-    SK_TRY(gemm(c, true, false, k, n, m, 1.0, Qc.as<double>(), m, A, lda, 0.0, W.as<double>(), k));
-    return gemm_sumsq(c, false, false, m, n, k, -1.0, Qc.as<double>(), m, W.as<double>(), k, 1.0, A, lda, sums);
+    SK_TRY(gemm_qta(c, Qc.as<double>(), m, A, m, n, lda, k, W.as<double>(), n));
+    return gemm_sumsq(c, false, true, m, n, k, -1.0, Qc.as<double>(), m, W.as<double>(), n, 1.0, A, lda, sums);
   }
   if (kind == SK_RES_ROW_ID) {
     SK_TRY(W.alloc(c, (size_t)m * k * sizeof(double)));
@@ -89,8 +90,8 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
   SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
   SK_TRY(Mid.alloc(c, (size_t)k * k * sizeof(double)));
   SK_TRY(B.alloc(c, (size_t)m * k * sizeof(double)));
-  SK_TRY(gemm(c, true, false, k, n, m, 1.0, Qc.as<double>(), m, A, lda, 0.0, W.as<double>(), k));
-  SK_TRY(gemm(c, false, false, k, k, n, 1.0, W.as<double>(), k, Qr.as<double>(), n, 0.0, Mid.as<double>(), k));
+  SK_TRY(gemm_qta(c, Qc.as<double>(), m, A, m, n, lda, k, W.as<double>(), n));            // W^T, n x k
+  SK_TRY(gemm(c, true, false, k, k, n, 1.0, W.as<double>(), n, Qr.as<double>(), n, 0.0, Mid.as<double>(), k));
   SK_TRY(gemm(c, false, false, m, k, k, 1.0, Qc.as<double>(), m, Mid.as<double>(), k, 0.0, B.as<double>(), m));
   return gemm_sumsq(c, false, true, m, n, k, -1.0, B.as<double>(), m, Qr.as<double>(), n, 1.0, A, lda, sums);
 }
@@ -106,8 +107,8 @@ sk_status residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_
   SK_TRY(orthonormal_basis(c, Cc.as<double>(), m, k, Qc.as<double>(), status_dev));
   Cc.release();
   SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
-  SK_TRY(gemm(c, true, false, k, n, m, 1.0, Qc.as<double>(), m, A, lda, 0.0, W.as<double>(), k));
-  return gemm_sumsq(c, false, false, m, n, k, -1.0, Qc.as<double>(), m, W.as<double>(), k, 1.0, A, lda, sums);
+  SK_TRY(gemm_qta(c, Qc.as<double>(), m, A, m, n, lda, k, W.as<double>(), n));
+  return gemm_sumsq(c, false, true, m, n, k, -1.0, Qc.as<double>(), m, W.as<double>(), n, 1.0, A, lda, sums);
 }
 
 }  // namespace skel
