@@ -33,6 +33,8 @@ struct sk_ctx {
 
 namespace skel {
 
+constexpr int kMaxDevices = 64;   // per-device caches of function attributes / library handles
+
 // ---- status helpers --------------------------------------------------------
 inline sk_status fail(sk_ctx* c, sk_status s, const std::string& msg) {
   if (c) c->err = msg;

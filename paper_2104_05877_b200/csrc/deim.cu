@@ -18,7 +18,8 @@ namespace skel {
 
 namespace {
 cusolverDnHandle_t solver(sk_ctx* c) {
-  static cusolverDnHandle_t h = nullptr;
+  static cusolverDnHandle_t hs[kMaxDevices] = {};          // one handle per device (created on it)
+  cusolverDnHandle_t& h = hs[c->device % kMaxDevices];
   if (!h) cusolverDnCreate(&h);
   cusolverDnSetStream(h, c->stream);
   return h;

@@ -319,7 +319,8 @@ constexpr size_t kDiagInvSmem = (2 * TB2 * (TB2 + 1) + 3 * DB * DB) * sizeof(dou
 constexpr size_t kRtmSmem = (TB2 + 32) * (TB2 + 1) * sizeof(double);
 
 sk_status dense_attrs(sk_ctx* c) {
-  static bool done = false;
+  static bool done_dev[kMaxDevices] = {};                  // function attributes are per device
+  bool& done = done_dev[c->device % kMaxDevices];
   if (done) return SK_OK;
   SK_CUDA(c, cudaFuncSetAttribute(k_diag_inv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagInvSmem));
   SK_CUDA(c, cudaFuncSetAttribute(k_diag_inv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagInvSmem));

@@ -211,7 +211,8 @@ __global__ void k_reduce_pairs(const double* part, int64_t count, double* out) {
 
 template <bool TA, bool TB, int MODE>
 sk_status launch(sk_ctx* c, const Params& p, dim3 grid) {
-  static bool attr_set = false;  // per-template-instance; attribute is per device function
+  static bool attr_dev[kMaxDevices] = {};  // per template instance and device
+  bool& attr_set = attr_dev[c->device % kMaxDevices];
   if (!attr_set) {
     SK_CUDA(c, cudaFuncSetAttribute(k_gemm<TA, TB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SMEM_BYTES));

@@ -958,8 +958,10 @@ struct ClusterCfg {
 };
 
 ClusterCfg pick_cluster(sk_ctx* c) {
-  static ClusterCfg cfg;
-  static bool done = false;
+  static ClusterCfg cfg_dev[kMaxDevices];                  // function attributes are per device
+  static bool done_dev[kMaxDevices] = {};
+  ClusterCfg& cfg = cfg_dev[c->device % kMaxDevices];
+  bool& done = done_dev[c->device % kMaxDevices];
   if (done) return cfg;
   done = true;
   cudaFuncAttributes fa{};
