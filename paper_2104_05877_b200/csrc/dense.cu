@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "dmma.cuh"
 #include "internal.h"
 
 namespace skel {
@@ -130,11 +131,14 @@ __global__ void __launch_bounds__(256) k_diag_inv(double* G, int64_t ld, int jb,
   __shared__ double rdg[TB2];                                        // 1 / L(c, c) (MODE 0)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) bad = 0;
-  for (int e = tid; e < TB2 * TB2; e += 256) {
+  for (int e = tid; e < TB2 * TB2; e += 256) {          // cp.async: all loads in flight at once
     const int i = e & (TB2 - 1), j = e >> 6;
-    a[i][j] = (i < jb && j < jb) ? G[i + j * ld] : (i == j ? 1.0 : 0.0);
+    if (i < jb && j < jb) dev::cp_async8(&a[i][j], G + i + j * ld, true);
+    else a[i][j] = i == j ? 1.0 : 0.0;
     w[i][j] = 0.0;
   }
+  dev::cp_async_commit();
+  dev::cp_async_wait<0>();
   __syncthreads();
   if (MODE == 0) {
     for (int c0 = 0; c0 < TB2; c0 += DB) {
@@ -252,43 +256,51 @@ __global__ void __launch_bounds__(256) k_diag_inv(double* G, int64_t ld, int jb,
   }
 }
 
-// X (rows x jb, ldx) <- X * M in place, M = W^T (TRANS) or W, W jb x jb (ldw).  A CTA owns 32 whole
-// rows, so reading and writing X never race.
+// X (rows x jb, ldx) <- X * M in place, M = W^T (TRANS) or W, W jb x jb (ldw).  A CTA owns 64 whole
+// rows, so reading and writing X never race.  DMMA m8n8k4: warp w computes rows 8w..8w+7 x the 64
+// columns (8 accumulator tiles) over K = 64; both shared tiles use a row stride of 68 doubles
+// (= 4 mod 16), which makes the 8x4 A-fragment and 4x8 B-fragment loads conflict-free.
+constexpr int RTS = TB2 + 4;
 template <bool TRANS>
 __global__ void __launch_bounds__(256) k_right_tri_mul(double* X, int64_t rows, int64_t ldx, const double* W,
                                                        int64_t ldw, int jb) {
   extern __shared__ double rtm_sm[];
-  double (*m)[TB2 + 1] = reinterpret_cast<double (*)[TB2 + 1]>(rtm_sm);              // m[t][c] = M(t, c)
-  double (*x)[TB2 + 1] = reinterpret_cast<double (*)[TB2 + 1]>(rtm_sm + TB2 * (TB2 + 1));
+  double (*m)[RTS] = reinterpret_cast<double (*)[RTS]>(rtm_sm);                  // m[t][c] = M(t, c)
+  double (*x)[RTS] = reinterpret_cast<double (*)[RTS]>(rtm_sm + TB2 * RTS);      // x[rr][t] = X(r0+rr, t)
+  // both tiles by 8-byte cp.async (zero-fill outside), all in flight at once: a load-then-store
+  // loop would serialise 32 global round trips per thread
   for (int e = threadIdx.x; e < TB2 * TB2; e += 256) {   // coalesced along W's leading dimension
     const int f = e % TB2, g = e / TB2;
-    const double v = (f < jb && g < jb) ? W[f + (int64_t)g * ldw] : 0.0;   // W(f, g)
-    if (TRANS) m[g][f] = v;                                               // M(t, c) = W(c, t)
-    else m[f][g] = v;                                                     // M(t, c) = W(t, c)
+    const bool ok = f < jb && g < jb;
+    dev::cp_async8(TRANS ? &m[g][f] : &m[f][g], ok ? W + f + (int64_t)g * ldw : W, ok);   // M(t,c) = W(c,t) / W(t,c)
   }
-  const int64_t r0 = (int64_t)blockIdx.x * 32;
-  for (int e = threadIdx.x; e < 32 * TB2; e += 256) {
-    const int rr = e % 32, t = e / 32;
+  const int64_t r0 = (int64_t)blockIdx.x * TB2;
+  for (int e = threadIdx.x; e < TB2 * TB2; e += 256) {
+    const int rr = e % TB2, t = e / TB2;
     const int64_t r = r0 + rr;
-    x[rr][t] = (r < rows && t < jb) ? X[r + t * ldx] : 0.0;
+    const bool ok = r < rows && t < jb;
+    dev::cp_async8(&x[rr][t], ok ? X + r + t * ldx : X, ok);
   }
+  dev::cp_async_commit();
+  dev::cp_async_wait<0>();
   __syncthreads();
-  // thread: row rr = tid % 32, columns c = tid / 32 + 8 q (8 per thread)
-  const int rr = threadIdx.x & 31, cb = threadIdx.x >> 5;
-  double o[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+  double acc[8][2];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) o[q] = 0.0;
-  for (int t = 0; t < jb; ++t) {
-    const double xv = x[rr][t];
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+  for (int kk = 0; kk < TB2 / 4; ++kk) {
+    const double a = x[8 * w + g][4 * kk + q];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) o[q] = fma(xv, m[t][cb + 8 * q], o[q]);
+    for (int j = 0; j < 8; ++j) dev::dmma_8x8x4(acc[j][0], acc[j][1], a, m[4 * kk + q][8 * j + g]);
   }
-  const int64_t r = r0 + rr;
+  const int64_t r = r0 + 8 * w + g;
   if (r < rows) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = cb + 8 * q;
-      if (c < jb) X[r + c * ldx] = o[q];
+    for (int j = 0; j < 8; ++j) {
+      const int c = 8 * j + 2 * q;
+      if (c < jb) X[r + c * ldx] = acc[j][0];
+      if (c + 1 < jb) X[r + (c + 1) * ldx] = acc[j][1];
     }
   }
 }
@@ -316,7 +328,7 @@ __global__ void k_upper_triangle(const double* B, int64_t ldb, int64_t n, double
 }
 
 constexpr size_t kDiagInvSmem = (2 * TB2 * (TB2 + 1) + 3 * DB * DB) * sizeof(double);
-constexpr size_t kRtmSmem = (TB2 + 32) * (TB2 + 1) * sizeof(double);
+constexpr size_t kRtmSmem = 2 * TB2 * RTS * sizeof(double);
 
 sk_status dense_attrs(sk_ctx* c) {
   static bool done_dev[kMaxDevices] = {};                  // function attributes are per device
@@ -384,7 +396,7 @@ sk_status potrf_lower(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t* stat
     const int64_t j1 = j0 + jb;
     if (j1 < k) {
       const int64_t rows = k - j1;
-      k_right_tri_mul<true><<<(unsigned)cdiv(rows, 32), 256, kRtmSmem, c->stream>>>(G + j1 + j0 * ld, rows, ld,
+      k_right_tri_mul<true><<<(unsigned)cdiv(rows, TB2), 256, kRtmSmem, c->stream>>>(G + j1 + j0 * ld, rows, ld,
                                                                              Wd.as<double>() + j0, k, jb);
       SK_TRY(launched(c));
       SK_TRY(gemm(c, false, true, rows, rows, jb, -1.0, G + j1 + j0 * ld, ld, G + j1 + j0 * ld, ld, 1.0,
@@ -411,7 +423,7 @@ sk_status trsm_right_lt(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t l
                                  jb * sizeof(double), jb, cudaMemcpyDeviceToDevice, c->stream));
     k_diag_inv<2><<<1, 256, kDiagInvSmem, c->stream>>>(Lc.as<double>(), TB2, jb, Wd.as<double>(), TB2, 0, nullptr);
     SK_TRY(launched(c));
-    k_right_tri_mul<true><<<(unsigned)cdiv(rows, 32), 256, kRtmSmem, c->stream>>>(X + j0 * ldx, rows, ldx, Wd.as<double>(),
+    k_right_tri_mul<true><<<(unsigned)cdiv(rows, TB2), 256, kRtmSmem, c->stream>>>(X + j0 * ldx, rows, ldx, Wd.as<double>(),
                                                                            TB2, jb);
     SK_TRY(launched(c));
   }
@@ -437,7 +449,7 @@ sk_status trsm_right_l_unit(sk_ctx* c, double* X, int64_t rows, int64_t k, int64
                                  jb * sizeof(double), jb, cudaMemcpyDeviceToDevice, c->stream));
     k_diag_inv<1><<<1, 256, kDiagInvSmem, c->stream>>>(Lc.as<double>(), TB2, jb, Wd.as<double>(), TB2, 0, nullptr);
     SK_TRY(launched(c));
-    k_right_tri_mul<false><<<(unsigned)cdiv(rows, 32), 256, kRtmSmem, c->stream>>>(X + j0 * ldx, rows, ldx,
+    k_right_tri_mul<false><<<(unsigned)cdiv(rows, TB2), 256, kRtmSmem, c->stream>>>(X + j0 * ldx, rows, ldx,
                                                                             Wd.as<double>(), TB2, jb);
     SK_TRY(launched(c));
   }

@@ -67,7 +67,7 @@ int main() {
       const int N = 200;
       cudaEventRecord(a);
       for (int it = 0; it < N; ++it)
-        skel::k_right_tri_mul<true><<<(rows + 31) / 32, 256, skel::kRtmSmem>>>(X, rows, rows, W, n, n);
+        skel::k_right_tri_mul<true><<<(rows + 63) / 64, 256, skel::kRtmSmem>>>(X, rows, rows, W, n, n);
       cudaEventRecord(b); cudaEventSynchronize(b);
       float ms; cudaEventElapsedTime(&ms, a, b);
       printf("k_right_tri_mul<true> rows=%d jb=64: %.2f us per launch err=%s\n", rows, 1e3 * ms / N,
