@@ -60,21 +60,39 @@ struct PanelParams {
   long long* tprobe;                     // experiments only (env SKEL_LUPP_PROBE): per-step clock64 marks
 };
 
+// W (n x k col-major) = the panel, rowstate = -1, maxbits = max |panel|.  Grid (n / 1024, k): no
+// 64-bit divisions, and each thread issues its 4 loads before its stores.
 __global__ void k_lupp_init(const double* P, bool row_major, int64_t n, int k, int64_t ld, double* W,
                             int* rowstate, unsigned long long* maxbits) {
-  double mx = 0.0;
-  const int64_t total = n * k;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e % n, t = e / n;
-    const double v = row_major ? P[t * ld + i] : P[i + t * ld];
-    W[e] = v;
-    mx = fmax(mx, fabs(v));
-    if (t == 0) rowstate[i] = -1;
+  const int64_t t = blockIdx.y;
+  const int64_t i0 = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  double v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t i = i0 + 256 * u;
+    v[u] = i < n ? (row_major ? P[t * ld + i] : P[i + t * ld]) : 0.0;
   }
+  double mx = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t i = i0 + 256 * u;
+    if (i < n) {
+      W[i + t * n] = v[u];
+      if (t == 0) rowstate[i] = -1;
+    }
+    mx = fmax(mx, fabs(v[u]));
+  }
+  __shared__ double wmx[8];
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(mx));
+  if ((threadIdx.x & 31) == 0) wmx[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {                                  // one atomic per CTA, not per warp
+    double b = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) b = fmax(b, wmx[q]);
+    if (b > 0.0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(b));
+  }
 }
 
 // Shared-memory layout of the panel kernel (bytes), shared by host and device.
@@ -1073,8 +1091,7 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   SK_CUDA(c, cudaMemsetAsync(maxb.p, 0, sizeof(unsigned long long), c->stream));
   SK_CUDA(c, cudaMemsetAsync(status_dev, 0, sizeof(int64_t), c->stream));
   {
-    const int blocks = (int)std::min<int64_t>(cdiv(n * k, 256), 8LL * c->num_sms);
-    k_lupp_init<<<blocks, 256, 0, c->stream>>>(Pin, row_major, n, (int)k, ld, Wb.as<double>(),
+    k_lupp_init<<<dim3((unsigned)cdiv(n, 1024), (unsigned)k), 256, 0, c->stream>>>(Pin, row_major, n, (int)k, ld, Wb.as<double>(),
                                                stateb.as<int>(), maxb.as<unsigned long long>());
     SK_TRY(launched(c));
   }
