@@ -183,18 +183,21 @@ __global__ void __launch_bounds__(NT) k_gemm(Params p) {
   }
 }
 
-__global__ void k_splitk_reduce(const double* part, int splits, int M, int N, double alpha,
-                                double beta, double* C, int64_t ldc) {
+// C(m, n) = alpha * sum_z part[z](m, n) + beta * C, z ascending.  Grid (row blocks, column n): no
+// 64-bit divisions; the split loads of an element are issued together.
+__global__ void k_splitk_reduce(const double* __restrict__ part, int splits, int M, int N, double alpha,
+                                double beta, double* __restrict__ C, int64_t ldc) {
   const int64_t total = (int64_t)M * N;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * total + e];
-    const int m = (int)(e % M), n = (int)(e / M);
-    double* cp = C + m + (int64_t)n * ldc;
-    const double v = alpha * s;
-    *cp = (beta == 0.0) ? v : fma(beta, *cp, v);
-  }
+  for (int64_t n = blockIdx.y; n < N; n += gridDim.y)
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < M; m += gridDim.x * blockDim.x) {
+      const double* src = part + m + n * M;
+      double s = 0.0;
+#pragma unroll 8
+      for (int z = 0; z < splits; ++z) s += __ldcs(src + (int64_t)z * total);
+      double* cp = C + m + n * ldc;
+      const double v = alpha * s;
+      *cp = (beta == 0.0) ? v : fma(beta, *cp, v);
+    }
 }
 
 __global__ void k_reduce_pairs(const double* part, int64_t count, double* out) {
@@ -262,10 +265,8 @@ sk_status gemm(sk_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
   SK_TRY(part.alloc(c, (size_t)splits * M * N * sizeof(double)));
   p.out = part.as<double>();
   SK_TRY(dispatch<EPI_PARTIAL>(c, ta, tb, p, grid));
-  const int64_t total = M * N;
-  const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 4LL * c->num_sms);
-  k_splitk_reduce<<<blocks, 256, 0, c->stream>>>(part.as<double>(), splits, (int)M, (int)N, alpha,
-                                                 beta, C, ldc);
+  const dim3 rg((unsigned)std::min<int64_t>(cdiv(M, 256), 64), (unsigned)std::min<int64_t>(N, 65535));
+  k_splitk_reduce<<<rg, 256, 0, c->stream>>>(part.as<double>(), splits, (int)M, (int)N, alpha, beta, C, ldc);
   return launched(c);
 }
 
