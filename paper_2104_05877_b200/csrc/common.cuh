@@ -29,6 +29,9 @@ struct sk_ctx {
   // lowest-priority helper stream + events for look-ahead overlap (LUPP trailing updates)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // launches made while set carry programmatic stream serialization (PDL): the kernel may start
+  // while its predecessor drains; every such kernel calls griddep_wait() before touching memory
+  bool pdl = false;
 };
 
 namespace skel {
@@ -113,6 +116,10 @@ struct Cand {
   double a2;    // second best magnitude (or -1)
   long long i1; // index of the best (LLONG_MAX if none)
 };
+
+// PDL: block until the preceding grid in the stream has completed and its memory is visible (a
+// no-op when the launch was not programmatic).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ Cand cand_none() { return Cand{-1.0, -1.0, 0x7fffffffffffffffLL}; }
 

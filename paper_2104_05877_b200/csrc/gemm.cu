@@ -68,6 +68,7 @@ __device__ __forceinline__ void load_tile(const Params& p, double* As, double* B
 
 template <bool TA, bool TB, int MODE>
 __global__ void __launch_bounds__(NT) k_gemm(Params p) {
+  dev::griddep_wait();
   extern __shared__ __align__(16) double sm[];
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int kbeg = blockIdx.z * p.k_per_split;
@@ -221,7 +222,20 @@ sk_status launch(sk_ctx* c, const Params& p, dim3 grid) {
                                     (int)SMEM_BYTES));
     attr_set = true;
   }
-  k_gemm<TA, TB, MODE><<<grid, NT, SMEM_BYTES, c->stream>>>(p);
+  if (c->pdl) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(NT);
+    lc.dynamicSmemBytes = SMEM_BYTES;
+    lc.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at; lc.numAttrs = 1;
+    SK_CUDA(c, cudaLaunchKernelEx(&lc, k_gemm<TA, TB, MODE>, p));
+  } else {
+    k_gemm<TA, TB, MODE><<<grid, NT, SMEM_BYTES, c->stream>>>(p);
+  }
   return launched(c);
 }
 

@@ -197,6 +197,7 @@ __device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
 //   C  bulk Schur update of columns >= s+2, overlapping the exchange of step s+1.
 template <bool GAPS>
 __global__ void __launch_bounds__(PNT, 1) k_lupp_panel(PanelParams p) {
+  dev::griddep_wait();
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
   const int csize = (int)cluster.num_blocks();
@@ -414,6 +415,7 @@ __host__ __device__ inline size_t reg_smem_bytes(int R, int bp, int nb, int stri
 
 template <bool GAPS, int RPT, int NB>
 __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_reg(PanelParams p) {
+  dev::griddep_wait();
   static_assert(NB % 8 == 0 && NB >= 16, "chunked window");
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
@@ -660,6 +662,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_reg(PanelParams p) {
 // One CTA barrier and one cluster exchange per pivot; no remote loads.
 template <int RPT, int NB, bool GAPS>
 __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
+  dev::griddep_wait();
   static_assert(NB % 8 == 0 && RPT * NB <= 64, "register window");
   constexpr int MSGD = 4 + NB;                       // doubles per message: key, idx, sec, L(s-1), row[NB]
   constexpr int MSG = MSGD / 2;                      // 16-byte chunks
@@ -909,6 +912,7 @@ constexpr size_t v2_smem_bytes() {
 __global__ void __launch_bounds__(256) k_lupp_u12(const double* W, int64_t n, int k, int c0, int bp,
                                                   const int64_t* Js, const double* Lf, int64_t ldlf,
                                                   double* Uw, const int64_t* status) {
+  dev::griddep_wait();
   if (*status != 0) return;
   extern __shared__ __align__(16) double u12sm[];
   double (*L11)[U12_BP + 1] = reinterpret_cast<double (*)[U12_BP + 1]>(u12sm);
@@ -1096,6 +1100,8 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     SK_TRY(launched(c));
   }
   static const bool no_lookahead = [] { const char* e = std::getenv("SKEL_LUPP_NO_LOOKAHEAD"); return e && e[0] == '1'; }();
+  // programmatic dependent launch along the panel -> u12 -> next-block GEMM -> panel chain
+  static const bool pdl = [] { const char* e = std::getenv("SKEL_NO_PDL"); return !(e && e[0] == '1'); }();
   const bool lookahead = !no_lookahead && bp < k;
   if (lookahead) SK_TRY(ensure_aux(c));
   bool rest_pending = false;
@@ -1113,24 +1119,42 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     lc.blockDim = dim3(PNT);
     lc.dynamicSmemBytes = smem_bytes;
     lc.stream = c->stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    lc.attrs = at; lc.numAttrs = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at; lc.numAttrs = (pdl && c0 > 0) ? 2 : 1;
     SK_CUDA(c, cudaLaunchKernelEx(&lc, fn, pp));
     SK_TRY(launched(c));
     const int64_t c1 = c0 + b;
     if (c1 < k) {
       // look-ahead: the next block's columns are updated on the main stream; the rest of the
       // trailing update runs on the low-priority aux stream, overlapping the next panel
+      const bool waited = rest_pending;
       if (rest_pending) SK_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_b, 0));   // before u12 reads W(piv, c1:)
       rest_pending = false;
-      k_lupp_u12<<<(unsigned)cdiv(k - c1, 32), 256, kU12Smem, c->stream>>>(Wb.as<double>(), n, (int)k, (int)c0, b, Js,
-                                                                  Lf, ldlf, Ub.as<double>(), status_dev);
-      SK_TRY(launched(c));
+      {
+        cudaLaunchConfig_t lu{};
+        lu.gridDim = dim3((unsigned)cdiv(k - c1, 32));
+        lu.blockDim = dim3(256);
+        lu.dynamicSmemBytes = kU12Smem;
+        lu.stream = c->stream;
+        cudaLaunchAttribute au[1];
+        au[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        au[0].val.programmaticStreamSerializationAllowed = 1;
+        lu.attrs = au; lu.numAttrs = (pdl && !waited) ? 1 : 0;      // an event wait keeps full ordering
+        SK_CUDA(c, cudaLaunchKernelEx(&lu, k_lupp_u12, (const double*)Wb.as<double>(), n, (int)k, (int)c0, b,
+                                      (const int64_t*)Js, (const double*)Lf, ldlf, Ub.as<double>(),
+                                      (const int64_t*)status_dev));
+        SK_TRY(launched(c));
+      }
       const int64_t nn = lookahead ? std::min<int64_t>(bp, k - c1) : k - c1;
-      SK_TRY(gemm(c, false, false, n, nn, b, -1.0, Lf + c0 * ldlf, ldlf, Ub.as<double>() + c0 + c1 * k,
-                  k, 1.0, Wb.as<double>() + c1 * n, n));
+      c->pdl = pdl;
+      const sk_status gs = gemm(c, false, false, n, nn, b, -1.0, Lf + c0 * ldlf, ldlf, Ub.as<double>() + c0 + c1 * k,
+                                k, 1.0, Wb.as<double>() + c1 * n, n);
+      c->pdl = false;
+      SK_TRY(gs);
       if (c1 + nn < k) {
         SK_CUDA(c, cudaEventRecord(c->ev_a, c->stream));
         SK_CUDA(c, cudaStreamWaitEvent(c->aux, c->ev_a, 0));
