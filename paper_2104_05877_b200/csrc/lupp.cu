@@ -1124,7 +1124,7 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
-    lc.attrs = at; lc.numAttrs = (pdl && c0 > 0) ? 2 : 1;
+    lc.attrs = at; lc.numAttrs = pdl ? 2 : 1;             // block 0: the predecessor is k_lupp_init
     SK_CUDA(c, cudaLaunchKernelEx(&lc, fn, pp));
     SK_TRY(launched(c));
     const int64_t c1 = c0 + b;
