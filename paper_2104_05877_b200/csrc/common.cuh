@@ -104,6 +104,25 @@ struct DBuf {
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
+// predecessor in the stream drains; it must call dev::griddep_wait() before touching memory.
+template <typename... KArgs, typename... Args>
+inline sk_status launch_pdl(sk_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) return fail(c, SK_E_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+  return launched(c);
+}
+
 }  // namespace skel
 
 // ---- device helpers ---------------------------------------------------------

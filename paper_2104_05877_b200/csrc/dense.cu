@@ -122,6 +122,7 @@ __device__ __forceinline__ bool block16(double (&r)[DB], double (&v)[DB], int la
 template <int MODE>
 __global__ void __launch_bounds__(256) k_diag_inv(double* G, int64_t ld, int jb, double* W, int64_t ldw,
                                                   int64_t col0, int64_t* status) {
+  dev::griddep_wait();
   if (status && *status != 0) return;
   extern __shared__ double dinv_sm[];
   double (*a)[TB2 + 1] = reinterpret_cast<double (*)[TB2 + 1]>(dinv_sm);
@@ -264,6 +265,7 @@ constexpr int RTS = TB2 + 4;
 template <bool TRANS>
 __global__ void __launch_bounds__(256) k_right_tri_mul(double* X, int64_t rows, int64_t ldx, const double* W,
                                                        int64_t ldw, int jb) {
+  dev::griddep_wait();
   extern __shared__ double rtm_sm[];
   double (*m)[RTS] = reinterpret_cast<double (*)[RTS]>(rtm_sm);                  // m[t][c] = M(t, c)
   double (*x)[RTS] = reinterpret_cast<double (*)[RTS]>(rtm_sm + TB2 * RTS);      // x[rr][t] = X(r0+rr, t)
@@ -391,16 +393,18 @@ sk_status potrf_lower(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t* stat
   SK_TRY(Wd.alloc(c, (size_t)k * TB2 * sizeof(double)));
   for (int64_t j0 = 0; j0 < k; j0 += TB2) {
     const int jb = (int)std::min<int64_t>(TB2, k - j0);
-    k_diag_inv<0><<<1, 256, kDiagInvSmem, c->stream>>>(G + j0 + j0 * ld, ld, jb, Wd.as<double>() + j0, k, j0, status_dev);
-    SK_TRY(launched(c));
+    SK_TRY(launch_pdl(c, k_diag_inv<0>, dim3(1), dim3(256), kDiagInvSmem, G + j0 + j0 * ld, ld, jb,
+                      Wd.as<double>() + j0, (int64_t)k, j0, status_dev));
     const int64_t j1 = j0 + jb;
     if (j1 < k) {
       const int64_t rows = k - j1;
-      k_right_tri_mul<true><<<(unsigned)cdiv(rows, TB2), 256, kRtmSmem, c->stream>>>(G + j1 + j0 * ld, rows, ld,
-                                                                             Wd.as<double>() + j0, k, jb);
-      SK_TRY(launched(c));
-      SK_TRY(gemm(c, false, true, rows, rows, jb, -1.0, G + j1 + j0 * ld, ld, G + j1 + j0 * ld, ld, 1.0,
-                  G + j1 + j1 * ld, ld));
+      SK_TRY(launch_pdl(c, k_right_tri_mul<true>, dim3((unsigned)cdiv(rows, TB2)), dim3(256), kRtmSmem,
+                        G + j1 + j0 * ld, rows, ld, (const double*)(Wd.as<double>() + j0), (int64_t)k, jb));
+      c->pdl = true;
+      const sk_status gs = gemm(c, false, true, rows, rows, jb, -1.0, G + j1 + j0 * ld, ld, G + j1 + j0 * ld, ld, 1.0,
+                                G + j1 + j1 * ld, ld);
+      c->pdl = false;
+      SK_TRY(gs);
     }
   }
   return SK_OK;
@@ -416,16 +420,19 @@ sk_status trsm_right_lt(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t l
   SK_TRY(Lc.alloc(c, (size_t)TB2 * TB2 * sizeof(double)));
   for (int64_t j0 = 0; j0 < k; j0 += TB2) {
     const int jb = (int)std::min<int64_t>(TB2, k - j0);
-    if (j0 > 0)
-      SK_TRY(gemm(c, false, true, rows, jb, j0, -1.0, X, ldx, L + j0, ldl, 1.0, X + j0 * ldx, ldx));
     // W = L_jj^{-1}: L_jj is already a Cholesky factor; invert it as a (non-unit) lower matrix
     SK_CUDA(c, cudaMemcpy2DAsync(Lc.p, TB2 * sizeof(double), L + j0 + j0 * ldl, ldl * sizeof(double),
                                  jb * sizeof(double), jb, cudaMemcpyDeviceToDevice, c->stream));
-    k_diag_inv<2><<<1, 256, kDiagInvSmem, c->stream>>>(Lc.as<double>(), TB2, jb, Wd.as<double>(), TB2, 0, nullptr);
-    SK_TRY(launched(c));
-    k_right_tri_mul<true><<<(unsigned)cdiv(rows, TB2), 256, kRtmSmem, c->stream>>>(X + j0 * ldx, rows, ldx, Wd.as<double>(),
-                                                                           TB2, jb);
-    SK_TRY(launched(c));
+    SK_TRY(launch_pdl(c, k_diag_inv<2>, dim3(1), dim3(256), kDiagInvSmem, Lc.as<double>(), (int64_t)TB2, jb,
+                      Wd.as<double>(), (int64_t)TB2, (int64_t)0, (int64_t*)nullptr));
+    if (j0 > 0) {
+      c->pdl = true;
+      const sk_status gs = gemm(c, false, true, rows, jb, j0, -1.0, X, ldx, L + j0, ldl, 1.0, X + j0 * ldx, ldx);
+      c->pdl = false;
+      SK_TRY(gs);
+    }
+    SK_TRY(launch_pdl(c, k_right_tri_mul<true>, dim3((unsigned)cdiv(rows, TB2)), dim3(256), kRtmSmem, X + j0 * ldx,
+                      rows, ldx, (const double*)Wd.as<double>(), (int64_t)TB2, jb));
   }
   return SK_OK;
 }
@@ -442,16 +449,19 @@ sk_status trsm_right_l_unit(sk_ctx* c, double* X, int64_t rows, int64_t k, int64
     const int64_t j0 = b * TB2;
     const int jb = (int)std::min<int64_t>(TB2, k - j0);
     const int64_t j1 = j0 + jb;
-    if (j1 < k)
-      SK_TRY(gemm(c, false, false, rows, jb, k - j1, -1.0, X + j1 * ldx, ldx, L + j1 + j0 * ldl, ldl, 1.0,
-                  X + j0 * ldx, ldx));
     SK_CUDA(c, cudaMemcpy2DAsync(Lc.p, TB2 * sizeof(double), L + j0 + j0 * ldl, ldl * sizeof(double),
                                  jb * sizeof(double), jb, cudaMemcpyDeviceToDevice, c->stream));
-    k_diag_inv<1><<<1, 256, kDiagInvSmem, c->stream>>>(Lc.as<double>(), TB2, jb, Wd.as<double>(), TB2, 0, nullptr);
-    SK_TRY(launched(c));
-    k_right_tri_mul<false><<<(unsigned)cdiv(rows, TB2), 256, kRtmSmem, c->stream>>>(X + j0 * ldx, rows, ldx,
-                                                                            Wd.as<double>(), TB2, jb);
-    SK_TRY(launched(c));
+    SK_TRY(launch_pdl(c, k_diag_inv<1>, dim3(1), dim3(256), kDiagInvSmem, Lc.as<double>(), (int64_t)TB2, jb,
+                      Wd.as<double>(), (int64_t)TB2, (int64_t)0, (int64_t*)nullptr));
+    if (j1 < k) {
+      c->pdl = true;
+      const sk_status gs = gemm(c, false, false, rows, jb, k - j1, -1.0, X + j1 * ldx, ldx, L + j1 + j0 * ldl, ldl,
+                                1.0, X + j0 * ldx, ldx);
+      c->pdl = false;
+      SK_TRY(gs);
+    }
+    SK_TRY(launch_pdl(c, k_right_tri_mul<false>, dim3((unsigned)cdiv(rows, TB2)), dim3(256), kRtmSmem,
+                      X + j0 * ldx, rows, ldx, (const double*)Wd.as<double>(), (int64_t)TB2, jb));
   }
   return SK_OK;
 }
