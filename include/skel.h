@@ -176,6 +176,35 @@ sk_status sk_lupp_dist_step(sk_ctx* ctx, void* state, int64_t nloc, int64_t k, i
                             double* U, int64_t ldu, double* cand);
 sk_status sk_lupp_dist_info(sk_ctx* ctx, const void* state, int64_t* info);
 
+/* ---- the same LUPP with the exchange fused into the step kernel (P2P mailboxes) ----
+ * Instead of an all-gather between steps, every rank owns a MAILBOX of
+ * sk_lupp_dist_mailbox_bytes(k, world) bytes = [2][world][REC] doubles (records by step parity)
+ * + [world] uint64 flags + 1 uint64 selection epoch, zero-initialised, mapped into every rank
+ * (NVLink peer memory via sk_ipc_export / sk_ipc_import, or plain device memory when all ranks
+ * share a GPU).  `peers` is a DEVICE array of world pointers, peers[q] = rank q's mailbox as seen
+ * from this rank; own_mailbox = peers[rank] (host copy of the address).  begin advances the
+ * mailbox's device-side epoch by k + 2 (so flags of earlier selections never satisfy a wait and a
+ * captured graph of the whole selection can be replayed).  The kernel of step t waits until every
+ * flag of its own mailbox reaches epoch + t, reads the records of step t-1 there, eliminates,
+ * and publishes its step-t record by storing it into slot [t & 1][rank] of every mailbox followed
+ * by a system-scope fence and flag release (epoch + t + 1).  Every rank must run the same sequence
+ * of selections on its mailbox.  Same results as sk_lupp_dist_begin/step; no host call or
+ * collective between steps. */
+size_t sk_lupp_dist_mailbox_bytes(int64_t k, int32_t world);
+sk_status sk_lupp_dist_begin_p2p(sk_ctx* ctx, const double* X, int64_t nloc, int64_t ldx, int64_t k, int64_t col0,
+                                 void* state, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand,
+                                 double* const* peers, double* own_mailbox, int32_t rank, int32_t world);
+sk_status sk_lupp_dist_step_p2p(sk_ctx* ctx, void* state, int64_t nloc, int64_t k, int64_t col0, int64_t t,
+                                double* const* peers, int32_t rank, int32_t world, int64_t* Js, double* Lf,
+                                int64_t ldlf, double* U, int64_t ldu, double* cand);
+/* Device memory shareable with other processes (cudaMalloc + zero fill, CUDA IPC): export writes a
+ * 64-byte handle to host memory, import maps a peer's handle into this process (close unmaps). */
+sk_status sk_ipc_alloc(sk_ctx* ctx, size_t bytes, void** ptr);
+sk_status sk_ipc_free(sk_ctx* ctx, void* ptr);
+sk_status sk_ipc_export(sk_ctx* ctx, void* ptr, void* handle);
+sk_status sk_ipc_import(sk_ctx* ctx, const void* handle, void** ptr);
+sk_status sk_ipc_close(sk_ctx* ctx, void* ptr);
+
 /* ---- S2': column skeletons by CPQR on the sketch (eq:def_QRCP; Sec. 5 "Rand-CPQR") ----
  * k steps of Householder QR with column pivoting on all l rows of X; the pivot
  * is the active column of largest remaining norm, norms recomputed

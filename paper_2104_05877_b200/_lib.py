@@ -37,6 +37,15 @@ _SIGS = {
     "sk_lupp_dist_step": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, ctypes.c_int32, c_dp, c_dp, c_i64, c_dp,
                           c_i64, c_dp],
     "sk_lupp_dist_info": [c_dp, c_dp, ctypes.POINTER(c_i64)],
+    "sk_lupp_dist_begin_p2p": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, c_dp, c_i64, c_dp, c_dp,
+                               c_dp, ctypes.c_int32, ctypes.c_int32],
+    "sk_lupp_dist_step_p2p": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, ctypes.c_int32, ctypes.c_int32,
+                              c_dp, c_dp, c_i64, c_dp, c_i64, c_dp],
+    "sk_ipc_alloc": [c_dp, ctypes.c_size_t, ctypes.POINTER(c_dp)],
+    "sk_ipc_free": [c_dp, c_dp],
+    "sk_ipc_export": [c_dp, c_dp, c_dp],
+    "sk_ipc_import": [c_dp, c_dp, ctypes.POINTER(c_dp)],
+    "sk_ipc_close": [c_dp, c_dp],
     "sk_rand_lupp": [c_dp, c_dp, c_int, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64,
                      c_i64, c_dp, c_dp, ctypes.POINTER(c_i64)],
 }
@@ -47,6 +56,7 @@ _OTHER = {
     "sk_workspace_bytes": ([c_dp], c_i64),
     "sk_launch_count": ([c_dp], c_i64),
     "sk_lupp_dist_state_bytes": ([c_i64, c_i64], ctypes.c_size_t),
+    "sk_lupp_dist_mailbox_bytes": ([c_i64, ctypes.c_int32], ctypes.c_size_t),
 }
 
 # every symbol include/skel.h declares

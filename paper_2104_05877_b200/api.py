@@ -314,3 +314,70 @@ class LuppDist:
         h = context(self.device.index)
         _check(lib().sk_lupp_dist_info(h, _ptr(self.state), ctypes.byref(info)), h, info.value)
         return 0
+
+
+class LuppDistP2P(LuppDist):
+    """LuppDist with the exchange fused into the step kernel (sk_lupp_dist_*_p2p): `peers` is a
+    CUDA int64 tensor of the world mailbox addresses as seen from this rank (peers[rank] = own,
+    `own` its host value).  No collective between steps: begin(X), then step(t) for t = 1..k, then
+    info().  begin() advances the mailbox's device-side epoch, so mailboxes are reusable and the
+    whole selection can be captured in a CUDA graph."""
+
+    def __init__(self, nloc, k, col0, world, rank, peers, own, device=None, want_factors=True):
+        super().__init__(nloc, k, col0, world, device, want_factors)
+        if peers.dtype != torch.int64 or not peers.is_cuda or peers.numel() != world:
+            raise ValueError("peers must be a CUDA int64 tensor of `world` mailbox addresses")
+        self.rank, self.peers, self.own = rank, peers, own
+
+    def begin(self, X_local):
+        if X_local.dtype != torch.float64 or not X_local.is_cuda or X_local.dim() != 2:
+            raise ValueError("X_local must be a 2-D float64 CUDA tensor")
+        if X_local.shape[1] != self.nloc or X_local.shape[0] < self.k:
+            raise ValueError("X_local must be l x nloc with l >= k")
+        ldx = max(X_local.stride(0), self.nloc) if X_local.shape[0] > 1 else max(self.nloc, 1)
+        h = context(self.device.index)
+        _check(lib().sk_lupp_dist_begin_p2p(h, _ptr(X_local), self.nloc, ldx, self.k, self.col0, _ptr(self.state),
+                                            _ptr(self.Lf), max(self.nloc, 1), _ptr(self.U), self.k, _ptr(self.cand),
+                                            _ptr(self.peers), ctypes.c_void_p(self.own), self.rank, self.world), h)
+
+    def step(self, t):
+        h = context(self.device.index)
+        _check(lib().sk_lupp_dist_step_p2p(h, _ptr(self.state), self.nloc, self.k, self.col0, t, _ptr(self.peers),
+                                           self.rank, self.world, _ptr(self.Js), _ptr(self.Lf),
+                                           max(self.nloc, 1), _ptr(self.U), self.k, _ptr(self.cand)), h)
+
+
+def mailbox_bytes(k, world):
+    return int(lib().sk_lupp_dist_mailbox_bytes(k, world))
+
+
+def ipc_alloc(nbytes, device=None):
+    """Zero-filled cudaMalloc memory that other processes can map (returns the device address)."""
+    h = context(device)
+    p = ctypes.c_void_p()
+    _check(lib().sk_ipc_alloc(h, nbytes, ctypes.byref(p)), h)
+    return p.value
+
+
+def ipc_free(ptr, device=None):
+    h = context(device)
+    _check(lib().sk_ipc_free(h, ctypes.c_void_p(ptr)), h)
+
+
+def ipc_export(ptr, device=None):
+    h = context(device)
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().sk_ipc_export(h, ctypes.c_void_p(ptr), buf), h)
+    return buf.raw
+
+
+def ipc_import(handle, device=None):
+    h = context(device)
+    p = ctypes.c_void_p()
+    _check(lib().sk_ipc_import(h, ctypes.c_char_p(bytes(handle)), ctypes.byref(p)), h)
+    return p.value
+
+
+def ipc_close(ptr, device=None):
+    h = context(device)
+    _check(lib().sk_ipc_close(h, ctypes.c_void_p(ptr)), h)

@@ -256,6 +256,78 @@ sk_status sk_lupp_dist_step(sk_ctx* c, void* state, int64_t nloc, int64_t k, int
   return lupp_dist_step(c, state, nloc, k, col0, t, gathered, world, Js, Lf, ldlf, U, ldu, cand);
 }
 
+size_t sk_lupp_dist_mailbox_bytes(int64_t k, int32_t world) {
+  if (k < 1 || world < 1 || world > 64) return 0;
+  return lupp_dist_mailbox_bytes(k, world);
+}
+
+sk_status sk_lupp_dist_begin_p2p(sk_ctx* c, const double* X, int64_t nloc, int64_t ldx, int64_t k, int64_t col0,
+                                 void* state, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand,
+                                 double* const* peers, double* own_mailbox, int32_t rank, int32_t world) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, state && cand && peers && own_mailbox && (X || nloc == 0), "sk_lupp_dist_begin_p2p: NULL pointer");
+  SK_ARG(c, nloc >= 0 && k >= 1 && col0 >= 0 && ldx >= nloc, "sk_lupp_dist_begin_p2p: bad sizes");
+  SK_ARG(c, world >= 1 && world <= 64 && rank >= 0 && rank < world, "sk_lupp_dist_begin_p2p: bad rank/world");
+  SK_ARG(c, !Lf || ldlf >= nloc, "sk_lupp_dist_begin_p2p: ldlf >= nloc required");
+  SK_ARG(c, !U || ldu >= k, "sk_lupp_dist_begin_p2p: ldu >= k required");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  return lupp_dist_begin(c, X, nloc, ldx, k, col0, state, Lf, ldlf, U, ldu, cand, peers, rank, world, own_mailbox);
+}
+
+sk_status sk_lupp_dist_step_p2p(sk_ctx* c, void* state, int64_t nloc, int64_t k, int64_t col0, int64_t t,
+                                double* const* peers, int32_t rank, int32_t world, int64_t* Js,
+                                double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, state && peers && Js && cand, "sk_lupp_dist_step_p2p: NULL pointer");
+  SK_ARG(c, nloc >= 0 && k >= 1 && t >= 1 && t <= k && col0 >= 0, "sk_lupp_dist_step_p2p: bad sizes");
+  SK_ARG(c, world >= 1 && world <= 64 && rank >= 0 && rank < world, "sk_lupp_dist_step_p2p: bad rank/world");
+  SK_ARG(c, !Lf || ldlf >= nloc, "sk_lupp_dist_step_p2p: ldlf >= nloc required");
+  SK_ARG(c, !U || ldu >= k, "sk_lupp_dist_step_p2p: ldu >= k required");
+  return lupp_dist_step(c, state, nloc, k, col0, t, nullptr, world, Js, Lf, ldlf, U, ldu, cand, peers, rank);
+}
+
+sk_status sk_ipc_alloc(sk_ctx* c, size_t bytes, void** ptr) {
+  if (!c || !ptr) return SK_E_ARG;
+  c->err.clear();
+  SK_CUDA(c, cudaSetDevice(c->device));
+  SK_CUDA(c, cudaMalloc(ptr, bytes ? bytes : 16));
+  SK_CUDA(c, cudaMemset(*ptr, 0, bytes ? bytes : 16));
+  return SK_OK;
+}
+
+sk_status sk_ipc_free(sk_ctx* c, void* ptr) {
+  if (!c) return SK_E_ARG;
+  SK_CUDA(c, cudaFree(ptr));
+  return SK_OK;
+}
+
+sk_status sk_ipc_export(sk_ctx* c, void* ptr, void* handle) {
+  if (!c || !ptr || !handle) return SK_E_ARG;
+  c->err.clear();
+  cudaIpcMemHandle_t h;
+  SK_CUDA(c, cudaIpcGetMemHandle(&h, ptr));
+  std::memcpy(handle, &h, sizeof(h));
+  return SK_OK;
+}
+
+sk_status sk_ipc_import(sk_ctx* c, const void* handle, void** ptr) {
+  if (!c || !handle || !ptr) return SK_E_ARG;
+  c->err.clear();
+  SK_CUDA(c, cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  SK_CUDA(c, cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SK_OK;
+}
+
+sk_status sk_ipc_close(sk_ctx* c, void* ptr) {
+  if (!c) return SK_E_ARG;
+  SK_CUDA(c, cudaIpcCloseMemHandle(ptr));
+  return SK_OK;
+}
+
 sk_status sk_lupp_dist_info(sk_ctx* c, const void* state, int64_t* info) {
   if (!c) return SK_E_ARG;
   c->err.clear();

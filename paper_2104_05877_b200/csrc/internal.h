@@ -63,11 +63,14 @@ int64_t lupp_max_rows(sk_ctx* c);
 // ---------------------------------------------------------------- distributed LUPP (lupp_dist.cu)
 // Per-step-exchange column LUPP on a column-sharded panel; see include/skel.h.
 size_t lupp_dist_state_bytes(int64_t nloc, int64_t k);
+size_t lupp_dist_mailbox_bytes(int64_t k, int world);
+// peers == nullptr: the caller all-gathers `cand` into `gathered` between steps; else P2P mailboxes
 sk_status lupp_dist_begin(sk_ctx* c, const double* X, int64_t nloc, int64_t ldx, int64_t k, int64_t col0, void* state,
-                          double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand);
+                          double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand, double* const* peers = nullptr,
+                          int rank = 0, int world = 1, double* own_mailbox = nullptr);
 sk_status lupp_dist_step(sk_ctx* c, void* state, int64_t nloc, int64_t k, int64_t col0, int64_t t,
                          const double* gathered, int world, int64_t* Js, double* Lf, int64_t ldlf, double* U,
-                         int64_t ldu, double* cand);
+                         int64_t ldu, double* cand, double* const* peers = nullptr, int rank = 0);
 sk_status lupp_dist_status(sk_ctx* c, const void* state, int64_t* status_dev_out);
 
 // ---------------------------------------------------------------- CPQR (cpqr.cu)

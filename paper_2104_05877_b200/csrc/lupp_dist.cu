@@ -45,6 +45,11 @@ struct DistLayout {
 };
 
 __host__ __device__ inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// mailbox of `world` ranks: [2][world][REC] records, [world] flags, [1] selection epoch (local)
+__device__ __forceinline__ unsigned long long* mb_flags(double* mb, int world, int64_t REC) {
+  return reinterpret_cast<unsigned long long*>(mb + 2 * (int64_t)world * REC);
+}
 __host__ __device__ inline int64_t dist_rb(int64_t nloc) { return nloc > 0 ? (nloc + DT - 1) / DT : 1; }
 
 __host__ __device__ inline DistLayout dist_layout(void* state, int64_t nloc) {
@@ -69,6 +74,11 @@ size_t dist_state_bytes(int64_t nloc, int64_t k) {
 }
 
 // M(i, c) = X(c, i) (X row-major, rows 0..k-1 of the local sketch block), flags = -1, lmax.
+__global__ void k_dist_begin_epoch(double* mb, int world, int64_t k) {
+  unsigned long long* e = mb_flags(mb, world, k + 4) + world;
+  *e = *e + (unsigned long long)(k + 2);            // above every flag of earlier selections
+}
+
 __global__ void k_dist_begin(const double* __restrict__ X, int64_t ldx, int64_t nloc, int64_t k, DistLayout L) {
   double mx = 0.0;
   const int64_t total = nloc * k;
@@ -92,7 +102,24 @@ struct StepArgs {
   const double* gathered; int world;
   int64_t* Js; double* Lf; int64_t ldlf; double* U; int64_t ldu;
   double* cand;
+  // P2P mode (peers != nullptr): every rank's mailbox = [2][world][REC] doubles (records by step
+  // parity) + [world] u64 flags; peers[q] is rank q's mailbox mapped into this process (NVLink peer
+  // memory / CUDA IPC), peers[rank] the local one.  The step kernel waits for the flags, reads the
+  // records from its own mailbox, and publishes its next record by storing it into every peer's
+  // mailbox and releasing the flags -- the exchange is part of the kernel, no collective call.
+  double* const* peers; int rank;
 };
+
+
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* f) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* f, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
+}
 
 __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
   __shared__ double su[DCW];
@@ -107,6 +134,22 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
   if (*(volatile long long*)&L.hdr->status != 0) return;           // failure latched in an earlier step
   const bool corner = blockIdx.x == 0 && blockIdx.y == 0;
   if (a.world > 64) return;                                          // checked on the host
+  const double* gathered = a.gathered;
+  unsigned long long epoch = 0;
+  if (a.peers != nullptr) {
+    // the selection's epoch: a device-side counter advanced by k_dist_begin, so captured graphs replay
+    double* mb = a.peers[a.rank];
+    unsigned long long* flags = mb_flags(mb, a.world, REC);
+    epoch = *(volatile unsigned long long*)(flags + a.world);
+    if (t > 0) {
+      // records of step t-1 sit in buffer (t-1) & 1 of the local mailbox once every flag >= epoch + t
+      if (tid < a.world)
+        while (ld_acquire_sys(flags + tid) < epoch + (unsigned long long)t) {
+        }
+      __syncthreads();
+      gathered = mb + (int64_t)((t - 1) & 1) * a.world * REC;
+    }
+  }
 
   const int64_t c0 = t + (int64_t)blockIdx.y * DCW;                  // this CTA's first updated column
   const int64_t i = (int64_t)blockIdx.x * DT + tid;
@@ -135,12 +178,12 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
       double gmax = 0.0;
       dev::Cand cd = dev::cand_none();
       for (int w = tid; w < a.world; w += 32) {
-        const double* r = a.gathered + (int64_t)w * REC;
-        gmax = fmax(gmax, r[2]);
-        const long long idx = (long long)r[1];
+        const double* r = gathered + (int64_t)w * REC;
+        gmax = fmax(gmax, __ldcg(r + 2));
+        const long long idx = (long long)__ldcg(r + 1);
         if (idx >= 0) {
           dev::Cand x = dev::cand_none();
-          x.a1 = r[0];
+          x.a1 = __ldcg(r);
           x.i1 = idx * 64 + w;                      // rank index rides in the low bits (world <= 64)
           cd = dev::cand_merge(cd, x);
         }
@@ -162,21 +205,21 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
       }
       return;
     }
-    rec = a.gathered + (int64_t)s_bw * REC;
+    rec = gathered + (int64_t)s_bw * REC;
     const long long g = s_g;
     if (g >= a.col0 && g < a.col0 + nloc) pl = g - a.col0;
     if (corner) {
       if (tid == 0) a.Js[t - 1] = g;
       if (a.U)
-        for (int64_t c = t - 1 + tid; c < k; c += DT) a.U[(t - 1) + c * a.ldu] = rec[4 + c];
+        for (int64_t c = t - 1 + tid; c < k; c += DT) a.U[(t - 1) + c * a.ldu] = __ldcg(rec + 4 + c);
     }
-    if (tid < DCW) su[tid] = c0 + tid < k ? rec[4 + c0 + tid] : 0.0;
+    if (tid < DCW) su[tid] = c0 + tid < k ? __ldcg(rec + 4 + c0 + tid) : 0.0;
     __syncthreads();
   }
   bool act = in && fl < 0 && i != pl;
   double mt = 0.0;                                                    // M(i, t) after the update
   if (t > 0) {
-    const double piv = rec[4 + t - 1];
+    const double piv = __ldcg(rec + 4 + t - 1);
     const double li = act ? __ddiv_rn(mprev, piv) : 0.0;
     if (blockIdx.y == 0 && in) {
       if (act) {
@@ -242,14 +285,31 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
     L.hdr->ctr = 0u;
   }
   for (int64_t c = tid; c < k; c += DT) a.cand[4 + c] = has ? __ldcg(L.M + cd.i1 + c * nloc) : 0.0;
+  if (a.peers != nullptr) {
+    // publish the record of step t into slot [t & 1][rank] of every mailbox, then the flags
+    __syncthreads();
+    const double hdr[4] = {a.cand[0], a.cand[1], a.cand[2], 0.0};
+    const int64_t off = (int64_t)(t & 1) * a.world * REC + (int64_t)a.rank * REC;
+    for (int q = 0; q < a.world; ++q) {
+      double* dst = a.peers[q] + off;
+      for (int64_t c = tid; c < REC; c += DT) dst[c] = c < 4 ? hdr[c] : a.cand[c];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid < a.world) st_release_sys(mb_flags(a.peers[tid], a.world, REC) + a.rank, epoch + (unsigned long long)t + 1ull);
+  }
 }
 
 }  // namespace
 
 size_t lupp_dist_state_bytes(int64_t nloc, int64_t k) { return dist_state_bytes(nloc, k); }
+size_t lupp_dist_mailbox_bytes(int64_t k, int world) {
+  return (size_t)8 * (2 * (size_t)world * (size_t)(k + 4) + (size_t)world + 1);
+}
 
 sk_status lupp_dist_begin(sk_ctx* c, const double* X, int64_t nloc, int64_t ldx, int64_t k, int64_t col0, void* state,
-                          double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand) {
+                          double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand, double* const* peers,
+                          int rank, int world, double* own_mailbox) {
   DistLayout L = dist_layout(state, nloc);
   SK_CUDA(c, cudaMemsetAsync(state, 0, 256, c->stream));
   if (Lf && nloc > 0) SK_CUDA(c, cudaMemset2DAsync(Lf, ldlf * sizeof(double), 0, nloc * sizeof(double), k, c->stream));
@@ -260,17 +320,22 @@ sk_status lupp_dist_begin(sk_ctx* c, const double* X, int64_t nloc, int64_t ldx,
     k_dist_begin<<<grid, 256, 0, c->stream>>>(X, ldx, nloc, k, L);
     SK_TRY(launched(c));
   }
-  return lupp_dist_step(c, state, nloc, k, col0, 0, nullptr, 0, nullptr, Lf, ldlf, U, ldu, cand);
+  if (peers) {
+    k_dist_begin_epoch<<<1, 1, 0, c->stream>>>(own_mailbox, world, k);
+    SK_TRY(launched(c));
+  }
+  return lupp_dist_step(c, state, nloc, k, col0, 0, nullptr, world, nullptr, Lf, ldlf, U, ldu, cand, peers, rank);
 }
 
 sk_status lupp_dist_step(sk_ctx* c, void* state, int64_t nloc, int64_t k, int64_t col0, int64_t t,
                          const double* gathered, int world, int64_t* Js, double* Lf, int64_t ldlf, double* U,
-                         int64_t ldu, double* cand) {
+                         int64_t ldu, double* cand, double* const* peers, int rank) {
   StepArgs a{};
   a.L = dist_layout(state, nloc);
   a.nloc = nloc; a.k = k; a.col0 = col0; a.t = t;
   a.gathered = gathered; a.world = world;
   a.Js = Js; a.Lf = Lf; a.ldlf = ldlf; a.U = U; a.ldu = ldu; a.cand = cand;
+  a.peers = peers; a.rank = rank;
   const int64_t cols = t == 0 ? 1 : std::max<int64_t>(1, cdiv(k - t, DCW));
   dim3 grid((unsigned)dist_rb(nloc), (unsigned)cols);
   k_dist_step<<<grid, DT, 0, c->stream>>>(a);

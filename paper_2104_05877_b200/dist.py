@@ -6,7 +6,7 @@ One process per GPU.  A (m x n) is split into contiguous column blocks, rank r o
   sketch      X_r = Gamma A_r on every rank, no communication: Gamma(r, i) depends only on the
               seed and the row index i of A (R1), which is not sharded, so every rank
               regenerates the same Gamma and X = [X_0, X_1, ...] column-wise (Alg. 2 line 2).
-  select_cols two exchange patterns, both equal to single-GPU LUPP on the unsharded sketch
+  select_cols three exchange patterns, all equal to single-GPU LUPP on the unsharded sketch
               (ties to the lowest GLOBAL index, R6):
               "step" (the per-step design): the panel stays sharded; at each of the
               k pivot steps every rank proposes its best active row as one record (value,
@@ -16,6 +16,8 @@ One process per GPU.  A (m x n) is split into contiguous column blocks, rank r o
               "replicate" (variant ii): the k sketch rows that column LUPP can read (R5) are
               all-gathered once (k x n doubles) and every rank runs the single-GPU cluster
               LUPP kernel on identical bytes.
+              "p2p" (variant i, ``P2PStepwise``): the per-step design with the exchange inside
+              the step kernel -- records stored into the peers' mailboxes over NVLink.
   gather C    each rank writes the skeleton columns it owns (zeros elsewhere,
               sk_gather_cols_shard) and a sum all-reduce assembles C = A(:, J_s) exactly.
   select_rows row LUPP on the replicated C, identical on every rank (Alg. 2 line 4).
@@ -140,6 +142,58 @@ class CapturedStepwise:
         return self.sel.Js, self.sel.Lf, self.sel.U
 
 
+class P2PStepwise:
+    """select_cols_stepwise with the exchange INSIDE the step kernel (SURVEY 8(e) variant i): each
+    rank owns a mailbox in device memory, maps every peer's mailbox through CUDA IPC (NVLink peer
+    memory on one node), and the step kernel stores its record straight into the peers' mailboxes
+    and releases a flag -- no collective and no host call between pivot steps.  The group is used
+    only once, to exchange the IPC handles.  ``run(X_local)`` -> (Js, Lf, U); ``close()`` unmaps."""
+
+    def __init__(self, n_global, k, group=None, device=None):
+        from . import api
+        self.api = api
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        col0, nloc = shard(n_global, world, rank)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.k, self.group, self.world, self.rank = k, group, world, rank
+        self.mailbox = api.ipc_alloc(api.mailbox_bytes(k, world), dev.index)
+        self.imported = []
+        if world == 1:
+            ptrs = [self.mailbox]
+        else:
+            handles = [None] * world
+            dist.all_gather_object(handles, api.ipc_export(self.mailbox, dev.index), group=group)
+            ptrs = []
+            for r in range(world):
+                if r == rank:
+                    ptrs.append(self.mailbox)
+                else:
+                    p = api.ipc_import(handles[r], dev.index)
+                    self.imported.append(p)
+                    ptrs.append(p)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=dev)
+        self.sel = api.LuppDistP2P(nloc, k, col0, world, rank, self.peers, self.mailbox, dev.index)
+
+    def run(self, X_local):
+        self.sel.begin(X_local)
+        for t in range(1, self.k + 1):
+            self.sel.step(t)
+        self.sel.info()
+        return self.sel.Js, self.sel.Lf, self.sel.U
+
+    def close(self):
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier(group=self.group)          # no peer still writes into our mailbox
+        for p in self.imported:
+            self.api.ipc_close(p)
+        self.imported = []
+        if self.mailbox:
+            self.api.ipc_free(self.mailbox)
+            self.mailbox = 0
+
+
 def dist_rand_lupp(A_local, n_global, k, l, embedding="gaussian", seed=0, zeta=8, rows=False,
                    residual=False, group=None, backend=None, exchange="replicate"):
     """Algorithm 2 on a column-sharded A.  A_local: this rank's block (m x ncols, column-major).
@@ -160,11 +214,17 @@ def dist_rand_lupp(A_local, n_global, k, l, embedding="gaussian", seed=0, zeta=8
     X_local = backend.sketch(A_local, l, embedding, seed, zeta)               # l x ncols
     if exchange == "step":
         Js, Lf, _ = select_cols_stepwise(X_local, n_global, k, group, backend)  # Lf: this rank's rows
+    elif exchange == "p2p":
+        p2p = P2PStepwise(n_global, k, group, X_local.device.index)
+        try:
+            Js, Lf, _ = p2p.run(X_local)
+        finally:
+            p2p.close()
     elif exchange == "replicate":
         Xk = _all_gather_cols(X_local[:k], n_global, group, world)            # k x n (rows 0..k-1)
         Js, Lf = backend.select_cols(Xk, k)
     else:
-        raise ValueError("exchange must be 'step' or 'replicate'")
+        raise ValueError("exchange must be 'step', 'p2p' or 'replicate'")
     out["Js"] = Js
     out["Lf"] = Lf
     if rows or residual:

@@ -148,3 +148,111 @@ def test_dist_rand_lupp_step_exchange_nccl_world1():
         assert out["Is"].cpu().tolist() == ipiv.tolist()
     finally:
         tdist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- exchange fused into the kernel
+def emulate_p2p(X, k, world, reps=1):
+    """P ranks on one GPU with P2P mailboxes: rank r's step-t kernel waits for the flags of all
+    ranks' step t-1 kernels, which were launched before it in program order on the same stream
+    (so no kernel ever waits for one that has not run).  Returns (Js, Lf, U, infos) of the last rep."""
+    n = X.shape[1]
+    boxes = [sk.ipc_alloc(sk.mailbox_bytes(k, world), 0) for _ in range(world)]
+    peers = torch.tensor(boxes, dtype=torch.int64, device=DEV)
+    try:
+        sels, blocks = [], []
+        for r in range(world):
+            c0, nc = shard(n, world, r)
+            sels.append(sk.LuppDistP2P(nc, k, c0, world, r, peers, boxes[r], 0))
+            blocks.append(torch.from_numpy(np.ascontiguousarray(X[:, c0:c0 + nc])).to(DEV))
+        for _ in range(reps):
+            for s, b in zip(sels, blocks):
+                s.begin(b)
+            for t in range(1, k + 1):
+                for s in sels:
+                    s.step(t)
+            infos = []
+            for s in sels:
+                try:
+                    infos.append(s.info())
+                except sk.SkelError as e:
+                    infos.append(e.info)
+        Js = [s.Js.cpu().numpy() for s in sels]
+        for j in Js[1:]:
+            np.testing.assert_array_equal(j, Js[0])
+        Lf = np.vstack([s.Lf.cpu().numpy()[:s.nloc] for s in sels])
+        return Js[0], Lf, sels[0].U.cpu().numpy(), infos
+    finally:
+        torch.cuda.synchronize()
+        for b in boxes:
+            sk.ipc_free(b, 0)
+
+
+@pytest.mark.parametrize("n,k,world", [(251, 20, 1), (251, 20, 3), (1000, 64, 8), (5, 5, 8)])
+def test_p2p_stepwise_bitwise_equals_oracle(n, k, world):
+    X = np.random.default_rng(11 * n + k).standard_normal((k + 5, n))
+    Js, Lf, U, infos = emulate_p2p(X, k, world, reps=2)                 # rep 2 reuses the mailboxes
+    piv, Lfo, Uo, _ = o_lupp.select_cols(X, k)
+    assert infos == [0] * world
+    np.testing.assert_array_equal(Js, piv)
+    np.testing.assert_array_equal(U, Uo)
+    np.testing.assert_array_equal(Lf, Lfo)
+
+
+def test_p2p_stepwise_ties_and_rank_failure():
+    l = 10
+    X = kahan_witness(l, 40)[:, np.r_[np.arange(l, 40), np.arange(l)]]
+    Js, _, _, infos = emulate_p2p(X, l, 3)
+    piv, _, _, _ = o_lupp.select_cols(X, l)
+    np.testing.assert_array_equal(Js, piv)
+    Z = np.zeros((6, 50))
+    Z[0, 31] = 3.0
+    Z[1, 7] = 1e-20
+    Js, _, _, infos = emulate_p2p(Z, 4, 3)
+    assert infos == [2, 2, 2] and Js[0] == 31 and (Js[1:] == -1).all()
+
+
+def test_p2p_dist_rand_lupp_world1():
+    from inputs import make_c1
+    from paper_2104_05877_b200.dist import dist_rand_lupp
+    tdist = _nccl_world1(29547)
+    try:
+        A, _ = make_c1(seed=1001)
+        Ad = sk.fortran(torch.from_numpy(A).to(DEV))
+        out = dist_rand_lupp(Ad, 256, 20, 40, "gaussian", 2001, rows=True, exchange="p2p")
+        X = o_sketch.sketch(A, 40, "gaussian", 2001)
+        piv, _, _, _ = o_lupp.select_cols(X, 20)
+        assert out["Js"].cpu().tolist() == piv.tolist()
+    finally:
+        tdist.destroy_process_group()
+
+
+def _ipc_child(handle, q):
+    from cuda.bindings import runtime as cudart
+    import paper_2104_05877_b200 as skc
+    torch.cuda.set_device(0)
+    ptr = skc.ipc_import(handle, 0)
+    host = np.zeros(4, dtype=np.float64)
+    err, = cudart.cudaMemcpy(host.ctypes.data, ptr, 32, cudart.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+    q.put((int(err), host.tolist()))
+    skc.ipc_close(ptr, 0)
+
+
+def test_ipc_handle_maps_the_buffer_in_another_process():
+    """The mailbox plumbing of P2PStepwise: a second process maps the buffer by its handle and reads
+    what the first wrote (no kernel waits on the other process)."""
+    import torch.multiprocessing as mp
+    from cuda.bindings import runtime as cudart
+    ptr = sk.ipc_alloc(64, 0)
+    try:
+        vals = np.array([1.5, -2.25, 3.0, 7.0])
+        err, = cudart.cudaMemcpy(ptr, vals.ctypes.data, 32, cudart.cudaMemcpyKind.cudaMemcpyHostToDevice)
+        assert int(err) == 0
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        p = ctx.Process(target=_ipc_child, args=(sk.ipc_export(ptr, 0), q))
+        p.start()
+        err, got = q.get(timeout=120)
+        p.join(timeout=60)
+        assert p.exitcode == 0 and err == 0 and got == vals.tolist()
+    finally:
+        sk.ipc_free(ptr, 0)

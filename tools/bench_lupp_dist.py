@@ -66,9 +66,29 @@ def main():
         ms2 = timed(gr.replay)
         sel.info()
         same2 = bool((sel.Js == Js_ref).all())
+        # exchange fused into the kernel (P2P mailbox, world 1): begin + k step kernels in one graph
+        # (the epoch lives on the device, so the graph replays)
+        box = sk.ipc_alloc(sk.mailbox_bytes(k, 1), 0)
+        peers = torch.tensor([box], dtype=torch.int64, device="cuda")
+        sp = sk.LuppDistP2P(n, k, 0, 1, 0, peers, box, 0)
+
+        def ploop():
+            sp.begin(X)
+            for t in range(1, k + 1):
+                sp.step(t)
+        ploop()
+        torch.cuda.synchronize()
+        gp = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gp):
+            ploop()
+        ms3 = timed(gp.replay)
+        sp.info()
+        same3 = bool((sp.Js == Js_ref).all())
+        sk.ipc_free(box, 0)
         ms_single = timed(lambda: sk.select_cols(X, k, want_factors=False))
         print(f"{name:42s} graph+nccl {ms:8.3f} ms ({1e3 * ms / k:6.2f} us/step, pivots==single {same})   "
               f"kernels P=8 {ms2:8.3f} ms ({1e3 * ms2 / k:6.2f} us/step, {same2})   "
+              f"P2P in-kernel exchange {ms3:8.3f} ms ({1e3 * ms3 / k:6.2f} us/step, {same3})   "
               f"single-GPU cluster LUPP {ms_single:7.3f} ms", flush=True)
     dist.destroy_process_group()
 
