@@ -54,9 +54,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--piter", type=int, default=0, help="plain power iterations (Rand-LUPP-qpiter, P:527)")
-    ap.add_argument("--dist-exchange", default="replicate", choices=["replicate", "step"],
-                    help="N > 1: column-LUPP exchange -- one k x n all-gather then replicated LUPP, or one "
-                         "all-gather of P records per pivot step (CUDA graph)")
+    ap.add_argument("--dist-exchange", default="replicate", choices=["replicate", "step", "p2p"],
+                    help="N > 1: column-LUPP exchange -- one k x n all-gather then replicated LUPP, one "
+                         "all-gather of P records per pivot step (CUDA graph), or the records stored into "
+                         "the peers' mailboxes by the step kernel itself (NVLink peer memory, CUDA graph)")
     return ap.parse_args()
 
 
@@ -223,6 +224,20 @@ def main_dist(args, world, rank, local):
                 from paper_2104_05877_b200.dist import CapturedStepwise
                 cap.append(CapturedStepwise(Xbuf, n_global, k))
             Js, _, _ = cap[0].run()
+        elif args.dist_exchange == "p2p":
+            if not cap:                      # mailboxes + one captured graph of begin + k steps
+                from paper_2104_05877_b200.dist import P2PStepwise
+                p2p = P2PStepwise(n_global, k, None, local)
+                p2p.run(Xbuf)
+                torch.cuda.synchronize(dev)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    p2p.sel.begin(Xbuf)
+                    for t in range(1, k + 1):
+                        p2p.sel.step(t)
+                cap.append((p2p, g))
+            cap[0][1].replay()
+            Js = cap[0][0].sel.Js
         else:
             Xk = _all_gather_cols(X[:k], n_global, None, world)
             Js, _, _, _ = sk.select_cols(Xk, k, check=False)
