@@ -155,6 +155,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg, k, l, seed, desc = workload(args)
+    if args.config == "C5":   # 68.7 GB: the host oracle cannot hold it (the GPU path builds it on device)
+        print(json.dumps({"impl": "reference", "unavailable": "C5 (131072 x 65536 FP64, 68.7 GB) exceeds the "
+                          "host oracle's memory; the reference arm runs C1-C4"}), flush=True)
+        return 0
     A, _ = make_input(args, cfg)
     cores, model = cpu_info()
     steps = max(1, min(args.steps, 3))
