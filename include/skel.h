@@ -95,7 +95,10 @@ int64_t sk_launch_count(const sk_ctx* ctx);
 
 /* ---- S0 + S1: sketch  (Algorithm 2 lines 1-2) ---------------- */
 
-/* X = Gamma A.  Gamma (l x m) is drawn from (emb, zeta, seed) on the fly.
+/* X = Gamma A.  Gamma (l x m) is drawn from (emb, zeta, seed) on every call (Philox4x32-10,
+ * R1-R4): the Gaussian one into a per-call workspace image consumed by the FP64 tensor-core GEMM
+ * (~8 l m bytes; above 8 GB it is generated per tile instead and nothing is stored), the sparse-sign
+ * structure into a per-call CSR (4 bytes per nonzero), SRTT's permutations and signs per CTA.
  *   A   m x n column-major (lda >= m), read only.
  *   X   l x n row-major (ldx >= n), written.
  *   Requires 1 <= l <= m, n >= 0; for SK_EMB_SPARSE_SIGN 2 <= zeta <= min(l, 64)
