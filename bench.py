@@ -98,11 +98,12 @@ def cpu_info():
     return cores, model
 
 
-def oracle_selection(A, k, l, seed, emb="gaussian"):
-    """The oracle's sketch + LUPP (test infrastructure; timed as the CPU baseline)."""
+def oracle_selection(A, k, l, seed, emb="gaussian", piter=0):
+    """The oracle's sketch (with q = piter plain power iterations) + LUPP (test infrastructure;
+    timed as the CPU baseline)."""
     from oracle import lupp as o_lupp
     from oracle import sketch as o_sketch
-    X = o_sketch.sketch(A, l, emb, seed)
+    X = o_sketch.sketch(A, l, emb, seed) if piter == 0 else o_sketch.sketch_power(A, l, emb, seed, piter)
     piv, _, _, _ = o_lupp.select_cols(X, k)
     return piv
 
@@ -164,11 +165,11 @@ def run_reference(args):
     steps = max(1, min(args.steps, 3))
     warm = min(args.warmup, 1)
     for _ in range(warm):
-        oracle_selection(A, k, l, seed, cfg["emb"])
+        oracle_selection(A, k, l, seed, cfg["emb"], args.piter)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        oracle_selection(A, k, l, seed, cfg["emb"])
+        oracle_selection(A, k, l, seed, cfg["emb"], args.piter)
         times.append((time.perf_counter() - t0) * 1e3)
     v = statistics.mean(times)
     line = {
@@ -177,7 +178,7 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "m": int(A.shape[0]), "n": int(A.shape[1]), "k": k, "l": l},
         "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "oracle",
-                         "sample": f"full {args.config} selection (oracle sketch + LUPP) on {model}"},
+                         "sample": f"full {args.config} selection (oracle sketch{' with %d power iteration(s)' % args.piter if args.piter else ''} + LUPP) on {model}"},
         "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -471,11 +472,11 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and A_np is not None:
         cores, model = cpu_info()
         t0 = time.perf_counter()
-        piv_o = oracle_selection(A_np, k, l, seed, emb)
+        piv_o = oracle_selection(A_np, k, l, seed, emb, args.piter)
         cpu_ms = (time.perf_counter() - t0) * 1e3
         same = int(np.sum(piv_o == Js.cpu().numpy()))
         cpu = {"value": cpu_ms, "unit": "ms", "cores": cores, "kind": "oracle",
-               "sample": f"one full {args.config} selection (sketch + LUPP), numpy/BLAS on {model}",
+               "sample": f"one full {args.config} selection (sketch{' with %d power iteration(s)' % args.piter if args.piter else ''} + LUPP), numpy/BLAS on {model}",
                "pivots_equal_to_gpu": f"{same}/{k}"}
 
     if rank == 0:

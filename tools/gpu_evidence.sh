@@ -9,7 +9,7 @@ timeout 600 python bench.py --config C1 > gpurun_out/bench_c1.log 2>&1
 timeout 900 python bench.py --config C3 --steps 5 > gpurun_out/bench_c3.log 2>&1
 timeout 900 python bench.py --config C4 --steps 5 > gpurun_out/bench_c4.log 2>&1
 timeout 900 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5.log 2>&1
-timeout 600 python bench.py --piter 1 --steps 5 --no-cpu-baseline > gpurun_out/bench_c2_1piter.log 2>&1
+timeout 600 python bench.py --piter 1 --steps 5 > gpurun_out/bench_c2_1piter.log 2>&1
 timeout 300 python tools/bench_sketch.py > gpurun_out/bench_sketch.log 2>&1
 timeout 300 python tools/bench_lupp.py > gpurun_out/bench_lupp.log 2>&1
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/plain.log 2>&1 && \
