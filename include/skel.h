@@ -192,7 +192,9 @@ sk_status sk_lupp_dist_info(sk_ctx* ctx, const void* state, int64_t* info);
  * and publishes its step-t record by storing it into slot [t & 1][rank] of every mailbox followed
  * by a system-scope fence and flag release (epoch + t + 1).  Every rank must run the same sequence
  * of selections on its mailbox.  Same results as sk_lupp_dist_begin/step; no host call or
- * collective between steps. */
+ * collective between steps.  The wait is bounded: if a peer's flag does not arrive within
+ * SKEL_PEER_TIMEOUT_MS (environment, read once; default 30000) the kernel latches -t and the
+ * remaining steps do nothing; sk_lupp_dist_info then returns SK_E_STATE with *info = -t. */
 size_t sk_lupp_dist_mailbox_bytes(int64_t k, int32_t world);
 sk_status sk_lupp_dist_begin_p2p(sk_ctx* ctx, const double* X, int64_t nloc, int64_t ldx, int64_t k, int64_t col0,
                                  void* state, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* cand,
@@ -227,7 +229,10 @@ sk_status sk_select_cols_cpqr(sk_ctx* ctx, const double* X, int64_t l, int64_t n
 sk_status sk_select_cols_deim(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* X,
                               int64_t l, int64_t ldx, int64_t k, int64_t* Js, int64_t* info);
 
-/* ---- S3: gather C = A(:, Js)  (eq:Js; columns in pivot order, R8) ---- */
+/* ---- S3: gather C = A(:, Js)  (eq:Js; columns in pivot order, R8) ----
+ * A m x n column-major (lda >= m); Js device int64[k]; C m x k column-major (ldc >= m).
+ * Js lives on the device and is not read on the host: an index outside [0, n) yields a zero
+ * column of C (no out-of-bounds read).  Asynchronous on the context stream. */
 sk_status sk_gather_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
                          const int64_t* Js, int64_t k, double* C, int64_t ldc);
 

@@ -212,9 +212,8 @@ sk_status sk_gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64
   c->err.clear();
   SK_ARG(c, A && Js && C, "sk_gather_cols: NULL pointer");
   SK_ARG(c, m >= 0 && n >= 0 && k >= 0 && lda >= m && ldc >= m, "sk_gather_cols: bad sizes");
-  (void)n;
   SK_CUDA(c, cudaSetDevice(c->device));
-  return gather_cols(c, A, m, lda, Js, k, C, ldc);
+  return gather_cols_shard(c, A, m, lda, 0, n, Js, k, C, ldc);   // Js outside [0, n): zero column
 }
 
 sk_status sk_gather_cols_shard(sk_ctx* c, const double* A, int64_t m, int64_t ncols, int64_t lda, int64_t col0,
@@ -253,6 +252,7 @@ sk_status sk_lupp_dist_step(sk_ctx* c, void* state, int64_t nloc, int64_t k, int
   SK_ARG(c, nloc >= 0 && k >= 1 && t >= 1 && t <= k && world >= 1 && world <= 64 && col0 >= 0, "sk_lupp_dist_step: bad sizes (world <= 64)");
   SK_ARG(c, !Lf || ldlf >= nloc, "sk_lupp_dist_step: ldlf >= nloc required");
   SK_ARG(c, !U || ldu >= k, "sk_lupp_dist_step: ldu >= k required");
+  SK_CUDA(c, cudaSetDevice(c->device));
   return lupp_dist_step(c, state, nloc, k, col0, t, gathered, world, Js, Lf, ldlf, U, ldu, cand);
 }
 
@@ -285,6 +285,7 @@ sk_status sk_lupp_dist_step_p2p(sk_ctx* c, void* state, int64_t nloc, int64_t k,
   SK_ARG(c, world >= 1 && world <= 64 && rank >= 0 && rank < world, "sk_lupp_dist_step_p2p: bad rank/world");
   SK_ARG(c, !Lf || ldlf >= nloc, "sk_lupp_dist_step_p2p: ldlf >= nloc required");
   SK_ARG(c, !U || ldu >= k, "sk_lupp_dist_step_p2p: ldu >= k required");
+  SK_CUDA(c, cudaSetDevice(c->device));
   return lupp_dist_step(c, state, nloc, k, col0, t, nullptr, world, Js, Lf, ldlf, U, ldu, cand, peers, rank);
 }
 
@@ -299,6 +300,7 @@ sk_status sk_ipc_alloc(sk_ctx* c, size_t bytes, void** ptr) {
 
 sk_status sk_ipc_free(sk_ctx* c, void* ptr) {
   if (!c) return SK_E_ARG;
+  SK_CUDA(c, cudaSetDevice(c->device));
   SK_CUDA(c, cudaFree(ptr));
   return SK_OK;
 }
@@ -324,6 +326,7 @@ sk_status sk_ipc_import(sk_ctx* c, const void* handle, void** ptr) {
 
 sk_status sk_ipc_close(sk_ctx* c, void* ptr) {
   if (!c) return SK_E_ARG;
+  SK_CUDA(c, cudaSetDevice(c->device));
   SK_CUDA(c, cudaIpcCloseMemHandle(ptr));
   return SK_OK;
 }
@@ -336,7 +339,13 @@ sk_status sk_lupp_dist_info(sk_ctx* c, const void* state, int64_t* info) {
   DBuf st;
   SK_TRY(st.alloc(c, sizeof(int64_t)));
   SK_TRY(lupp_dist_status(c, state, st.as<int64_t>()));
-  return finish_info(c, st.as<int64_t>(), info, "sk_lupp_dist");
+  int64_t v = 0;
+  SK_TRY(to_host(c, &v, st.p, sizeof(int64_t)));
+  *info = v;
+  if (v < 0)
+    return fail(c, SK_E_STATE, "sk_lupp_dist: no record from a peer within the timeout (SKEL_PEER_TIMEOUT_MS, default 30 s) at step " + std::to_string(-v));
+  if (v > 0) return fail(c, SK_E_RANK, "sk_lupp_dist: rank deficiency at step " + std::to_string(v));
+  return SK_OK;
 }
 
 sk_status sk_residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* C, int64_t k,
@@ -466,8 +475,9 @@ sk_status sk_rand_lupp(sk_ctx* c, const double* A, int a_on_host, int64_t m, int
   SK_TRY(lupp(c, Xd.as<double>(), true, n, k, n, Jd.as<int64_t>(), nullptr, 0, nullptr, 0, nullptr,
               st.as<int64_t>()));
   int64_t inf = 0;
-  SK_TRY(finish_info(c, st.as<int64_t>(), &inf, "sk_rand_lupp (columns)"));
-  if (info) *info = inf;
+  sk_status rc = finish_info(c, st.as<int64_t>(), &inf, "sk_rand_lupp (columns)");
+  if (info) *info = inf;                                   // set on SK_E_RANK too (the failing step)
+  SK_TRY(rc);
   if (Is) {
     SK_ARG(c, k <= m, "sk_rand_lupp: k <= m required for row skeletons");
     SK_TRY(Cd.alloc(c, (size_t)m * k * sizeof(double)));
@@ -475,8 +485,9 @@ sk_status sk_rand_lupp(sk_ctx* c, const double* A, int a_on_host, int64_t m, int
     SK_TRY(gather_cols(c, Adev, m, ldad, Jd.as<int64_t>(), k, Cd.as<double>(), m));
     SK_TRY(lupp(c, Cd.as<double>(), false, m, k, m, Id.as<int64_t>(), nullptr, 0, nullptr, 0, nullptr,
                 st.as<int64_t>()));
-    SK_TRY(finish_info(c, st.as<int64_t>(), &inf, "sk_rand_lupp (rows)"));
+    rc = finish_info(c, st.as<int64_t>(), &inf, "sk_rand_lupp (rows)");
     if (info) *info = inf;
+    SK_TRY(rc);
     SK_TRY(to_host(c, Is, Id.p, (size_t)k * sizeof(int64_t)));
   }
   SK_TRY(to_host(c, Js, Jd.p, (size_t)k * sizeof(int64_t)));

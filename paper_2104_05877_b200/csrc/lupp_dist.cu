@@ -19,6 +19,7 @@
 // Record layout (double[k + 4]): [0] |value| or -1 if the rank has no active row, [1] global row
 // index or -1, [2] the rank's max |panel| (for R7), [3] reserved (0), [4 + c] M(i, c), c < k.
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -30,7 +31,7 @@ constexpr int DT = 256;   // panel rows per CTA (one row per thread)
 constexpr int DCW = 32;   // panel columns per CTA
 
 struct DistHdr {
-  long long status;            // 0 or the 1-based failing step (latched)
+  long long status;            // 0, the 1-based failing step (latched), or -t: peer timeout at step t
   unsigned ctr;                // last-CTA ticket counter (reset by the last CTA)
   unsigned pad;
   unsigned long long lmax;     // bits of max |M| over this rank's panel (non-negative doubles order as u64)
@@ -108,6 +109,7 @@ struct StepArgs {
   // records from its own mailbox, and publishes its next record by storing it into every peer's
   // mailbox and releasing the flags -- the exchange is part of the kernel, no collective call.
   double* const* peers; int rank;
+  unsigned long long timeout_ns;   // bound on the wait for a peer's record (P2P mode)
 };
 
 
@@ -115,6 +117,11 @@ struct StepArgs {
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* f) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
   return v;
 }
 __device__ __forceinline__ void st_release_sys(unsigned long long* f, unsigned long long v) {
@@ -143,10 +150,24 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
     epoch = *(volatile unsigned long long*)(flags + a.world);
     if (t > 0) {
       // records of step t-1 sit in buffer (t-1) & 1 of the local mailbox once every flag >= epoch + t
-      if (tid < a.world)
-        while (ld_acquire_sys(flags + tid) < epoch + (unsigned long long)t) {
-        }
+      // bounded wait: a peer that never publishes (crashed rank) latches status -t after
+      // a.timeout_ns (30 s; SKEL_PEER_TIMEOUT_MS) instead of hanging the GPU; sk_lupp_dist_info
+      // reports it as SK_E_STATE
+      __shared__ int s_late;
+      if (tid == 0) s_late = 0;
       __syncthreads();
+      if (tid < a.world) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_sys(flags + tid) < epoch + (unsigned long long)t) {
+          if (globaltimer_ns() - t0 > a.timeout_ns) { s_late = 1; break; }
+        }
+      }
+      __syncthreads();
+      if (s_late) {
+        if (tid == 0) atomicCAS(reinterpret_cast<unsigned long long*>(&L.hdr->status), 0ull,
+                                (unsigned long long)(-(long long)t));
+        return;
+      }
       gathered = mb + (int64_t)((t - 1) & 1) * a.world * REC;
     }
   }
@@ -336,6 +357,12 @@ sk_status lupp_dist_step(sk_ctx* c, void* state, int64_t nloc, int64_t k, int64_
   a.gathered = gathered; a.world = world;
   a.Js = Js; a.Lf = Lf; a.ldlf = ldlf; a.U = U; a.ldu = ldu; a.cand = cand;
   a.peers = peers; a.rank = rank;
+  static const unsigned long long timeout_ns = [] {
+    const char* v = std::getenv("SKEL_PEER_TIMEOUT_MS");
+    const long long ms = v ? std::atoll(v) : 30000;
+    return (unsigned long long)(ms > 0 ? ms : 30000) * 1000000ull;
+  }();
+  a.timeout_ns = timeout_ns;
   const int64_t cols = t == 0 ? 1 : std::max<int64_t>(1, cdiv(k - t, DCW));
   dim3 grid((unsigned)dist_rb(nloc), (unsigned)cols);
   k_dist_step<<<grid, DT, 0, c->stream>>>(a);

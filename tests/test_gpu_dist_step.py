@@ -256,3 +256,36 @@ def test_ipc_handle_maps_the_buffer_in_another_process():
         assert p.exitcode == 0 and err == 0 and got == vals.tolist()
     finally:
         sk.ipc_free(ptr, 0)
+
+
+_TIMEOUT_CHILD = r"""
+import numpy as np, torch
+import paper_2104_05877_b200 as sk
+from paper_2104_05877_b200._lib import SK_E_STATE
+k, world = 6, 2
+X = torch.from_numpy(np.random.default_rng(1).standard_normal((k + 2, 40))).to("cuda:0")
+boxes = [sk.ipc_alloc(sk.mailbox_bytes(k, world), 0) for _ in range(world)]
+peers = torch.tensor(boxes, dtype=torch.int64, device="cuda:0")
+s = sk.LuppDistP2P(20, k, 0, world, 0, peers, boxes[0], 0)   # rank 1 never runs
+s.begin(X[:, :20].contiguous())
+for t in range(1, k + 1):
+    s.step(t)
+try:
+    s.info()
+    raise SystemExit("no error")
+except sk.SkelError as e:
+    assert e.status == SK_E_STATE and e.info == -1, (e.status, e.info)
+torch.cuda.synchronize()
+print("TIMEOUT-OK")
+"""
+
+
+def test_p2p_missing_peer_times_out_instead_of_hanging():
+    """Rank 1 of 2 never publishes: rank 0's step-1 kernel gives up after SKEL_PEER_TIMEOUT_MS,
+    latches -1, and the remaining steps return at once (child process, bounded by timeout)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, SKEL_PEER_TIMEOUT_MS="300")
+    r = subprocess.run([sys.executable, "-c", _TIMEOUT_CHILD], env=env, capture_output=True, text=True,
+                       timeout=180, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "TIMEOUT-OK" in r.stdout, r.stdout + r.stderr

@@ -113,3 +113,27 @@ def test_argument_errors_are_reported(call):
             sk.residual(A, torch.zeros(2, dtype=torch.int64, device=DEV), None, "nope")
     if isinstance(e.value, sk.SkelError):
         assert e.value.status == 1
+
+
+def test_gather_cols_out_of_range_index_gives_zero_column():
+    # Js is device data the host never reads: an index outside [0, n) must not read out of bounds
+    A = np.random.default_rng(3).standard_normal((37, 9))
+    Js = torch.tensor([4, 9, -1, 0, 1 << 40], dtype=torch.int64, device=DEV)
+    C = sk.gather_cols(dev_f(A), Js).cpu().numpy()
+    np.testing.assert_array_equal(C[:, 0], A[:, 4])
+    np.testing.assert_array_equal(C[:, 3], A[:, 0])
+    for t in (1, 2, 4):
+        assert not C[:, t].any()
+
+
+def test_rand_lupp_rank_failure_reports_the_step():
+    # two nonzero columns, k = 4: the sketch has exactly two nonzero columns, so the column LUPP
+    # finds no pivot at step 3; the error carries that step (device and host A)
+    from paper_2104_05877_b200._lib import SK_E_RANK
+    A = np.zeros((60, 40))
+    A[:, 5] = np.random.default_rng(8).standard_normal(60)
+    A[:, 17] = np.random.default_rng(9).standard_normal(60)
+    for At in (torch.from_numpy(np.asfortranarray(A)), dev_f(A)):
+        with pytest.raises(sk.SkelError) as e:
+            sk.rand_lupp(At, 4, 12, "gaussian", 1)
+        assert e.value.status == SK_E_RANK and e.value.info == 3
