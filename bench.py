@@ -8,6 +8,8 @@ Haar U, V (seed 1002); Gaussian Omega, k = 512, l = k + 10 = 522 (seed 2002 + k)
 One step = the whole hot path of SURVEY.md section 8(a) for C2:
     S0+S1 sketch X = Omega A  ->  S2 select_cols (LUPP)  ->  S2' select_cols_cpqr (comparison)
     ->  S5 id_coeffs  ->  S6 residual ||A - CC^+A||_F (gather S3 + LUPP-basis S4 inside).
+The other configs follow their SURVEY 8(d) path: C3 / C4 add S3 gather + S4 select_rows as
+stages and take the CUR (C3) / column- and row-ID (C4) residuals; S2' runs on C2 only.
 value = the BASELINE.json metric "skeleton-selection time (sketch+LUPP)" = S1 + S2 device time
 per step (ms, lower is better), max over ranks.  ms_per_step = the whole step.
 L2 policy: a 512 MiB buffer is overwritten between timed steps (untimed), so every step
@@ -66,6 +68,10 @@ def workload(args):
     cfg = CONFIGS[args.config]
     if args.k is None:
         args.k = {"C1": 20, "C2": 512, "C3": 500, "C4": 200, "C5": 1000}[args.config]
+        if getattr(args, "piter", 0) and args.config == "C2":
+            # X = Omega (A^T A)^q squares the C2 spectrum (10^(-i/25)): beyond k ~ 390 the sketch is
+            # rank deficient at LUPP's 1e-14 threshold (both the oracle and the GPU stop there)
+            args.k = 256
     k = args.k
     l = cfg["l"](k)
     seed = cfg["sk_seed"] + (k if args.config in ("C2", "C4") else 0)
@@ -315,7 +321,7 @@ def main_dist(args, world, rank, local):
                        "m": m, "n": n_global, "k": k, "l": l, "parallelism": f"column-sharded x{world}", "lupp_exchange": args.dist_exchange,
                        "l2": "flushed: 512 MiB overwrite between timed steps (untimed)"},
             "residual": {"col_id_fro": math.sqrt(max(float(sums[0]), 0.0)), "normA_fro": math.sqrt(float(sums[1]))},
-            "roofline": {"kernel": "k_sketch_tma", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+            "roofline": {"kernel": "sk_sketch Gaussian = k_omega_image + k_sketch_pre (+ split-K reduce)", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None},
             "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
         }
@@ -363,27 +369,40 @@ def main():
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    # the step follows each configuration's path in SURVEY 8(d): S2' (CPQR) on C2, S3 + S4 (gather,
+    # row LUPP) on C3 / C4, the residual kinds per config (CUR on C3, column and row ID on C4)
+    do_cpqr = args.config == "C2"
+    do_rows = args.config in ("C3", "C4")
+    res_kinds = {"C3": ["cur"], "C4": ["col_id", "row_id"]}.get(args.config, ["col_id"])
+    stage_names = (["sketch", "select_cols_lupp"] + (["select_cols_cpqr"] if do_cpqr else [])
+                   + (["gather_cols", "select_rows_lupp"] if do_rows else []) + ["id_coeffs", "residual"])
+
     def step(record):
-        """One pass of the hot path; record(name, start_event, end_event)."""
-        e = [ev() for _ in range(6)]
+        """One pass of the hot path; record(events), one event per stage boundary."""
+        e = [ev() for _ in range(len(stage_names) + 1)]
+        nxt = iter(e[1:])
         e[0].record(stream)
         X = (sk.sketch(A, l, emb, seed, cfg.get("zeta", 8)) if args.piter == 0
              else sk.sketch_power(A, l, emb, seed, args.piter, cfg.get("zeta", 8)))
-        e[1].record(stream)
+        next(nxt).record(stream)
         Js, Lf, _, _ = sk.select_cols(X, k, check=False)
-        e[2].record(stream)
-        Jc, _ = sk.select_cols_cpqr(X, k, check=False)
-        e[3].record(stream)
+        next(nxt).record(stream)
+        Jc = Is = None
+        if do_cpqr:
+            Jc, _ = sk.select_cols_cpqr(X, k, check=False)
+            next(nxt).record(stream)
+        if do_rows:
+            C = sk.gather_cols(A, Js)
+            next(nxt).record(stream)
+            Is, _, _, _ = sk.select_rows(C, k, want_factors=False, check=False)
+            next(nxt).record(stream)
         Z, _ = sk.id_coeffs(Lf, Js)
-        e[4].record(stream)
-        # (with power iterations the trailing skeletons of C2 k=512 are numerically dependent --
-        # sigma^2 spans 1e-20 -- and the residual's LUPP basis reports SK_E_RANK; not part of the metric)
-        res, nA = sk.residual(A, Js, None, "col_id") if args.piter == 0 else (float("nan"), float("nan"))
-        e[5].record(stream)
+        next(nxt).record(stream)
+        res = {kind: sk.residual(A, Js, Is, kind) for kind in res_kinds}
+        next(nxt).record(stream)
         record(e)
-        return Js, Jc, res, nA
+        return Js, Jc, res
 
-    stage_names = ["sketch", "select_cols_lupp", "select_cols_cpqr", "id_coeffs", "residual"]
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             step(lambda e: None)
@@ -406,7 +425,7 @@ def main():
     for e in recs:
         for i, nm in enumerate(stage_names):
             stage_ms[nm].append(e[i].elapsed_time(e[i + 1]))
-        step_ms.append(e[0].elapsed_time(e[5]))
+        step_ms.append(e[0].elapsed_time(e[-1]))
     sel = [a + b for a, b in zip(stage_ms["sketch"], stage_ms["select_cols_lupp"])]
     value = statistics.mean(sel)
     ms_step = statistics.mean(step_ms)
@@ -415,9 +434,14 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         value, ms_step = float(t[0]), float(t[1])
 
-    Js, Jc, res, nA = out
+    Js, Jc, res = out
     from oracle.residual import optimal_error  # closed form sum_{i>k} sigma_i^2 (Eckart-Young)
     opt = optimal_error(sigma, k) if sigma is not None else None   # C4 has no closed-form spectrum
+    resid = {"opt_fro": opt}
+    for kind, (r, nA) in res.items():
+        resid[f"{kind}_fro"] = r
+        resid["normA_fro"] = nA
+        resid[f"{kind}_ratio"] = r / opt if opt else None
 
     # roofline of the dominant kernel of the selection: the sketch (one launch per call)
     sk_ms = statistics.mean(stage_ms["sketch"])
@@ -447,7 +471,7 @@ def main():
 
     # end to end through the public API with host buffers (Algorithm 2 entry point)
     e2e = None
-    if not args.no_e2e and A_np is not None:
+    if not args.no_e2e and A_np is not None and args.piter == 0:   # sk_rand_lupp has no power iterations
         A_host = torch.from_numpy(np.ascontiguousarray(A_np.T)).pin_memory().t()
         with torch.cuda.stream(stream):
             for _ in range(2):
@@ -472,12 +496,18 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and A_np is not None:
         cores, model = cpu_info()
         t0 = time.perf_counter()
-        piv_o = oracle_selection(A_np, k, l, seed, emb, args.piter)
+        from oracle.lupp import RankError
+        try:
+            piv_o = oracle_selection(A_np, k, l, seed, emb, args.piter)
+        except RankError as err:          # the selection is rank deficient at this k (both sides stop)
+            piv_o = None
+            fail_step = err.step
         cpu_ms = (time.perf_counter() - t0) * 1e3
-        same = int(np.sum(piv_o == Js.cpu().numpy()))
+        same = (f"{int(np.sum(piv_o == Js.cpu().numpy()))}/{k}" if piv_o is not None else
+                f"n/a: oracle rank failure at step {fail_step}, GPU Js[{fail_step - 1}] = {int(Js[fail_step - 1])}")
         cpu = {"value": cpu_ms, "unit": "ms", "cores": cores, "kind": "oracle",
                "sample": f"one full {args.config} selection (sketch{' with %d power iteration(s)' % args.piter if args.piter else ''} + LUPP), numpy/BLAS on {model}",
-               "pivots_equal_to_gpu": f"{same}/{k}"}
+               "pivots_equal_to_gpu": same}
 
     if rank == 0:
         line = {
@@ -490,8 +520,8 @@ def main():
                        "parallelism": "replicas" if world > 1 else "1 GPU"},
             "stages_ms": {nm: statistics.mean(v) for nm, v in stage_ms.items()},
             "sketch_rate": {"value": achieved, "unit": roofline["unit"]},
-            "residual": {"col_id_fro": res, "normA_fro": nA, "opt_fro": opt, "ratio": res / opt if opt else None},
-            "cpqr_overlap": int(len(set(Js.cpu().tolist()) & set(Jc.cpu().tolist()))),
+            "residual": resid,
+            "cpqr_overlap": int(len(set(Js.cpu().tolist()) & set(Jc.cpu().tolist()))) if Jc is not None else None,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
