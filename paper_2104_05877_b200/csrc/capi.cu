@@ -31,6 +31,8 @@ sk_status finish_info(sk_ctx* c, const int64_t* status_dev, int64_t* info, const
   int64_t st = 0;
   SK_TRY(to_host(c, &st, status_dev, sizeof(int64_t)));
   *info = st;
+  if (st < 0)   // a bounded device-side wait gave up (multi-cluster LUPP exchange): a launch problem, not data
+    return fail(c, SK_E_STATE, std::string(what) + ": cross-cluster exchange timed out at step " + std::to_string(-st));
   if (st != 0)
     return fail(c, SK_E_RANK, std::string(what) + ": rank deficiency at step " + std::to_string(st));
   return SK_OK;

@@ -210,5 +210,12 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return r;
 }
 
+// Nanosecond wall clock (bounded spin waits).
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+
 }  // namespace dev
 }  // namespace skel

@@ -40,6 +40,7 @@ constexpr int PNT = 256;            // threads per panel CTA
 constexpr int PNW = PNT / 32;       // warps
 constexpr int MAXCS = 16;           // max cluster size
 constexpr int U12_BP = 64;          // max block width when there is a trailing update
+constexpr int kMaxG = 32;           // max clusters of one multi-cluster LUPP panel (one warp reduces them)
 
 struct Slot {            // a warp's pivot candidate, published to every CTA of the cluster
   unsigned long long key;  // bits(|v|) + 1 (0 = none): orders like |v|
@@ -58,6 +59,12 @@ struct PanelParams {
   const unsigned long long* maxbits;     // max |M| (bit pattern)
   int64_t* status;                       // 0 or 1-based failing step
   long long* tprobe;                     // experiments only (env SKEL_LUPP_PROBE): per-step clock64 marks
+  // several clusters (v2 kernel, G > 1, tall panels): the cluster winners of every step meet in
+  // global memory -- gbox [2][G][4 + NB] messages by step parity, gflag [G] = last published step + 1
+  int G;
+  double* gbox;
+  unsigned long long* gflag;
+  unsigned long long timeout_ns;
 };
 
 // W (n x k col-major) = the panel, rowstate = -1, maxbits = max |panel|.  Grid (n / 1024, k): no
@@ -683,13 +690,17 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
   const unsigned mbar0 = dev::smem_u32(mbar);
   const unsigned mbox_u = dev::smem_u32(mbox);
   __shared__ int s_stop;
+  __shared__ int s_late;
+  __shared__ __align__(16) double gall[kMaxG * (4 + NB)];   // G > 1: every cluster's winning message
+  const int g = (int)blockIdx.x / csize;             // cluster index (G > 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int bp = p.bp;
-  const int64_t r0 = (int64_t)crank * p.R;
+  const int64_t r0 = ((int64_t)g * csize + crank) * p.R;
   const int Rc = (int)std::max<int64_t>(0, std::min<int64_t>(p.R, p.n - r0));
 
   if (tid == 0) {
+    s_late = 0;
     s_stop = (*p.status != 0);
     mbar_init(mbar0, 1);
     mbar_init(mbar0 + 8, 1);
@@ -725,7 +736,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       const int s = cb + i;
       if (s >= s_end) break;
       const int t = p.c0 + s, par = s & 1;
-      const bool probe = p.tprobe != nullptr && crank == 0 && tid == 0;
+      const bool probe = p.tprobe != nullptr && g == 0 && crank == 0 && tid == 0;
       if (probe) p.tprobe[(int64_t)t * 16 + 0] = clock64();
       // (A) local candidate of column s, owner copies its row (block coordinates)
       unsigned long long ckey = 0ull, csec = 0ull;
@@ -828,9 +839,59 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       unsigned long long wkey, wsec;
       unsigned wlane;
       warp_argmax(gk, gk ? (unsigned)lane : 0xffffffffu, gs8, wkey, wlane, wsec, GAPS);
+      long long widx = __shfl_sync(0xffffffffu, gi8, (int)wlane);
+      const double* row = box + (size_t)wlane * MSGD + 4;
+      double lp = s > 0 ? box[(size_t)wlane * MSGD + 3] : 0.0;
+      if (p.G > 1) {
+        // (D') the G cluster winners meet in global memory: CTA 0 of each cluster publishes its
+        // cluster's winning message (release at gpu scope), every CTA waits for all G flags of this
+        // step and takes the same winner (max key, ties -> lowest cluster = lowest rows).  Double
+        // buffering by parity is safe for the same reason as the cluster mailbox: a cluster publishes
+        // step s+2 only after every cluster has published step s+1, i.e. finished reading step s.
+        double* gb = p.gbox + (size_t)par * p.G * MSGD;
+        const unsigned long long seq = (unsigned long long)t + 1ull;
+        if (crank == 0 && tid == 0) {     // one thread writes the message, then releases its flag
+          double* dst = gb + (size_t)g * MSGD;
+          dst[0] = __longlong_as_double((long long)wkey);
+          dst[1] = __longlong_as_double(widx);
+          dst[2] = __longlong_as_double((long long)wsec);
+          dst[3] = lp;
+          for (int j = (s & ~1); j < NB; j += 2)    // live columns, 16-byte stores
+            *reinterpret_cast<double2*>(dst + 4 + j) = *reinterpret_cast<const double2*>(row + j);
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.gflag + g), "l"(seq) : "memory");
+        }
+        if (tid < p.G) {
+          const unsigned long long t0 = dev::globaltimer_ns();
+          unsigned long long f;
+          do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(p.gflag + tid) : "memory");
+            if (f < seq && dev::globaltimer_ns() - t0 > p.timeout_ns) { s_late = 1; break; }
+          } while (f < seq);
+        }
+        asm volatile("bar.sync 4, %0;" ::"n"(PNT) : "memory");
+        if (s_late) {
+          if (tid == 0) atomicCAS(reinterpret_cast<unsigned long long*>(p.status), 0ull,
+                                  (unsigned long long)(-(long long)(t + 1)));
+          s_done = s;
+          stop = true;
+          break;
+        }
+        // all G messages in one round trip (16-byte loads, every one in flight), then the reduction
+        for (int j = tid; j < p.G * (MSGD / 2); j += PNT)
+          reinterpret_cast<double2*>(gall)[j] = __ldcg(reinterpret_cast<const double2*>(gb) + j);
+        asm volatile("bar.sync 5, %0;" ::"n"(PNT) : "memory");
+        const unsigned long long hk = lane < p.G ? (unsigned long long)__double_as_longlong(gall[lane * MSGD]) : 0ull;
+        const unsigned long long hs = lane < p.G ? (unsigned long long)__double_as_longlong(gall[lane * MSGD + 2]) : 0ull;
+        unsigned wg;
+        warp_argmax(hk, hk ? (unsigned)lane : 0xffffffffu, hs, wkey, wg, wsec, GAPS);
+        const double* gwin = gall + (size_t)wg * MSGD;
+        widx = __double_as_longlong(gwin[1]);
+        row = gwin + 4;
+        lp = s > 0 ? gwin[3] : 0.0;
+      }
       const double a1 = wkey ? __longlong_as_double((long long)(wkey - 1ull)) : -1.0;
       if (!(a1 > tol)) {
-        if (crank == 0 && tid == 0) {
+        if (g == 0 && crank == 0 && tid == 0) {
           *p.status = t + 1;
           for (int tt = t; tt < p.k; ++tt) p.Js[tt] = -1;
         }
@@ -838,10 +899,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
         stop = true;
         break;
       }
-      const long long widx = __shfl_sync(0xffffffffu, gi8, (int)wlane);
-      const double* row = box + (size_t)wlane * MSGD + 4;
       const double* uprev = ub + (size_t)(s > 0 ? s - 1 : 0) * NB;
-      const double lp = s > 0 ? box[(size_t)wlane * MSGD + 3] : 0.0;
       const double piv = row[s];
       const double u1 = s + 1 < bp ? (s > 0 ? fma(-lp, uprev[s + 1], row[s + 1]) : row[s + 1]) : 0.0;
       if (warp == PNW - 1) {   // U(s, :) for the bulk update of the next step, fix-ups and the output
@@ -883,7 +941,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       for (int q = 0; q < NB; ++q) v[r][q] = (q + 8 < NB) ? v[r][q + 8] : 0.0;
   }
   __syncthreads();
-  if (crank == 0) {
+  if (g == 0 && crank == 0) {
     for (int s = tid; s < s_done; s += PNT) {
       p.Js[p.c0 + s] = js[s];
       if (GAPS) p.gaps[p.c0 + s] = gp[s];
@@ -1044,8 +1102,52 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
                int64_t* status_dev) {
   const ClusterCfg cfg = pick_cluster(c);
   if (!cfg.ok) return fail(c, SK_E_CUDA, "no thread-block cluster configuration for the LUPP panel: " + cfg.why);
-  const int cs = cfg.cs;
-  const int64_t R = cdiv(n, cs);
+  int cs = cfg.cs;
+  int64_t R = cdiv(n, cs);
+  static const bool force_v1 = [] { const char* e = std::getenv("SKEL_LUPP_V1"); return e && e[0] == '1'; }();
+  static const bool one_cluster = [] { const char* e = std::getenv("SKEL_LUPP_ONE_CLUSTER"); return e && e[0] == '1'; }();
+  // Tall panels (more than 4 rows per thread in one cluster): G co-resident clusters of the
+  // register-resident v2 kernel, whose winners meet in global memory once per step, instead of
+  // one cluster streaming thousands of rows per CTA.  For k >= 512 the fewest rows per thread
+  // first (wider column blocks, fewer block transitions: C5 columns 10.5 vs 11.4 us/step), else the
+  // fewest clusters (cheaper per-step exchange: C4 rows 6.0 vs 7.0 us/step); then the larger cluster.
+  int G = 1;
+  if (cdiv(R, PNT) > 4 && !force_v1 && !one_cluster) {
+    bool found = false;
+    const int order_wide[3] = {1, 2, 4}, order_few[3] = {4, 2, 1};
+    const int* order = k >= 512 ? order_wide : order_few;
+    for (int oi = 0; oi < 3; ++oi) {
+      const int target = order[oi];
+      for (int ccs : {cfg.cs, cfg.cs / 2, cfg.cs / 4}) {
+        if (ccs < 2) continue;
+        const int gg = (int)cdiv(n, (int64_t)ccs * PNT * target);
+        if (gg < 2 || gg > kMaxG) continue;
+        PanelFn f = target == 1 ? k_lupp_panel_v2<1, 64, true> : target == 2 ? k_lupp_panel_v2<2, 32, true>
+                                                                             : k_lupp_panel_v2<4, 16, true>;
+        cudaLaunchConfig_t oc{};
+        oc.gridDim = dim3((unsigned)(ccs * gg));
+        oc.blockDim = dim3(PNT);
+        oc.dynamicSmemBytes = v2_smem_bytes<64>();
+        cudaLaunchAttribute oa[1];
+        oa[0].id = cudaLaunchAttributeClusterDimension;
+        oa[0].val.clusterDim.x = ccs; oa[0].val.clusterDim.y = 1; oa[0].val.clusterDim.z = 1;
+        oc.attrs = oa; oc.numAttrs = 1;
+        int active = 0;
+        if (cudaOccupancyMaxActiveClusters(&active, f, &oc) != cudaSuccess) { cudaGetLastError(); active = 0; }
+        static const bool dbg = [] { const char* e = std::getenv("SKEL_LUPP_DEBUG"); return e && e[0] == '1'; }();
+        if (dbg) std::fprintf(stderr, "[lupp] n=%lld target rpt %d cluster %d: need %d clusters, %d active\n",
+                              (long long)n, target, ccs, gg, active);
+        if (gg <= active) {
+          G = gg;
+          cs = ccs;
+          R = cdiv(n, (int64_t)cs * G);
+          found = true;
+          break;
+        }
+      }
+      if (found) break;
+    }
+  }
   if (R > 16 * PNT) return fail(c, SK_E_ARG, "LUPP panel too tall for one cluster (n too large)");
   // register-resident kernel when a thread's rows x block fit 64 doubles, else the
   // shared-memory kernel with the widest block whose rows fit the cluster's shared memory
@@ -1053,7 +1155,6 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   int64_t bp = 0;
   size_t smem_bytes = 0;
   const int rpt = (int)cdiv(R, PNT);
-  static const bool force_v1 = [] { const char* e = std::getenv("SKEL_LUPP_V1"); return e && e[0] == '1'; }();
   if (rpt <= 4 && !force_v1) {
     const int nb = rpt == 1 ? 64 : rpt == 2 ? 32 : 16;
     bp = std::min<int64_t>(k, nb);
@@ -1082,6 +1183,13 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   if (want_probe) {
     SK_TRY(probeb.alloc(c, (size_t)k * 16 * sizeof(long long)));
     SK_CUDA(c, cudaMemsetAsync(probeb.p, 0, (size_t)k * 16 * sizeof(long long), c->stream));
+  }
+  DBuf gxb;
+  const size_t gbox_doubles = (size_t)2 * G * (4 + 64);
+  if (G > 1) {
+    SK_TRY(gxb.alloc(c, gbox_doubles * sizeof(double) + (size_t)G * sizeof(unsigned long long)));
+    SK_CUDA(c, cudaMemsetAsync(gxb.p, 0, gbox_doubles * sizeof(double) + (size_t)G * sizeof(unsigned long long),
+                               c->stream));
   }
   SK_TRY(Wb.alloc(c, (size_t)n * k * sizeof(double)));
   SK_TRY(Ub.alloc(c, (size_t)k * k * sizeof(double)));
@@ -1114,8 +1222,12 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     pp.Js = Js; pp.Lf = Lf; pp.ldlf = ldlf; pp.Uw = Ub.as<double>(); pp.gaps = gaps;
     pp.maxbits = maxb.as<unsigned long long>(); pp.status = status_dev;
     pp.tprobe = want_probe ? probeb.as<long long>() : nullptr;
+    pp.G = G;
+    pp.gbox = G > 1 ? gxb.as<double>() : nullptr;
+    pp.gflag = G > 1 ? reinterpret_cast<unsigned long long*>(gxb.as<double>() + gbox_doubles) : nullptr;
+    pp.timeout_ns = 10ull * 1000 * 1000 * 1000;      // a cluster that never publishes: SK_E_STATE, not a hang
     cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(cs);
+    lc.gridDim = dim3((unsigned)(cs * G));
     lc.blockDim = dim3(PNT);
     lc.dynamicSmemBytes = smem_bytes;
     lc.stream = c->stream;

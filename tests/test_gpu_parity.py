@@ -173,6 +173,9 @@ def test_sketch_sparse_parity(m, n, l, zeta, seed):
     (3000, 140, 130, 3),         # several panels + trailing GEMM
     (777, 70, 70, 4),            # k = l, ragged n
     (70, 70, 70, 5),             # k = n (square)
+    (40001, 80, 70, 6),          # tall: several clusters exchanging winners in global memory, ragged
+    (70000, 40, 36, 7),          # taller than one cluster can hold (> 65536 rows)
+    (131000, 30, 24, 8),         # C5 row-LUPP height class (32 clusters of 4), ragged
 ])
 def test_select_cols_parity(n, l, k, seed):
     rng = np.random.default_rng(seed)
