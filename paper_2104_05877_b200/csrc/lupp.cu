@@ -1112,7 +1112,8 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   // first (wider column blocks, fewer block transitions: C5 columns 10.5 vs 11.4 us/step), else the
   // fewest clusters (cheaper per-step exchange: C4 rows 6.0 vs 7.0 us/step); then the larger cluster.
   int G = 1;
-  if (cdiv(R, PNT) > 4 && !force_v1 && !one_cluster) {
+  static const int multi_above = [] { const char* e = std::getenv("SKEL_LUPP_MULTI_ABOVE_RPT"); return e ? std::atoi(e) : 4; }();
+  if (cdiv(R, PNT) > multi_above && !force_v1 && !one_cluster) {
     bool found = false;
     const int order_wide[3] = {1, 2, 4}, order_few[3] = {4, 2, 1};
     const int* order = k >= 512 ? order_wide : order_few;
