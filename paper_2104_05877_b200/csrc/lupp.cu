@@ -667,7 +667,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_reg(PanelParams p) {
 //       U(s, c) = row(c) - row(s-1) * U(s-1, c);
 //   (E) multipliers and column s+1 of the own rows (the next step's search column).
 // One CTA barrier and one cluster exchange per pivot; no remote loads.
-template <int RPT, int NB, bool GAPS>
+template <int RPT, int NB, bool GAPS, bool MULTI>
 __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
   dev::griddep_wait();
   static_assert(NB % 8 == 0 && RPT * NB <= 64, "register window");
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
   const unsigned mbox_u = dev::smem_u32(mbox);
   __shared__ int s_stop;
   __shared__ int s_late;
-  __shared__ __align__(16) double gall[kMaxG * (4 + NB)];   // G > 1: every cluster's winning message
+  __shared__ __align__(16) double gall[MULTI ? kMaxG * (4 + NB) : 2];   // G > 1: every cluster's winning message
   const int g = (int)blockIdx.x / csize;             // cluster index (G > 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       long long widx = __shfl_sync(0xffffffffu, gi8, (int)wlane);
       const double* row = box + (size_t)wlane * MSGD + 4;
       double lp = s > 0 ? box[(size_t)wlane * MSGD + 3] : 0.0;
-      if (p.G > 1) {
+      if (MULTI && p.G > 1) {
         // (D') the G cluster winners meet in global memory: CTA 0 of each cluster publishes its
         // cluster's winning message (release at gpu scope), every CTA waits for all G flags of this
         // step and takes the same winner (max key, ties -> lowest cluster = lowest rows).  Double
@@ -1053,8 +1053,12 @@ ClusterCfg pick_cluster(sk_ctx* c) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.max_dyn);
   }
-  for (PanelFn fn : {k_lupp_panel_v2<1, 64, true>, k_lupp_panel_v2<1, 64, false>, k_lupp_panel_v2<2, 32, true>,
-                     k_lupp_panel_v2<2, 32, false>, k_lupp_panel_v2<4, 16, true>, k_lupp_panel_v2<4, 16, false>}) {
+  for (PanelFn fn : {k_lupp_panel_v2<1, 64, true, false>, k_lupp_panel_v2<1, 64, false, false>,
+                     k_lupp_panel_v2<2, 32, true, false>, k_lupp_panel_v2<2, 32, false, false>,
+                     k_lupp_panel_v2<4, 16, true, false>, k_lupp_panel_v2<4, 16, false, false>,
+                     k_lupp_panel_v2<1, 64, true, true>, k_lupp_panel_v2<1, 64, false, true>,
+                     k_lupp_panel_v2<2, 32, true, true>, k_lupp_panel_v2<2, 32, false, true>,
+                     k_lupp_panel_v2<4, 16, true, true>, k_lupp_panel_v2<4, 16, false, true>}) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem_bytes<64>());
   }
@@ -1123,8 +1127,8 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
         if (ccs < 2) continue;
         const int gg = (int)cdiv(n, (int64_t)ccs * PNT * target);
         if (gg < 2 || gg > kMaxG) continue;
-        PanelFn f = target == 1 ? k_lupp_panel_v2<1, 64, true> : target == 2 ? k_lupp_panel_v2<2, 32, true>
-                                                                             : k_lupp_panel_v2<4, 16, true>;
+        PanelFn f = target == 1 ? k_lupp_panel_v2<1, 64, true, true> : target == 2 ? k_lupp_panel_v2<2, 32, true, true>
+                                                                                   : k_lupp_panel_v2<4, 16, true, true>;
         cudaLaunchConfig_t oc{};
         oc.gridDim = dim3((unsigned)(ccs * gg));
         oc.blockDim = dim3(PNT);
@@ -1159,9 +1163,20 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   if (rpt <= 4 && !force_v1) {
     const int nb = rpt == 1 ? 64 : rpt == 2 ? 32 : 16;
     bp = std::min<int64_t>(k, nb);
-    if (rpt == 1) { fn = gaps ? k_lupp_panel_v2<1, 64, true> : k_lupp_panel_v2<1, 64, false>; smem_bytes = v2_smem_bytes<64>(); }
-    else if (rpt == 2) { fn = gaps ? k_lupp_panel_v2<2, 32, true> : k_lupp_panel_v2<2, 32, false>; smem_bytes = v2_smem_bytes<32>(); }
-    else { fn = gaps ? k_lupp_panel_v2<4, 16, true> : k_lupp_panel_v2<4, 16, false>; smem_bytes = v2_smem_bytes<16>(); }
+    const bool multi = G > 1;      // the cross-cluster exchange is compiled only into the G > 1 variants
+    if (rpt == 1) {
+      fn = multi ? (gaps ? k_lupp_panel_v2<1, 64, true, true> : k_lupp_panel_v2<1, 64, false, true>)
+                 : (gaps ? k_lupp_panel_v2<1, 64, true, false> : k_lupp_panel_v2<1, 64, false, false>);
+      smem_bytes = v2_smem_bytes<64>();
+    } else if (rpt == 2) {
+      fn = multi ? (gaps ? k_lupp_panel_v2<2, 32, true, true> : k_lupp_panel_v2<2, 32, false, true>)
+                 : (gaps ? k_lupp_panel_v2<2, 32, true, false> : k_lupp_panel_v2<2, 32, false, false>);
+      smem_bytes = v2_smem_bytes<32>();
+    } else {
+      fn = multi ? (gaps ? k_lupp_panel_v2<4, 16, true, true> : k_lupp_panel_v2<4, 16, false, true>)
+                 : (gaps ? k_lupp_panel_v2<4, 16, true, false> : k_lupp_panel_v2<4, 16, false, false>);
+      smem_bytes = v2_smem_bytes<16>();
+    }
   } else if (rpt <= 4) {
     const int nb = rpt == 1 ? 64 : rpt == 2 ? 32 : 16;
     const int rv = rpt == 1 ? 1 : rpt == 2 ? 2 : 4;
