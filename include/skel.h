@@ -143,7 +143,12 @@ sk_status sk_sketch_power(sk_ctx* ctx, const double* A, int64_t m, int64_t n, in
  *   info  NULL or host int64: 0, or the 1-based step of a rank failure (R7).
  *         Non-NULL info synchronises the stream and makes a rank failure
  *         return SK_E_RANK; with NULL the call is asynchronous and a rank
- *         failure leaves Js[t..k-1] = -1. */
+ *         failure leaves Js[t..k-1] = -1.
+ * Panel height: up to 16384 rows run in one 16-CTA cluster; taller panels run in several
+ * co-resident clusters exchanging each step's winner through global memory (on a B200 up to
+ * 32 clusters of 4 CTAs, i.e. 131072 rows at 4 rows per thread; beyond that the one-cluster
+ * shared-memory kernel, up to 65536 rows, else SK_E_ARG).  The bounded cross-cluster wait
+ * reports SK_E_STATE (info = -step) instead of hanging if the clusters are not co-resident. */
 sk_status sk_select_cols(sk_ctx* ctx, const double* X, int64_t l, int64_t n, int64_t ldx,
                          int64_t k, int64_t* Js, double* Lf, int64_t ldlf, double* U,
                          int64_t ldu, double* gaps, int64_t* info);
