@@ -203,6 +203,21 @@ def test_select_cols_kahan_all_ties():
     assert eta >= 2.0 ** (l - 1)
 
 
+@pytest.mark.parametrize("n", [40001, 70000, 131000])
+def test_select_cols_tall_all_ties_across_clusters(n):
+    """Lemma 2's all-ties witness spread over a panel tall enough to run in several clusters:
+    every step is an exact tie between rows in different clusters, so the lowest global index
+    must win each cross-cluster exchange (R6); gaps are exactly 0."""
+    l = 12
+    W = kahan_witness(l, l + 9)
+    pos = np.sort(np.random.default_rng(n).choice(n, size=l + 9, replace=False))
+    X = np.zeros((l, n))
+    X[:, pos] = W
+    Js, _, _, gaps = sk.select_cols(dev_rowmajor(X), l, want_gaps=True)
+    assert Js.cpu().tolist() == pos[:l].tolist()
+    assert not gaps.cpu().numpy().any()
+
+
 def test_select_cols_ties_lowest_original_index():
     X = np.array([[1.0, 1.0, 3.0], [5.0, -5.0, 0.0]])
     Js, _, _, _ = sk.select_cols(dev_rowmajor(X), 2)
