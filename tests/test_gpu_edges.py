@@ -68,6 +68,22 @@ def test_select_cols_all_zero_is_rank_failure_at_step_1():
     assert e.value.status == 2 and e.value.info == 1
 
 
+@pytest.mark.parametrize("n", [70000, 131000])
+def test_select_cols_tall_rank_failure_across_clusters(n):
+    # two nonzero sketch columns in different clusters of a multi-cluster panel: steps 1-2 pick
+    # them (the larger first), step 3 finds no pivot in any cluster -> SK_E_RANK, info 3, and the
+    # asynchronous form leaves Js[2:] = -1
+    X = np.zeros((4, n))
+    X[:, 7] = [1.0, 2.0, 3.0, 4.0]
+    X[:, n - 5] = [-2.0, 1.0, 0.5, 0.25]
+    Xd = torch.from_numpy(X).to(DEV)
+    with pytest.raises(sk.SkelError) as e:
+        sk.select_cols(Xd, 4)
+    assert e.value.status == 2 and e.value.info == 3
+    Js, _, _, _ = sk.select_cols(Xd, 4, check=False)
+    assert Js.cpu().tolist() == [n - 5, 7, -1, -1]
+
+
 def test_select_cols_exact_ties_everywhere():
     # every entry of the first row equal: the lowest index wins each tie (R6)
     X = np.ones((2, 64))
