@@ -194,7 +194,7 @@ sk_status sk_lupp_dist_info(sk_ctx* ctx, const void* state, int64_t* info);
  * mailbox's device-side epoch by k + 2 (so flags of earlier selections never satisfy a wait and a
  * captured graph of the whole selection can be replayed).  The kernel of step t waits until every
  * flag of its own mailbox reaches epoch + t, reads the records of step t-1 there, eliminates,
- * and publishes its step-t record by storing it into slot [t & 1][rank] of every mailbox followed
+ * and publishes its step-t record by storing it into slot [(epoch + t) & 1][rank] of every mailbox followed
  * by a system-scope fence and flag release (epoch + t + 1).  Every rank must run the same sequence
  * of selections on its mailbox.  Same results as sk_lupp_dist_begin/step; no host call or
  * collective between steps.  The wait is bounded: if a peer's flag does not arrive within

@@ -23,9 +23,15 @@ at step t, Lf[p_t, t] = 1 and Lf[p_t, t'] = 0 for t' > t; U (k x k) upper with
 U[t, t:] the pivot row at step t; gaps[t] = (a1 - a2) / a1 for the two largest
 candidate magnitudes at step t.
 """
+import ctypes
+import os
+import subprocess
+
 import numpy as np
 
 RANK_TOL = 1e-14
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_CLIB = None
 
 
 class RankError(Exception):
@@ -75,17 +81,68 @@ def lupp_panel(M, k, forced=None):
     return piv, Lf, U, gaps
 
 
-def select_cols(X, k, forced=None):
-    """J_s by column-wise LUPP on the sketch X (l x n), Algorithm 2 line 3."""
+def build_c(force=False):
+    """Compile oracle/c/lupp.c (plain C + OpenMP, -ffp-contract=off) to oracle/c/liboracle_lupp.so."""
+    src = os.path.join(_HERE, "c", "lupp.c")
+    so = os.path.join(_HERE, "c", "liboracle_lupp.so")
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        subprocess.run(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared", src, "-o", so + ".tmp"],
+                       check=True)
+        os.replace(so + ".tmp", so)
+    return so
+
+
+def _clib():
+    global _CLIB
+    if _CLIB is None:
+        lib = ctypes.CDLL(build_c())
+        lib.or_lupp_panel.restype = ctypes.c_int64
+        P = ctypes.c_void_p
+        lib.or_lupp_panel.argtypes = [P, ctypes.c_int64, ctypes.c_int64, P, P, P, P, P, P]
+        _CLIB = lib
+    return _CLIB
+
+
+def lupp_panel_c(M, k, forced=None):
+    """lupp_panel in plain C (oracle/c/lupp.c): the same steps and the same rounding, for panels
+    too large for the numpy loop (tests/test_oracle_path.py checks the two agree bit for bit)."""
+    n = M.shape[0]
+    if k > M.shape[1] or k > n:
+        raise ValueError("LUPP needs k <= min(n, panel width)")
+    W = np.ascontiguousarray(np.asarray(M, dtype=np.float64)[:, :k]).copy()
+    piv = np.zeros(k, dtype=np.int64)
+    Lf = np.zeros((n, k))
+    U = np.zeros((k, k))
+    gaps = np.zeros(k)
+    act = np.zeros(n, dtype=np.uint8)
+    fz = None
+    if forced:
+        fz = np.full(k, -1, dtype=np.int64)
+        for t, p in forced.items():
+            fz[t] = p
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p) if a is not None else None  # noqa: E731
+    st = _clib().or_lupp_panel(ptr(W), n, k, ptr(fz), ptr(piv), ptr(Lf), ptr(U), ptr(gaps), ptr(act))
+    if st:
+        raise RankError(int(st))
+    return piv, Lf, U, gaps
+
+
+def _panel(M, k, forced, fast):
+    return lupp_panel_c(M, k, forced) if fast else lupp_panel(M, k, forced)
+
+
+def select_cols(X, k, forced=None, fast=False):
+    """J_s by column-wise LUPP on the sketch X (l x n), Algorithm 2 line 3.
+    fast=True runs the same algorithm in plain C (lupp_panel_c)."""
     X = np.asarray(X, dtype=np.float64)
     if k > X.shape[0]:
         raise ValueError("k <= l required")
-    return lupp_panel(X[:k, :].T, k, forced)
+    return _panel(X[:k, :].T, k, forced, fast)
 
 
-def select_rows(C, k, forced=None):
+def select_rows(C, k, forced=None, fast=False):
     """I_s by row-wise LUPP on C = A(:, J_s) (m x k), Algorithm 2 line 4."""
-    return lupp_panel(np.asarray(C, dtype=np.float64), k, forced)
+    return _panel(np.asarray(C, dtype=np.float64), k, forced, fast)
 
 
 def growth(Lf, piv):

@@ -47,3 +47,25 @@ def optimal_error(sigma, k):
     """||A - A_k||_F = sqrt(sum_{i>k} sigma_i^2) (Eckart-Young, P:204)."""
     s = np.sort(np.asarray(sigma, dtype=np.float64))[::-1]
     return float(np.sqrt(np.sum(s[k:] ** 2)))
+
+
+def residual_col_id_streamed(get_cols, m, n, Js, block=4096):
+    """(||A - Q_C Q_C^T A||_F, ||A||_F) of the column ID (eq:def_column_id) for an A taken
+    in column blocks from get_cols(j0, j1): C = A(:, J_s) is gathered first, Q_C = ortho(C) (the one
+    library step), then for every column block the residual block A_b - Q_C (Q_C^T A_b) is formed
+    explicitly and squared.  ||E||_F^2 is the sum over columns, so the result is the definition's
+    (BASELINE C5, which does not fit in host memory at once)."""
+    Js = np.asarray(Js, dtype=np.int64)
+    C = np.empty((m, Js.size))
+    for t, j in enumerate(Js):
+        C[:, t] = np.asarray(get_cols(int(j), int(j) + 1), dtype=np.float64)[:, 0]
+    Qc = ortho(C)
+    del C
+    r2 = a2 = 0.0
+    for j0 in range(0, n, block):
+        j1 = min(n, j0 + block)
+        Ab = np.asarray(get_cols(j0, j1), dtype=np.float64)
+        E = Ab - Qc @ (Qc.T @ Ab)
+        r2 += float(np.sum(E * E))
+        a2 += float(np.sum(Ab * Ab))
+    return float(np.sqrt(r2)), float(np.sqrt(a2))

@@ -62,3 +62,16 @@ def sketch_cols(A, l, kind="gaussian", seed=0, zeta=8):
     A = np.asarray(A, dtype=np.float64)
     Om = omega.embedding(kind, seed, l, A.shape[1], zeta)
     return A @ Om.T
+
+
+def sketch_streamed(get_cols, m, n, l, kind="gaussian", seed=0, zeta=8, block=4096):
+    """X = Gamma A for an A too large to hold at once (BASELINE C5, 68.7 GB): X = Gamma A is
+    column-separable, X(:, J) = Gamma A(:, J), so A is taken in column blocks from
+    get_cols(j0, j1) (an m x (j1 - j0) array) and each block is multiplied by the same explicit
+    Gamma (oracle.omega).  The value is the definition's; only the column order of the work differs."""
+    G = omega.embedding(kind, seed, l, m, zeta)
+    X = np.empty((l, n))
+    for j0 in range(0, n, block):
+        j1 = min(n, j0 + block)
+        X[:, j0:j1] = G @ np.asarray(get_cols(j0, j1), dtype=np.float64)
+    return X

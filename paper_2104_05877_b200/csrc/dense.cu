@@ -31,12 +31,14 @@ __global__ void k_gather_cols(const double* A, int64_t m, int64_t lda, const int
 }
 
 // Rt(:, t) = A(I[t], :)^T  (row gather; reads are strided by lda, writes coalesced)
-__global__ void k_gather_rows_t(const double* A, int64_t n, int64_t lda, const int64_t* I, int64_t k,
+// Rt(:, t) = A(I[t], :)^T; a row index outside [0, m) gives a zero column (no out-of-bounds read).
+__global__ void k_gather_rows_t(const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* I, int64_t k,
                                 double* Rt, int64_t ldrt) {
   const int64_t t = blockIdx.y;
   const int64_t i = I[t];
+  const bool ok = i >= 0 && i < m;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    Rt[j + t * ldrt] = A[i + j * lda];
+    Rt[j + t * ldrt] = ok ? A[i + j * lda] : 0.0;
 }
 
 
@@ -376,11 +378,11 @@ sk_status gather_cols_shard(sk_ctx* c, const double* A, int64_t m, int64_t lda, 
   return launched(c);
 }
 
-sk_status gather_rows_t(sk_ctx* c, const double* A, int64_t n, int64_t lda, const int64_t* I, int64_t k,
+sk_status gather_rows_t(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* I, int64_t k,
                         double* Rt, int64_t ldrt) {
   if (k == 0 || n == 0) return SK_OK;
   const int bx = (int)std::min<int64_t>(cdiv(n, 256), 64);
-  k_gather_rows_t<<<dim3(bx, (unsigned)k), 256, 0, c->stream>>>(A, n, lda, I, k, Rt, ldrt);
+  k_gather_rows_t<<<dim3(bx, (unsigned)k), 256, 0, c->stream>>>(A, m, n, lda, I, k, Rt, ldrt);
   return launched(c);
 }
 

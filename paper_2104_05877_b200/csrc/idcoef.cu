@@ -17,12 +17,14 @@
 namespace skel {
 namespace {
 
-__global__ void k_gather_rows(const double* In, int64_t ldin, const int64_t* I, int64_t k, int64_t ncols,
-                              double* Out, int64_t ldout) {
+// Out(t, c) = In(I[t], c); an index outside [0, nrows) (e.g. the -1 of a rank failure) gives 0.
+__global__ void k_gather_rows(const double* In, int64_t ldin, int64_t nrows, const int64_t* I, int64_t k,
+                              int64_t ncols, double* Out, int64_t ldout) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k * ncols;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e % k, c = e / k;
-    Out[t + c * ldout] = In[I[t] + c * ldin];
+    const int64_t i = I[t];
+    Out[t + c * ldout] = (i >= 0 && i < nrows) ? In[i + c * ldin] : 0.0;
   }
 }
 
@@ -51,12 +53,16 @@ __global__ void k_transpose(const double* Y, int64_t n, int64_t k, double* Z, in
 }
 
 // Z(:, Js[t]) = e_t exactly; Y(Js[t], :) = 0 (so that Y^T Y = T T^T).
+// Z(:, Js) = I_k and the skeleton rows of Y zeroed; indices outside [0, n) are skipped (no
+// out-of-bounds store for the Js = -1 left by a rank failure).
 __global__ void k_identity_block(const int64_t* Js, int64_t k, double* Z, int64_t ldz, double* Y, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k * k;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t tp = e % k, t = e / k;
-    Z[tp + Js[t] * ldz] = (tp == t) ? 1.0 : 0.0;
-    Y[Js[t] + tp * n] = 0.0;
+    const int64_t j = Js[t];
+    if (j < 0 || j >= n) continue;
+    Z[tp + j * ldz] = (tp == t) ? 1.0 : 0.0;
+    Y[j + tp * n] = 0.0;
   }
 }
 
@@ -71,7 +77,7 @@ sk_status id_coeffs(sk_ctx* c, const double* Lf, int64_t n, int64_t k, int64_t l
   SK_TRY(Y.alloc(c, (size_t)n * k * sizeof(double)));
   const int blocks = (int)std::min<int64_t>(cdiv(n * k, 256), 8LL * c->num_sms);
   k_gather_rows<<<(unsigned)std::min<int64_t>(cdiv(k * k, 256), 4LL * c->num_sms), 256, 0, c->stream>>>(
-      Lf, ldlf, Js, k, k, L1.as<double>(), k);
+      Lf, ldlf, n, Js, k, k, L1.as<double>(), k);
   SK_TRY(launched(c));
   k_copy_cols<<<blocks, 256, 0, c->stream>>>(Lf, ldlf, n, k, Y.as<double>(), n);
   SK_TRY(launched(c));

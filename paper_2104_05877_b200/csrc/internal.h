@@ -86,8 +86,8 @@ sk_status transpose(sk_ctx* c, const double* In, int64_t rows, int64_t cols, int
 // Shard-aware gather: C(:, t) = A(:, J[t] - col0) if the column is in [col0, col0 + ncols), else 0.
 sk_status gather_cols_shard(sk_ctx* c, const double* A, int64_t m, int64_t lda, int64_t col0, int64_t ncols,
                             const int64_t* J, int64_t k, double* C, int64_t ldc);
-// R^T (n x k, col-major ld n) = A(I, :)^T
-sk_status gather_rows_t(sk_ctx* c, const double* A, int64_t n, int64_t lda, const int64_t* I,
+// R^T (n x k, col-major ld n) = A(I, :)^T, A m x n; indices outside [0, m) give zero columns
+sk_status gather_rows_t(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const int64_t* I,
                         int64_t k, double* Rt, int64_t ldrt);
 // In-place blocked Cholesky of the SPD k x k matrix G (lower, col-major ld); status_dev = 0 or
 // 1-based failing column.

@@ -58,7 +58,6 @@ struct PanelParams {
   double* gaps;
   const unsigned long long* maxbits;     // max |M| (bit pattern)
   int64_t* status;                       // 0 or 1-based failing step
-  long long* tprobe;                     // experiments only (env SKEL_LUPP_PROBE): per-step clock64 marks
   // several clusters (v2 kernel, G > 1, tall panels): the cluster winners of every step meet in
   // global memory -- gbox [2][G][4 + NB] messages by step parity, gflag [G] = last published step + 1
   int G;
@@ -396,262 +395,6 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel(PanelParams p) {
   cluster.sync();   // no CTA leaves while a peer may still read its shared memory
 }
 
-// Register-resident variant of k_lupp_panel: each thread keeps its RPT rows of the block
-// (NB columns, RPT*NB = 64 doubles) in registers, so the bulk Schur update is pure DFMA
-// with no shared-memory traffic.  The step loop is unrolled in chunks of 8 pivots so every
-// register index is static; after a chunk the register window slides left by 8 columns.
-// The shared-memory "mirror" P keeps, per row, the multipliers L(i, s) (written every step)
-// and a snapshot of the remaining columns taken once per chunk (just before the candidate
-// of the chunk's first step is published).  A CTA reconstructs the winning row from the
-// owner's mirror and the U rows of the current chunk (k_ring):
-//     U(s, j) = mirror(p, j) - sum_{s' = cb-1}^{s-1} L(p, s') U(s', j)      (j >= s)
-// so no per-step row copy is needed on the publishing side.
-constexpr int KRING = 64;   // U rows of the block (bp <= 64 for the register kernel)
-
-__host__ __device__ inline size_t reg_smem_bytes(int R, int bp, int nb, int stride) {
-  size_t o = (((size_t)R * stride + 1) & ~(size_t)1) * sizeof(double);   // mirror
-  o += (size_t)KRING * ((bp + nb + 3) & ~1) * sizeof(double);   // U-row ring (+ zero tail), as in the kernel
-  o += (size_t)(bp + 2) * sizeof(double);                 // fetched raw row
-  o = (o + 15) & ~(size_t)15;
-  o += (size_t)2 * MAXCS * PNW * sizeof(Slot);
-  o += (size_t)bp * sizeof(long long) + (size_t)bp * sizeof(double);
-  o += (size_t)R * sizeof(int);                           // row states
-  o = (o + 15) & ~(size_t)15;
-  return o + 2 * sizeof(unsigned long long) + 64;
-}
-
-template <bool GAPS, int RPT, int NB>
-__global__ void __launch_bounds__(PNT, 1) k_lupp_panel_reg(PanelParams p) {
-  dev::griddep_wait();
-  static_assert(NB % 8 == 0 && NB >= 16, "chunked window");
-  cg::cluster_group cluster = cg::this_cluster();
-  const int crank = (int)cluster.block_rank();
-  const int csize = (int)cluster.num_blocks();
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int bp = p.bp;
-  const int ps = ((bp + 1) | 1);                              // odd stride: per-row lane access
-  const int urs = (bp + NB + 3) & ~1;                         // ring row stride (even)
-  double* P = reinterpret_cast<double*>(smraw);               // mirror [R][ps]
-  double* ring = P + (((size_t)p.R * ps + 1) & ~(size_t)1);    // [KRING][urs], 16-byte aligned
-  double* xraw = ring + (size_t)KRING * urs;                  // [bp + 2]
-  unsigned char* q8 = reinterpret_cast<unsigned char*>(xraw + bp + 2);
-  q8 = reinterpret_cast<unsigned char*>(((uintptr_t)q8 + 15) & ~(uintptr_t)15);
-  Slot* slots = reinterpret_cast<Slot*>(q8);                  // [2][MAXCS*PNW]
-  long long* js = reinterpret_cast<long long*>(slots + 2 * MAXCS * PNW);   // [bp]
-  double* gp = reinterpret_cast<double*>(js + bp);                        // [bp]
-  int* state = reinterpret_cast<int*>(gp + bp);                           // [R]
-  unsigned char* mb = reinterpret_cast<unsigned char*>(state + p.R);
-  mb = reinterpret_cast<unsigned char*>(((uintptr_t)mb + 15) & ~(uintptr_t)15);
-  const unsigned mbar0 = dev::smem_u32(mb);
-  const unsigned slots_u32 = dev::smem_u32(slots);
-  const unsigned P_u32 = dev::smem_u32(P);
-  __shared__ int s_stop;
-
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int warp = tid >> 5;
-  const int64_t r0 = (int64_t)crank * p.R;
-  const int Rc = (int)std::max<int64_t>(0, std::min<int64_t>(p.R, p.n - r0));
-  const int nslots = csize * PNW;
-
-  if (tid == 0) {
-    s_stop = (*p.status != 0);
-    mbar_init(mbar0, 1);
-    mbar_init(mbar0 + 8, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int e = tid; e < KRING * urs; e += PNT) ring[e] = 0.0;   // zero tails stay zero
-  for (int e = tid; e < Rc * bp; e += PNT) {
-    const int li = e % Rc, s = e / Rc;
-    dev::cp_async8(P + (size_t)li * ps + s, p.W + (r0 + li) + (int64_t)(p.c0 + s) * p.n, true);
-  }
-  dev::cp_async_commit();
-  const double tol = 1e-14 * __longlong_as_double((long long)*p.maxbits);
-  dev::cp_async_wait<0>();
-  __syncthreads();
-  (void)state;
-  double v[RPT][NB];
-  int st[RPT];
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int li = tid + PNT * r;
-    st[r] = li < Rc ? p.rowstate[r0 + li] : -2;
-#pragma unroll
-    for (int q = 0; q < NB; ++q) v[r][q] = (li < Rc && q < bp) ? P[(size_t)li * ps + q] : 0.0;
-  }
-  cluster.sync();
-  const int s_end = s_stop ? 0 : bp;
-
-  auto publish = [&](int sn, unsigned long long ckey, long long cidx, unsigned long long csec) {
-    const int par = sn & 1;
-    if (tid == 0) mbar_arm(mbar0 + 8 * par, (unsigned)(nslots * sizeof(Slot)));
-    unsigned long long wk, ws;
-    unsigned wi;
-    warp_argmax(ckey, (unsigned)cidx, csec, wk, wi, ws, GAPS);
-    __syncwarp();   // mirror writes of the lanes precede the release of the st.async below
-    if (lane < csize) {
-      const unsigned off = (unsigned)((par * (MAXCS * PNW) + crank * PNW + warp) * sizeof(Slot));
-      const unsigned ra = mapa(slots_u32 + off, (unsigned)lane);
-      const unsigned rb = mapa(mbar0 + 8 * par, (unsigned)lane);
-      const long long gi = wk ? (long long)(r0 + wi) : 0x7fffffffffffffffLL;
-      st_async_v2(ra, wk, (unsigned long long)gi, rb);
-      st_async_v2(ra + 16, ws, 0ull, rb);
-    }
-  };
-
-  if (s_end > 0) {
-    unsigned long long ckey = 0ull, csec = 0ull;
-    long long cidx = 0x7fffffffffffffffLL;
-#pragma unroll
-    for (int r = 0; r < RPT; ++r)
-      if (st[r] == -1) cand_push(mag_key(v[r][0]), tid + PNT * r, ckey, cidx, csec);
-    publish(0, ckey, cidx, csec);
-  }
-  int s_done = s_end;
-  bool stop = false;
-  for (int cb = 0; cb < s_end && !stop; cb += 8) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int s = cb + i;
-      if (s >= s_end) break;
-      const int t = p.c0 + s, par = s & 1;
-      // (A) mailbox -> winner
-      mbar_wait(mbar0 + 8 * par, (unsigned)((s >> 1) & 1));
-      unsigned long long bk = 0ull, bs = 0ull;
-      long long bi = 0x7fffffffffffffffLL;
-      for (int e = lane; e < nslots; e += 32) {
-        const Slot sl = slots[par * (MAXCS * PNW) + e];
-        if (sl.key) cand_push(sl.key, sl.idx, bk, bi, bs);
-        if (GAPS) bs = sl.sec > bs ? sl.sec : bs;
-      }
-      unsigned long long wk, ws;
-      unsigned wi;
-      warp_argmax(bk, bk ? (unsigned)bi : 0xffffffffu, bs, wk, wi, ws, GAPS);
-      const double a1 = wk ? __longlong_as_double((long long)(wk - 1ull)) : -1.0;
-      if (!(a1 > tol)) {
-        if (crank == 0 && tid == 0) {
-          *p.status = t + 1;
-          for (int tt = t; tt < p.k; ++tt) p.Js[tt] = -1;
-        }
-        s_done = s;
-        stop = true;
-        break;
-      }
-      const long long widx = (long long)wi;
-      // (F) the winning row: the owner's mirror (remote) corrected by this chunk's pivots
-      const int s0 = cb > 0 ? cb - 1 : 0;          // first step whose update the mirror lacks
-      {
-        const int wr = (int)(widx / p.R);
-        const int wl = (int)(widx - (int64_t)wr * p.R);
-        const unsigned src = mapa(P_u32 + (unsigned)((size_t)wl * ps * sizeof(double)), (unsigned)wr);
-        for (int j = s0 + tid; j < bp; j += PNT) {
-          double x;
-          asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(x) : "r"(src + 8u * j));
-          xraw[j] = x;
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(PNT) : "memory");
-        double* ucur = ring + (size_t)s * urs;
-        for (int j = s + tid; j < bp; j += PNT) {
-          double u = xraw[j];
-          for (int sp = s0; sp < s; ++sp)
-            if (!(sp == cb - 1 && j == cb)) u = fma(-xraw[sp], ring[(size_t)sp * urs + j], u);
-          ucur[j] = u;
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(PNT) : "memory");
-      }
-      const double* ucur = ring + (size_t)s * urs;
-      if (crank == 0 && tid == 0) {
-        js[s] = widx;
-        if (GAPS) {
-          const double a2 = ws ? __longlong_as_double((long long)(ws - 1ull)) : 0.0;
-          gp[s] = (a1 - a2) / a1;
-        }
-      }
-      // (B) multipliers (also into the mirror), column s+1, candidate for step s+1
-      const double piv = ucur[s];
-      const bool more = s + 1 < bp;
-      const double u1 = ucur[s + 1];
-      unsigned long long ckey = 0ull, csec = 0ull;
-      long long cidx = 0x7fffffffffffffffLL;
-      double Lm[RPT];
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        Lm[r] = 0.0;
-        const int li = tid + PNT * r;
-        if (st[r] == -1) {
-          if (r0 + li == widx) {
-            st[r] = t;
-          } else {
-            Lm[r] = v[r][i] / piv;
-            v[r][i] = Lm[r];
-            P[(size_t)li * ps + s] = Lm[r];
-            v[r][i + 1] = fma(-Lm[r], u1, v[r][i + 1]);
-            if (more) cand_push(mag_key(v[r][i + 1]), li, ckey, cidx, csec);
-          }
-        }
-      }
-      if (i == 7 && more) {   // snapshot of columns >= cb+8 for the next chunk's reconstruction
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const int li = tid + PNT * r;
-          if (li < Rc) {
-#pragma unroll
-            for (int q = 8; q < NB; ++q)
-              if (cb + q < bp) P[(size_t)li * ps + cb + q] = v[r][q];
-          }
-        }
-      }
-      if (more) publish(s + 1, ckey, cidx, csec);
-      // (C) bulk update of columns >= s+2 in registers (zero tail of U beyond bp)
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const double lm = Lm[r];
-        if (lm != 0.0) {
-          if ((i + 2) & 1) v[r][i + 2] = fma(-lm, ucur[cb + i + 2], v[r][i + 2]);
-#pragma unroll
-          for (int q = ((i + 3) & ~1); q < NB; q += 2) {
-            const double2 u = *reinterpret_cast<const double2*>(ucur + cb + q);
-            v[r][q] = fma(-lm, u.x, v[r][q]);
-            v[r][q + 1] = fma(-lm, u.y, v[r][q + 1]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RPT; ++r)
-#pragma unroll
-      for (int q = 0; q < NB; ++q) v[r][q] = (q + 8 < NB) ? v[r][q + 8] : 0.0;
-  }
-  __syncthreads();
-  if (crank == 0) {
-    for (int s = tid; s < s_done; s += PNT) {
-      p.Js[p.c0 + s] = js[s];
-      if (GAPS) p.gaps[p.c0 + s] = gp[s];
-    }
-    for (int e = tid; e < s_done * bp; e += PNT) {
-      const int s = e / bp, j = e % bp;
-      if (j >= s) p.Uw[(p.c0 + s) + (int64_t)(p.c0 + j) * p.k] = ring[(size_t)s * urs + j];
-    }
-  }
-  // L block (multipliers kept in the mirror) and row states
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int li = tid + PNT * r;
-    if (li < Rc) {
-      state[li] = st[r];
-      p.rowstate[r0 + li] = st[r];
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < Rc * bp; e += PNT) {
-    const int li = e % Rc, j = e / Rc;
-    const int sr = state[li], t = p.c0 + j;
-    const double val = (sr < 0 || sr > t) ? P[(size_t)li * ps + j] : (sr == t ? 1.0 : 0.0);
-    p.Lf[(r0 + li) + (int64_t)t * p.ldlf] = val;
-  }
-  __syncthreads();
-  cluster.sync();
-}
-
 // ------------------------------------------------------------------------------------------
 // v2 panel: CTA-reduced candidates + a row-carrying all-to-all.
 // Per pivot step s (measured primitives, profiles/round1/mailbox_lat.txt: a 16-CTA all-to-all
@@ -736,8 +479,6 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       const int s = cb + i;
       if (s >= s_end) break;
       const int t = p.c0 + s, par = s & 1;
-      const bool probe = p.tprobe != nullptr && g == 0 && crank == 0 && tid == 0;
-      if (probe) p.tprobe[(int64_t)t * 16 + 0] = clock64();
       // (A) local candidate of column s, owner copies its row (block coordinates)
       unsigned long long ckey = 0ull, csec = 0ull;
       long long cidx = 0x7fffffffffffffffLL;
@@ -747,8 +488,6 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       unsigned long long wk, ws;
       unsigned wi;
       warp_argmax(ckey, (unsigned)cidx, csec, wk, wi, ws, GAPS);
-      if (probe) p.tprobe[(int64_t)t * 16 + 8] = clock64();
-      if (probe) p.tprobe[(int64_t)t * 16 + 10] = clock64();
       if (lane == 0) {
         wck[par * PNW + warp] = wk;
         wci[par * PNW + warp] = wk ? (long long)(r0 + wi) : 0x7fffffffffffffffLL;
@@ -758,9 +497,7 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       const int jrow0 = 2 + (s >> 1);
       const int nchunk = 2 + (MSG - jrow0);
       if (tid == 0) mbar_arm(mbar0 + 8 * par, (unsigned)(csize * nchunk * 16));
-      if (probe) p.tprobe[(int64_t)t * 16 + 1] = clock64();
       asm volatile("bar.sync 1, %0;" ::"n"(PNT) : "memory");
-      if (probe) p.tprobe[(int64_t)t * 16 + 2] = clock64();
       // (B) CTA candidate -> every CTA of the cluster
       {
         const unsigned long long k8 = lane < PNW ? wck[par * PNW + lane] : 0ull;
@@ -772,7 +509,6 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
         const unsigned wl = __ballot_sync(0xffffffffu, k8 == bk && k8 != 0ull && (unsigned)(i8 - r0) == bl);
         const int cw = wl ? __ffs(wl) - 1 : 0;
         const long long gidx = bk ? r0 + (long long)bl : 0x7fffffffffffffffLL;
-        if (probe) p.tprobe[(int64_t)t * 16 + 9] = clock64();
         // only the CTA-winning warp's owner lane copies its row (one warp's 16-byte stores instead
         // of all 8 warps'), then every warp sends to its 2 destination CTAs
         if (warp == cw && bk && (int)(bl & 31u) == lane) {
@@ -806,7 +542,6 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
           }
         }
       }
-      if (probe) p.tprobe[(int64_t)t * 16 + 3] = clock64();
       // (C) deferred bulk update of step s-1: columns >= s+1 (window q with cb+q >= s+1)
       if (s > 0) {
         const double* uprev = ub + (size_t)(s - 1) * NB + cb;
@@ -827,10 +562,8 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
           }
         }
       }
-      if (probe) p.tprobe[(int64_t)t * 16 + 4] = clock64();
       // (D) the cluster's winner and its row
       mbar_wait(mbar0 + 8 * par, (unsigned)((s >> 1) & 1));
-      if (probe) p.tprobe[(int64_t)t * 16 + 5] = clock64();
       const double* box = mbox + (size_t)par * MAXCS * MSGD;
       const unsigned long long gk = lane < csize ? __double_as_longlong(box[lane * MSGD]) : 0ull;
       const long long gi8 = lane < csize ? __double_as_longlong(box[lane * MSGD + 1]) : 0x7fffffffffffffffLL;
@@ -839,6 +572,10 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
       unsigned long long wkey, wsec;
       unsigned wlane;
       warp_argmax(gk, gk ? (unsigned)lane : 0xffffffffu, gs8, wkey, wlane, wsec, GAPS);
+      // no active row left in this cluster (every key 0, possible when G > 1 and k exceeds the
+      // cluster's rows): take slot 0's message so every read below stays in bounds; its key 0
+      // never wins the cross-cluster reduction unless every cluster is exhausted (rank failure)
+      if (!wkey) wlane = 0;
       long long widx = __shfl_sync(0xffffffffu, gi8, (int)wlane);
       const double* row = box + (size_t)wlane * MSGD + 4;
       double lp = s > 0 ? box[(size_t)wlane * MSGD + 3] : 0.0;
@@ -872,6 +609,8 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
         if (s_late) {
           if (tid == 0) atomicCAS(reinterpret_cast<unsigned long long*>(p.status), 0ull,
                                   (unsigned long long)(-(long long)(t + 1)));
+          if (g == 0 && crank == 0)   // as on a rank failure: the undecided pivots read -1
+            for (int tt = t + tid; tt < p.k; tt += PNT) p.Js[tt] = -1;
           s_done = s;
           stop = true;
           break;
@@ -913,7 +652,6 @@ __global__ void __launch_bounds__(PNT, 1) k_lupp_panel_v2(PanelParams p) {
           gp[s] = (a1 - a2) / a1;
         }
       }
-      if (probe) p.tprobe[(int64_t)t * 16 + 6] = clock64();
       // (E) multipliers, the next search column, the L column of step s
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
@@ -1047,9 +785,7 @@ ClusterCfg pick_cluster(sk_ctx* c) {
   cudaFuncAttributes fa{};
   cudaFuncGetAttributes(&fa, k_lupp_panel<true>);
   cfg.max_dyn = c->max_smem_optin - (int)fa.sharedSizeBytes - 64;
-  for (PanelFn fn : {k_lupp_panel<true>, k_lupp_panel<false>, k_lupp_panel_reg<true, 1, 64>,
-                     k_lupp_panel_reg<false, 1, 64>, k_lupp_panel_reg<true, 2, 32>, k_lupp_panel_reg<false, 2, 32>,
-                     k_lupp_panel_reg<true, 4, 16>, k_lupp_panel_reg<false, 4, 16>}) {
+  for (PanelFn fn : {k_lupp_panel<true>, k_lupp_panel<false>}) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.max_dyn);
   }
@@ -1108,16 +844,13 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   if (!cfg.ok) return fail(c, SK_E_CUDA, "no thread-block cluster configuration for the LUPP panel: " + cfg.why);
   int cs = cfg.cs;
   int64_t R = cdiv(n, cs);
-  static const bool force_v1 = [] { const char* e = std::getenv("SKEL_LUPP_V1"); return e && e[0] == '1'; }();
-  static const bool one_cluster = [] { const char* e = std::getenv("SKEL_LUPP_ONE_CLUSTER"); return e && e[0] == '1'; }();
   // Tall panels (more than 4 rows per thread in one cluster): G co-resident clusters of the
   // register-resident v2 kernel, whose winners meet in global memory once per step, instead of
   // one cluster streaming thousands of rows per CTA.  For k >= 512 the fewest rows per thread
   // first (wider column blocks, fewer block transitions: C5 columns 10.5 vs 11.4 us/step), else the
   // fewest clusters (cheaper per-step exchange: C4 rows 6.0 vs 7.0 us/step); then the larger cluster.
   int G = 1;
-  static const int multi_above = [] { const char* e = std::getenv("SKEL_LUPP_MULTI_ABOVE_RPT"); return e ? std::atoi(e) : 4; }();
-  if (cdiv(R, PNT) > multi_above && !force_v1 && !one_cluster) {
+  if (cdiv(R, PNT) > 4) {
     bool found = false;
     const int order_wide[3] = {1, 2, 4}, order_few[3] = {4, 2, 1};
     const int* order = k >= 512 ? order_wide : order_few;
@@ -1139,9 +872,6 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
         oc.attrs = oa; oc.numAttrs = 1;
         int active = 0;
         if (cudaOccupancyMaxActiveClusters(&active, f, &oc) != cudaSuccess) { cudaGetLastError(); active = 0; }
-        static const bool dbg = [] { const char* e = std::getenv("SKEL_LUPP_DEBUG"); return e && e[0] == '1'; }();
-        if (dbg) std::fprintf(stderr, "[lupp] n=%lld target rpt %d cluster %d: need %d clusters, %d active\n",
-                              (long long)n, target, ccs, gg, active);
         if (gg <= active) {
           G = gg;
           cs = ccs;
@@ -1160,7 +890,7 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   int64_t bp = 0;
   size_t smem_bytes = 0;
   const int rpt = (int)cdiv(R, PNT);
-  if (rpt <= 4 && !force_v1) {
+  if (rpt <= 4) {
     const int nb = rpt == 1 ? 64 : rpt == 2 ? 32 : 16;
     bp = std::min<int64_t>(k, nb);
     const bool multi = G > 1;      // the cross-cluster exchange is compiled only into the G > 1 variants
@@ -1177,14 +907,6 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
                  : (gaps ? k_lupp_panel_v2<4, 16, true, false> : k_lupp_panel_v2<4, 16, false, false>);
       smem_bytes = v2_smem_bytes<16>();
     }
-  } else if (rpt <= 4) {
-    const int nb = rpt == 1 ? 64 : rpt == 2 ? 32 : 16;
-    const int rv = rpt == 1 ? 1 : rpt == 2 ? 2 : 4;
-    bp = std::min<int64_t>(k, nb);
-    smem_bytes = reg_smem_bytes((int)R, (int)bp, nb, (int)((bp + 1) | 1));
-    if (rv == 1) fn = gaps ? k_lupp_panel_reg<true, 1, 64> : k_lupp_panel_reg<false, 1, 64>;
-    if (rv == 2) fn = gaps ? k_lupp_panel_reg<true, 2, 32> : k_lupp_panel_reg<false, 2, 32>;
-    if (rv == 4) fn = gaps ? k_lupp_panel_reg<true, 4, 16> : k_lupp_panel_reg<false, 4, 16>;
   } else {
     bp = std::min<int64_t>(k, 1024);
     while (bp > 1 && (int64_t)PanelSmem((int)R, (int)bp).total > cfg.max_dyn) bp = (bp > 64) ? bp / 2 : bp - 1;
@@ -1194,12 +916,7 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
   }
   if ((int64_t)smem_bytes > cfg.max_dyn) return fail(c, SK_E_ARG, "LUPP panel staging exceeds shared memory");
 
-  DBuf Wb, Ub, stateb, maxb, Lfb, probeb;
-  static const bool want_probe = [] { const char* e = std::getenv("SKEL_LUPP_PROBE"); return e && e[0] == '1'; }();
-  if (want_probe) {
-    SK_TRY(probeb.alloc(c, (size_t)k * 16 * sizeof(long long)));
-    SK_CUDA(c, cudaMemsetAsync(probeb.p, 0, (size_t)k * 16 * sizeof(long long), c->stream));
-  }
+  DBuf Wb, Ub, stateb, maxb, Lfb;
   DBuf gxb;
   const size_t gbox_doubles = (size_t)2 * G * (4 + 64);
   if (G > 1) {
@@ -1223,10 +940,9 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
                                                stateb.as<int>(), maxb.as<unsigned long long>());
     SK_TRY(launched(c));
   }
-  static const bool no_lookahead = [] { const char* e = std::getenv("SKEL_LUPP_NO_LOOKAHEAD"); return e && e[0] == '1'; }();
   // programmatic dependent launch along the panel -> u12 -> next-block GEMM -> panel chain
-  static const bool pdl = [] { const char* e = std::getenv("SKEL_NO_PDL"); return !(e && e[0] == '1'); }();
-  const bool lookahead = !no_lookahead && bp < k;
+  constexpr bool pdl = true;
+  const bool lookahead = bp < k;
   if (lookahead) SK_TRY(ensure_aux(c));
   bool rest_pending = false;
   for (int64_t c0 = 0; c0 < k; c0 += bp) {
@@ -1237,7 +953,6 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     pp.rowstate = stateb.as<int>();
     pp.Js = Js; pp.Lf = Lf; pp.ldlf = ldlf; pp.Uw = Ub.as<double>(); pp.gaps = gaps;
     pp.maxbits = maxb.as<unsigned long long>(); pp.status = status_dev;
-    pp.tprobe = want_probe ? probeb.as<long long>() : nullptr;
     pp.G = G;
     pp.gbox = G > 1 ? gxb.as<double>() : nullptr;
     pp.gflag = G > 1 ? reinterpret_cast<unsigned long long*>(gxb.as<double>() + gbox_doubles) : nullptr;
@@ -1298,30 +1013,6 @@ sk_status lupp(sk_ctx* c, const double* Pin, bool row_major, int64_t n, int64_t 
     }
   }
   if (rest_pending) SK_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_b, 0));
-  if (want_probe) {   // experiments: per-step phase durations (cycles) of CTA 0, thread 0, to stderr
-    std::vector<long long> h((size_t)k * 16);
-    SK_CUDA(c, cudaMemcpyAsync(h.data(), probeb.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    SK_CUDA(c, cudaStreamSynchronize(c->stream));
-    // marks: 0 start, 8 warp argmax, 1 row copy+slot write, 2 CTA barrier, 9 CTA reduce, 3 sends,
-    // 4 bulk, 5 wait, 6 reduce+U, next 0
-    const int order[] = {0, 8, 10, 1, 2, 9, 3, 4, 5, 6};
-    const char* names[] = {"argmax", "copy", "slots", "bar", "ctared", "send", "bulk", "wait", "red+U", "E+next"};
-    double acc[10] = {0};
-    int cnt = 0;
-    for (int64_t t = 1; t + 1 < k; ++t) {
-      const long long* a = &h[(size_t)t * 16];
-      const long long* b = &h[(size_t)(t + 1) * 16];
-      if (!a[0] || !b[0] || b[0] < a[0]) continue;
-      for (int j = 0; j < 9; ++j) acc[j] += (double)(a[order[j + 1]] - a[order[j]]);
-      acc[9] += (double)(b[0] - a[6]);
-      ++cnt;
-    }
-    if (cnt) {
-      std::fprintf(stderr, "[lupp probe] n=%lld k=%lld steps=%d ", (long long)n, (long long)k, cnt);
-      for (int j = 0; j < 10; ++j) std::fprintf(stderr, " %s %.0f", names[j], acc[j] / cnt);
-      std::fprintf(stderr, " cycles\n");
-    }
-  }
   if (U) {
     const int blocks = (int)std::min<int64_t>(cdiv(k * k, 256), 4LL * c->num_sms);
     k_copy_u<<<blocks, 256, 0, c->stream>>>(Ub.as<double>(), (int)k, U, ldu);

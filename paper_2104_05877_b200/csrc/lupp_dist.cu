@@ -168,7 +168,10 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
                                 (unsigned long long)(-(long long)t));
         return;
       }
-      gathered = mb + (int64_t)((t - 1) & 1) * a.world * REC;
+      // buffer parity (epoch + t - 1) & 1, not (t - 1) & 1: epochs advance by k + 2 per selection, so
+      // step 0 of the NEXT selection (buffer (epoch + k + 2) & 1 = (epoch + k) & 1) never overwrites
+      // the buffer the last step of this one reads ((epoch + k - 1) & 1), even for odd k
+      gathered = mb + (int64_t)((epoch + (unsigned long long)t - 1ull) & 1ull) * a.world * REC;
     }
   }
 
@@ -307,10 +310,10 @@ __global__ void __launch_bounds__(DT) k_dist_step(StepArgs a) {
   }
   for (int64_t c = tid; c < k; c += DT) a.cand[4 + c] = has ? __ldcg(L.M + cd.i1 + c * nloc) : 0.0;
   if (a.peers != nullptr) {
-    // publish the record of step t into slot [t & 1][rank] of every mailbox, then the flags
+    // publish the record of step t into slot [(epoch + t) & 1][rank] of every mailbox, then the flags
     __syncthreads();
     const double hdr[4] = {a.cand[0], a.cand[1], a.cand[2], 0.0};
-    const int64_t off = (int64_t)(t & 1) * a.world * REC + (int64_t)a.rank * REC;
+    const int64_t off = (int64_t)((epoch + (unsigned long long)t) & 1ull) * a.world * REC + (int64_t)a.rank * REC;
     for (int q = 0; q < a.world; ++q) {
       double* dst = a.peers[q] + off;
       for (int64_t c = tid; c < REC; c += DT) dst[c] = c < 4 ? hdr[c] : a.cand[c];

@@ -70,7 +70,7 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
   if (kind == SK_RES_ROW_ID || kind == SK_RES_CUR) {
     SK_TRY(Rt.alloc(c, (size_t)n * k * sizeof(double)));
     SK_TRY(Qr.alloc(c, (size_t)n * k * sizeof(double)));
-    SK_TRY(gather_rows_t(c, A, n, lda, Is, k, Rt.as<double>(), n));
+    SK_TRY(gather_rows_t(c, A, m, n, lda, Is, k, Rt.as<double>(), n));
     SK_TRY(orthonormal_basis(c, Rt.as<double>(), n, k, Qr.as<double>(), status_dev));
     Rt.release();
   }

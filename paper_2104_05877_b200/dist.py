@@ -237,7 +237,7 @@ def dist_rand_lupp(A_local, n_global, k, l, embedding="gaussian", seed=0, zeta=8
             out["Is"] = backend.select_rows(C, k)
         if residual:
             r2, a2 = backend.residual_cols(A_local, C)
-            sums = torch.tensor([r2, a2], dtype=torch.float64, device=Xk.device)
+            sums = torch.tensor([r2, a2], dtype=torch.float64, device=A_local.device)
             dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
             out["residual"] = math.sqrt(max(float(sums[0]), 0.0))
             out["normA"] = math.sqrt(float(sums[1]))

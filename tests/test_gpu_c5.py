@@ -1,11 +1,16 @@
 """C5 (BASELINE configs[4]) at full size on one B200: A 131072 x 65536 FP64 (68.7 GB), k=1000,
 l=1100, Gaussian sketch, column LUPP, column-ID residual.
 
-The oracle cannot run this size end to end, so parity is checked on outputs it can compute one
-by one: sampled columns of A against the reflector-by-reflector definition,
-sampled sketch columns X(:, j) = Gamma A(:, j) against the oracle's Gamma, and properties that
-hold at any size: the first pivot is argmax |X(0, :)|, pivots are distinct, |L| <= 1
-with L(J_s[t], t) = 1, and the residual respects Eckart-Young.
+Two checks:
+* test_c5_full: sampled columns of A against the reflector-by-reflector definition, sampled
+  sketch columns X(:, j) = Gamma A(:, j) against the oracle's Gamma, and properties that hold at
+  any size (first pivot = argmax |X(0, :)|, distinct pivots, |L| <= 1 with
+  L(J_s[t], t) = 1, Eckart-Young);
+* test_c5_oracle_streamed: the whole path against the oracle.  A does not fit in host memory at
+  once, so the oracle takes it from the device in column blocks: its own X = Gamma A
+  (column-separable), its own LUPP on X (the plain-C loop, bitwise equal to the numpy one) and
+  its own column-ID residual with the residual blocks formed explicitly.  X within 1e-12, J_s
+  identical up to documented near-ties, residual within 1e-9 r + 4u||A||_F.
 """
 import numpy as np
 import pytest
@@ -13,8 +18,11 @@ import torch
 
 import paper_2104_05877_b200 as sk
 from inputs import c5
+from oracle import lupp as o_lupp
 from oracle import omega as o_omega
 from oracle import residual as o_res
+from oracle import sketch as o_sketch
+from tests.parity import lupp_parity, rel_fro
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
@@ -57,3 +65,30 @@ def test_c5_full(c5_data):
     opt = o_res.optimal_error(sigma, k)
     assert abs(nA - np.sqrt(np.sum(sigma ** 2))) <= 1e-12 * nA
     assert opt * (1 - 1e-9) <= r <= 100 * opt
+
+
+def test_c5_oracle_streamed(c5_data):
+    A, sigma, Y, Yp = c5_data
+    m, n = A.shape
+    k, l, seed = 1000, 1100, 2005
+    At = A.t()                                               # n x m contiguous: row j = column j of A
+
+    def get_cols(j0, j1):                                    # the input, column block by column block
+        return At[j0:j1].cpu().numpy().T
+
+    X = sk.sketch(A, l, "gaussian", seed)
+    Js, Lf, _, _ = sk.select_cols(X, k)
+    r, nA = sk.residual(A, Js, None, "col_id")
+    Xg = X.cpu().numpy()
+    jg = Js.cpu().numpy()
+    del X, Lf
+    torch.cuda.empty_cache()
+
+    Xo = o_sketch.sketch_streamed(get_cols, m, n, l, "gaussian", seed)
+    assert rel_fro(Xg, Xo) <= 1e-12
+    (piv, _, _, _), ties = lupp_parity(jg, lambda f: o_lupp.select_cols(Xo, k, f, fast=True))
+    del Xo
+    ro, nAo = o_res.residual_col_id_streamed(get_cols, m, n, piv)
+    assert abs(nA - nAo) <= 1e-12 * nAo
+    assert abs(r - ro) <= 1e-9 * ro + 4 * 2.0 ** -53 * nAo, (r, ro)
+    assert ro >= o_res.optimal_error(sigma, k) * (1 - 1e-9)

@@ -13,6 +13,7 @@ import torch
 
 import paper_2104_05877_b200 as sk
 from inputs import make_c2, make_c3, make_c4
+from oracle import cpqr as o_cpqr
 from oracle import idcoef as o_id
 from oracle import lupp as o_lupp
 from oracle import omega as o_omega
@@ -39,9 +40,9 @@ def c2():
     return A, sigma, dev_f(A)
 
 
-@pytest.mark.parametrize("k", [16, 512])
+@pytest.mark.parametrize("k", [16, 64, 256, 512])
 def test_c2_full_path(c2, k):
-    """C2 at the bench configuration (k=512, l=522) and the smallest k."""
+    """C2 at every k of BASELINE configs[1] (k = 512, l = 522 is the bench's C2 line)."""
     A, sigma, Ad = c2
     l, seed = k + 10, 2002 + k
     X = sk.sketch(Ad, l, "gaussian", seed)
@@ -60,6 +61,21 @@ def test_c2_full_path(c2, k):
     ro, nAo = o_res.residual(A, piv, kind="col_id")
     assert res_ok(r, ro, nAo), (r, ro)
     assert r >= o_res.optimal_error(sigma, k) * (1 - 1e-9)
+
+
+@pytest.mark.parametrize("k", [64, 512])
+def test_c2_cpqr_bench_shape(c2, k):
+    """S2' at the shape bench.py times (X 522 x 4096, k = 512) and k = 64: CPQR on the GPU's
+    sketch against the oracle's CPQR on the oracle's sketch (reading R9)."""
+    A, _, Ad = c2
+    l, seed = k + 10, 2002 + k
+    X = sk.sketch(Ad, l, "gaussian", seed)
+    Jc, R = sk.select_cols_cpqr(X, k, want_r=True)
+    Xo = o_sketch.sketch(A, l, "gaussian", seed)
+    piv, Ro = o_cpqr.select_cols_cpqr(Xo, k)
+    assert Jc.cpu().tolist() == piv.tolist()
+    # R's rows carry the Householder sign convention of both sides (alpha = -sign(x0) ||x||)
+    assert rel_fro(R.cpu().numpy(), Ro) <= 1e-9
 
 
 def test_c2_sketch_cluster_paths(c2):
@@ -99,10 +115,10 @@ def test_c3_full_cur(c3):
 
     Xo = oracle_sparse_sketch(A, l, seed, 8)
     assert rel_fro(X.cpu().numpy(), Xo) <= 1e-12
-    (piv, _, _, _), _ = lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(Xo, k, f))
+    (piv, _, _, _), _ = lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(Xo, k, f, fast=True))
     Co = A[:, piv]
     np.testing.assert_array_equal(C.cpu().numpy(), Co)
-    (ipiv, _, _, _), _ = lupp_parity(Is.cpu().numpy(), lambda f: o_lupp.select_rows(Co, k, f))
+    (ipiv, _, _, _), _ = lupp_parity(Is.cpu().numpy(), lambda f: o_lupp.select_rows(Co, k, f, fast=True))
     ro, nAo = o_res.residual(A, piv, ipiv, kind="cur")
     assert res_ok(r_cur, ro, nAo), (r_cur, ro)
     assert abs(nA - nAo) <= 1e-13 * nAo
@@ -114,7 +130,7 @@ def c4():
     return A, dev_f(A)
 
 
-@pytest.mark.parametrize("k", [50, 200])
+@pytest.mark.parametrize("k", [50, 100, 200])
 def test_c4_full_row_and_col_id(c4, k):
     """C4: 65536 x 784 nonnegative, Gaussian l=2k; column ID and row ID."""
     A, Ad = c4

@@ -55,11 +55,12 @@ def test_sketch_dense_parity(m, n, l, seed):
 
 
 def test_sketch_dense_odd_lda():
-    m, n, l = 301, 50, 20
+    m, n, l = 300, 50, 20
     A = rand_mat(m, n, 3)
     buf = torch.zeros((n, m + 3), dtype=torch.float64, device=DEV)
     buf[:, :m] = torch.from_numpy(A.T.copy()).to(DEV)
-    Av = buf.t()[:m]                       # column-major view, lda = m + 3 (odd)
+    Av = buf.t()[:m]                       # column-major view, lda = m + 3 = 303 (odd: no TMA)
+    assert Av.stride(1) % 2 == 1
     X = sk.sketch(Av, l, "gaussian", 11).cpu().numpy()
     assert rel_fro(X, o_sketch.sketch(A, l, "gaussian", 11)) <= 1e-12
 
@@ -176,12 +177,22 @@ def test_sketch_sparse_parity(m, n, l, zeta, seed):
     (40001, 80, 70, 6),          # tall: several clusters exchanging winners in global memory, ragged
     (70000, 40, 36, 7),          # taller than one cluster can hold (> 65536 rows)
     (131000, 30, 24, 8),         # C5 row-LUPP height class (32 clusters of 4), ragged
+    # k >= 512 takes the planner's "fewest rows per thread" order (lupp.cu): these reach the
+    # multi-cluster instantiations C5's column LUPP runs
+    (30000, 522, 512, 9),        # v2<1,64,multi>: 15 clusters of 8, 1 row per thread
+    (65536, 522, 512, 10),       # v2<2,32,multi>: 32 clusters of 4 (C5 columns, k = 512)
+    (65536, 1010, 1000, 11),     # v2<2,32,multi> at C5's k = 1000
+    (131072, 522, 512, 12),      # v2<4,16,multi>: 32 clusters of 4, 4 rows per thread
 ])
 def test_select_cols_parity(n, l, k, seed):
     rng = np.random.default_rng(seed)
     X = rng.standard_normal((l, n))
-    Js, Lf, Ug, gaps = sk.select_cols(dev_rowmajor(X), k, want_gaps=True)
-    (piv, Lo, Uo, go), ties = lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(X, k, f))
+    fast = n * k > 4_000_000                 # the plain-C oracle LUPP (bitwise equal to the numpy loop)
+    Xd = dev_rowmajor(X)
+    Js, Lf, Ug, gaps = sk.select_cols(Xd, k, want_gaps=True)
+    Js2, _, _, _ = sk.select_cols(Xd, k)     # the instantiation without the gap output (the bench's)
+    assert torch.equal(Js, Js2)
+    (piv, Lo, Uo, go), ties = lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(X, k, f, fast=fast))
     Lg = Lf.cpu().numpy()
     assert np.max(np.abs(Lg)) <= 1.0 + 1e-14
     np.testing.assert_array_equal(Lg[Js.cpu().numpy(), np.arange(k)], 1.0)
@@ -189,6 +200,21 @@ def test_select_cols_parity(n, l, k, seed):
         assert rel_fro(Lg, Lo) <= 1e-10
         assert rel_fro(Ug.cpu().numpy(), Uo) <= 1e-10
         np.testing.assert_allclose(gaps.cpu().numpy(), go, atol=1e-9)
+
+
+def test_select_cols_cluster_exhausted_first():
+    """Multi-cluster panel (30000 rows: 15 clusters of 2048 rows at k >= 512) where k exceeds the
+    rows of one cluster: cluster 0's rows are scaled up so they are all pivoted first, after which
+    that cluster has no active row and its message carries key 0 while the others keep going."""
+    n, k = 30000, 2100
+    rng = np.random.default_rng(21)
+    X = rng.standard_normal((k, n))
+    X[:, :2048] *= 1e6
+    Js, Lf, _, _ = sk.select_cols(dev_rowmajor(X), k)
+    jg = Js.cpu().numpy()
+    assert sorted(jg[:2048].tolist()) == list(range(2048))
+    (piv, Lo, _, _), ties = lupp_parity(jg, lambda f: o_lupp.select_cols(X, k, f, fast=True))
+    assert np.max(np.abs(Lf.cpu().numpy())) <= 1.0 + 1e-14
 
 
 def test_select_cols_kahan_all_ties():

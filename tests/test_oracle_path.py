@@ -118,29 +118,32 @@ def test_rsvd_deim_exact_rank_recovers_true_singular_vectors():
 
 
 # ----------------------------------------------------------------------------- LUPP
-def test_lupp_spec_2x2_case():
+@pytest.mark.parametrize("fast", [False, True], ids=["numpy", "c"])
+def test_lupp_spec_2x2_case(fast):
     # X = [[4,2],[1,3]] -> pivots [1,2] (1-based), L_l = [[4,0],[1,2.5]], R = [[1,.5],[0,1]].
     X = np.array([[4.0, 2.0], [1.0, 3.0]])
-    piv, Lf, U, _ = lupp.select_cols(X, 2)
+    piv, Lf, U, _ = lupp.select_cols(X, 2, fast=fast)
     assert piv.tolist() == [0, 1]
     np.testing.assert_array_equal(U.T, [[4.0, 0.0], [1.0, 2.5]])          # L_l = U^T
     np.testing.assert_array_equal(Lf.T, [[1.0, 0.5], [0.0, 1.0]])         # R^{LU} = Lf^T
 
 
-def test_lupp_identity_and_ties_lowest_original_index():
-    piv, _, _, _ = lupp.select_cols(np.eye(6), 6)
+@pytest.mark.parametrize("fast", [False, True], ids=["numpy", "c"])
+def test_lupp_identity_and_ties_lowest_original_index(fast):
+    piv, _, _, _ = lupp.select_cols(np.eye(6), 6, fast=fast)
     assert piv.tolist() == list(range(6))
     # tie demo: lowest ORIGINAL index wins -> [2, 0]; LAPACK's swapped order gives [2, 1]
     X = np.array([[1.0, 1.0, 3.0], [5.0, -5.0, 0.0]])
-    piv, _, _, _ = lupp.select_cols(X, 2)
+    piv, _, _, _ = lupp.select_cols(X, 2, fast=fast)
     assert piv.tolist() == [2, 0]
 
 
-def test_lupp_factorization_and_bounds():
+@pytest.mark.parametrize("fast", [False, True], ids=["numpy", "c"])
+def test_lupp_factorization_and_bounds(fast):
     rng = np.random.default_rng(5)
     for (n, k) in [(50, 8), (200, 30), (31, 31)]:
         X = rng.standard_normal((k + 3, n))
-        piv, Lf, U, gaps = lupp.select_cols(X, k)
+        piv, Lf, U, gaps = lupp.select_cols(X, k, fast=fast)
         assert len(set(piv.tolist())) == k
         assert np.max(np.abs(Lf)) <= 1.0 + 1e-15                        # |R^{LU}| <= 1
         np.testing.assert_array_equal(Lf[piv, np.arange(k)], 1.0)
@@ -153,13 +156,14 @@ def test_lupp_factorization_and_bounds():
         assert np.all((gaps >= 0) & (gaps <= 1))
 
 
-def test_lupp_matches_lapack_getrf_tie_free():
+@pytest.mark.parametrize("fast", [False, True], ids=["numpy", "c"])
+def test_lupp_matches_lapack_getrf_tie_free(fast):
     # scipy's getrf on X^T (partial pivoting) picks the same k pivots on tie-free random input
     rng = np.random.default_rng(6)
     for trial in range(20):
         n, k = 120, 25
         X = rng.standard_normal((k, n))
-        piv, _, _, _ = lupp.select_cols(X, k)
+        piv, _, _, _ = lupp.select_cols(X, k, fast=fast)
         lu, ipiv = sla.lu_factor(X.T.copy())
         perm = np.arange(n)
         for i, p in enumerate(ipiv):
@@ -167,22 +171,24 @@ def test_lupp_matches_lapack_getrf_tie_free():
         assert piv.tolist() == perm[:k].tolist()
 
 
-def test_lupp_k_row_invariance_and_duality():
+@pytest.mark.parametrize("fast", [False, True], ids=["numpy", "c"])
+def test_lupp_k_row_invariance_and_duality(fast):
     rng = np.random.default_rng(7)
     X = rng.standard_normal((40, 300))
-    p_all = lupp.select_cols(X, 20)[0]
-    p_k = lupp.select_cols(X[:20], 20)[0]
+    p_all = lupp.select_cols(X, 20, fast=fast)[0]
+    p_k = lupp.select_cols(X[:20], 20, fast=fast)[0]
     assert p_all.tolist() == p_k.tolist()                              # reading R5
     C = rng.standard_normal((8, 3))
-    assert lupp.select_rows(C, 3)[0].tolist() == lupp.select_cols(C.T, 3)[0].tolist()
+    assert lupp.select_rows(C, 3, fast=fast)[0].tolist() == lupp.select_cols(C.T, 3, fast=fast)[0].tolist()
 
 
-def test_lupp_kahan_witness_lemma2():
+@pytest.mark.parametrize("fast", [False, True], ids=["numpy", "c"])
+def test_lupp_kahan_witness_lemma2(fast):
     # Lemma 2 tightness: every step is a tie; pivots 0..l-1; max|R1^{-1}R2| = 2^{l-1},
     # row-wise 2^{l-i} (1-based i).
     for l in (5, 10, 20):
         X = kahan_witness(l, l + 7)
-        piv, Lf, U, gaps = lupp.select_cols(X, l)
+        piv, Lf, U, gaps = lupp.select_cols(X, l, fast=fast)
         assert piv.tolist() == list(range(l))
         assert np.all(gaps == 0.0)
         g = lupp.growth(Lf, piv)
@@ -192,13 +198,34 @@ def test_lupp_kahan_witness_lemma2():
         assert eta >= 2.0 ** (l - 1)
 
 
-def test_lupp_rank_deficiency():
+@pytest.mark.parametrize("fast", [False, True], ids=["numpy", "c"])
+def test_lupp_rank_deficiency(fast):
     rng = np.random.default_rng(8)
     C = rng.standard_normal((30, 3)) @ rng.standard_normal((3, 4))      # rank 3
-    lupp.select_rows(C[:, :3], 3)
+    lupp.select_rows(C[:, :3], 3, fast=fast)
     with pytest.raises(lupp.RankError) as e:
-        lupp.select_rows(C, 4)
+        lupp.select_rows(C, 4, fast=fast)
     assert e.value.step == 4
+
+
+@pytest.mark.parametrize("n,k,seed", [(500, 40, 1), (3001, 100, 2), (70, 70, 3), (20000, 64, 4)])
+def test_lupp_c_equals_numpy_bitwise(n, k, seed):
+    """The plain-C LUPP (oracle/c/lupp.c, used for the C5-size panels) reproduces the numpy loop
+    bit for bit: pivots, multipliers, U and gaps; also with a forced pivot (near-tie rule) and on
+    the all-ties Kahan witness."""
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((k + 3, n))
+    for forced in (None, {k // 2: None}):
+        if forced is not None:
+            ref = lupp.select_cols(X, k)[0]
+            forced = {k // 2: int(ref[k // 2 + 1])}        # a valid, non-argmax pivot
+        a = lupp.select_cols(X, k, forced)
+        b = lupp.select_cols(X, k, forced, fast=True)
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+    W = kahan_witness(12, 40)
+    for x, y in zip(lupp.select_cols(W, 12), lupp.select_cols(W, 12, fast=True)):
+        np.testing.assert_array_equal(x, y)
 
 
 # ----------------------------------------------------------------------------- CPQR
@@ -371,3 +398,19 @@ def test_generators_spectra():
     np.testing.assert_allclose(s, sigma, rtol=1e-12, atol=1e-15)
     Q = haar(50, 10, np.random.default_rng(0))
     np.testing.assert_allclose(Q.T @ Q, np.eye(10), atol=1e-14)
+
+
+def test_streamed_sketch_and_residual_equal_the_plain_definitions():
+    """The column-block forms used at C5 (68.7 GB) equal the plain definitions they restate:
+    X(:, J) = Gamma A(:, J) and ||E||_F^2 = sum over column blocks."""
+    rng = np.random.default_rng(12)
+    A = make_lowrank(300, 211, 0.9 ** np.arange(211), rng)
+    get = lambda a, b: A[:, a:b]  # noqa: E731
+    for kind in ("gaussian", "sparse_sign"):
+        X = sketch.sketch(A, 30, kind, 5)
+        np.testing.assert_allclose(sketch.sketch_streamed(get, 300, 211, 30, kind, 5, block=64), X,
+                                   rtol=0, atol=1e-14 * np.abs(X).max())
+    piv = lupp.select_cols(sketch.sketch(A, 20, "gaussian", 3), 20)[0]
+    r, nA = residual.residual(A, piv, kind="col_id")
+    rs, nAs = residual.residual_col_id_streamed(get, 300, 211, piv, block=50)
+    assert abs(r - rs) <= 1e-12 * r and abs(nA - nAs) <= 1e-13 * nA
