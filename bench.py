@@ -1,22 +1,25 @@
 #!/usr/bin/env python
 """Benchmark of the randomized-LUPP skeleton-selection hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--k 512] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--k 1000] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1], "C2"): A = U diag(10^(-i/50)) V^T, 4096 x 4096 FP64,
-Haar U, V (seed 1002); Gaussian Omega, k = 512, l = k + 10 = 522 (seed 2002 + k).
-One step = the whole hot path of SURVEY.md section 8(a) for C2:
-    S0+S1 sketch X = Omega A  ->  S2 select_cols (LUPP)  ->  S2' select_cols_cpqr (comparison)
-    ->  S5 id_coeffs  ->  S6 residual ||A - CC^+A||_F (gather S3 + LUPP-basis S4 inside).
-The other configs follow their SURVEY 8(d) path: C3 / C4 add S3 gather + S4 select_rows as
-stages and take the CUR (C3) / column- and row-ID (C4) residuals; S2' runs on C2 only.
-value = the BASELINE.json metric "skeleton-selection time (sketch+LUPP)" = S1 + S2 device time
-per step (ms, lower is better), max over ranks.  ms_per_step = the whole step.
-L2 policy: a 512 MiB buffer is overwritten between timed steps (untimed), so every step
-starts cold; per-step CUDA events on the library's stream.
+Workload (default, BASELINE.json configs[4], "C5" -- the largest configuration, and the one that
+fits one B200): A = U diag(i^-1.5) V^T, 131072 x 65536 FP64 (68.7 GB), U and V products of 64
+Householder reflectors, built on the device from seed 1005; Gaussian Omega, k = 1000, l = 1100
+(seed 2005).  One step = the C5 path of SURVEY.md section 8(d):
+    S0+S1 sketch X = Omega A  ->  S2 select_cols (LUPP)  ->  S5 id_coeffs  ->  S6 residual ||A - CC^+A||_F.
+value = the BASELINE.json metric "skeleton-selection time (sketch+LUPP)" = S1 + S2 device time per
+step (ms, lower is better), max over ranks; ms_per_step = the whole step.  With N > 1 (torchrun)
+the same matrix is column-sharded over the N GPUs (strong scaling): every rank builds
+and sketches its own column block, the column LUPP exchanges per pivot step or gathers the k
+LUPP-visible sketch rows once, and the residual is reduced across ranks.
+--config C1..C4 run the other configurations' paths (C2 adds S2' CPQR, C3/C4 add S3 + S4).
+L2 policy: a 512 MiB buffer is overwritten between timed steps (untimed); per-step CUDA events on
+the library's stream.
 
---impl reference times the plain CPU oracle (oracle/) on the same config on the host cores
-(the reference arm for this paper-only build).
+--impl reference times the plain CPU oracle (oracle/) on the same config on the host cores (the
+reference arm of this paper-only build); at C5 each step is a bounded sample
+of the workload scaled to the whole selection (the sample is stated in the line).
 """
 import argparse
 import json
@@ -50,7 +53,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--k", type=int, default=None, help="default: C1 20, C2 512, C3 500, C4 200, C5 1000")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -114,6 +117,75 @@ def oracle_selection(A, k, l, seed, emb="gaussian", piter=0):
     return piv
 
 
+C5_SAMPLE_COLS = 1024
+
+
+def c5_oracle_sample(get_block, m, n, k, l, seed):
+    """The oracle on a bounded sample of C5's selection, scaled to the whole selection (ms):
+    the full Gamma (l x m) generated as the oracle does it, the sketch of C5_SAMPLE_COLS columns of
+    A (X = Gamma A is column-separable, so the whole sketch costs n / C5_SAMPLE_COLS times that), and
+    the oracle's LUPP on a seeded n x k Gaussian panel of C5's panel shape (the LUPP's work does not
+    depend on the values).  Returns (value_ms, parts, X block) -- test infrastructure on the host."""
+    from oracle import lupp as o_lupp
+    from oracle import omega as o_omega
+    Ab = np.asarray(get_block(0, C5_SAMPLE_COLS), dtype=np.float64)
+    t0 = time.perf_counter()
+    G = o_omega.gaussian(seed, l, m)
+    t1 = time.perf_counter()
+    Xb = G @ Ab
+    t2 = time.perf_counter()
+    del G
+    P = np.random.default_rng(7).standard_normal((k, n))
+    t3 = time.perf_counter()
+    o_lupp.select_cols(P, k, fast=True)
+    t4 = time.perf_counter()
+    parts = {"gamma_gen_ms": (t1 - t0) * 1e3, "sketch_ms": (t2 - t1) * 1e3 * n / C5_SAMPLE_COLS,
+             "lupp_ms": (t4 - t3) * 1e3}
+    return sum(parts.values()), parts, Xb
+
+
+def c5_sample_desc(model):
+    return (f"C5 oracle sample scaled to the whole selection: full Gamma generation (numpy Philox), sketch of "
+            f"{C5_SAMPLE_COLS} of 65536 columns x 64, plain-C oracle LUPP on a 65536 x 1000 seeded panel; on {model}")
+
+
+def c5_e2e(args, sk, A, m, n, k, l, seed, local, stream, ev, Js_dev):
+    """e2e at C5 through the public Algorithm-2 call sk_rand_lupp with A in pinned HOST memory
+    (68.7 GB, page-locked with cudaHostRegister): every call copies all of A host -> device in
+    column blocks (a 3-slot device ring, copy of block b overlapping the sketch of block b - 1)
+    and returns J_s on the host."""
+    import torch
+    Ah = np.empty((n, m), dtype=np.float64)                       # rows = columns of A
+    cudart = torch.cuda.cudart()
+    reg = cudart.cudaHostRegister(Ah.ctypes.data, Ah.nbytes, 0)
+    if int(reg) != 0:
+        return {"value": None, "unit": "ms", "error": f"cudaHostRegister failed ({int(reg)})"}
+    try:
+        Aht = torch.from_numpy(Ah)
+        At = A.t()
+        for j0 in range(0, n, 4096):                                 # device -> registered host, untimed
+            Aht[j0:j0 + 4096].copy_(At[j0:j0 + 4096])
+        torch.cuda.synchronize()
+        A_host = Aht.t()
+        times = []
+        with torch.cuda.stream(stream):
+            for it in range(max(1, min(args.warmup, 2)) + max(2, min(args.steps, 5))):
+                e0, e1 = ev(), ev()
+                e0.record(stream)
+                Jh, _ = sk.rand_lupp(A_host, k, l, seed=seed, device=local)
+                e1.record(stream)
+                e1.synchronize()
+                if it >= max(1, min(args.warmup, 2)):
+                    times.append(e0.elapsed_time(e1))
+        same = int(np.sum(np.asarray(Jh) == Js_dev.cpu().numpy()))
+        return {"value": statistics.mean(times), "unit": "ms", "h2d_bytes_per_step": int(m * n * 8),
+                "d2h_bytes_per_step": int(k * 8), "api": "sk_rand_lupp (host A, page-locked) -> Js on host",
+                "pivots_equal_to_device_path": f"{same}/{k}"}
+    finally:
+        cudart.cudaHostUnregister(Ah.ctypes.data)
+        del Ah
+
+
 class ClockSampler:
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -162,9 +234,28 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg, k, l, seed, desc = workload(args)
-    if args.config == "C5":   # 68.7 GB: the host oracle cannot hold it (the GPU path builds it on device)
-        print(json.dumps({"impl": "reference", "unavailable": "C5 (131072 x 65536 FP64, 68.7 GB) exceeds the "
-                          "host oracle's memory; the reference arm runs C1-C4"}), flush=True)
+    if args.config == "C5":   # 68.7 GB does not fit the host oracle: a bounded sample per step (stated)
+        from inputs import c5 as c5in
+        m, n = c5in.M5, c5in.N5
+        cores, model = cpu_info()
+        steps = max(1, min(args.steps, 3))
+        warm = min(args.warmup, 1)
+        times = []
+        for it in range(warm + steps):
+            v, parts, _ = c5_oracle_sample(lambda a, b: c5in.build_block_host(a, b), m, n, k, l, seed)
+            if it >= warm:
+                times.append(v)
+        v = statistics.mean(times)
+        line = {
+            "impl": "reference", "metric": "skeleton-selection time (sketch+LUPP)", "value": v, "unit": "ms",
+            "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": v, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "m": m, "n": n, "k": k, "l": l},
+            "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "oracle", "sample": c5_sample_desc(model),
+                             "parts_ms": parts},
+            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
         return 0
     A, _ = make_input(args, cfg)
     cores, model = cpu_info()
@@ -192,79 +283,57 @@ def run_reference(args):
 
 
 def main_dist(args, world, rank, local):
-    """N > 1 GPUs (torchrun): the column-sharded path of SURVEY 8(e), weak scaling.
-
-    Rank r holds a 4096 x 4096 C2-type block (own Haar factors, seed 1002 + r), so the global A is
-    4096 x 4096N.  One step = sketch of the local block (Omega regenerated from the seed, no
-    communication) -> all-gather of the k LUPP-visible sketch rows -> column LUPP on the full panel
-    (replicated, identical J_s on every rank) -> C = A(:, J_s) by a sum all-reduce -> column-ID
-    residual (local squared sums + all-reduce).  value = sketch + selection time, max over ranks."""
+    """N > 1 GPUs (torchrun): the column-sharded path of SURVEY 8(e) on the same C5 matrix
+    (strong scaling: rank r builds and holds only its contiguous block of A's 65536 columns, built
+    on its device from the same seed).  The library's distributed context (sk_create_dist, one
+    NCCL communicator owned by the library) does every exchange.  One step = sketch of the local
+    block (Gamma regenerated from the seed, no communication) -> column LUPP (exchange
+    "replicate": one all-gather of the k LUPP-visible sketch rows, then the cluster LUPP on
+    identical bytes; "step": one all-gather of P candidate records per pivot step, CUDA graph) ->
+    ID coefficients of the local columns -> column-ID residual (C by one all-gather, Q_C by
+    Cholesky QR over row blocks with k x k all-reduces, one all-reduce of the squared sums).
+    value = sketch + selection time, max over ranks."""
     import torch
     import torch.distributed as dist
 
     import paper_2104_05877_b200 as sk
-    from inputs import make_c2
-    from paper_2104_05877_b200.dist import _all_gather_cols
+    from paper_2104_05877_b200.dist import shard
 
-    dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)
-    k = args.k if args.k is not None else 512              # C2's bench k
-    l = k + 10
-    seed = 2002 + k
-    A_np, _ = make_c2(seed=1002 + rank)
-    m, nloc = A_np.shape
-    n_global = nloc * world
-    col0 = rank * nloc
+    cfg, k, l, seed, desc = workload(args)
+    if args.config != "C5":
+        raise SystemExit("the multi-GPU bench runs the column-sharded C5 workload (--config C5)")
+    from inputs import c5 as c5in
+    m, n = c5in.M5, c5in.N5
+    col0, ncols = shard(n, world, rank)
     with torch.cuda.stream(stream):
-        A = sk.fortran(torch.from_numpy(np.ascontiguousarray(A_np)).to(dev))
+        A, sigma = c5in.build_on_device(dev, col0=col0, ncols=ncols)
         flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
-        Xbuf = torch.empty((l, nloc), dtype=torch.float64, device=dev)
+        Xbuf = torch.empty((l, ncols), dtype=torch.float64, device=dev)
     torch.cuda.synchronize(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    cap = []
+    exchange = "step" if args.dist_exchange == "step" else "replicate"
+    with torch.cuda.stream(stream):
+        sess = sk.DistSession(n, None, local, exchange)
 
     def step(record):
         e = [ev() for _ in range(5)]
         e[0].record(stream)
         X = sk.sketch(A, l, "gaussian", seed, out=Xbuf)
         e[1].record(stream)
-        if args.dist_exchange == "step":
-            if not cap:
-                from paper_2104_05877_b200.dist import CapturedStepwise
-                cap.append(CapturedStepwise(Xbuf, n_global, k))
-            Js, _, _ = cap[0].run()
-        elif args.dist_exchange == "p2p":
-            if not cap:                      # mailboxes + one captured graph of begin + k steps
-                from paper_2104_05877_b200.dist import P2PStepwise
-                p2p = P2PStepwise(n_global, k, None, local)
-                p2p.run(Xbuf)
-                torch.cuda.synchronize(dev)
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    p2p.sel.begin(Xbuf)
-                    for t in range(1, k + 1):
-                        p2p.sel.step(t)
-                cap.append((p2p, g))
-            cap[0][1].replay()
-            Js = cap[0][0].sel.Js
-        else:
-            Xk = _all_gather_cols(X[:k], n_global, None, world)
-            Js, _, _, _ = sk.select_cols(Xk, k, check=False)
+        Js, Lf, _, _ = sk.select_cols(X, k, check=False)
         e[2].record(stream)
-        C = sk.gather_cols_shard(A, Js, col0)
-        Ct = C.t().contiguous()
-        dist.all_reduce(Ct)
+        Z, _ = sk.id_coeffs(Lf, Js)
         e[3].record(stream)
-        r2, a2 = sk.residual_cols(A, Ct.t())
-        sums = torch.tensor([r2, a2], dtype=torch.float64, device=dev)
-        dist.all_reduce(sums)
+        r, nA = sk.residual(A, Js, None, "col_id")
         e[4].record(stream)
         record(e)
-        return Js, sums
+        return Js, r, nA
 
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream), sess:
         for _ in range(args.warmup):
             step(lambda e: None)
         torch.cuda.synchronize(dev)
@@ -279,51 +348,46 @@ def main_dist(args, world, rank, local):
             torch.cuda.synchronize(dev)
         launches = sk.launch_count(local) - launches0
         dist.barrier()
+        e2e = None
+        if not args.no_e2e:   # sk_rand_lupp on the distributed context, each rank's block in host memory
+            e2e = c5_e2e(args, sk, A, m, ncols, k, l, seed, local, stream, ev, out[0])
+            v = torch.tensor([e2e["value"] if e2e.get("value") is not None else float("nan")], dtype=torch.float64,
+                             device=dev)
+            dist.all_reduce(v, op=dist.ReduceOp.MAX)
+            e2e["value"] = float(v[0])
+            e2e["h2d_bytes_per_step"] = int(m * n * 8)
+            e2e["api"] += f" on the column-sharded context, {world} ranks (host block per rank), max over ranks"
+    sess.close()
     sk_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in recs)
     sel_ms = statistics.mean(e[0].elapsed_time(e[2]) for e in recs)
     step_ms = statistics.mean(e[0].elapsed_time(e[4]) for e in recs)
-    t = torch.tensor([sel_ms, step_ms, sk_ms], dtype=torch.float64, device=dev)
+    stage = {"sketch": sk_ms, "select_cols_lupp": statistics.mean(e[1].elapsed_time(e[2]) for e in recs),
+             "id_coeffs": statistics.mean(e[2].elapsed_time(e[3]) for e in recs),
+             "residual": statistics.mean(e[3].elapsed_time(e[4]) for e in recs)}
+    t = torch.tensor([sel_ms, step_ms, sk_ms] + list(stage.values()), dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     sel_ms, step_ms, sk_ms_max = float(t[0]), float(t[1]), float(t[2])
-    Js, sums = out
-    achieved = 2.0 * l * m * nloc / (sk_ms * 1e-3) / 1e12
-    # end to end: pinned host block -> device (inside the timed region) -> sketch -> selection -> J_s on host
-    e2e = None
-    if not args.no_e2e:
-        A_host = torch.from_numpy(np.ascontiguousarray(A_np.T)).pin_memory()      # rows = columns of A
-        A_dev = torch.empty_like(A_host, device=dev)
-        times = []
-        with torch.cuda.stream(stream):
-            for it in range(2 + max(3, min(args.steps, 10))):
-                e0, e1 = ev(), ev()
-                e0.record(stream)
-                A_dev.copy_(A_host, non_blocking=True)
-                Ad = A_dev.t()
-                X = sk.sketch(Ad, l, "gaussian", seed)
-                Xk = _all_gather_cols(X[:k], n_global, None, world)
-                Js_d, _, _, _ = sk.select_cols(Xk, k, check=False)
-                Js_h = Js_d.cpu()
-                e1.record(stream)
-                e1.synchronize()
-                if it >= 2:
-                    times.append(e0.elapsed_time(e1))
-        t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(t[0]), "unit": "ms", "h2d_bytes_per_step": int(m * nloc * 8),
-               "d2h_bytes_per_step": int(k * 8), "api": "dist path (torch.distributed + libskel.so), host A block per rank"}
+    stage = dict(zip(stage, [float(x) for x in t[3:]]))
+    Js, r, nA = out
+    achieved = 2.0 * l * m * ncols / (sk_ms * 1e-3) / 1e12
     if rank == 0:
+        from oracle.residual import optimal_error
+        opt = optimal_error(sigma, k)
         line = {
             "metric": "skeleton-selection time (sketch+LUPP)", "value": sel_ms, "unit": "ms",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2-type blocks: A 4096 x {n_global} FP64 column-sharded, 4096 x 4096 "
-                                   f"U diag(10^(-i/50)) V^T per rank, Gaussian Omega, k={k}, l={l}",
-                       "m": m, "n": n_global, "k": k, "l": l, "parallelism": f"column-sharded x{world}", "lupp_exchange": args.dist_exchange,
-                       "l2": "flushed: 512 MiB overwrite between timed steps (untimed)"},
-            "residual": {"col_id_fro": math.sqrt(max(float(sums[0]), 0.0)), "normA_fro": math.sqrt(float(sums[1]))},
-            "roofline": {"kernel": "sk_sketch Gaussian = k_omega_image + k_sketch_pre (+ split-K reduce)", "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc + f", column-sharded over {world} GPUs", "m": m, "n": n, "k": k, "l": l,
+                       "parallelism": f"column-sharded x{world}", "lupp_exchange": exchange,
+                       "l2": "flushed: 512 MiB overwrite between timed steps (untimed); A (68.7 GB) >> L2"},
+            "stages_ms": stage,
+            "residual": {"col_id_fro": r, "normA_fro": nA, "opt_fro": opt, "col_id_ratio": r / opt},
+            "roofline": {"kernel": "sk_sketch Gaussian (k_omega_image + k_sketch_pre per K-chunk), rank 0's block",
+                         "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None},
-            "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "cpu_baseline": None,
+            "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -401,7 +465,7 @@ def main():
         res = {kind: sk.residual(A, Js, Is, kind) for kind in res_kinds}
         next(nxt).record(stream)
         record(e)
-        return Js, Jc, res
+        return Js, Jc, res, X
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -434,7 +498,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         value, ms_step = float(t[0]), float(t[1])
 
-    Js, Jc, res = out
+    Js, Jc, res, X_last = out
     from oracle.residual import optimal_error  # closed form sum_{i>k} sigma_i^2 (Eckart-Young)
     opt = optimal_error(sigma, k) if sigma is not None else None   # C4 has no closed-form spectrum
     resid = {"opt_fro": opt}
@@ -498,8 +562,19 @@ def main():
             e2e_v = float(t[0])
         e2e = {"value": e2e_v, "unit": "ms", "h2d_bytes_per_step": int(m * n * 8), "d2h_bytes_per_step": int(k * 8),
                "api": "sk_rand_lupp (host A, pinned) -> Js on host"}
+    elif not args.no_e2e and args.config == "C5" and args.piter == 0:
+        e2e = c5_e2e(args, sk, A, m, n, k, l, seed, local, stream, ev, Js)
 
     cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "C5":
+        cores, model = cpu_info()
+        At = A.t()
+        v, parts, Xb = c5_oracle_sample(lambda a, b: At[a:b].cpu().numpy().T, m, n, k, l, seed)
+        xg = X_last[:, :C5_SAMPLE_COLS].cpu().numpy()
+        cpu = {"value": v, "unit": "ms", "cores": cores, "kind": "oracle", "sample": c5_sample_desc(model),
+               "parts_ms": parts,
+               "sample_check": f"oracle X(:, 0:{C5_SAMPLE_COLS}) vs GPU: rel. Frobenius "
+                               f"{float(np.linalg.norm(xg - Xb) / np.linalg.norm(Xb)):.2e}"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and A_np is not None:
         cores, model = cpu_info()
         t0 = time.perf_counter()

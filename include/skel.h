@@ -82,6 +82,42 @@ typedef enum {
 sk_status sk_create(sk_ctx** ctx, int device, void* stream);
 /* Re-target the context to another stream of the same device. */
 sk_status sk_set_stream(sk_ctx* ctx, void* stream);
+/* ---- column-sharded (multi-GPU) context -------------------------------
+ * One process per GPU; A (m x n_global) is split into contiguous column blocks in rank order, this
+ * rank holding columns [col0, col0 + ncols) (ncols may be 0).  The context owns an NCCL
+ * communicator over the `world` ranks (NCCL resolved at run time from libnccl.so.2) and issues
+ * every exchange of the path itself, on the context's stream:
+ *   sk_sketch       unchanged: this rank's block, no communication (Gamma depends on the row index
+ *                   of A only, R1, so every rank regenerates the same Gamma).
+ *   sk_select_cols  X = this rank's l x ncols sketch block (n = ncols); Js, U, gaps replicated
+ *                   (GLOBAL column indices), Lf = this rank's ncols x k rows.  Exchange
+ *                   (sk_set_dist_exchange): 0 (default) one all-gather of the k LUPP-visible sketch
+ *                   rows then the single-GPU LUPP on identical bytes; 1 one all-gather of the
+ *                   ranks' candidate records per pivot step (the begin + k steps captured once in a
+ *                   CUDA graph owned by the context; gaps != NULL falls back to 0).  Both equal
+ *                   sk_select_cols on the unsharded sketch (ties to the lowest GLOBAL index, R6).
+ *   sk_gather_cols  A = this rank's block (n = ncols), Js global; C (m x k) = A_global(:, Js) on
+ *                   every rank (one all-gather of the owners' columns).  Synchronises.
+ *   sk_id_coeffs    Lf = this rank's rows (n = ncols); Z (k x ncols) = this rank's columns of Z;
+ *                   eta over all ranks.
+ *   sk_residual     A = this rank's block; res_fro / normA_fro over the whole A (all kinds): Q_C by
+ *                   Cholesky QR distributed over row blocks (one k x k all-reduce per pass), Q_R
+ *                   kept sharded with A's columns, one all-reduce of the squared sums.
+ *   sk_rand_lupp    A = this rank's block (device or host); Js / Is global, on every rank.
+ * Every rank must make the same sequence of calls (collectives).  Errors: SK_E_NCCL when NCCL
+ * cannot be loaded or a collective fails; SK_E_ARG when the ranks' blocks are not contiguous in
+ * rank order or do not cover [0, n_global). */
+#define SK_NCCL_UNIQUE_ID_BYTES 128
+/* Write a fresh NCCL unique id (SK_NCCL_UNIQUE_ID_BYTES bytes, host) -- on one rank, then share it. */
+sk_status sk_nccl_unique_id(void* out);
+/* Collective over the `world` ranks: create a column-sharded context on `device` / `stream`. */
+sk_status sk_create_dist(sk_ctx** ctx, int device, void* stream, const void* nccl_uid, int rank, int world,
+                         int64_t n_global, int64_t col0, int64_t ncols);
+/* Select the column-LUPP exchange of a distributed context: 0 gather-then-replicate, 1 per step. */
+sk_status sk_set_dist_exchange(sk_ctx* ctx, int32_t exchange);
+/* This context's place in the partition (world = 1, n_global = 0 for a single-GPU context). */
+sk_status sk_dist_info(const sk_ctx* ctx, int32_t* rank, int32_t* world, int64_t* n_global, int64_t* col0,
+                       int64_t* ncols);
 /* Release the workspace and the context (synchronises its stream). NULL is a no-op. */
 void sk_destroy(sk_ctx* ctx);
 /* Message of the last non-OK status returned through ctx ("" if none). Never NULL. */
@@ -96,9 +132,10 @@ int64_t sk_launch_count(const sk_ctx* ctx);
 /* ---- S0 + S1: sketch  (Algorithm 2 lines 1-2) ---------------- */
 
 /* X = Gamma A.  Gamma (l x m) is drawn from (emb, zeta, seed) on every call (Philox4x32-10,
- * R1-R4): the Gaussian one into a per-call workspace image consumed by the FP64 tensor-core GEMM
- * (~8 l m bytes; above 8 GB it is generated per tile instead and nothing is stored), the sparse-sign
- * structure into a per-call CSR (4 bytes per nonzero), SRTT's permutations and signs per CTA.
+ * R1-R4) and never held in HBM as a whole: the Gaussian one is generated one K-chunk of A's rows
+ * at a time into an L2-sized workspace slot (<= ~40 MB) that the FP64 tensor-core GEMM reads
+ * before the next chunk overwrites it; the sparse-sign structure goes into a per-call CSR
+ * (4 bytes per nonzero, values never stored), SRTT's permutations and signs are drawn per CTA.
  *   A   m x n column-major (lda >= m), read only.
  *   X   l x n row-major (ldx >= n), written.
  *   Requires 1 <= l <= m, n >= 0; for SK_EMB_SPARSE_SIGN 2 <= zeta <= min(l, 64)
@@ -106,6 +143,17 @@ int64_t sk_launch_count(const sk_ctx* ctx);
 sk_status sk_sketch(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
                     int64_t l, sk_embedding emb, int32_t zeta, uint64_t seed,
                     double* X, int64_t ldx);
+
+/* Tuning of the dense (Gaussian) sketch for this context; 0 everywhere = automatic (the default).
+ *   path        0 automatic (TMA + DMMA over K-chunks), 1 the fallback kernel that generates each
+ *               Gamma tile in shared memory (used automatically when A's layout rules out TMA),
+ *               2 / 3 the TMA path with K-splits summed through HBM partials / through the
+ *               distributed shared memory of a cluster of the splits
+ *   bm          CTA row-tile height: 0 or one of 32, 40, 48, 64
+ *   splits      K-splits per chunk (0 = planner, 1..64)
+ *   chunk_rows  rows of A per K-chunk, rounded up to 16 (0 = the largest whose Gamma slot fits ~40 MB)
+ * Results are identical up to summation order (parity tests use it to reach every plan). */
+sk_status sk_set_sketch_tuning(sk_ctx* ctx, int32_t path, int32_t bm, int32_t splits, int64_t chunk_rows);
 
 /* ---- column sketch for streaming two-sided selection (Algorithm 3) ----
  * Y = A Omega^T with Omega an l x n embedding drawn like sk_sketch's Gamma over the column index

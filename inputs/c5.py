@@ -53,10 +53,12 @@ def wy_operands(Y, Yp, sigma):
     return W, Z
 
 
-def build_on_device(device, seed=1005, m=M5, n=N5, b=B5, col_block=4096, factors_out=None):
-    """A (m x n) as a column-major float64 CUDA tensor (A.t() contiguous), plus sigma.
-    factors_out: optional list that receives (Y, Yp) for checks."""
+def build_on_device(device, seed=1005, m=M5, n=N5, b=B5, col_block=4096, factors_out=None, col0=0, ncols=None):
+    """A(:, col0 : col0 + ncols) (default: all n columns) as a column-major float64 CUDA tensor
+    (A.t() contiguous), plus sigma (all n).  The column block is what one rank of the column-sharded
+    multi-GPU path holds.  factors_out: optional list that receives (Y, Yp) for checks."""
     import torch
+    ncols = n - col0 if ncols is None else ncols
     Y, Yp, sigma = factors(seed, m, n, b)
     if factors_out is not None:
         factors_out.extend([Y, Yp])
@@ -66,15 +68,31 @@ def build_on_device(device, seed=1005, m=M5, n=N5, b=B5, col_block=4096, factors
     Wd = torch.from_numpy(W).to(device)
     Ypd = torch.from_numpy(Yp).to(device)
     sd = torch.from_numpy(sigma).to(device)
-    At = torch.empty((n, m), dtype=torch.float64, device=device)       # rows of At = columns of A
-    for j0 in range(0, n, col_block):
-        j1 = min(n, j0 + col_block)
+    At = torch.empty((ncols, m), dtype=torch.float64, device=device)   # rows of At = columns of A
+    for j0 in range(col0, col0 + ncols, col_block):
+        j1 = min(col0 + ncols, j0 + col_block)
         blk = -(Yd @ Wd[:, j0:j1]) - Zd @ Ypd[j0:j1].T                # m x (j1 - j0)
         idx = torch.arange(j0, j1, device=device)
         blk[idx, idx - j0] += sd[j0:j1]
-        At[j0:j1] = blk.t()
+        At[j0 - col0:j1 - col0] = blk.t()
         del blk
     return At.t(), sigma
+
+
+def build_block_host(j0, j1, seed=1005, m=M5, n=N5, b=B5, cache={}):
+    """A(:, j0:j1) in host memory (numpy), the same compact-WY formula as build_on_device: for the
+    CPU-only reference arm, which must not touch the GPU."""
+    key = (seed, m, n, b)
+    if key not in cache:
+        Y, Yp, sigma = factors(seed, m, n, b)
+        W, Z = wy_operands(Y, Yp, sigma)
+        cache.clear()
+        cache[key] = (Y, Yp, sigma, W, Z)
+    Y, Yp, sigma, W, Z = cache[key]
+    blk = -(Y @ W[:, j0:j1]) - Z @ Yp[j0:j1].T
+    idx = np.arange(j0, j1)
+    blk[idx, idx - j0] += sigma[j0:j1]
+    return blk
 
 
 def column_by_reflectors(j, Y, Yp, sigma):

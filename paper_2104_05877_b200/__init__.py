@@ -6,8 +6,8 @@ coefficients and the residual), as hand-written sm_100a kernels behind the C ABI
 include/skel.h (libskel.so) with this thin ctypes binding on top.
 """
 from .api import (  # noqa: F401
-    COL_ID, CUR, GAUSSIAN, ID_COEFFS, ROW_ID, SPARSE_SIGN, SkelError, context, fortran, gather_cols,
+    DistSession, COL_ID, CUR, GAUSSIAN, ID_COEFFS, ROW_ID, SPARSE_SIGN, SkelError, context, fortran, gather_cols,
     gather_cols_shard, id_coeffs, launch_count, rand_lupp, residual, residual_cols, select_cols, select_cols_cpqr, select_cols_deim,
     LuppDist, LuppDistP2P, ipc_alloc, ipc_close, ipc_export, ipc_free, ipc_import, mailbox_bytes, select_rows,
-    sketch, sketch_cols, sketch_power, stream_select,
+    set_sketch_tuning, sketch, sketch_cols, sketch_power, stream_select,
 )

@@ -17,6 +17,12 @@ STATUS_NAMES = {0: "SK_OK", 1: "SK_E_ARG", 2: "SK_E_RANK", 3: "SK_E_CUDA", 4: "S
 _SIGS = {
     "sk_create": [ctypes.POINTER(c_dp), c_int, c_dp],
     "sk_set_stream": [c_dp, c_dp],
+    "sk_set_sketch_tuning": [c_dp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_i64],
+    "sk_nccl_unique_id": [c_dp],
+    "sk_create_dist": [ctypes.POINTER(c_dp), c_int, c_dp, c_dp, c_int, c_int, c_i64, c_i64, c_i64],
+    "sk_set_dist_exchange": [c_dp, ctypes.c_int32],
+    "sk_dist_info": [c_dp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(c_i64),
+                     ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)],
     "sk_sketch": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64, c_dp, c_i64],
     "sk_sketch_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64, c_dp, c_i64],
     "sk_sketch_power": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64,

@@ -54,6 +54,65 @@ def context(device=None):
     return h
 
 
+class DistSession:
+    """A column-sharded library context (sk_create_dist) installed as this
+    device's context while the session is open: the library owns the NCCL communicator and every
+    call below (sketch, select_cols, gather_cols, id_coeffs, residual, rand_lupp) takes this rank's
+    column block and performs the exchanges itself.  The torch.distributed group is used once, to
+    share the NCCL unique id.  exchange: "replicate" (one all-gather of the k sketch rows LUPP
+    reads) or "step" (one all-gather of candidate records per pivot step, CUDA graph)."""
+
+    def __init__(self, n_global, group=None, device=None, exchange="replicate"):
+        import torch.distributed as tdist
+
+        from .dist import shard
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.rank = tdist.get_rank(group)
+        self.world = tdist.get_world_size(group)
+        self.n_global = n_global
+        self.col0, self.ncols = shard(n_global, self.world, self.rank)
+        uid = (ctypes.c_char * 128)()
+        if self.rank == 0:
+            st = lib().sk_nccl_unique_id(uid)
+            if st != 0:
+                raise SkelError(st, "sk_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+        obj = [bytes(uid)]
+        tdist.broadcast_object_list(obj, src=tdist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        ctypes.memmove(uid, obj[0], 128)
+        h = ctypes.c_void_p()
+        st = lib().sk_create_dist(ctypes.byref(h), self.dev.index,
+                                  ctypes.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream), uid, self.rank,
+                                  self.world, n_global, self.col0, self.ncols)
+        if st != 0:
+            raise SkelError(st, "sk_create_dist failed")
+        self.h = h
+        _check(lib().sk_set_dist_exchange(h, {"replicate": 0, "step": 1}[exchange]), h)
+        self._prev = None
+
+    def __enter__(self):
+        self._prev = _ctxs.get(self.dev.index)
+        _ctxs[self.dev.index] = self.h
+        return self
+
+    def __exit__(self, *exc):
+        if self._prev is not None:
+            _ctxs[self.dev.index] = self._prev
+        else:
+            _ctxs.pop(self.dev.index, None)
+        self._prev = None
+
+    def close(self):
+        if self.h:
+            lib().sk_destroy(self.h)
+            self.h = None
+
+
+def set_sketch_tuning(path=0, bm=0, splits=0, chunk_rows=0, device=None):
+    """sk_set_sketch_tuning: pin the dense sketch's plan on this device's context (0 = automatic)."""
+    h = context(device)
+    _check(lib().sk_set_sketch_tuning(h, int(path), int(bm), int(splits), ctypes.c_int64(int(chunk_rows))), h)
+
+
 def launch_count(device=None):
     return int(lib().sk_launch_count(context(device)))
 
@@ -136,7 +195,7 @@ def select_cols(X, k, want_factors=True, want_gaps=False, check=True):
     gaps = torch.empty(k, dtype=torch.float64, device=dev) if want_gaps else None
     info = ctypes.c_int64(0)
     h = context(dev.index)
-    st = lib().sk_select_cols(h, _ptr(X), l, n, max(X.stride(0), n), k, _ptr(Js), _ptr(Lf), n, _ptr(U), k,
+    st = lib().sk_select_cols(h, _ptr(X), l, n, max(X.stride(0), n, 1), k, _ptr(Js), _ptr(Lf), max(n, 1), _ptr(U), k,
                               _ptr(gaps), ctypes.byref(info) if check else None)
     _check(st, h, info.value)
     return Js, Lf, U, gaps

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libskel.so")
-SOURCES = ["capi.cu", "gemm.cu", "sketch.cu", "srtt.cu", "lupp.cu", "cpqr.cu", "dense.cu", "idcoef.cu", "residual.cu", "deim.cu", "lupp_dist.cu"]
+SOURCES = ["capi.cu", "gemm.cu", "sketch.cu", "srtt.cu", "lupp.cu", "cpqr.cu", "dense.cu", "idcoef.cu", "residual.cu", "deim.cu", "lupp_dist.cu", "dist.cu"]
 HEADERS = ["common.cuh", "dmma.cuh", "philox.cuh", "internal.h", "sync.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -63,7 +63,7 @@ def build(force=False, verbose=False):
             if out and verbose:
                 print(out)
     if force or jobs or _newer(LIB, objs):
-        cmd = [cc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcusolver"]
+        cmd = [cc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcusolver", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)

@@ -49,7 +49,6 @@ sk_status sk_create(sk_ctx** out, int device, void* stream) {
   if (!c) return SK_E_NOMEM;
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
-  if (const char* v = std::getenv("SKEL_SKETCH_LEGACY")) c->force_legacy_sketch = v[0] == '1';
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess)
@@ -86,6 +85,19 @@ sk_status sk_create(sk_ctx** out, int device, void* stream) {
   return SK_OK;
 }
 
+sk_status sk_set_sketch_tuning(sk_ctx* c, int32_t path, int32_t bm, int32_t splits, int64_t chunk_rows) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, path >= 0 && path <= 3, "sk_set_sketch_tuning: path must be 0..3");
+  SK_ARG(c, bm == 0 || bm == 32 || bm == 40 || bm == 48 || bm == 64, "sk_set_sketch_tuning: bm must be 0, 32, 40, 48 or 64");
+  SK_ARG(c, splits >= 0 && splits <= 64 && chunk_rows >= 0, "sk_set_sketch_tuning: bad splits / chunk_rows");
+  c->tune_sketch_path = path;
+  c->tune_sketch_bm = bm;
+  c->tune_sketch_splits = splits;
+  c->tune_sketch_chunk = chunk_rows;
+  return SK_OK;
+}
+
 sk_status sk_set_stream(sk_ctx* c, void* stream) {
   if (!c) return SK_E_ARG;
   c->stream = static_cast<cudaStream_t>(stream);
@@ -95,6 +107,7 @@ sk_status sk_set_stream(sk_ctx* c, void* stream) {
 void sk_destroy(sk_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
+  dist_destroy(c);
   if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
@@ -168,9 +181,19 @@ sk_status sk_select_cols(sk_ctx* c, const double* X, int64_t l, int64_t n, int64
   if (!c) return SK_E_ARG;
   c->err.clear();
   SK_ARG(c, X && Js, "sk_select_cols: NULL X or Js");
-  SK_ARG(c, k >= 1 && k <= l && k <= n && ldx >= n, "sk_select_cols: need 1 <= k <= min(l, n), ldx >= n");
   SK_ARG(c, !Lf || ldlf >= n, "sk_select_cols: ldlf >= n required");
   SK_ARG(c, !U || ldu >= k, "sk_select_cols: ldu >= k required");
+  if (dist_on(c)) {   // X is this rank's l x ncols block; Js / U / gaps replicated, Lf this rank's rows
+    const DistView v = dist_view(c);
+    SK_ARG(c, n == v.ncols && ldx >= std::max<int64_t>(n, 1) && k >= 1 && k <= l && k <= v.n_global,
+           "sk_select_cols (distributed): n must be this rank's ncols, 1 <= k <= min(l, n_global)");
+    SK_CUDA(c, cudaSetDevice(c->device));
+    DBuf st;
+    SK_TRY(st.alloc(c, sizeof(int64_t)));
+    SK_TRY(dist_select_cols(c, X, n, ldx, k, Js, Lf, ldlf, U, ldu, gaps, st.as<int64_t>()));
+    return finish_info(c, st.as<int64_t>(), info, "sk_select_cols (distributed)");
+  }
+  SK_ARG(c, k >= 1 && k <= l && k <= n && ldx >= n, "sk_select_cols: need 1 <= k <= min(l, n), ldx >= n");
   SK_CUDA(c, cudaSetDevice(c->device));
   DBuf st;
   SK_TRY(st.alloc(c, sizeof(int64_t)));
@@ -212,9 +235,13 @@ sk_status sk_gather_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64
                          int64_t k, double* C, int64_t ldc) {
   if (!c) return SK_E_ARG;
   c->err.clear();
-  SK_ARG(c, A && Js && C, "sk_gather_cols: NULL pointer");
+  SK_ARG(c, (A || (dist_on(c) && n == 0)) && Js && C, "sk_gather_cols: NULL pointer");
   SK_ARG(c, m >= 0 && n >= 0 && k >= 0 && lda >= m && ldc >= m, "sk_gather_cols: bad sizes");
   SK_CUDA(c, cudaSetDevice(c->device));
+  if (dist_on(c)) {   // A is this rank's block, Js global; C replicated (synchronises)
+    SK_ARG(c, n == dist_view(c).ncols, "sk_gather_cols (distributed): n must be this rank's ncols");
+    return dist_gather_cols(c, A, false, m, lda, Js, k, C, ldc);
+  }
   return gather_cols_shard(c, A, m, lda, 0, n, Js, k, C, ldc);   // Js outside [0, n): zero column
 }
 
@@ -385,12 +412,19 @@ sk_status sk_id_coeffs(sk_ctx* c, const double* Lf, int64_t n, int64_t k, int64_
                        double* Z, int64_t ldz, double* eta) {
   if (!c) return SK_E_ARG;
   c->err.clear();
-  SK_ARG(c, Lf && Js && Z, "sk_id_coeffs: NULL pointer");
-  SK_ARG(c, k >= 1 && k <= n && ldlf >= n && ldz >= k, "sk_id_coeffs: bad sizes");
+  SK_ARG(c, (Lf || (dist_on(c) && n == 0)) && Js && Z, "sk_id_coeffs: NULL pointer");
   SK_CUDA(c, cudaSetDevice(c->device));
   DBuf e;
   if (eta) SK_TRY(e.alloc(c, sizeof(double)));
-  SK_TRY(id_coeffs(c, Lf, n, k, ldlf, Js, Z, ldz, eta ? e.as<double>() : nullptr));
+  if (dist_on(c)) {   // Lf: this rank's rows (n = ncols), Z: this rank's columns; eta over all ranks
+    const DistView v = dist_view(c);
+    SK_ARG(c, n == v.ncols && k >= 1 && k <= v.n_global && ldlf >= std::max<int64_t>(n, 1) && ldz >= k,
+           "sk_id_coeffs (distributed): bad sizes");
+    SK_TRY(dist_id_coeffs(c, Lf, k, ldlf, Js, Z, ldz, eta ? e.as<double>() : nullptr));
+  } else {
+    SK_ARG(c, k >= 1 && k <= n && ldlf >= n && ldz >= k, "sk_id_coeffs: bad sizes");
+    SK_TRY(id_coeffs(c, Lf, n, k, ldlf, Js, Z, ldz, eta ? e.as<double>() : nullptr));
+  }
   if (eta) SK_TRY(to_host(c, eta, e.p, sizeof(double)));
   return SK_OK;
 }
@@ -400,8 +434,14 @@ sk_status sk_residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t 
                       double* res_fro, double* normA_fro) {
   if (!c) return SK_E_ARG;
   c->err.clear();
-  SK_ARG(c, A && res_fro, "sk_residual: NULL A or res_fro");
-  SK_ARG(c, m >= 1 && n >= 1 && lda >= m && k >= 1 && k <= m && k <= n, "sk_residual: bad sizes");
+  SK_ARG(c, (A || (dist_on(c) && n == 0)) && res_fro, "sk_residual: NULL A or res_fro");
+  if (dist_on(c)) {
+    const DistView v = dist_view(c);
+    SK_ARG(c, n == v.ncols && m >= 1 && lda >= m && k >= 1 && k <= m && k <= v.n_global,
+           "sk_residual (distributed): n must be this rank's ncols, 1 <= k <= min(m, n_global)");
+  } else {
+    SK_ARG(c, m >= 1 && n >= 1 && lda >= m && k >= 1 && k <= m && k <= n, "sk_residual: bad sizes");
+  }
   SK_ARG(c, kind >= SK_RES_COL_ID && kind <= SK_RES_ID_COEFFS, "sk_residual: unknown kind");
   const bool need_js = kind != SK_RES_ROW_ID, need_is = kind == SK_RES_ROW_ID || kind == SK_RES_CUR;
   SK_ARG(c, !need_js || Js, "sk_residual: Js required");
@@ -411,7 +451,8 @@ sk_status sk_residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t 
   DBuf sums, st;
   SK_TRY(sums.alloc(c, 2 * sizeof(double)));
   SK_TRY(st.alloc(c, sizeof(int64_t)));
-  SK_TRY(residual(c, A, m, n, lda, Js, Is, k, (int)kind, Z, ldz, sums.as<double>(), st.as<int64_t>()));
+  if (dist_on(c)) SK_TRY(dist_residual(c, A, m, lda, Js, Is, k, (int)kind, Z, ldz, sums.as<double>(), st.as<int64_t>()));
+  else SK_TRY(residual(c, A, m, n, lda, Js, Is, k, (int)kind, Z, ldz, sums.as<double>(), st.as<int64_t>()));
   int64_t info = 0;
   SK_TRY(finish_info(c, st.as<int64_t>(), &info, "sk_residual (basis of the skeleton)"));
   double h[2];
@@ -427,64 +468,80 @@ sk_status sk_rand_lupp(sk_ctx* c, const double* A, int a_on_host, int64_t m, int
   if (!c) return SK_E_ARG;
   c->err.clear();
   SK_ARG(c, A && Js, "sk_rand_lupp: NULL A or Js");
-  SK_ARG(c, m >= 1 && n >= 1 && lda >= m && l >= 1 && l <= m && k >= 1 && k <= l && k <= n,
-         "sk_rand_lupp: need 1 <= k <= l <= m, k <= n");
+  const bool dist = dist_on(c);
+  SK_ARG(c, m >= 1 && (n >= 1 || dist) && lda >= m && l >= 1 && l <= m && k >= 1 && k <= l &&
+                k <= (dist ? dist_view(c).n_global : n) && (!dist || n == dist_view(c).ncols),
+         "sk_rand_lupp: need 1 <= k <= l <= m, k <= n (distributed: n = this rank's ncols, k <= n_global)");
   SK_CUDA(c, cudaSetDevice(c->device));
-  DBuf Ad, Xd, Jd, Cd, Id, st;
-  const double* Adev = A;
-  int64_t ldad = lda;
+  DBuf Xd, Jd, Cd, Id, st;
   SK_TRY(Xd.alloc(c, (size_t)l * n * sizeof(double)));
   SK_TRY(Jd.alloc(c, (size_t)k * sizeof(int64_t)));
   SK_TRY(st.alloc(c, sizeof(int64_t)));
   if (a_on_host) {
-    // X = Gamma A is column-separable: the host->device copy of column block b+1 (on the aux
-    // stream) overlaps the sketch of block b (on the context stream).
-    SK_TRY(Ad.alloc(c, (size_t)m * n * sizeof(double)));
+    // A stays in host memory.  X = Gamma A is column-separable: column blocks of A stream through a
+    // ring of NR device slots -- the host->device copy of block b (helper stream) overlaps the sketch
+    // of block b-1 (context stream); a slot is refilled only after the sketch that read it is done.
+    // Device memory: NR slots of W columns (<= 2 GB each), not the whole of A.
+    constexpr int NR = 3;
+    const int64_t wmax = std::max<int64_t>(128, ((int64_t)(2.0 * (1 << 30) / (8.0 * (double)m)) / 128) * 128);
+    const int64_t W = std::min(wmax, std::max<int64_t>(128, cdiv(cdiv(n, 8), 128) * 128));
+    const int64_t nb = cdiv(n, W);
+    const int nr = (int)std::min<int64_t>(NR, nb);
+    DBuf slot[NR];
+    for (int r = 0; r < nr; ++r) SK_TRY(slot[r].alloc(c, (size_t)m * W * sizeof(double)));
     SK_TRY(ensure_aux(c));
-    Adev = Ad.as<double>();
-    ldad = m;
-    const int64_t nb = ((double)m * n * 8 >= 64.0 * (1 << 20) && n >= 1024) ? std::min<int64_t>(8, n / 256) : 1;
-    const int64_t W = cdiv(cdiv(n, nb), 128) * 128;
-    cudaEvent_t ev[9];
-    int nev = 0;
+    cudaEvent_t ev[2 * NR + 1] = {};
     sk_status rs = SK_OK;
-    auto mk = [&](cudaStream_t s) -> cudaEvent_t {
-      cudaEvent_t e = nullptr;
-      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-      ev[nev++] = e;
-      cudaEventRecord(e, s);
-      return e;
-    };
-    cudaEvent_t e0 = mk(c->stream);                        // Ad's allocation is ordered on the context stream
-    if (!e0 || cudaStreamWaitEvent(c->aux, e0, 0) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event");
-    for (int64_t j0 = 0; j0 < n && rs == SK_OK; j0 += W) {
-      const int64_t jw = std::min(W, n - j0);
-      if (cudaMemcpy2DAsync(Ad.as<double>() + j0 * m, (size_t)m * sizeof(double), A + j0 * lda,
-                            (size_t)lda * sizeof(double), (size_t)m * sizeof(double), (size_t)jw,
-                            cudaMemcpyHostToDevice, c->aux) != cudaSuccess) {
+    for (int e = 0; e < 2 * nr + 1 && rs == SK_OK; ++e)
+      if (cudaEventCreateWithFlags(&ev[e], cudaEventDisableTiming) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event");
+    cudaEvent_t* copied = ev;            // [nr]: block in slot r has landed
+    cudaEvent_t* consumed = ev + nr;     // [nr]: the sketch of the block in slot r is done
+    if (rs == SK_OK && (cudaEventRecord(ev[2 * nr], c->stream) != cudaSuccess ||      // slots allocated (stream order)
+                        cudaStreamWaitEvent(c->aux, ev[2 * nr], 0) != cudaSuccess))
+      rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event");
+    for (int64_t b = 0; b < nb && rs == SK_OK; ++b) {
+      const int r = (int)(b % nr);
+      const int64_t j0 = b * W, jw = std::min(W, n - j0);
+      double* dst = slot[r].as<double>();
+      if (b >= nr && cudaStreamWaitEvent(c->aux, consumed[r], 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event"); break; }
+      if (cudaMemcpy2DAsync(dst, (size_t)m * sizeof(double), A + j0 * lda, (size_t)lda * sizeof(double),
+                            (size_t)m * sizeof(double), (size_t)jw, cudaMemcpyHostToDevice, c->aux) != cudaSuccess ||
+          cudaEventRecord(copied[r], c->aux) != cudaSuccess || cudaStreamWaitEvent(c->stream, copied[r], 0) != cudaSuccess) {
         rs = fail(c, SK_E_CUDA, "sk_rand_lupp: host-to-device copy");
         break;
       }
-      cudaEvent_t eb = mk(c->aux);
-      if (!eb || cudaStreamWaitEvent(c->stream, eb, 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event"); break; }
-      rs = sk_sketch(c, Adev + j0 * m, m, jw, m, l, emb, zeta, seed, Xd.as<double>() + j0, n);
+      rs = sk_sketch(c, dst, m, jw, m, l, emb, zeta, seed, Xd.as<double>() + j0, n);
+      if (rs == SK_OK && cudaEventRecord(consumed[r], c->stream) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event");
     }
-    for (int e = 0; e < nev; ++e) cudaEventDestroy(ev[e]);
+    // (every copy was waited for by the context stream, so the slots are freed after their last use)
+    for (int e = 0; e < 2 * nr + 1; ++e)
+      if (ev[e]) cudaEventDestroy(ev[e]);
     SK_TRY(rs);
   } else {
-    SK_TRY(sk_sketch(c, Adev, m, n, ldad, l, emb, zeta, seed, Xd.as<double>(), n));
+    SK_TRY(sk_sketch(c, A, m, n, lda, l, emb, zeta, seed, Xd.as<double>(), n));
   }
-  SK_TRY(lupp(c, Xd.as<double>(), true, n, k, n, Jd.as<int64_t>(), nullptr, 0, nullptr, 0, nullptr,
-              st.as<int64_t>()));
+  if (dist) SK_TRY(dist_select_cols(c, Xd.as<double>(), n, std::max<int64_t>(n, 1), k, Jd.as<int64_t>(), nullptr, 0,
+                                    nullptr, 0, nullptr, st.as<int64_t>()));
+  else SK_TRY(lupp(c, Xd.as<double>(), true, n, k, n, Jd.as<int64_t>(), nullptr, 0, nullptr, 0, nullptr,
+                   st.as<int64_t>()));
   int64_t inf = 0;
   sk_status rc = finish_info(c, st.as<int64_t>(), &inf, "sk_rand_lupp (columns)");
   if (info) *info = inf;                                   // set on SK_E_RANK too (the failing step)
   SK_TRY(rc);
+  SK_TRY(to_host(c, Js, Jd.p, (size_t)k * sizeof(int64_t)));
   if (Is) {
     SK_ARG(c, k <= m, "sk_rand_lupp: k <= m required for row skeletons");
     SK_TRY(Cd.alloc(c, (size_t)m * k * sizeof(double)));
     SK_TRY(Id.alloc(c, (size_t)k * sizeof(int64_t)));
-    SK_TRY(gather_cols(c, Adev, m, ldad, Jd.as<int64_t>(), k, Cd.as<double>(), m));
+    if (dist) {          // C = A_global(:, J_s) assembled across ranks
+      SK_TRY(dist_gather_cols(c, A, a_on_host != 0, m, lda, Jd.as<int64_t>(), k, Cd.as<double>(), m));
+    } else if (a_on_host) {     // C = A(:, J_s) straight from the host columns (pivot order, R8)
+      for (int64_t t = 0; t < k; ++t)
+        SK_CUDA(c, cudaMemcpyAsync(Cd.as<double>() + t * m, A + Js[t] * lda, (size_t)m * sizeof(double),
+                                   cudaMemcpyHostToDevice, c->stream));
+    } else {
+      SK_TRY(gather_cols(c, A, m, lda, Jd.as<int64_t>(), k, Cd.as<double>(), m));
+    }
     SK_TRY(lupp(c, Cd.as<double>(), false, m, k, m, Id.as<int64_t>(), nullptr, 0, nullptr, 0, nullptr,
                 st.as<int64_t>()));
     rc = finish_info(c, st.as<int64_t>(), &inf, "sk_rand_lupp (rows)");
@@ -492,7 +549,6 @@ sk_status sk_rand_lupp(sk_ctx* c, const double* A, int a_on_host, int64_t m, int
     SK_TRY(rc);
     SK_TRY(to_host(c, Is, Id.p, (size_t)k * sizeof(int64_t)));
   }
-  SK_TRY(to_host(c, Js, Jd.p, (size_t)k * sizeof(int64_t)));
   return SK_OK;
 }
 

@@ -12,6 +12,8 @@
 #ifndef __CUDA_ARCH_LIST__
 #endif
 
+namespace skel { struct DistState; }
+
 struct sk_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -23,12 +25,16 @@ struct sk_ctx {
   int64_t ws_hwm = 0;       // high-water mark of pooled bytes
   // pinned host scratch for small device->host results (info, scalars)
   void* host_scratch = nullptr;
-  // A/B switch (env SKEL_SKETCH_LEGACY=1 at sk_create): use the cp.async sketch kernel
-  // instead of the TMA + cluster-shared-Omega one.
-  bool force_legacy_sketch = false;
+  // dense-sketch tuning (sk_set_sketch_tuning; 0 = automatic): path 1 = the fallback kernel that
+  // generates Omega tiles in shared memory; row-tile height, K-splits per chunk, rows per K-chunk
+  int tune_sketch_path = 0, tune_sketch_bm = 0, tune_sketch_splits = 0;
+  int64_t tune_sketch_chunk = 0;
   // lowest-priority helper stream + events for look-ahead overlap (LUPP trailing updates)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // column-sharded (distributed) context, sk_create_dist: this rank's block of A's columns and the
+  // library-owned NCCL communicator (dist.cu); nullptr for a single-GPU context
+  skel::DistState* dist = nullptr;
   // launches made while set carry programmatic stream serialization (PDL): the kernel may start
   // while its predecessor drains; every such kernel calls griddep_wait() before touching memory
   bool pdl = false;

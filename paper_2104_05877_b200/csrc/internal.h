@@ -119,4 +119,40 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
 sk_status residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* C, int64_t k,
                         int64_t ldc, double* sums_dev, int64_t* status_dev);
 
+// ---------------------------------------------------------------- column-sharded context (dist.cu)
+// A context made by sk_create_dist owns an NCCL communicator and this rank's column block
+// [col0, col0 + ncols) of an m x n_global A (partition of every rank known to all).
+struct DistView {
+  int rank = 0, world = 1;
+  int64_t n_global = 0, col0 = 0, ncols = 0;
+  int exchange = 0;   // 0 gather-then-replicate, 1 per-step all-gather (CUDA graph)
+};
+bool dist_on(const sk_ctx* c);
+DistView dist_view(const sk_ctx* c);
+void dist_destroy(sk_ctx* c);
+// in-place sum over ranks (count doubles) / all-gather of count doubles per rank, on the ctx stream
+sk_status dist_allreduce_sum(sk_ctx* c, double* buf, int64_t count);
+sk_status dist_allgather(sk_ctx* c, const double* send, double* recv, int64_t count);
+// S2 on this rank's sketch block X (l x ncols): Js replicated, Lf this rank's rows, U/gaps replicated
+sk_status dist_select_cols(sk_ctx* c, const double* X, int64_t ncols, int64_t ldx, int64_t k, int64_t* Js, double* Lf,
+                           int64_t ldlf, double* U, int64_t ldu, double* gaps, int64_t* status_dev);
+// S3: C = A_global(:, Js) replicated on every rank (synchronises: reads Js on the host).  A is this
+// rank's block (device, or host when a_on_host).
+sk_status dist_gather_cols(sk_ctx* c, const double* A, bool a_on_host, int64_t m, int64_t lda, const int64_t* Js,
+                           int64_t k, double* C, int64_t ldc);
+// S5 on this rank's rows of Lf: Z (k x ncols) for this rank's columns; eta over all ranks
+sk_status dist_id_coeffs(sk_ctx* c, const double* Lf, int64_t k, int64_t ldlf, const int64_t* Js, double* Z,
+                         int64_t ldz, double* eta_dev);
+// S6: squared sums over all ranks of the residual of `kind` and of A (sums_dev[2])
+sk_status dist_residual(sk_ctx* c, const double* A, int64_t m, int64_t lda, const int64_t* Js, const int64_t* Is,
+                        int64_t k, int kind, const double* Z, int64_t ldz, double* sums_dev, int64_t* status_dev);
+// G <- G + s I, the shift of shifted CholeskyQR3 for a basis of `rows` rows (residual.cu)
+sk_status add_shift(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t rows);
+// ID-coefficient pieces shared with the distributed path (idcoef.cu): L1 = Lf(Js - off, :) with rows
+// outside [0, nrows) zero; Z = Y^T with Z(:, Js - off) = I and those rows of Y zeroed; eta from Y^T Y
+sk_status id_l1(sk_ctx* c, const double* Lf, int64_t nrows, int64_t ldlf, const int64_t* Js, int64_t k, int64_t off,
+                double* L1);
+sk_status id_finish(sk_ctx* c, double* Y, int64_t nrows, int64_t k, const int64_t* Js, int64_t off, double* Z,
+                    int64_t ldz);
+
 }  // namespace skel

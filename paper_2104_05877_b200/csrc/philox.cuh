@@ -1,7 +1,7 @@
 // philox.cuh -- device-side counter-based generation of the embedding Gamma.
 //
-// Gamma is never stored in HBM: every kernel that needs Gamma(r, i) regenerates
-// it from (seed, r, i).  Counter layout = DESIGN.md readings R1/R2 (the paper
+// Gamma is never held in HBM as a whole: every kernel that needs Gamma(r, i) regenerates it from
+// (seed, r, i) -- the dense sketch one K-chunk at a time into an L2-sized slot (sketch.cu).  Counter layout = DESIGN.md readings R1/R2 (the paper
 // only fixes the distributions, P:176 Gaussian N(0,1/l), P:182 sparse sign):
 //   Gaussian pair p of column i:  Philox4x32-10(ctr = (i lo, i hi, p, 'GAUS'), key = seed)
 //       u1 = U53(w0, w1), u2 = U53(w2, w3);  z_{2p} = r cos(2 pi u2), z_{2p+1} = r sin(2 pi u2),

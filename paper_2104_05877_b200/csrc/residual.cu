@@ -27,6 +27,11 @@ __global__ void k_add_shift(double* G, int64_t k, int64_t ld, int64_t rows) {
   for (int64_t i = threadIdx.x; i < k; i += blockDim.x) G[i + i * ld] += s;
 }
 
+sk_status add_shift(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t rows) {
+  k_add_shift<<<1, 1024, 0, c->stream>>>(G, k, ld, rows);
+  return launched(c);
+}
+
 // Columns of C whose row LUPP does not fit one cluster (rows > 16 x 256): shifted CholeskyQR3.
 static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q,
                                        int64_t* status_dev) {

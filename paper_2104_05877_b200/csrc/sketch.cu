@@ -1,14 +1,14 @@
 // sketch.cu -- S0+S1 (dense Gaussian sketch) and S1' (sparse-sign sketch):  X = Gamma A.
 //
 // Paper: Algorithm 2 lines 1-2; embeddings P:176 (Gaussian)
-// (sparse sign, zeta = min(l, 8)); costs Table 1.  Gamma is regenerated
-// tile by tile from the Philox counter (philox.cuh) and never written to HBM.
+// (sparse sign, zeta = min(l, 8)); costs Table 1.  Gamma is regenerated from the
+// Philox counter (philox.cuh) on every call and never held in HBM as a whole.
 //
-// Dense: a DMMA GEMM with M = l (rows of Gamma), N = n, K = m.  CTA tile 32 x 256 x 16,
-// 256 threads (8 warps along N, 32 x 32 each).  The Gamma tile (32 x 16 = 256 Box-Muller
-// pairs) is generated by the CTA into shared memory once per K-step and reused by all 256
-// columns; the A tile streams through a 3-stage cp.async pipeline.  Split-K with a
-// fixed-order reduction when the tile grid is smaller than the machine.
+// Dense: a DMMA GEMM with M = l (rows of Gamma), N = n, K = m, run over K-chunks of A's rows:
+// per chunk k_omega_image generates that chunk's columns of Gamma (<= ~40 MB, an L2-resident
+// slot reused chunk after chunk) in the layout the GEMM's bulk copies read, and k_sketch_pre
+// (TMA + DMMA) accumulates Gamma(:, chunk) A(chunk, :) into X.  A fallback kernel for A that
+// the tensor map cannot describe (odd lda, misaligned) generates each Gamma tile in shared memory.
 //
 // Sparse sign: X(r, j) = zeta^{-1/2} sum_{i : r in S_i} s_{i,r} A(i, j).  A CTA owns 32
 // columns (lane = column) and all l rows; per chunk of 128 rows of A it stages the A tile
@@ -48,7 +48,8 @@ struct DenseParams {
   double* X; int64_t ldx;
   double* part;          // split-K partials [splits][l][n] (row-major, ld n)
   int64_t k_per_split;
-  int dbg;               // experiments only (env SKEL_SKETCH_DBG): 1 = no Box-Muller, 2 = no DMMA
+  int64_t k0;            // first row of A in this K-chunk (rows k0 .. m-1 of A; m = the chunk's end)
+  int accum;             // 1: X += the chunk's product (chunks after the first), 0: X = it
 };
 
 template <bool VEC>
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(DNT, 1) k_sketch_dense(DenseParams p) {
 // they are in flight together.
 template <int U>
 __global__ void k_sketch_splitk_reduce(const double* __restrict__ part, int splits, int l, int64_t n, double scale,
-                                       double* __restrict__ X, int64_t ldx) {
+                                       double* __restrict__ X, int64_t ldx, int accum) {
   dev::griddep_wait();                                   // PDL: the partials are complete
   const int64_t total = (int64_t)l * n;
   for (int64_t r = blockIdx.y; r < l; r += gridDim.y)
@@ -196,14 +197,14 @@ __global__ void k_sketch_splitk_reduce(const double* __restrict__ part, int spli
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t col = c0 + (int64_t)u * blockDim.x;
-        if (col < n) X[r * ldx + col] = s[u] * scale;
+        if (col < n) X[r * ldx + col] = accum ? X[r * ldx + col] + s[u] * scale : s[u] * scale;
       }
     }
 }
 
 // 4 columns per thread for wide X (whole 1024-column blocks, two CTAs per SM), else 1
 inline sk_status splitk_reduce(sk_ctx* c, const double* part, int splits, int64_t l, int64_t n, double scale, double* X,
-                               int64_t ldx) {
+                               int64_t ldx, int accum = 0) {
   const unsigned gy = (unsigned)std::min<int64_t>(l, 65535);
   const bool wide = n >= 2048 && (int64_t)gy * cdiv(n, 1024) >= 2LL * c->num_sms;
   cudaLaunchConfig_t lc{};
@@ -214,232 +215,27 @@ inline sk_status splitk_reduce(sk_ctx* c, const double* part, int splits, int64_
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;    // PDL behind the GEMM
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at; lc.numAttrs = 1;
-  if (wide) SK_CUDA(c, cudaLaunchKernelEx(&lc, k_sketch_splitk_reduce<4>, part, splits, (int)l, n, scale, X, ldx));
-  else SK_CUDA(c, cudaLaunchKernelEx(&lc, k_sketch_splitk_reduce<1>, part, splits, (int)l, n, scale, X, ldx));
+  if (wide) SK_CUDA(c, cudaLaunchKernelEx(&lc, k_sketch_splitk_reduce<4>, part, splits, (int)l, n, scale, X, ldx, accum));
+  else SK_CUDA(c, cudaLaunchKernelEx(&lc, k_sketch_splitk_reduce<1>, part, splits, (int)l, n, scale, X, ldx, accum));
   return launched(c);
 }
 
-// ============================================================ dense sketch, TMA + cluster-shared Omega
-// Warp-specialised: TCW consumer warps (DMMA, CTA tile BM x 256; 8 warps along n x TCW/8 along l,
-// warp tile WR x 32 -- 16 warps of 16 x 32 for BM = 32 so 4 DMMA warps per SMSP hide latency),
-// then 4 Omega producer warps.  Two independent rings:
-//   A ring (TSA stages, CTA-local): 16 rows of m x 256 columns of A by TMA with the 128-byte
-//     swizzle, issued by lane 0 of warp 0 up to a full ring ahead.
-//       fullA[s]  1 arrive (expect_tx = 32 KB) + the TMA bytes;  emptyA[s]  8 local warp arrivals
-//   Omega ring (TSO stages, cluster-shared): the Omega tile (BM rows x 16 columns of m) is
-//     generated ONCE per cluster -- the CS CTAs of a cluster lie along n and share Omega; each
-//     generates 16/CS of the tile's columns and st.async's them into every peer's slot.
-//       fullO[s]  1 local arrive (expect_tx = Omega bytes) + the peers' st.async bytes
-//       emptyO[s] 8*CS consumer-warp arrivals (every CTA's consumers release every CTA's slot)
-// The Omega ring is deep (Omega tiles are small) so producer jitter and the skew between the
-// CTAs of a cluster are absorbed without coupling the A ring across CTAs.  Producers compute
-// their Box-Muller chains for a group of stages into registers first (branch-free, interleaved
-// -- each chain is latency bound behind the consumers' DMMAs on the shared FP64 pipe), then
-// wait for the slots and store.
-// B-fragment bank conflicts under the swizzle are avoided by permuting the 8 logical MMA
-// columns onto physical columns sig(g) = 2(g&3) + (g>>2) (half-warps then hit disjoint
-// 16-byte chunks); the epilogue applies the same permutation.
-constexpr int TBN = 256, TBK = 16;
-constexpr int TPW = 4;                                        // Omega producer warps
-constexpr int T_A_BYTES = TBN * TBK * 8;                      // 32 KB, 1024-aligned
-template <int BM> struct TCfg {
-  static constexpr int OS = BM + 4;                           // Omega tile Os[k][r] stride (= 4 mod 16)
-  static constexpr int O_BYTES = TBK * OS * 8;
-  static constexpr int O_TX = TBK * BM * 8;                   // Omega bytes delivered per stage
-  static constexpr int TCW = 8;                               // consumer warps along n (16 measured slower at BM=32)
-  static constexpr int NT = (TCW + TPW) * 32;
-  static constexpr int WR = BM / (TCW / 8);                   // rows per consumer warp
-  static constexpr int TSA = BM == 64 ? 4 : 5;                // A ring
-  static constexpr int TSO = BM == 64 ? 10 : 12;              // Omega ring
-  static constexpr int BAR = 2 * (TSA + TSO) * 8;
-  static constexpr size_t SMEM = (size_t)TSA * T_A_BYTES + (size_t)TSO * O_BYTES + BAR + 1024;
-};
+// ============================================================ dense sketch helpers
+constexpr int TBK = 16;                                       // k rows (of A) per pipeline stage
 
+// B-fragment bank conflicts under the 128-byte swizzle are avoided by permuting the 8 logical MMA
+// columns onto physical columns sig(g) = 2(g&3) + (g>>2) (half-warps then hit disjoint 16-byte
+// chunks); the epilogue applies the same permutation.
 __device__ __forceinline__ int sig8(int g) { return 2 * (g & 3) + (g >> 2); }
 
 __device__ __forceinline__ void mbar_arrive_local(unsigned addr) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
 }
 
-template <int BM, int CS, bool SPLIT>
-__global__ void __launch_bounds__(TCfg<BM>::NT, 1) k_sketch_tma(const __grid_constant__ CUtensorMap tmA, DenseParams p) {
-  using C = TCfg<BM>;
-  constexpr int TSA = C::TSA, TSO = C::TSO;
-  constexpr int TCW = C::TCW;
-  constexpr int FI = C::WR / 8;                               // row fragments per warp
-  extern __shared__ __align__(1024) unsigned char tsm_raw[];
-  unsigned char* base = tsm_raw + ((1024u - (dev::smem_addr(tsm_raw) & 1023u)) & 1023u);   // stays __shared__
-  const unsigned base_u = dev::smem_addr(base);
-  const double* Osm = reinterpret_cast<const double*>(base + TSA * T_A_BYTES);
-  const unsigned a_u = base_u;                                  // A ring      [TSA][32 KB]
-  const unsigned o_u = base_u + TSA * T_A_BYTES;                // Omega ring  [TSO][O_BYTES]
-  const unsigned fullA = o_u + TSO * C::O_BYTES;                // mbarriers
-  const unsigned emptyA = fullA + 8 * TSA;
-  const unsigned fullO = emptyA + 8 * TSA;
-  const unsigned emptyO = fullO + 8 * TSO;
-
-  constexpr unsigned ncta = CS;
-  const unsigned crank = dev::cluster_ctarank();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int r0 = blockIdx.x * BM;
-  const int64_t n0 = (int64_t)blockIdx.y * TBN;
-  const int64_t kbeg = (int64_t)blockIdx.z * p.k_per_split;
-  const int64_t kend = min(p.m, kbeg + p.k_per_split);
-  const int ktiles = (int)((kend - kbeg + TBK - 1) / TBK);
-  const bool has_cols = n0 < p.n;
-
-  if (tid == 0) {
-    for (int s = 0; s < TSA; ++s) {
-      dev::mbar_init(fullA + 8 * s, 1);
-      dev::mbar_init(emptyA + 8 * s, TCW);
-    }
-    for (int s = 0; s < TSO; ++s) {
-      dev::mbar_init(fullO + 8 * s, 1);
-      dev::mbar_init(emptyO + 8 * s, TCW * ncta);
-    }
-    dev::fence_mbar_init_cluster();
-    dev::prefetch_tmap(&tmA);
-  }
-  __syncthreads();
-  dev::cluster_arrive();
-  dev::cluster_wait();
-
-  if (warp >= TCW) {
-    // ------------------------------------------------------------ Omega producers
-    constexpr int NP = TPW * 32;
-    constexpr int cols = TBK / CS;                    // Omega columns generated by this CTA
-    constexpr int npairs = cols * (BM / 2);           // pairs per stage generated by this CTA
-    constexpr int PPS = (npairs + NP - 1) / NP;       // pairs per thread per stage
-    constexpr int TG = PPS >= 4 ? 1 : 4 / PPS;        // stages per group: TG * PPS = 4 chains in flight
-    const int ptid = tid - TCW * 32;
-    for (int kg = 0; kg < ktiles; kg += TG) {
-      double z[TG][PPS][2];
-#pragma unroll
-      for (int u = 0; u < TG; ++u) {
-#pragma unroll
-        for (int h = 0; h < PPS; ++h) {
-          const int kt = kg + u, e = ptid + h * NP;
-          const int kc = (int)crank * cols + e / (BM / 2);
-          const int pr = e % (BM / 2);
-          const int64_t i = kbeg + (int64_t)kt * TBK + kc;
-          const int row = r0 + 2 * pr;
-          double z0 = 1.0, z1 = 1.0;
-          if (p.dbg != 1) dev::gauss_pair((uint64_t)i, (uint32_t)(row >> 1), p.key, z0, z1);
-          const bool ok = kt < ktiles && (npairs % NP == 0 || e < npairs) && i < kend && row < p.l;
-          z[u][h][0] = ok ? z0 : 0.0;
-          z[u][h][1] = (ok && row + 1 < p.l) ? z1 : 0.0;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < TG; ++u) {
-        const int kt = kg + u;
-        if (kt >= ktiles) break;
-        const int s = kt % TSO;
-        if (kt >= TSO) dev::mbar_wait(emptyO + 8 * s, ((unsigned)(kt / TSO) & 1u) ^ 1u);
-        if (ptid == 0) dev::mbar_arm(fullO + 8 * s, C::O_TX);
-#pragma unroll
-        for (int h = 0; h < PPS; ++h) {
-          const int e = ptid + h * NP;
-          if (npairs % NP == 0 || e < npairs) {
-            const int kc = (int)crank * cols + e / (BM / 2);
-            const int pr = e % (BM / 2);
-            const unsigned dst = o_u + s * C::O_BYTES + (unsigned)(kc * C::OS + 2 * pr) * 8u;
-#pragma unroll
-            for (unsigned c = 0; c < ncta; ++c)
-              dev::st_async_v2f(dev::mapa(dst, c), z[u][h][0], z[u][h][1], dev::mapa(fullO + 8 * s, c));
-          }
-        }
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ consumers
-    const int g = lane >> 2, q = lane & 3;
-    const int wn = (warp & 7) * 32;
-    const int wm = (warp >> 3) * C::WR;
-    const int sg = sig8(g);
-    double acc[FI][4][2];
-#pragma unroll
-    for (int i = 0; i < FI; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    // Lane 0 of warp 0 issues the A-tile TMAs: before waiting for stage kt it makes sure TMA(kt)
-    // is issued (blocking on the slot if needed) and probes, without blocking, for free slots up
-    // to kt + TSA - 1, so loads run up to a full ring ahead of the math.
-    int tma_next = 0;
-    auto issue_tma = [&](int upto, bool block) {
-      while (tma_next < upto && tma_next < ktiles) {
-        const int kq = tma_next, sq = kq % TSA;
-        if (kq >= TSA) {
-          const unsigned par = ((unsigned)(kq / TSA) & 1u) ^ 1u;
-          if (block) dev::mbar_wait(emptyA + 8 * sq, par);
-          else if (!dev::mbar_test(emptyA + 8 * sq, par)) break;
-        }
-        dev::mbar_arm(fullA + 8 * sq, T_A_BYTES);
-        dev::tma_load_2d(a_u + sq * T_A_BYTES, &tmA, (int)(kbeg + (int64_t)kq * TBK), (int)n0, fullA + 8 * sq);
-        ++tma_next;
-      }
-    };
-    const bool tma_thread = tid == 0 && has_cols;
-    for (int kt = 0; kt < ktiles; ++kt) {
-      const int sa = kt % TSA, so = kt % TSO;
-      if (tma_thread) {
-        issue_tma(kt + 1, true);
-        issue_tma(kt + TSA, false);
-      }
-      __syncwarp();
-      dev::mbar_wait(fullO + 8 * so, (unsigned)(kt / TSO) & 1u);
-      if (has_cols) {
-        dev::mbar_wait(fullA + 8 * sa, (unsigned)(kt / TSA) & 1u);
-        if (p.dbg == 2) goto skip_mma;
-        const double* Os = Osm + (size_t)so * (C::O_BYTES / 8) + q * C::OS + wm + g;
-        const unsigned char* At = base + (size_t)sa * T_A_BYTES + (wn + sg) * 128 + ((q & 1) << 3);
-#pragma unroll
-        for (int kk = 0; kk < TBK / 4; ++kk) {
-          double a[FI], b[4];
-#pragma unroll
-          for (int i = 0; i < FI; ++i) a[i] = Os[kk * 4 * C::OS + i * 8];
-          const int inrow = ((2 * kk + (q >> 1)) ^ sg) << 4;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const double*>(At + j * 8 * 128 + inrow);
-#pragma unroll
-          for (int i = 0; i < FI; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dev::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-        }
-      }
-    skip_mma:
-      __syncwarp();
-      if (lane == 0 && has_cols) mbar_arrive_local(emptyA + 8 * sa);
-      if (lane < (int)ncta) dev::mbar_arrive_remote(dev::mapa(emptyO + 8 * so, (unsigned)lane));
-    }
-    if (has_cols) {
-      const int c0 = sig8(2 * q), c1 = sig8(2 * q + 1);
-#pragma unroll
-      for (int i = 0; i < FI; ++i) {
-        const int r = r0 + wm + i * 8 + g;
-        if (r >= p.l) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t cb = n0 + wn + j * 8;
-          if (SPLIT) {
-            double* dst = p.part + ((int64_t)blockIdx.z * p.l + r) * p.n;
-            if (cb + c0 < p.n) dst[cb + c0] = acc[i][j][0];
-            if (cb + c1 < p.n) dst[cb + c1] = acc[i][j][1];
-          } else {
-            double* dst = p.X + (int64_t)r * p.ldx;
-            if (cb + c0 < p.n) dst[cb + c0] = acc[i][j][0] * p.scale;
-            if (cb + c1 < p.n) dst[cb + c1] = acc[i][j][1] * p.scale;
-          }
-        }
-      }
-    }
-  }
-  dev::cluster_arrive();   // no CTA leaves while peers may still write into it
-  dev::cluster_wait();
-}
-
-// ------------------------------------------------------------ dense sketch, pre-generated Omega
-// Omega is generated ONCE per call (k_omega_image, ~l*m/2 Box-Muller pairs) into an HBM/L2 image
+// ------------------------------------------------------------ dense sketch, K-chunked Omega image
+// Omega is generated once per call, one K-chunk at a time (k_omega_image, ~l*chunk/2 Box-Muller
+// pairs per chunk), into a slot of at most kOmegaSlotBytes that stays in L2 and is reused by
+// the next chunk -- the whole l x m Omega never exists in memory.  The slot is
 // laid out exactly as the consumers read it: per (row tile rt, k tile kt) a [TBK][OS] block,
 // OS = BM + 4 (= 4 mod 16: the 8x4 DMMA A-fragment loads are conflict-free).  k_sketch_pre is then
 // a plain TMA-fed DMMA GEMM X = Omega A with no generation inside: per stage one 1-D bulk copy of
@@ -462,7 +258,7 @@ template <int BM, int NW> struct PCfg {
 
 // One CTA per image block (row tile rt, k tile kt): blockIdx.x = rt * KT + kt, so no 64-bit
 // division per element; pair e of the block -> column kk = e / (OS/2), rows 2 pr, 2 pr + 1.
-__global__ void __launch_bounds__(128) k_omega_image(uint2 key, int l, int64_t m, int BM, int OS, int64_t KT,
+__global__ void __launch_bounds__(128) k_omega_image(uint2 key, int l, int64_t i0, int64_t m, int BM, int OS, int64_t KT,
                                                      double* __restrict__ img) {
   const int64_t tile = blockIdx.x;
   const int64_t rt = tile / KT, kt = tile - (tile / KT) * KT;
@@ -470,7 +266,7 @@ __global__ void __launch_bounds__(128) k_omega_image(uint2 key, int l, int64_t m
   double2* blk = reinterpret_cast<double2*>(img + tile * (int64_t)(TBK * OS));
   for (int e = threadIdx.x; e < np; e += 128) {
     const int kk = e / hp, pr = e - kk * hp;
-    const int64_t i = kt * TBK + kk;
+    const int64_t i = i0 + kt * TBK + kk;           // row of A (column of Omega); m = the chunk's end
     const int row = (int)(rt * BM) + 2 * pr;
     double z0 = 0.0, z1 = 0.0;
     if (2 * pr < BM && i < m && row < l) {
@@ -484,14 +280,14 @@ __global__ void __launch_bounds__(128) k_omega_image(uint2 key, int l, int64_t m
 // The same image from a GIVEN Omega: Omega(r, i) = Q(i, r), Q m x l column-major (ld ldq), e.g. an
 // orthonormal basis for W = Q^T A in the residual.  One CTA per image block; thread -> (kk, r) with
 // kk fastest, so a warp reads 128-byte column segments of Q.
-__global__ void __launch_bounds__(128) k_omega_pack(const double* __restrict__ Q, int64_t ldq, int l, int64_t m, int BM,
-                                                    int OS, int64_t KT, double* __restrict__ img) {
+__global__ void __launch_bounds__(128) k_omega_pack(const double* __restrict__ Q, int64_t ldq, int l, int64_t i0, int64_t m,
+                                                    int BM, int OS, int64_t KT, double* __restrict__ img) {
   const int64_t tile = blockIdx.x;
   const int64_t rt = tile / KT, kt = tile - (tile / KT) * KT;
   double* blk = img + tile * (int64_t)(TBK * OS);
   for (int e = threadIdx.x; e < TBK * OS; e += 128) {
     const int kk = e % TBK, r = e / TBK;
-    const int64_t i = kt * TBK + kk;
+    const int64_t i = i0 + kt * TBK + kk;
     const int64_t row = rt * BM + r;
     blk[kk * OS + r] = (r < BM && row < l && i < m) ? Q[i + row * ldq] : 0.0;
   }
@@ -519,10 +315,10 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rt = blockIdx.x;
   const int64_t n0 = (int64_t)blockIdx.y * C::TBNP;
-  const int64_t kbeg = (int64_t)blockIdx.z * p.k_per_split;
+  const int64_t kbeg = p.k0 + (int64_t)blockIdx.z * p.k_per_split;
   const int64_t kend = min(p.m, kbeg + p.k_per_split);
   const int ktiles = (int)((kend - kbeg + TBK - 1) / TBK);
-  const int64_t kt0 = kbeg / TBK;
+  const int64_t kt0 = (kbeg - p.k0) / TBK;              // k tile within the chunk's Omega image
   if (tid == 0) {
     for (int s = 0; s < TS; ++s) {
       dev::mbar_init(fullB + 8 * s, 1);
@@ -620,7 +416,10 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
       }
       const int r = rt * BM + rl;
       const int64_t cn = n0 + col;
-      if (r < p.l && cn < p.n) p.X[(int64_t)r * p.ldx + cn] = sum * p.scale;
+      if (r < p.l && cn < p.n) {
+        double* dst = p.X + (int64_t)r * p.ldx + cn;
+        *dst = p.accum ? *dst + sum * p.scale : sum * p.scale;
+      }
     }
     dev::cluster_arrive();                                  // no CTA leaves while peers read it
     dev::cluster_wait();
@@ -640,8 +439,13 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
         if (cb + c1 < p.n) dst[cb + c1] = acc[i][j][1];
       } else {
         double* dst = p.X + (int64_t)r * p.ldx;
-        if (cb + c0 < p.n) dst[cb + c0] = acc[i][j][0] * p.scale;
-        if (cb + c1 < p.n) dst[cb + c1] = acc[i][j][1] * p.scale;
+        if (p.accum) {
+          if (cb + c0 < p.n) dst[cb + c0] += acc[i][j][0] * p.scale;
+          if (cb + c1 < p.n) dst[cb + c1] += acc[i][j][1] * p.scale;
+        } else {
+          if (cb + c0 < p.n) dst[cb + c0] = acc[i][j][0] * p.scale;
+          if (cb + c1 < p.n) dst[cb + c1] = acc[i][j][1] * p.scale;
+        }
       }
     }
   }
@@ -1117,134 +921,15 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
-using TmaFn = void (*)(const CUtensorMap, DenseParams);
-template <int BM, int CS> TmaFn tma_fn(bool split) { return split ? k_sketch_tma<BM, CS, true> : k_sketch_tma<BM, CS, false>; }
-TmaFn pick_tma_fn(int bm, int cs, bool split) {
-  if (bm == 64) return cs == 4 ? tma_fn<64, 4>(split) : cs == 2 ? tma_fn<64, 2>(split) : tma_fn<64, 1>(split);
-  return cs == 4 ? tma_fn<32, 4>(split) : cs == 2 ? tma_fn<32, 2>(split) : tma_fn<32, 1>(split);
-}
-
-// Co-resident clusters of the TMA sketch per (BM, cluster size), queried once per process.
-int tma_max_clusters(int bm, int cs) {
-  static int cached[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  const int bi = bm == 64 ? 1 : 0, li = cs == 4 ? 2 : cs == 2 ? 1 : 0;
-  if (cached[bi][li] == 0) {
-    const size_t smem = bm == 64 ? TCfg<64>::SMEM : TCfg<32>::SMEM;
-    for (bool sp : {false, true})
-      cudaFuncSetAttribute(pick_tma_fn(bm, cs, sp), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(1, cs, 1);
-    lc.blockDim = dim3(bm == 64 ? TCfg<64>::NT : TCfg<32>::NT);
-    lc.dynamicSmemBytes = smem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1; at[0].val.clusterDim.y = cs; at[0].val.clusterDim.z = 1;
-    lc.attrs = at; lc.numAttrs = 1;
-    int ncl = 0;
-    const cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, pick_tma_fn(bm, cs, false), &lc);
-    cudaGetLastError();
-    cached[bi][li] = (e == cudaSuccess && ncl > 0) ? ncl : -1;
-  }
-  return cached[bi][li];
-}
-
-struct TmaPlan {
-  int bm = 0, cs = 0, splits = 1;
-  double cost = 1e300;
-};
-
-// Pick (BM, cluster size, split-K) minimising the modelled time: waves x per-CTA work, where a
-// wave holds max_clusters x cs CTAs and the per-CTA stage costs BM*256*16 DMMA FMAs plus the
-// CTA's share of the Omega tile (BM*16/(2 cs) Box-Muller pairs at ~128 FP64-pipe FMA-equivalents
-// each, tools/microbench fp64_pipes: 0.5 pairs/clk/SM vs 64 FMA/clk/SM) plus a share of the
-// A-tile L2 traffic (A is re-read by each of the l/BM row tiles; ~26 B/clk/SM sustained).
-TmaPlan plan_tma(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
-  TmaPlan best;
-  if (const char* ov = std::getenv("SKEL_TMA_PLAN")) {   // "bm,cs,splits" (experiments only)
-    int bm = 0, cs = 0, sp = 0;
-    if (std::sscanf(ov, "%d,%d,%d", &bm, &cs, &sp) == 3 && (bm == 32 || bm == 64) && (cs == 1 || cs == 2 || cs == 4) &&
-        sp >= 1 && tma_max_clusters(bm, cs) > 0) {
-      best.bm = bm; best.cs = cs; best.splits = sp; best.cost = 0;
-      return best;
-    }
-  }
-  const int64_t ntiles = cdiv(n, TBN);
-  for (int bm : {32, 64}) {
-    for (int cs : {1, 2, 4}) {
-      if (cs > 1 && ntiles < cs) continue;
-      const int ncl = tma_max_clusters(bm, cs);
-      if (ncl <= 0) continue;
-      const int64_t mb = cdiv(l, bm), nb = cdiv(ntiles, cs) * cs;
-      for (int splits = 1; splits <= 64; splits *= 2) {
-        if (splits > 1 && m / splits < 512) break;
-        const int64_t kps = cdiv(cdiv(m, splits), TBK) * TBK;
-        const int64_t sp = cdiv(m, kps);
-        const int64_t ctas = mb * nb * sp;
-        const int64_t waves = cdiv(ctas, (int64_t)ncl * cs);
-        // + the stage's A tile (32 KB) pulled from L2 by every l-tile: measured to overlap the
-        // DMMAs only partly (C2 k=512: BM=32 1.16x slower than BM=64 at equal waves-work)
-        const double stage = (double)bm * TBN * TBK + 128.0 * bm * TBK / (2.0 * cs) + 0.5 * 80000.0;
-        double cost = (double)waves * (double)cdiv(kps, TBK) * stage;
-        // split-K: partials written and re-read (16 sp l n bytes at ~6.4 TB/s, ~0.3 FMA-equivalents
-        // per byte-pair at 64 FMA/clk/SM and 1.9 GHz) plus one extra launch (~3 us)
-        if (sp > 1) cost += 0.3 * (double)sp * l * n + 3.6e5;
-        if (cost < best.cost) { best.bm = bm; best.cs = cs; best.splits = (int)sp; best.cost = cost; }
-      }
-    }
-  }
-  return best;
-}
-
-sk_status launch_tma(sk_ctx* c, const CUtensorMap& tm, const DenseParams& p, int bm, int cs, int64_t mb, int64_t nb,
-                     int splits) {
-  cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3((unsigned)mb, (unsigned)nb, (unsigned)splits);
-  lc.blockDim = dim3(bm == 64 ? TCfg<64>::NT : TCfg<32>::NT);
-  lc.dynamicSmemBytes = bm == 64 ? TCfg<64>::SMEM : TCfg<32>::SMEM;
-  lc.stream = c->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1; at[0].val.clusterDim.y = cs; at[0].val.clusterDim.z = 1;
-  lc.attrs = at; lc.numAttrs = 1;
-  SK_CUDA(c, cudaLaunchKernelEx(&lc, pick_tma_fn(bm, cs, splits > 1), tm, p));
-  return launched(c);
-}
-
-sk_status sketch_dense_tma(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_t l, const TmaPlan& pl) {
-  DenseParams p = p0;
-  CUtensorMap tm;
-  const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
-  const cuuint64_t strides[1] = {(cuuint64_t)p.lda * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)TBK, (cuuint32_t)TBN};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p.A), dims, strides,
-                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(c, SK_E_CUDA, "cuTensorMapEncodeTiled failed for A");
-  const int64_t mb = cdiv(l, pl.bm), nb = cdiv(cdiv(n, TBN), pl.cs) * pl.cs;
-  p.k_per_split = cdiv(cdiv(m, pl.splits), TBK) * TBK;
-  const int splits = (int)cdiv(m, p.k_per_split);
-  DBuf part;
-  if (splits > 1) {
-    SK_TRY(part.alloc(c, (size_t)splits * l * n * sizeof(double)));
-    p.part = part.as<double>();
-  }
-  SK_TRY(launch_tma(c, tm, p, pl.bm, pl.cs, mb, nb, splits));
-  if (splits == 1) return SK_OK;
-  return splitk_reduce(c, p.part, splits, l, n, p.scale, p.X, p.ldx);
-}
-
-// ---- pre-generated-Omega path (k_omega_image + k_sketch_pre)
-template <int BM, int NW> using PreFn = void (*)(const CUtensorMap, DenseParams, const double*, int64_t);
 struct PrePlan {
   int bm = 0, nw = 0, splits = 1;
   bool cluster = true;     // K-splits reduced in-cluster when eligible (<= 8, dividing BM)
+  int64_t chunk = 0;       // rows of A per K-chunk (the Omega image slot holds one chunk)
   double cost = 1e300;
 };
-// (BM, NW) candidates: whole waves x per-CTA DMMA work + split-K overhead as in plan_tma; a
-// candidate must beat the incumbent by 1% (fewer splits, less partial traffic, win ties).  Checked against a measured sweep
-// (tools/sweep_pre.py, profiles/round1/sweep_pre.txt): picks within 2% of the best plan on the
-// C2, C4 and C5-block shapes.
+// An Omega image slot at most this large stays in the 126 MB L2 next to the streaming A tiles.
+constexpr double kOmegaSlotBytes = 40.0 * (1 << 20);
+
 // co-resident CTAs of k_sketch_pre<BM, NW> launched in clusters of S along z (cached per process)
 template <int BM, int NW> int pre_max_ctas(int S) {
   static int cached[9] = {0};
@@ -1272,40 +957,55 @@ int pre_capacity(int bm, int nw, int S) {
   if (bm == 48 && nw == 8) return pre_max_ctas<48, 8>(S);
   if (bm == 64 && nw == 8) return pre_max_ctas<64, 8>(S);
   if (bm == 32 && nw == 8) return pre_max_ctas<32, 8>(S);
+  if (bm == 40 && nw == 8) return pre_max_ctas<40, 8>(S);
   return -1;
 }
 
+// rows of A per K-chunk for a row-tile height bm: the largest multiple of 1024 whose Omega image
+// fits kOmegaSlotBytes (at least 1024), or all of m
+int64_t chunk_rows(int64_t m, int64_t l, int bm, int64_t forced) {
+  if (forced > 0) return std::min<int64_t>(m, cdiv(forced, TBK) * TBK);
+  const double per_row = (double)cdiv(l, bm) * (bm + 4) * 8.0;
+  const int64_t ch = std::max<int64_t>(1024, (int64_t)(kOmegaSlotBytes / per_row) / 1024 * 1024);
+  return ch >= m ? m : ch;
+}
+
+// (BM, NW, K-splits per chunk) by a cost model: whole waves of the co-resident CTA count x per-CTA
+// DMMA work (padded tiles included) + split-K overhead, summed over the K-chunks; a candidate must
+// beat the incumbent by 1% (fewer splits, less partial traffic, win ties).  Checked against a
+// measured sweep of every plan (tools/sweep_pre.py, profiles/round1/sweep_pre.txt).  The context's
+// tuning (sk_set_sketch_tuning) can pin BM, the split count and the chunk height.
 PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
   PrePlan best;
-  if (const char* ov = std::getenv("SKEL_PRE_PLAN")) {   // "bm,nw,splits" (experiments only)
-    int bm = 0, nw = 0, sp = 0, cl = 1;
-    if (std::sscanf(ov, "%d,%d,%d,%d", &bm, &nw, &sp, &cl) >= 3) {
-      best.bm = bm; best.nw = nw; best.splits = sp; best.cluster = cl != 0;
-      return best;
-    }
-  }
-  const int cand[][2] = {{48, 8}, {64, 8}, {32, 8}};
+  const int cand[][2] = {{48, 8}, {64, 8}, {32, 8}, {40, 8}};
   for (auto& cd : cand) {
     const int bm = cd[0], nw = cd[1];
+    if (c->tune_sketch_bm && c->tune_sketch_bm != bm) continue;
     const int64_t mb = cdiv(l, bm), nb = cdiv(n, nw * 32);
-    // K-splits 1..8 (any count: 5 fills the waves at C2 k=512), then powers of two up to 64
+    const int64_t ch = chunk_rows(m, l, bm, c->tune_sketch_chunk);
+    const int64_t nch = cdiv(m, ch);
+    // K-splits per chunk 1..8 (any count: 5 fills the waves at C2 k=512), then powers of two up to 64
     for (int splits = 1; splits <= 64; splits = splits < 8 ? splits + 1 : splits * 2) {
-      if (splits > 1 && m / splits < 512) break;
-      const int64_t kps = cdiv(cdiv(m, splits), TBK) * TBK;
-      const int64_t sp = cdiv(m, kps);
+      if (c->tune_sketch_splits && splits != c->tune_sketch_splits) continue;
+      if (splits > 1 && ch / splits < 512 && !c->tune_sketch_splits) break;
+      const int64_t kps = cdiv(cdiv(ch, splits), TBK) * TBK;
+      const int64_t sp = cdiv(ch, kps);
       const int64_t ctas = mb * nb * sp;
       for (int clus = 0; clus < 2; ++clus) {
         if (clus && !(sp > 1 && sp <= 8 && bm % sp == 0)) continue;
+        if ((c->tune_sketch_path == 2 && clus) || (c->tune_sketch_path == 3 && !clus && sp > 1)) continue;
         const int cap = pre_capacity(bm, nw, clus ? (int)sp : 1);   // clusters of 4/8 strand SMs per GPC
         if (cap <= 0) continue;
         const double waves = (double)cdiv(ctas, cap);
         const double stage = (double)bm * nw * 32 * TBK;
         double cost = waves * (double)cdiv(kps, TBK) * stage;
         // K-splits summed in-cluster through DSMEM (~0.05 FMA-equivalents per partial element) or
-        // through HBM partials + a reduce launch
+        // through HBM partials + a reduce launch; chunks after the first add X into X
         if (sp > 1) cost += clus ? 0.05 * (double)sp * l * n : 0.3 * (double)sp * l * n + 3.6e5;
+        cost = cost * nch + (nch - 1) * (0.3 * (double)l * n + 3.6e5);
         if (cost < 0.99 * best.cost) {
           best.bm = bm; best.nw = nw; best.splits = (int)sp; best.cluster = clus != 0; best.cost = cost;
+          best.chunk = ch;
         }
       }
     }
@@ -1313,8 +1013,10 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
   return best;
 }
 
+// X = Omega A chunk by chunk: per K-chunk, the chunk's Omega image (generated from Philox, or packed
+// from a given Q when Qom != nullptr) then the TMA + DMMA GEMM accumulating into X.
 template <int BM, int NW>
-sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_t l, int splits_req, bool allow_cl,
+sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_t l, const PrePlan& pl,
                   const double* Qom = nullptr, int64_t ldq = 0) {
   using C = PCfg<BM, NW>;
   DenseParams p = p0;
@@ -1327,65 +1029,75 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(c, SK_E_CUDA, "cuTensorMapEncodeTiled failed for A");
-  const int64_t mb = cdiv(l, BM), nb = cdiv(n, C::TBNP), KT = cdiv(m, TBK);
-  // Omega image: mb x KT blocks of [TBK][OS]
-  DBuf img;
-  const int64_t pairs = mb * KT * TBK * (C::OS / 2);
-  SK_TRY(img.alloc(c, (size_t)pairs * 16));
-  if (Qom) {
-    k_omega_pack<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(Qom, ldq, (int)l, m, BM, C::OS, KT, img.as<double>());
+  const int64_t mb = cdiv(l, BM), nb = cdiv(n, C::TBNP);
+  const int64_t chunk = pl.chunk > 0 ? pl.chunk : m;
+  const int64_t KTmax = cdiv(chunk, TBK);
+  DBuf img, part;
+  SK_TRY(img.alloc(c, (size_t)mb * KTmax * TBK * C::OS * sizeof(double)));   // one chunk's Omega: the slot
+  const int64_t kps_max = cdiv(cdiv(chunk, pl.splits), TBK) * TBK;
+  const int sp_max = (int)cdiv(chunk, kps_max);
+  const bool cl = pl.cluster && sp_max > 1 && sp_max <= 8 && BM % sp_max == 0;
+  if (sp_max > 1 && !cl) SK_TRY(part.alloc(c, (size_t)sp_max * l * n * sizeof(double)));
+  for (int64_t i0 = 0; i0 < m; i0 += chunk) {
+    const int64_t i1 = std::min(m, i0 + chunk);
+    const int64_t KT = cdiv(i1 - i0, TBK);
+    if (Qom) {
+      k_omega_pack<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(Qom, ldq, (int)l, i0, i1, BM, C::OS, KT, img.as<double>());
+    } else {
+      k_omega_image<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(p.key, (int)l, i0, i1, BM, C::OS, KT, img.as<double>());
+    }
     SK_TRY(launched(c));
-  } else {
-    k_omega_image<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(p.key, (int)l, m, BM, C::OS, KT, img.as<double>());
-    SK_TRY(launched(c));
-  }
-  p.k_per_split = cdiv(cdiv(m, splits_req), TBK) * TBK;
-  const int splits = (int)cdiv(m, p.k_per_split);
-  DBuf part;
-  const bool cl = allow_cl && splits > 1 && splits <= 8 && BM % splits == 0;
-  if (splits == 1 || cl) {
-    auto kern = cl ? k_sketch_pre<BM, NW, 2> : k_sketch_pre<BM, NW, 0>;
-    SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    p.k0 = i0;
+    p.m = i1;
+    p.accum = i0 > 0;
+    p.k_per_split = cdiv(cdiv(i1 - i0, pl.splits), TBK) * TBK;
+    const int splits = (int)cdiv(i1 - i0, p.k_per_split);
+    const bool clu = cl && splits == sp_max;
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3((unsigned)mb, (unsigned)nb, (unsigned)splits);
     lc.blockDim = dim3(C::NT);
     lc.dynamicSmemBytes = C::SMEM;
     lc.stream = c->stream;
     cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = (unsigned)splits;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL behind the image kernel
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    lc.attrs = at; lc.numAttrs = 2;
+    int na = 0;
+    if (clu) {
+      at[na].id = cudaLaunchAttributeClusterDimension;
+      at[na].val.clusterDim.x = 1; at[na].val.clusterDim.y = 1; at[na].val.clusterDim.z = (unsigned)splits;
+      ++na;
+    }
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL behind the image kernel
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+    lc.attrs = at; lc.numAttrs = na;
+    if (splits == 1 || clu) {
+      auto kern = clu ? k_sketch_pre<BM, NW, 2> : k_sketch_pre<BM, NW, 0>;
+      SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, (const double*)img.as<double>(), KT));
+      SK_TRY(launched(c));
+      continue;
+    }
+    p.part = part.as<double>();
+    auto kern = k_sketch_pre<BM, NW, 1>;
+    SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, (const double*)img.as<double>(), KT));
-    return launched(c);
+    SK_TRY(launched(c));
+    SK_TRY(splitk_reduce(c, p.part, splits, l, n, p.scale, p.X, p.ldx, p.accum));
   }
-  SK_TRY(part.alloc(c, (size_t)splits * l * n * sizeof(double)));
-  p.part = part.as<double>();
-  auto kern = k_sketch_pre<BM, NW, 1>;
-  SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-  {
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3((unsigned)mb, (unsigned)nb, (unsigned)splits);
-    lc.blockDim = dim3(C::NT);
-    lc.dynamicSmemBytes = C::SMEM;
-    lc.stream = c->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL behind the image kernel
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    lc.attrs = at; lc.numAttrs = 1;
-    SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, (const double*)img.as<double>(), KT));
-  }
-  SK_TRY(launched(c));
-  return splitk_reduce(c, p.part, splits, l, n, p.scale, p.X, p.ldx);
+  return SK_OK;
 }
 
 sk_status sketch_dense_pre(sk_ctx* c, const DenseParams& p, int64_t m, int64_t n, int64_t l, const PrePlan& pl,
                            const double* Qom = nullptr, int64_t ldq = 0) {
-  if (pl.bm == 48 && pl.nw == 8) return run_pre<48, 8>(c, p, m, n, l, pl.splits, pl.cluster, Qom, ldq);
-  if (pl.bm == 64 && pl.nw == 8) return run_pre<64, 8>(c, p, m, n, l, pl.splits, pl.cluster, Qom, ldq);
-  if (pl.bm == 32 && pl.nw == 8) return run_pre<32, 8>(c, p, m, n, l, pl.splits, pl.cluster, Qom, ldq);
-  return fail(c, SK_E_ARG, "sketch: no pre-generated-Omega configuration");
+  if (pl.bm == 48 && pl.nw == 8) return run_pre<48, 8>(c, p, m, n, l, pl, Qom, ldq);
+  if (pl.bm == 64 && pl.nw == 8) return run_pre<64, 8>(c, p, m, n, l, pl, Qom, ldq);
+  if (pl.bm == 32 && pl.nw == 8) return run_pre<32, 8>(c, p, m, n, l, pl, Qom, ldq);
+  if (pl.bm == 40 && pl.nw == 8) return run_pre<40, 8>(c, p, m, n, l, pl, Qom, ldq);
+  return fail(c, SK_E_ARG, "sketch: no tensor-core plan for this shape");
+}
+
+bool tma_ok_for(const double* A, int64_t m, int64_t n, int64_t lda) {
+  return (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && tmap_encoder() != nullptr &&
+         m < (1LL << 31) && n < (1LL << 31);
 }
 
 }  // namespace
@@ -1398,22 +1110,12 @@ sk_status sketch_dense(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t
   p.key = dev::seed_key(seed);
   p.scale = 1.0 / std::sqrt((double)l);
   p.X = X; p.ldx = ldx;
-  if (const char* d = std::getenv("SKEL_SKETCH_DBG")) p.dbg = std::atoi(d);
   // TMA path: A 16-byte aligned with a 16-byte multiple column stride (the tensor-map rules)
-  const bool tma_ok = (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && tmap_encoder() != nullptr &&
-                      m < (1LL << 31) && n < (1LL << 31) && !c->force_legacy_sketch;
-  const char* fe = std::getenv("SKEL_SKETCH_FUSED");       // experiments/tests: the fused-generation kernel
-  // the Omega image costs ~8 l m bytes of workspace: beyond 8 GB (e.g. l and m both ~3e4) the
-  // kernel that generates Omega per tile, storing nothing, is used instead
-  const bool fused_omega = (fe && fe[0] == '1') || (double)l * (double)m * 8.0 * 1.1 > 8.0 * (1 << 30);
-  if (tma_ok && !fused_omega) {
+  if (tma_ok_for(A, m, n, lda) && c->tune_sketch_path != 1) {
     const PrePlan pl = plan_pre(c, m, n, l);
     if (pl.bm > 0) return sketch_dense_pre(c, p, m, n, l, pl);
   }
-  if (tma_ok) {
-    const TmaPlan pl = plan_tma(c, m, n, l);
-    if (pl.bm > 0) return sketch_dense_tma(c, p, m, n, l, pl);
-  }
+  // fallback (A the tensor map cannot describe): each CTA generates its Omega tiles in shared memory
   const int64_t mb = cdiv(l, DBM), nb = cdiv(n, DBN);
   int splits = 1;
   while (mb * nb * splits < c->num_sms && m / (splits * 2) >= 1024 && splits < 64) splits *= 2;
@@ -1442,9 +1144,7 @@ sk_status sketch_dense(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t
 sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int64_t m, int64_t n, int64_t lda,
                    int64_t l, double* X, int64_t ldx) {
   if (n == 0 || l == 0) return SK_OK;
-  const bool tma_ok = (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && tmap_encoder() != nullptr &&
-                      m < (1LL << 31) && n < (1LL << 31);
-  if (!tma_ok) {   // X^T (n x l col-major, ld ldx) = A^T Q
+  if (!tma_ok_for(A, m, n, lda)) {   // X^T (n x l col-major, ld ldx) = A^T Q
     return gemm(c, true, false, n, l, m, 1.0, A, lda, Q, ldq, 0.0, X, ldx);
   }
   DenseParams p{};

@@ -18,17 +18,19 @@ One process per GPU.  A (m x n) is split into contiguous column blocks, rank r o
               LUPP kernel on identical bytes.
               "p2p" (variant i, ``P2PStepwise``): the per-step design with the exchange inside
               the step kernel -- records stored into the peers' mailboxes over NVLink.
-  gather C    each rank writes the skeleton columns it owns (zeros elsewhere,
-              sk_gather_cols_shard) and a sum all-reduce assembles C = A(:, J_s) exactly.
+  gather C    each rank packs the skeleton columns it owns; ONE all-gather of the packed blocks
+              (padded to the largest owner count) gives C = A(:, J_s) on every rank.
   select_rows row LUPP on the replicated C, identical on every rank (Alg. 2 line 4).
-  residual    Q = ortho(C) is computed identically on every rank; each rank returns
-              ||A_r - Q Q^T A_r||_F^2 and ||A_r||_F^2 (sk_residual_cols) and one sum all-reduce
-              gives the global Frobenius residual of the column ID.
+  residual    Q = ortho(C) by Cholesky QR distributed over row blocks of the basis (a local Gram
+              matrix and ONE k x k all-reduce per pass, one all-gather of the row blocks); each
+              rank returns ||A_r - Q Q^T A_r||_F^2 and ||A_r||_F^2 and one sum all-reduce gives the
+              global Frobenius residual of the column ID.
 
-All arithmetic runs in the library kernels (``backend``); this module only moves tensors
-between ranks.  The backend is an object with the library's call signatures; the default is
-the CUDA library (paper_2104_05877_b200.api).  The multi-process CPU tests substitute a
-host backend to exercise this protocol with the gloo backend (tests/test_dist_gloo.py).
+On CUDA tensors (backend=None) the library does all of this itself: ``api.DistSession`` creates
+a column-sharded context (sk_create_dist) that owns its NCCL communicator and issues every
+collective above on its own stream (dist.cu).  With an explicit ``backend`` the same protocol
+runs here over torch.distributed -- the multi-process CPU tests substitute a host backend to
+exercise it with the gloo backend (tests/test_dist_gloo.py).
 """
 import math
 
@@ -194,14 +196,99 @@ class P2PStepwise:
             self.mailbox = 0
 
 
+def _owners(Js, n_global, world):
+    """Owner rank of every skeleton column and each rank's columns in pivot order (host lists)."""
+    blocks = [shard(n_global, world, r) for r in range(world)]
+    owner = []
+    for j in Js:
+        owner.append(next((r for r, (c0, nc) in enumerate(blocks) if c0 <= j < c0 + nc), -1))
+    return owner, blocks
+
+
+def gather_cols_allgather(A_local, Js, n_global, group=None, backend=None):
+    """C = A_global(:, J_s) on every rank (S3 on a column-sharded A): every rank packs the
+    skeleton columns it owns (in pivot order) into a block padded to the largest owner count, ONE
+    all-gather moves the blocks, and C's columns are taken from them in pivot order -- m k doubles
+    received per rank, half of what a sum all-reduce of zero-padded copies moves."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    J = [int(j) for j in Js.tolist()]
+    owner, blocks = _owners(J, n_global, world)
+    col0 = blocks[rank][0]
+    cnt = [owner.count(r) for r in range(world)]
+    cmax = max(1, max(cnt))
+    mine = [j - col0 for j, o in zip(J, owner) if o == rank]
+    send = backend.pack_cols(A_local, mine, cmax)                   # (cmax, m): row i = packed column i
+    parts = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send, group=group)
+    seen = [0] * world
+    cols = []
+    for o in owner:
+        cols.append(parts[o][seen[o]])
+        seen[o] += 1
+    return torch.stack(cols, 0).t()                                  # m x k, column-major
+
+
+def cholqr_rows_dist(B, passes, shift, group=None, backend=None):
+    """Q = ortho(B) for a replicated basis B (m x k) by Cholesky QR distributed over row blocks
+    (rank r: rows [r mb, (r+1) mb), mb = ceil(m / P)): per pass a local Gram matrix, ONE k x k sum
+    all-reduce, the replicated Cholesky factor L and the local solve B_r <- B_r L^{-T} (the first
+    pass shifted for shifted CholeskyQR3); one all-gather of the row blocks replicates Q."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    m, k = B.shape
+    mb = -(-m // world)
+    r0 = min(m, rank * mb)
+    Bl = backend.row_block(B, r0, min(mb, m - r0), mb)                # mb x k, zero rows past m
+    for p in range(passes):
+        G = backend.gram(Bl)
+        dist.all_reduce(G, op=dist.ReduceOp.SUM, group=group)
+        Bl = backend.chol_right_solve(Bl, G, m if (shift and p == 0) else 0)
+    parts = [torch.empty_like(Bl) for _ in range(world)]
+    dist.all_gather(parts, Bl.contiguous(), group=group)
+    return torch.cat(parts, 0)[:m]
+
+
+def _dist_rand_lupp_lib(A_local, n_global, k, l, embedding, seed, zeta, rows, residual, group, exchange):
+    """The product path: a library-owned column-sharded context (api.DistSession); every exchange
+    (sketch rows or per-step records, C's columns, Gram matrices, squared sums) is a collective the
+    library issues on its own NCCL communicator."""
+    from . import api
+    out = {}
+    sess = api.DistSession(n_global, group, A_local.device.index, "step" if exchange == "step" else "replicate")
+    try:
+        with sess:
+            out["col0"], out["ncols"] = sess.col0, sess.ncols
+            X_local = api.sketch(A_local, l, embedding, seed, zeta)
+            if exchange == "p2p":
+                p2p = P2PStepwise(n_global, k, group, A_local.device.index)
+                try:
+                    Js, Lf, _ = p2p.run(X_local)
+                finally:
+                    p2p.close()
+            else:
+                Js, Lf, _, _ = api.select_cols(X_local, k)
+            out["Js"], out["Lf"] = Js, Lf
+            if rows or residual:
+                out["C"] = api.gather_cols(A_local, Js)
+                if rows:
+                    out["Is"] = api.select_rows(out["C"], k)[0]
+                if residual:
+                    out["residual"], out["normA"] = api.residual(A_local, Js, None, "col_id")
+    finally:
+        sess.close()
+    return out
+
+
 def dist_rand_lupp(A_local, n_global, k, l, embedding="gaussian", seed=0, zeta=8, rows=False,
                    residual=False, group=None, backend=None, exchange="replicate"):
     """Algorithm 2 on a column-sharded A.  A_local: this rank's block (m x ncols, column-major).
 
     Returns a dict with J_s (global column indices, replicated), I_s (if rows), the skeleton
     matrix C (replicated, if rows or residual) and the column-ID residual / ||A||_F (if residual).
+    backend=None (CUDA tensors): the library's distributed context does everything.  An explicit
+    backend runs the same protocol here over torch.distributed (the CPU tests' host backend).
     """
-    backend = backend or CudaBackend()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     col0, ncols = shard(n_global, world, rank)
@@ -210,33 +297,30 @@ def dist_rand_lupp(A_local, n_global, k, l, embedding="gaussian", seed=0, zeta=8
         raise ValueError(f"rank {rank}: A_local has {A_local.shape[1]} columns, shard() expects {ncols}")
     if not (1 <= k <= l <= m) or k > n_global:
         raise ValueError("need 1 <= k <= l <= m and k <= n")
+    if exchange not in ("step", "p2p", "replicate"):
+        raise ValueError("exchange must be 'step', 'p2p' or 'replicate'")
+    if backend is None:
+        return _dist_rand_lupp_lib(A_local, n_global, k, l, embedding, seed, zeta, rows, residual, group, exchange)
     out = {"col0": col0, "ncols": ncols}
     X_local = backend.sketch(A_local, l, embedding, seed, zeta)               # l x ncols
     if exchange == "step":
         Js, Lf, _ = select_cols_stepwise(X_local, n_global, k, group, backend)  # Lf: this rank's rows
     elif exchange == "p2p":
-        p2p = P2PStepwise(n_global, k, group, X_local.device.index)
-        try:
-            Js, Lf, _ = p2p.run(X_local)
-        finally:
-            p2p.close()
-    elif exchange == "replicate":
+        raise ValueError("exchange='p2p' needs the CUDA library (backend=None)")
+    else:
         Xk = _all_gather_cols(X_local[:k], n_global, group, world)            # k x n (rows 0..k-1)
         Js, Lf = backend.select_cols(Xk, k)
-    else:
-        raise ValueError("exchange must be 'step', 'p2p' or 'replicate'")
     out["Js"] = Js
     out["Lf"] = Lf
     if rows or residual:
-        C = backend.gather_cols_shard(A_local, Js, col0)                      # m x k, zeros off-shard
-        Ct = C.t().contiguous()                                                # k x m: row t = column t of C
-        dist.all_reduce(Ct, op=dist.ReduceOp.SUM, group=group)                 # exact: one owner per column
-        C = Ct.t()                                                             # column-major m x k
+        C = gather_cols_allgather(A_local, Js, n_global, group, backend)
         out["C"] = C
         if rows:
             out["Is"] = backend.select_rows(C, k)
         if residual:
-            r2, a2 = backend.residual_cols(A_local, C)
+            B, passes, shift = backend.basis(C)                              # LUPP basis or C itself
+            Q = cholqr_rows_dist(B, passes, shift, group, backend)
+            r2, a2 = backend.residual_q(A_local, Q)
             sums = torch.tensor([r2, a2], dtype=torch.float64, device=A_local.device)
             dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
             out["residual"] = math.sqrt(max(float(sums[0]), 0.0))

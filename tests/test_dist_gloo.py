@@ -2,9 +2,11 @@
 
 * oracle.dist (per-step exchange with the lowest-global-index merge rule) == single-process LUPP,
   pivots and factors bit for bit, including exact ties that straddle a shard boundary.
-* paper_2104_05877_b200.dist.dist_rand_lupp over a world-size-2 gloo group, with a host backend
-  built from the oracle standing in for the CUDA kernels, reproduces the unsharded oracle path:
-  J_s, C = A(:, J_s), I_s and the column-ID residual.
+* paper_2104_05877_b200.dist.dist_rand_lupp over world-size-2 and -3 gloo groups, with a host
+  backend built from the oracle standing in for the CUDA kernels, reproduces the unsharded oracle
+  path: J_s, C = A(:, J_s) (one all-gather of the owners' packed columns), I_s and the column-ID
+  residual (Q by Cholesky QR distributed over row blocks: k x k all-reduces + one all-gather),
+  with the gather-then-replicate and the per-step exchanges.
 """
 import math
 import os
@@ -12,6 +14,7 @@ import socket
 
 import numpy as np
 import pytest
+import scipy.linalg as sla
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -88,8 +91,42 @@ class HostBackend:
         E = A - Q @ (Q.T @ A)
         return float(np.sum(E * E)), float(np.sum(A * A))
 
+    # the pieces of the distributed residual protocol (dist.gather_cols_allgather, cholqr_rows_dist)
+    def pack_cols(self, A_local, idx, cmax):
+        out = torch.zeros((cmax, A_local.shape[0]), dtype=torch.float64)
+        for i, j in enumerate(idx):
+            out[i] = A_local[:, j]
+        return out
 
-def _worker(rank, world, port, A, k, l, seed, q):
+    def basis(self, C):
+        # as the library: the LUPP factor of C (range(C) = range(Lf_C)) with CholeskyQR2
+        _, Lf, _, _ = o_lupp.select_rows(C.numpy(), C.shape[1])
+        return torch.from_numpy(Lf), 2, False
+
+    def row_block(self, B, r0, rows, mb):
+        out = torch.zeros((mb, B.shape[1]), dtype=torch.float64)
+        out[:rows] = B[r0:r0 + rows]
+        return out
+
+    def gram(self, Bl):
+        return Bl.t() @ Bl
+
+    def chol_right_solve(self, Bl, G, shift_rows):
+        G = G.numpy().copy()
+        k = G.shape[0]
+        if shift_rows:
+            G += 11.0 * (shift_rows * k + k * (k + 1)) * 2.0 ** -53 * np.trace(G) * np.eye(k)
+        L = np.linalg.cholesky(G)
+        return torch.from_numpy(sla.solve_triangular(L, Bl.numpy().T, lower=True).T.copy())
+
+    def residual_q(self, A_local, Q):
+        A = A_local.numpy()
+        Qn = Q.numpy()
+        E = A - Qn @ (Qn.T @ A)
+        return float(np.sum(E * E)), float(np.sum(A * A))
+
+
+def _worker(rank, world, port, A, k, l, seed, q, exchange="replicate"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -97,7 +134,8 @@ def _worker(rank, world, port, A, k, l, seed, q):
         n = A.shape[1]
         c0, nc = shard(n, world, rank)
         A_local = torch.from_numpy(np.asfortranarray(A[:, c0:c0 + nc]))
-        out = dist_rand_lupp(A_local, n, k, l, "gaussian", seed, rows=True, residual=True, backend=HostBackend())
+        out = dist_rand_lupp(A_local, n, k, l, "gaussian", seed, rows=True, residual=True, backend=HostStepBackend(),
+                             exchange=exchange)
         q.put((rank, out["Js"].tolist(), out["Is"].tolist(), out["C"].numpy().copy(), out["residual"], out["normA"]))
     finally:
         dist.destroy_process_group()
@@ -111,15 +149,15 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_dist_rand_lupp_gloo_matches_unsharded_oracle(world):
+@pytest.mark.parametrize("world,exchange", [(2, "replicate"), (3, "replicate"), (2, "step"), (3, "step")])
+def test_dist_rand_lupp_gloo_matches_unsharded_oracle(world, exchange):
     A, _ = make_c1(seed=1001)
     A = A[:, :251]                                           # ragged shards
     k, l, seed = 20, 40, 2001
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, A, k, l, seed, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, A, k, l, seed, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
@@ -132,7 +170,7 @@ def test_dist_rand_lupp_gloo_matches_unsharded_oracle(world):
     r_or, n_or = o_res.residual(A, piv, kind="col_id")
     for rank, Js, Is, C, r, nA in res:
         assert Js == piv.tolist(), rank
-        np.testing.assert_array_equal(C, A[:, piv])          # assembled exactly by the sum all-reduce
+        np.testing.assert_array_equal(C, A[:, piv])          # assembled exactly by the all-gather
         assert Is == ipiv.tolist()
         assert abs(r - r_or) <= 1e-12 * r_or + 4 * 2.0 ** -53 * n_or
         assert abs(nA - n_or) <= 1e-14 * n_or

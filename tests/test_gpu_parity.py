@@ -443,19 +443,22 @@ def test_rand_lupp_host_pipelined(emb):
     lupp_parity(Is.numpy(), lambda f: o_lupp.select_rows(A[:, Js.numpy()], k, f))
 
 
-@pytest.mark.parametrize("plan", ["48,8,1,0", "64,8,1,0", "32,8,1,0", "48,8,4,0", "48,8,4,1", "64,8,2,1", "32,8,8,1",
-                                  "fused"])
-def test_sketch_dense_plans(plan, monkeypatch):
-    """Every dense-sketch kernel configuration against the oracle: the pre-generated-Omega GEMM at
-    each tile height, K-splits through HBM partials (cl 0) and through cluster DSMEM (cl 1), and the
-    fused-generation kernel (SKEL_SKETCH_FUSED).  Ragged l, m and n span several tiles."""
+@pytest.mark.parametrize("plan", [
+    (0, 48, 1, 0), (0, 64, 1, 0), (0, 32, 1, 0), (0, 40, 1, 0),        # tile heights, one K range
+    (2, 48, 4, 0), (3, 48, 4, 0), (3, 64, 2, 0), (3, 32, 8, 0),        # K-splits via HBM partials / cluster DSMEM
+    (0, 48, 1, 256), (2, 40, 3, 320), (3, 48, 2, 512),                  # K-chunked Omega (ragged last chunk)
+    (1, 0, 0, 0),                                                       # shared-memory generation fallback
+])
+def test_sketch_dense_plans(plan):
+    """Every dense-sketch kernel configuration against the oracle (sk_set_sketch_tuning): the
+    TMA + DMMA GEMM at each tile height, K-splits through HBM partials and through cluster DSMEM,
+    Omega generated chunk by chunk into the reused slot with X accumulated across chunks, and the
+    fallback kernel.  Ragged l, m and n span several tiles."""
     m, n, l = 1000, 700, 61
     A = rand_mat(m, n, 41)
-    if plan == "fused":
-        monkeypatch.setenv("SKEL_SKETCH_FUSED", "1")
-    else:
-        monkeypatch.setenv("SKEL_PRE_PLAN", plan)
-    X = sk.sketch(dev_f(A), l, "gaussian", 77).cpu().numpy()
-    monkeypatch.delenv("SKEL_PRE_PLAN", raising=False)
-    monkeypatch.delenv("SKEL_SKETCH_FUSED", raising=False)
+    sk.set_sketch_tuning(*plan)
+    try:
+        X = sk.sketch(dev_f(A), l, "gaussian", 77).cpu().numpy()
+    finally:
+        sk.set_sketch_tuning()
     assert rel_fro(X, o_sketch.sketch(A, l, "gaussian", 77)) <= 1e-12

@@ -22,6 +22,7 @@ SHAPES = [  # (name, m, n, l, embedding)
     ("C4 k=50", 65536, 784, 100, "gaussian"),
     ("C4 k=100", 65536, 784, 200, "gaussian"),
     ("C4 k=200", 65536, 784, 400, "gaussian"),
+    ("C5 block", 131072, 8192, 1100, "gaussian"),
     ("C3 sparse", 16384, 16384, 510, "sparse_sign"),
     ("C2 srtt k=512", 4096, 4096, 522, "srtt"),
     ("C3 srtt", 16384, 16384, 510, "srtt"),
@@ -32,7 +33,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--only", default="", help="substring filter on the shape name")
+    ap.add_argument("--tune", default="", help="path,bm,splits,chunk for sk_set_sketch_tuning")
     a = ap.parse_args()
+    if a.tune:
+        sk.set_sketch_tuning(*[int(x) for x in a.tune.split(",")])
     dev = torch.device("cuda", 0)
     flush = torch.empty(512 << 18, dtype=torch.int32, device=dev)
     for name, m, n, l, emb in SHAPES:
