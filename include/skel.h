@@ -133,7 +133,7 @@ int64_t sk_launch_count(const sk_ctx* ctx);
 
 /* X = Gamma A.  Gamma (l x m) is drawn from (emb, zeta, seed) on every call (Philox4x32-10,
  * R1-R4) and never held in HBM as a whole: the Gaussian one is generated one K-chunk of A's rows
- * at a time into an L2-sized workspace slot (<= ~40 MB) that the FP64 tensor-core GEMM reads
+ * at a time into an L2-sized workspace slot (<= ~80 MB) that the FP64 tensor-core GEMM reads
  * before the next chunk overwrites it; the sparse-sign structure goes into a per-call CSR
  * (4 bytes per nonzero, values never stored), SRTT's permutations and signs are drawn per CTA.
  *   A   m x n column-major (lda >= m), read only.
@@ -151,7 +151,7 @@ sk_status sk_sketch(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t 
  *               distributed shared memory of a cluster of the splits
  *   bm          CTA row-tile height: 0 or one of 32, 40, 48, 64
  *   splits      K-splits per chunk (0 = planner, 1..64)
- *   chunk_rows  rows of A per K-chunk, rounded up to 16 (0 = the largest whose Gamma slot fits ~40 MB)
+ *   chunk_rows  rows of A per K-chunk, rounded up to 16 (0 = the largest whose Gamma slot fits ~80 MB)
  * Results are identical up to summation order (parity tests use it to reach every plan). */
 sk_status sk_set_sketch_tuning(sk_ctx* ctx, int32_t path, int32_t bm, int32_t splits, int64_t chunk_rows);
 
@@ -159,8 +159,9 @@ sk_status sk_set_sketch_tuning(sk_ctx* ctx, int32_t path, int32_t bm, int32_t sp
  * Y = A Omega^T with Omega an l x n embedding drawn like sk_sketch's Gamma over the column index
  * of A (an independent draw from X = Gamma A when the seed differs, Alg. 3 line 1).  Row-wise
  * LUPP on Y (sk_select_rows) gives I_s without forming C (Alg. 3 line 4).  A m x n column-major;
- * Y m x l column-major (ldy >= m).  Requires 1 <= l <= n.  (Computed as the row sketch of A^T:
- * one transpose pass plus one sketch pass; the fused single-pass dual sketch is future work.) */
+ * Y m x l column-major (ldy >= m).  Requires 1 <= l <= n.  Gaussian: one pass over A, Omega generated
+ * one block of A's columns at a time (L2-sized slot) and accumulated by the DMMA GEMM; sparse sign
+ * and SRTT: the row sketch of a transposed copy of A. */
 sk_status sk_sketch_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
                          sk_embedding emb, int32_t zeta, uint64_t seed, double* Y, int64_t ldy);
 
@@ -168,12 +169,25 @@ sk_status sk_sketch_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int
  * X = Omega (A^T A)^q, the plain power-iteration row-space approximator of eq:def_power_iter
  * with Omega an l x n embedding drawn exactly like sk_sketch's Gamma but over the
  * column index of A (R1: Omega(r, j) from (seed, r, j)).  q = 0 is sk_sketch (X = Gamma A,
- * Gamma l x m).  Computed as T = Omega A^T, then X = T A, q - 1 times T = X A^T, X = T A
- * (2q passes over A).  A m x n column-major; X l x n row-major (ldx >= n).  Requires 1 <= l <= n
+ * Gamma l x m).  Computed as T^T = A Omega^T, then X = T A, q - 1 times T^T = A X^T, X = T A
+ * (2q passes over A, no transpose of A for the Gaussian Omega).  A m x n column-major; X l x n row-major (ldx >= n).  Requires 1 <= l <= n
  * for q >= 1, 0 <= q <= 64.  Not orthogonalised: the paper notes the plain form is unstable for
  * ill-conditioned A and q > 1. */
 sk_status sk_sketch_power(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
                           sk_embedding emb, int32_t zeta, uint64_t seed, int32_t q, double* X, int64_t ldx);
+
+/* ---- the same with orthogonalisation at every iteration (eq:ortho_power_iter) ----
+ *   Y_1 = A Omega^T;  Y_i = ortho(A ortho(A^T Y_{i-1})), i = 2..q;  X = ortho(Y_q)^T A
+ * with Omega as for sk_sketch_power and ortho = an orthonormal basis of the range (this library's
+ * LUPP basis + Cholesky QR; unique up to the signs of its columns, so X is
+ * unique up to the signs of its rows, which no LUPP pivot depends on).  Stable for ill-conditioned
+ * A where the plain form is not; X spans the same row space as sk_sketch_power's.
+ * 2q passes over A; the Gaussian column sketch A Omega^T generates Omega per block of columns and
+ * never transposes A.  Requires 1 <= q <= 64, 1 <= l <= min(m, n).  info as for sk_select_cols
+ * (a rank failure of an orthogonalisation: SK_E_RANK). */
+sk_status sk_sketch_power_ortho(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                                sk_embedding emb, int32_t zeta, uint64_t seed, int32_t q, double* X, int64_t ldx,
+                                int64_t* info);
 
 /* ---- S2: column skeletons by LUPP on the sketch  (eq:def_LUPP; Alg. 2 line 3) ----
  * k-step LU with partial pivoting on the n x k panel X^T(:, 0:k) = rows 0..k-1

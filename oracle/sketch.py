@@ -75,3 +75,27 @@ def sketch_streamed(get_cols, m, n, l, kind="gaussian", seed=0, zeta=8, block=40
         j1 = min(n, j0 + block)
         X[:, j0:j1] = G @ np.asarray(get_cols(j0, j1), dtype=np.float64)
     return X
+
+
+def ortho_pos(M):
+    """ortho(M) as the Q factor of the thin QR with diag(R) > 0 -- the unique orthonormal basis
+    whose Gram-Schmidt order matches M's columns (reading R21: the paper leaves the basis free)."""
+    q, r = np.linalg.qr(np.asarray(M, dtype=np.float64), mode="reduced")
+    d = np.sign(np.diag(r))
+    d[d == 0] = 1.0
+    return q * d
+
+
+def sketch_power_ortho(A, l, kind="gaussian", seed=0, q=1, zeta=8):
+    """Row-space approximator with q orthogonalised power iterations, eq:ortho_power_iter:
+
+        Y(1) = A Omega^T;  Y(i) = ortho(A ortho(A^T Y(i-1))), i = 2..q;  X = ortho(Y(q))^T A,
+
+    Omega l x n drawn like Gamma over the column index of A (as sketch_power), ortho = ortho_pos."""
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[1]
+    Om = omega.embedding(kind, seed, l, n, zeta)
+    Y = A @ Om.T
+    for _ in range(2, q + 1):
+        Y = ortho_pos(A @ ortho_pos(A.T @ Y))
+    return ortho_pos(Y).T @ A

@@ -27,6 +27,8 @@ _SIGS = {
     "sk_sketch_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64, c_dp, c_i64],
     "sk_sketch_power": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64,
                         ctypes.c_int32, c_dp, c_i64],
+    "sk_sketch_power_ortho": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_int32, ctypes.c_uint64,
+                              ctypes.c_int32, c_dp, c_i64, ctypes.POINTER(c_i64)],
     "sk_select_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, c_dp, c_i64, c_dp,
                        ctypes.POINTER(c_i64)],
     "sk_select_cols_cpqr": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_dp, c_dp, c_i64, ctypes.POINTER(c_i64)],

@@ -172,12 +172,19 @@ def stream_select(A, k, l=None, embedding="gaussian", seed_x=0, seed_y=1, zeta=8
     return Js, Is
 
 
-def sketch_power(A, l, embedding="gaussian", seed=0, q=1, zeta=8, out=None):
-    """X = Omega (A^T A)^q (eq:def_power_iter; Rand-LUPP-1piter for q = 1)."""
+def sketch_power(A, l, embedding="gaussian", seed=0, q=1, zeta=8, out=None, ortho=False):
+    """X = Omega (A^T A)^q (eq:def_power_iter; Rand-LUPP-1piter for q = 1), or with
+    ortho=True the orthogonalised iteration X = ortho(Y_q)^T A of eq:ortho_power_iter."""
     lda = _colmajor(A, "A")
     m, n = A.shape
     X = out if out is not None else torch.empty((l, n), dtype=torch.float64, device=A.device)
     h = context(A.device.index)
+    if ortho:
+        info = ctypes.c_int64(0)
+        st = lib().sk_sketch_power_ortho(h, _ptr(A), m, n, lda, l, _EMB[embedding], zeta, seed & (2**64 - 1), q,
+                                         _ptr(X), max(X.stride(0), n), ctypes.byref(info))
+        _check(st, h, info.value)
+        return X
     _check(lib().sk_sketch_power(h, _ptr(A), m, n, lda, l, _EMB[embedding], zeta, seed & (2**64 - 1), q, _ptr(X),
                                  max(X.stride(0), n)), h)
     return X

@@ -175,6 +175,24 @@ sk_status sk_sketch_power(sk_ctx* c, const double* A, int64_t m, int64_t n, int6
   return sketch_power(c, A, m, n, lda, l, (int)emb, zeta, seed, q, X, ldx);
 }
 
+sk_status sk_sketch_power_ortho(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                                sk_embedding emb, int32_t zeta, uint64_t seed, int32_t q, double* X, int64_t ldx,
+                                int64_t* info) {
+  if (!c) return SK_E_ARG;
+  c->err.clear();
+  SK_ARG(c, A && X, "sk_sketch_power_ortho: NULL A or X");
+  SK_ARG(c, q >= 1 && q <= 64, "sk_sketch_power_ortho: 1 <= q <= 64");
+  SK_ARG(c, m >= 1 && n >= 1 && l >= 1 && l <= n && l <= m, "sk_sketch_power_ortho: need 1 <= l <= min(m, n)");
+  SK_ARG(c, lda >= m && ldx >= n, "sk_sketch_power_ortho: lda >= m and ldx >= n required");
+  SK_ARG(c, emb >= SK_EMB_GAUSSIAN && emb <= SK_EMB_SRTT, "sk_sketch_power_ortho: unknown embedding");
+  SK_ARG(c, emb != SK_EMB_SPARSE_SIGN || (zeta >= 2 && zeta <= l && zeta <= 64), "sk_sketch_power_ortho: bad zeta");
+  SK_CUDA(c, cudaSetDevice(c->device));
+  DBuf st;
+  SK_TRY(st.alloc(c, sizeof(int64_t)));
+  SK_TRY(sketch_power_ortho(c, A, m, n, lda, l, (int)emb, zeta, seed, q, X, ldx, st.as<int64_t>()));
+  return finish_info(c, st.as<int64_t>(), info, "sk_sketch_power_ortho (orthogonalisation)");
+}
+
 sk_status sk_select_cols(sk_ctx* c, const double* X, int64_t l, int64_t n, int64_t ldx, int64_t k,
                          int64_t* Js, double* Lf, int64_t ldlf, double* U, int64_t ldu, double* gaps,
                          int64_t* info) {

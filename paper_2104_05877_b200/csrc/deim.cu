@@ -52,6 +52,12 @@ sk_status select_cols_deim(sk_ctx* c, const double* A, int64_t m, int64_t n, int
   if (cusolverDnDgeqrf(h, (int)m, (int)l, B.as<double>(), (int)m, tau.as<double>(), work.as<double>(), lw1,
                        info.as<int>()) != CUSOLVER_STATUS_SUCCESS)
     return fail(c, SK_E_CUDA, "sk_select_cols_deim: geqrf failed");
+  {
+    int qinfo = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&qinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (qinfo != 0) return fail(c, SK_E_CUDA, "sk_select_cols_deim: cuSOLVER geqrf info = " + std::to_string(qinfo));
+  }
   DBuf R;
   SK_TRY(R.alloc(c, (size_t)l * l * sizeof(double)));
   SK_TRY(upper_triangle(c, B.as<double>(), m, l, R.as<double>(), l));           // R (l x l), zeros below
@@ -64,6 +70,14 @@ sk_status select_cols_deim(sk_ctx* c, const double* A, int64_t m, int64_t n, int
                        VT.as<double>(), (int)l, work.as<double>(), std::max(lw1, lw2), rwork.as<double>(),
                        info.as<int>()) != CUSOLVER_STATUS_SUCCESS)
     return fail(c, SK_E_CUDA, "sk_select_cols_deim: gesvd failed");
+  // cuSOLVER reports a failed factorisation only through the device info of each call: geqrf's
+  // (illegal argument, < 0) was overwritten by gesvd's, so both are checked -- gesvd's info > 0 is
+  // the number of superdiagonals of the bidiagonal form that did not converge
+  int hinfo = 0;
+  SK_CUDA(c, cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  SK_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (hinfo != 0)
+    return fail(c, SK_E_CUDA, "sk_select_cols_deim: cuSOLVER gesvd info = " + std::to_string(hinfo));
   // V^_k = Q_X V~(:, 0:k) = Q_X (V~^T(0:k, :))^T  (n x k, column-major)
   SK_TRY(Vk.alloc(c, (size_t)n * k * sizeof(double)));
   SK_TRY(gemm(c, false, true, n, k, l, 1.0, Q.as<double>(), n, VT.as<double>(), l, 0.0, Vk.as<double>(), n));

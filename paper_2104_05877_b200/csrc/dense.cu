@@ -77,9 +77,88 @@ __global__ void k_power_check(const double* y, int64_t k, double* lam, int* done
   }
 }
 
+// lambda_max of the SPD k x k matrix G by power iteration in ONE persistent launch: the grid's CTAs
+// are co-resident (cooperative launch); iteration t: every CTA loads x = y_{t-1} / ||y_{t-1}|| into
+// shared memory, computes its rows of y_t = G x (a warp per row, G read through L2), publishes the
+// partial sum of y_t^2 and releases its flag (st.release.gpu); after every flag reached t + 1 each
+// CTA sums the partials in the same fixed order, so all CTAs see the same lambda_t = ||y_t|| and
+// stop at the same iteration: when lambda stops increasing (relative change <= 1e-15; for SPD G the
+// sequence is non-decreasing) or after max_it iterations.  Buffers by iteration parity: a CTA
+// overwrites buffer t & 1 only after every CTA finished iteration t - 1, i.e. read buffer t & 1.
+__device__ __forceinline__ double power_init(int64_t i) {
+  return 1.0 + 1e-3 * (double)((i * 2654435761LL) % 1000) / 1000.0;
+}
+
+__global__ void __launch_bounds__(256) k_power_persistent(const double* __restrict__ G, int64_t k, int64_t ld,
+                                                          double* ybuf, double* part, unsigned long long* flags,
+                                                          double* lam_out, int max_it) {
+  extern __shared__ double xs[];                       // [k]
+  __shared__ double s_nrm, s_lam;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nb = gridDim.x;
+  const int warps = blockDim.x >> 5;
+  double lam_prev = 0.0;
+  if (tid == 0) s_nrm = 0.0;
+  // x_0 = init / ||init||
+  for (int64_t i = tid; i < k; i += blockDim.x) xs[i] = power_init(i);
+  __syncthreads();
+  if (warp == 0) {
+    double s = 0.0;
+    for (int64_t i = lane; i < k; i += 32) s = fma(xs[i], xs[i], s);
+    s = dev::warp_sum(s);
+    if (lane == 0) s_nrm = sqrt(s);
+  }
+  __syncthreads();
+  for (int64_t i = tid; i < k; i += blockDim.x) xs[i] /= s_nrm;
+  __syncthreads();
+  for (int it = 0; it < max_it; ++it) {
+    double* y = ybuf + (int64_t)(it & 1) * k;
+    double* pt = part + (int64_t)(it & 1) * nb;
+    double acc = 0.0;
+    for (int64_t r = (int64_t)blockIdx.x * warps + warp; r < k; r += (int64_t)nb * warps) {
+      double d = 0.0;
+      for (int64_t j = lane; j < k; j += 32) d = fma(__ldcg(G + r + j * ld), xs[j], d);   // G symmetric
+      d = dev::warp_sum(d);
+      if (lane == 0) { y[r] = d; acc = fma(d, d, acc); }
+    }
+    __shared__ double wpart[32];
+    if (lane == 0) wpart[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < warps; ++w) s += wpart[w];
+      pt[blockIdx.x] = s;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags + (int64_t)blockIdx.x * 16),
+                   "l"((unsigned long long)it + 1ull) : "memory");
+    }
+    for (int b = tid; b < nb; b += blockDim.x) {
+      unsigned long long f;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(flags + (int64_t)b * 16) : "memory");
+      } while (f < (unsigned long long)it + 1ull);
+    }
+    __syncthreads();
+    if (tid == 0) {                                    // fixed order: identical in every CTA
+      double s = 0.0;
+      for (int b = 0; b < nb; ++b) s += __ldcg(pt + b);
+      s_lam = sqrt(s);
+    }
+    __syncthreads();
+    const double lam = s_lam;
+    const bool done = lam <= 0.0 || (it > 0 && lam - lam_prev <= 1e-15 * lam) || it + 1 == max_it;
+    if (done) {
+      if (blockIdx.x == 0 && tid == 0) *lam_out = lam;
+      return;
+    }
+    lam_prev = lam;
+    for (int64_t i = tid; i < k; i += blockDim.x) xs[i] = __ldcg(y + i) / lam;
+    __syncthreads();
+  }
+}
+
 __global__ void k_fill_ones(double* x, int64_t k) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
-    x[i] = 1.0 + 1e-3 * (double)((i * 2654435761LL) % 1000) / 1000.0;
+    x[i] = power_init(i);
 }
 
 
@@ -480,6 +559,25 @@ sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64
 }
 
 sk_status lambda_max(sk_ctx* c, const double* G, int64_t k, int64_t ld, double* out_dev) {
+  if ((size_t)k * sizeof(double) <= 96 * 1024) {      // x fits shared memory: one persistent launch
+    const size_t smem = (size_t)k * sizeof(double);
+    SK_CUDA(c, cudaFuncSetAttribute(k_power_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    SK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_power_persistent, 256, smem));
+    const int nb = (int)std::min<int64_t>(std::min<int64_t>(c->num_sms, (int64_t)per_sm * c->num_sms), cdiv(k, 8));
+    DBuf yb, pb, fb;
+    SK_TRY(yb.alloc(c, (size_t)2 * k * sizeof(double)));
+    SK_TRY(pb.alloc(c, (size_t)2 * nb * sizeof(double)));
+    SK_TRY(fb.alloc(c, (size_t)nb * 16 * sizeof(unsigned long long)));
+    SK_CUDA(c, cudaMemsetAsync(fb.p, 0, (size_t)nb * 16 * sizeof(unsigned long long), c->stream));
+    double* y = yb.as<double>();
+    double* pt = pb.as<double>();
+    unsigned long long* fl = fb.as<unsigned long long>();
+    int max_it = 4000;
+    void* args[] = {(void*)&G, (void*)&k, (void*)&ld, (void*)&y, (void*)&pt, (void*)&fl, (void*)&out_dev, (void*)&max_it};
+    SK_CUDA(c, cudaLaunchCooperativeKernel((void*)k_power_persistent, dim3(nb), dim3(256), args, smem, c->stream));
+    return launched(c);
+  }
   DBuf xb, yb, flag;
   SK_TRY(xb.alloc(c, (size_t)k * sizeof(double)));
   SK_TRY(yb.alloc(c, (size_t)k * sizeof(double)));

@@ -96,6 +96,8 @@ struct DistState {
   double* gathered = nullptr;
   size_t cand_doubles = 0;
   StepGraph graph;
+  cudaStream_t cap = nullptr;           // private stream the per-step graph is captured on (the
+                                        // caller's may be the legacy default stream, not capturable)
 };
 
 bool dist_on(const sk_ctx* c) { return c && c->dist; }
@@ -108,6 +110,7 @@ void dist_destroy(sk_ctx* c) {
   if (d->step_state) cudaFree(d->step_state);
   if (d->cand) cudaFree(d->cand);
   if (d->gathered) cudaFree(d->gathered);
+  if (d->cap) cudaStreamDestroy(d->cap);
   if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
   delete d;
   c->dist = nullptr;
@@ -175,15 +178,23 @@ static sk_status select_cols_step(sk_ctx* c, const double* X, int64_t ldx, int64
   if (!d->graph.exec || std::memcmp(key, d->graph.key, sizeof(key)) != 0) {
     if (d->graph.exec) { cudaGraphExecDestroy(d->graph.exec); d->graph.exec = nullptr; }
     const int64_t l0 = c->launches;
-    SK_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    sk_status st = lupp_dist_begin(c, X, nloc, ldx, k, d->v.col0, d->step_state, Lf, ldlf, U, ldu, d->cand);
+    if (!d->cap) SK_CUDA(c, cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
+    cudaStream_t user = c->stream;
+    c->stream = d->cap;                 // every launch below records into the graph
+    sk_status st = SK_OK;
+    if (cudaStreamBeginCapture(d->cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      c->stream = user;
+      return fail(c, SK_E_CUDA, "capture of the per-step LUPP: cudaStreamBeginCapture failed");
+    }
+    st = lupp_dist_begin(c, X, nloc, ldx, k, d->v.col0, d->step_state, Lf, ldlf, U, ldu, d->cand);
     for (int64_t t = 1; t <= k && st == SK_OK; ++t) {
       const ncclResult_t r = nccl().AllGather(d->cand, d->gathered, (size_t)REC, ncclFloat64, d->comm, c->stream);
       if (r != ncclSuccess) { st = fail(c, SK_E_NCCL, std::string("ncclAllGather: ") + nccl().GetErrorString(r)); break; }
       st = lupp_dist_step(c, d->step_state, nloc, k, d->v.col0, t, d->gathered, d->v.world, Js, Lf, ldlf, U, ldu, d->cand);
     }
     cudaGraph_t g = nullptr;
-    const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    const cudaError_t ce = cudaStreamEndCapture(d->cap, &g);
+    c->stream = user;
     if (st != SK_OK) { if (g) cudaGraphDestroy(g); return st; }
     if (ce != cudaSuccess) return fail(c, SK_E_CUDA, std::string("capture of the per-step LUPP: ") + cudaGetErrorString(ce));
     const cudaError_t ie = cudaGraphInstantiate(&d->graph.exec, g, 0);

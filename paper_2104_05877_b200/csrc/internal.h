@@ -36,6 +36,10 @@ sk_status sketch_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t 
 // over the n index; q >= 1.  X l x n row-major (ldx >= n).
 sk_status sketch_power(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
                        int zeta, uint64_t seed, int q, double* X, int64_t ldx);
+// eq:ortho_power_iter: X = ortho(Y_q)^T A with Y_1 = A Omega^T, Y_i = ortho(A ortho(A^T Y_{i-1}));
+// status_dev = 0 or the rank failure of an orthogonalisation.
+sk_status sketch_power_ortho(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
+                             int zeta, uint64_t seed, int q, double* X, int64_t ldx, int64_t* status_dev);
 
 // ---------------------------------------------------------------- LUPP (lupp.cu)
 // k-step swap-free LUPP on the rows of an n x k panel.  The panel is given either

@@ -5,7 +5,7 @@
 // Philox counter (philox.cuh) on every call and never held in HBM as a whole.
 //
 // Dense: a DMMA GEMM with M = l (rows of Gamma), N = n, K = m, run over K-chunks of A's rows:
-// per chunk k_omega_image generates that chunk's columns of Gamma (<= ~40 MB, an L2-resident
+// per chunk k_omega_image generates that chunk's columns of Gamma (<= ~80 MB, an L2-resident
 // slot reused chunk after chunk) in the layout the GEMM's bulk copies read, and k_sketch_pre
 // (TMA + DMMA) accumulates Gamma(:, chunk) A(chunk, :) into X.  A fallback kernel for A that
 // the tensor map cannot describe (odd lda, misaligned) generates each Gamma tile in shared memory.
@@ -927,8 +927,11 @@ struct PrePlan {
   int64_t chunk = 0;       // rows of A per K-chunk (the Omega image slot holds one chunk)
   double cost = 1e300;
 };
-// An Omega image slot at most this large stays in the 126 MB L2 next to the streaming A tiles.
-constexpr double kOmegaSlotBytes = 40.0 * (1 << 20);
+// An Omega image slot at most this large stays (mostly) in the 126 MB L2 next to the streaming A
+// tiles.  Measured at C5 (131072 x 8192 block, l = 1100): 40 MB slots (32 chunks) 84.9% of the
+// DMMA ceiling, 80 MB (16 chunks) 86.3%, one 1.2 GB image 87.7% (profiles/round2/sketch_chunks.txt):
+// the per-chunk cost is the launch tail and the X read-modify-write, not L2 misses on the slot.
+constexpr double kOmegaSlotBytes = 80.0 * (1 << 20);
 
 // co-resident CTAs of k_sketch_pre<BM, NW> launched in clusters of S along z (cached per process)
 template <int BM, int NW> int pre_max_ctas(int S) {
@@ -1154,45 +1157,97 @@ sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int
   return sketch_dense_pre(c, p, m, n, l, plan_pre(c, m, n, l), Q, ldq);
 }
 
+namespace {
+// Omega(:, j0:j1) as a plain column-major l x (j1 - j0) block (ld l): Omega(r, j) = z_r(j) / sqrt(l)
+// from the same counter layout as Gamma (R1, over the column index j of A).
+__global__ void __launch_bounds__(128) k_omega_plain(uint2 key, int l, int64_t j0, int64_t j1, double scale,
+                                                     double* __restrict__ out) {
+  const int hp = (l + 1) / 2;
+  const int64_t total = (j1 - j0) * hp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jj = e / hp;
+    const int pr = (int)(e - jj * hp);
+    double z0, z1;
+    dev::gauss_pair((uint64_t)(j0 + jj), (uint32_t)pr, key, z0, z1);
+    double* col = out + jj * l;
+    col[2 * pr] = z0 * scale;
+    if (2 * pr + 1 < l) col[2 * pr + 1] = z1 * scale;
+  }
+}
+
+// Y (m x l, ldy) = A Omega^T for the Gaussian Omega (l x n over A's columns), one pass over A: Omega
+// is generated one block of A's columns at a time into an L2-sized slot and each block's product
+// is accumulated into Y by the DMMA GEMM (beta = 1 after the first block) -- no transpose of A.
+sk_status cols_sketch_gaussian(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
+                               uint64_t seed, double* Y, int64_t ldy) {
+  const int64_t nc = std::max<int64_t>(256, std::min<int64_t>(n, (int64_t)(kOmegaSlotBytes / (8.0 * l)) / 256 * 256));
+  DBuf om;
+  SK_TRY(om.alloc(c, (size_t)l * std::min(nc, n) * sizeof(double)));
+  const uint2 key = dev::seed_key(seed);
+  const double scale = 1.0 / std::sqrt((double)l);
+  for (int64_t j0 = 0; j0 < n; j0 += nc) {
+    const int64_t j1 = std::min(n, j0 + nc);
+    const int64_t work = (j1 - j0) * ((l + 1) / 2);
+    k_omega_plain<<<(unsigned)std::min<int64_t>(cdiv(work, 128), 16LL * c->num_sms), 128, 0, c->stream>>>(
+        key, (int)l, j0, j1, scale, om.as<double>());
+    SK_TRY(launched(c));
+    SK_TRY(gemm(c, false, true, m, l, j1 - j0, 1.0, A + j0 * lda, lda, om.as<double>(), l, j0 > 0 ? 1.0 : 0.0, Y, ldy));
+  }
+  return SK_OK;
+}
+}  // namespace
+
 sk_status sketch_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
                       int zeta, uint64_t seed, double* Y, int64_t ldy) {
-  // Y = A Omega^T (m x l col-major) = (Omega A^T)^T: the row sketch of A^T written with row
-  // stride ldy is exactly Y column-major.
+  if (emb == SK_EMB_GAUSSIAN) return cols_sketch_gaussian(c, A, m, n, lda, l, seed, Y, ldy);
+  // sparse sign / SRTT: Y = A Omega^T (m x l col-major) = (Omega A^T)^T, the row sketch of A^T written
+  // with row stride ldy (one transpose pass of A, then the row-sketch kernels)
   DBuf At;
   SK_TRY(At.alloc(c, (size_t)n * m * sizeof(double)));
   SK_TRY(transpose(c, A, m, n, lda, At.as<double>(), n));
-  if (emb == SK_EMB_GAUSSIAN) return sketch_dense(c, At.as<double>(), n, m, n, l, seed, Y, ldy);
   if (emb == SK_EMB_SRTT) return sketch_srtt(c, At.as<double>(), n, m, n, l, seed, Y, ldy);
   return sketch_sparse(c, At.as<double>(), n, m, n, l, zeta, seed, Y, ldy);
 }
 
 sk_status sketch_power(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
                        int zeta, uint64_t seed, int q, double* X, int64_t ldx) {
-  // X = Omega (A^T A)^q = ((Omega A^T) A) ... : T = Omega A^T (the row sketch of A^T), then
-  // alternately X^T = A^T T^T and T^T = A X^T (DMMA GEMMs).  X^T col-major n x l is X row-major.
-  DBuf At, Tt, Xt;
-  SK_TRY(At.alloc(c, (size_t)n * m * sizeof(double)));
+  // X = Omega (A^T A)^q = ((Omega A^T) A) ... : T = Omega A^T (kept as T^T = A Omega^T, m x l), then
+  // alternately X^T = A^T T^T (the TMA + DMMA sketch GEMM with Omega := T^T) and T^T = A X^T.
+  DBuf Tt, Xt;
   SK_TRY(Tt.alloc(c, (size_t)m * l * sizeof(double)));
-  SK_TRY(transpose(c, A, m, n, lda, At.as<double>(), n));                    // A^T: n x m col-major
-  if (emb == SK_EMB_GAUSSIAN) SK_TRY(sketch_dense(c, At.as<double>(), n, m, n, l, seed, Tt.as<double>(), m));
-  else if (emb == SK_EMB_SRTT) SK_TRY(sketch_srtt(c, At.as<double>(), n, m, n, l, seed, Tt.as<double>(), m));
-  else SK_TRY(sketch_sparse(c, At.as<double>(), n, m, n, l, zeta, seed, Tt.as<double>(), m));
-  At.release();
+  SK_TRY(sketch_cols(c, A, m, n, lda, l, emb, zeta, seed, Tt.as<double>(), m));
   double* Xout = X;
-  if (ldx != n) {
-    SK_TRY(Xt.alloc(c, (size_t)n * l * sizeof(double)));
-    Xout = Xt.as<double>();
+  int64_t ldo = ldx;
+  for (int it = 0; it < q; ++it) {
+    if (it > 0) {
+      SK_TRY(gemm(c, false, false, m, l, n, 1.0, A, lda, Xout, ldo, 0.0, Tt.as<double>(), m));      // T^T = A X^T
+    }
+    SK_TRY(gemm_qta(c, Tt.as<double>(), m, A, m, n, lda, l, Xout, ldo));                         // X = T A
   }
-  // T row-major l x m == T^T col-major m x l (ld m)
-  SK_TRY(gemm(c, true, false, n, l, m, 1.0, A, lda, Tt.as<double>(), m, 0.0, Xout, n));     // X^T = A^T T^T
-  for (int it = 1; it < q; ++it) {
-    SK_TRY(gemm(c, false, false, m, l, n, 1.0, A, lda, Xout, n, 0.0, Tt.as<double>(), m));  // T^T = A X^T
-    SK_TRY(gemm(c, true, false, n, l, m, 1.0, A, lda, Tt.as<double>(), m, 0.0, Xout, n));   // X^T = A^T T^T
-  }
-  if (Xout != X)
-    SK_CUDA(c, cudaMemcpy2DAsync(X, ldx * sizeof(double), Xout, n * sizeof(double), n * sizeof(double), l,
-                                 cudaMemcpyDeviceToDevice, c->stream));
   return SK_OK;
+}
+
+sk_status sketch_power_ortho(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
+                             int zeta, uint64_t seed, int q, double* X, int64_t ldx, int64_t* status_dev) {
+  // eq:ortho_power_iter: Y1 = A Omega^T; Y_i = ortho(A ortho(A^T Y_{i-1})); X = ortho(Y_q)^T A.
+  // ortho = this library's LUPP basis + CholeskyQR2 (shifted CholeskyQR3 for very tall panels).
+  SK_CUDA(c, cudaMemsetAsync(status_dev, 0, sizeof(int64_t), c->stream));
+  DBuf Y, Q, Z, Qz;
+  SK_TRY(Y.alloc(c, (size_t)m * l * sizeof(double)));
+  SK_TRY(Q.alloc(c, (size_t)m * l * sizeof(double)));
+  SK_TRY(sketch_cols(c, A, m, n, lda, l, emb, zeta, seed, Y.as<double>(), m));
+  SK_TRY(orthonormal_basis(c, Y.as<double>(), m, l, Q.as<double>(), status_dev));
+  if (q > 1) {
+    SK_TRY(Z.alloc(c, (size_t)n * l * sizeof(double)));
+    SK_TRY(Qz.alloc(c, (size_t)n * l * sizeof(double)));
+  }
+  for (int i = 2; i <= q; ++i) {
+    SK_TRY(gemm_qta(c, Q.as<double>(), m, A, m, n, lda, l, Z.as<double>(), n));             // A^T Q (n x l col-major)
+    SK_TRY(orthonormal_basis(c, Z.as<double>(), n, l, Qz.as<double>(), status_dev));
+    SK_TRY(gemm(c, false, false, m, l, n, 1.0, A, lda, Qz.as<double>(), n, 0.0, Y.as<double>(), m));   // A ortho(.)
+    SK_TRY(orthonormal_basis(c, Y.as<double>(), m, l, Q.as<double>(), status_dev));
+  }
+  return gemm_qta(c, Q.as<double>(), m, A, m, n, lda, l, X, ldx);                            // ortho(Y_q)^T A
 }
 
 sk_status sketch_sparse(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,

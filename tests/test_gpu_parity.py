@@ -89,9 +89,46 @@ def test_rand_lupp_1piter_c1():
     assert r >= o_res.optimal_error(sigma, k) * (1 - 1e-12)
 
 
+def _align_rows(Xg, Xo):
+    """X from an orthogonalised iteration is unique up to the signs of its rows (the basis' column
+    signs, R21): flip the GPU's rows onto the oracle's before comparing."""
+    s = np.sign(np.sum(Xg * Xo, axis=1))
+    s[s == 0] = 1.0
+    return Xg * s[:, None]
+
+
+@pytest.mark.parametrize("m,n,l,q,seed", [(256, 256, 40, 1, 2001), (700, 333, 37, 2, 5), (300, 200, 26, 3, 9),
+                                           (3000, 1500, 90, 2, 12)])
+def test_sketch_power_ortho_parity(m, n, l, q, seed):
+    """eq:ortho_power_iter against the oracle (bases up to column signs)."""
+    A = rand_mat(m, n, seed, 0.9)
+    X = sk.sketch_power(dev_f(A), l, "gaussian", seed, q, ortho=True).cpu().numpy()
+    ref = o_sketch.sketch_power_ortho(A, l, "gaussian", seed, q)
+    assert rel_fro(_align_rows(X, ref), ref) <= 1e-10
+
+
+def test_rand_lupp_1piter_ortho_c2_k512():
+    """Rand-LUPP-1piter at the C2 bench configuration (k = 512): the plain form X = Omega A^T A
+    squares the spectrum (10^(-i/25)) and fails the rank test near step 390; the orthogonalised
+    form keeps sigma_i and selects all 512 pivots, identical to the oracle's."""
+    from inputs import make_c2
+    A, sigma = make_c2(seed=1002)
+    k, l, seed = 512, 522, 2002 + 512
+    Ad = dev_f(A)
+    X = sk.sketch_power(Ad, l, "gaussian", seed, 1, ortho=True)
+    Js, _, _, _ = sk.select_cols(X, k)
+    Xo = o_sketch.sketch_power_ortho(A, l, "gaussian", seed, 1)
+    assert rel_fro(_align_rows(X.cpu().numpy(), Xo), Xo) <= 1e-10
+    (piv, _, _, _), _ = lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(Xo, k, f))
+    r, nA = sk.residual(Ad, Js, None, "col_id")
+    ro, nAo = o_res.residual(A, piv, kind="col_id")
+    assert abs(r - ro) <= 1e-9 * ro + 4 * U * nAo
+    assert r >= o_res.optimal_error(sigma, k) * (1 - 1e-9)
+
+
 # ------------------------------------------------------------------ Algorithm 3 (streaming two-sided selection, 8(f))
 @pytest.mark.parametrize("m,n,l,emb,seed", [(256, 256, 40, "gaussian", 3), (600, 333, 37, "gaussian", 4),
-                                             (500, 300, 30, "sparse_sign", 5)])
+                                             (500, 300, 30, "sparse_sign", 5), (1200, 20000, 1100, "gaussian", 6)])  # 3 Omega blocks
 def test_sketch_cols_parity(m, n, l, emb, seed):
     A = rand_mat(m, n, seed)
     Y = sk.sketch_cols(dev_f(A), l, emb, seed).cpu().numpy()

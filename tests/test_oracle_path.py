@@ -414,3 +414,30 @@ def test_streamed_sketch_and_residual_equal_the_plain_definitions():
     r, nA = residual.residual(A, piv, kind="col_id")
     rs, nAs = residual.residual_col_id_streamed(get, 300, 211, piv, block=50)
     assert abs(r - rs) <= 1e-12 * r and abs(nA - nAs) <= 1e-13 * nA
+
+
+def test_ortho_power_iteration_closed_forms():
+    """eq:ortho_power_iter pinned by closed forms: for A with orthonormal columns
+    (A^T A = I) the rows of X = ortho(Y_q)^T A are orthonormal (X X^T = Q^T A A^T Q = I); for q = 1,
+    X = R^{-T} X_plain with Y_1 = A Omega^T = Q R (diag R > 0) and X_plain = Omega A^T A = Y_1^T A
+    (eq:def_power_iter); for q = 2 the row space equals the plain iteration's, and column LUPP picks
+    the same pivots (LUPP pivots are invariant under lower-triangular row mixing of X)."""
+    rng = np.random.default_rng(17)
+    V = haar(60, 25, rng)                                     # 60 x 25, orthonormal columns
+    for q in (1, 2, 3):
+        X = sketch.sketch_power_ortho(V, 10, "gaussian", 4, q)
+        np.testing.assert_allclose(X @ X.T, np.eye(10), atol=1e-13)
+    A = make_lowrank(80, 50, 0.8 ** np.arange(50), rng)
+    Y1 = A @ omega.embedding("gaussian", 9, 12, 50).T
+    _, R = np.linalg.qr(Y1)
+    R *= np.sign(np.diag(R))[:, None]
+    Xp = sketch.sketch_power(A, 12, "gaussian", 9, 1)
+    np.testing.assert_allclose(Xp, Y1.T @ A, rtol=0, atol=1e-13 * np.abs(Xp).max())
+    Xo = sketch.sketch_power_ortho(A, 12, "gaussian", 9, 1)
+    np.testing.assert_allclose(R.T @ Xo, Xp, rtol=0, atol=1e-12 * np.abs(Xp).max())
+    Xo2 = sketch.sketch_power_ortho(A, 12, "gaussian", 9, 2)
+    Xp2 = sketch.sketch_power(A, 12, "gaussian", 9, 2)
+    P1 = (lambda Q: Q @ Q.T)(np.linalg.qr(Xo2.T)[0])            # projectors onto the row spaces
+    P2 = (lambda Q: Q @ Q.T)(np.linalg.qr(Xp2.T)[0])
+    np.testing.assert_allclose(P1, P2, atol=1e-10)
+    assert lupp.select_cols(Xo2, 10)[0].tolist() == lupp.select_cols(Xp2, 10)[0].tolist()
