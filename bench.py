@@ -58,7 +58,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--piter", type=int, default=0, help="plain power iterations (Rand-LUPP-qpiter, P:527)")
+    ap.add_argument("--piter", type=int, default=0,
+                    help="power iterations (Rand-LUPP-qpiter, P:527): orthogonalised, eq:ortho_power_iter (P:216-224)")
+    ap.add_argument("--plain-piter", action="store_true", help="the plain X = Omega (A^T A)^q of eq:def_power_iter instead")
     ap.add_argument("--dist-exchange", default="replicate", choices=["replicate", "step", "p2p"],
                     help="N > 1: column-LUPP exchange -- one k x n all-gather then replicated LUPP, one "
                          "all-gather of P records per pivot step (CUDA graph), or the records stored into "
@@ -71,9 +73,10 @@ def workload(args):
     cfg = CONFIGS[args.config]
     if args.k is None:
         args.k = {"C1": 20, "C2": 512, "C3": 500, "C4": 200, "C5": 1000}[args.config]
-        if getattr(args, "piter", 0) and args.config == "C2":
-            # X = Omega (A^T A)^q squares the C2 spectrum (10^(-i/25)): beyond k ~ 390 the sketch is
-            # rank deficient at LUPP's 1e-14 threshold (both the oracle and the GPU stop there)
+        if getattr(args, "piter", 0) and args.config == "C2" and getattr(args, "plain_piter", False):
+            # the PLAIN X = Omega (A^T A)^q squares the C2 spectrum (10^(-i/25)): beyond k ~ 390 the
+            # sketch is rank deficient at LUPP's 1e-14 threshold (both the oracle and the GPU stop there);
+            # the orthogonalised iteration (the default) runs at k = 512
             args.k = 256
     k = args.k
     l = cfg["l"](k)
@@ -84,7 +87,10 @@ def workload(args):
               f"reflectors, built on the device; Gaussian Omega, k={k}, l={l}",
     }.get(args.config, f"{args.config} k={k} l={l}")
     if getattr(args, "piter", 0):
-        desc += f", {args.piter} plain power iteration(s) X = Omega (A^T A)^q (Rand-LUPP-{args.piter}piter)"
+        desc += (f", {args.piter} plain power iteration(s) X = Omega (A^T A)^q (Rand-LUPP-{args.piter}piter)"
+                 if getattr(args, "plain_piter", False) else
+                 f", {args.piter} orthogonalised power iteration(s) X = ortho(Y_q)^T A (eq:ortho_power_iter, "
+                 f"Rand-LUPP-{args.piter}piter)")
     return cfg, k, l, seed, desc
 
 
@@ -107,12 +113,17 @@ def cpu_info():
     return cores, model
 
 
-def oracle_selection(A, k, l, seed, emb="gaussian", piter=0):
-    """The oracle's sketch (with q = piter plain power iterations) + LUPP (test infrastructure;
-    timed as the CPU baseline)."""
+def oracle_selection(A, k, l, seed, emb="gaussian", piter=0, plain=False):
+    """The oracle's sketch (with q = piter power iterations, orthogonalised unless plain) + LUPP
+    (test infrastructure; timed as the CPU baseline)."""
     from oracle import lupp as o_lupp
     from oracle import sketch as o_sketch
-    X = o_sketch.sketch(A, l, emb, seed) if piter == 0 else o_sketch.sketch_power(A, l, emb, seed, piter)
+    if piter == 0:
+        X = o_sketch.sketch(A, l, emb, seed)
+    elif plain:
+        X = o_sketch.sketch_power(A, l, emb, seed, piter)
+    else:
+        X = o_sketch.sketch_power_ortho(A, l, emb, seed, piter)
     piv, _, _, _ = o_lupp.select_cols(X, k)
     return piv
 
@@ -262,11 +273,11 @@ def run_reference(args):
     steps = max(1, min(args.steps, 3))
     warm = min(args.warmup, 1)
     for _ in range(warm):
-        oracle_selection(A, k, l, seed, cfg["emb"], args.piter)
+        oracle_selection(A, k, l, seed, cfg["emb"], args.piter, args.plain_piter)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        oracle_selection(A, k, l, seed, cfg["emb"], args.piter)
+        oracle_selection(A, k, l, seed, cfg["emb"], args.piter, args.plain_piter)
         times.append((time.perf_counter() - t0) * 1e3)
     v = statistics.mean(times)
     line = {
@@ -447,7 +458,7 @@ def main():
         nxt = iter(e[1:])
         e[0].record(stream)
         X = (sk.sketch(A, l, emb, seed, cfg.get("zeta", 8)) if args.piter == 0
-             else sk.sketch_power(A, l, emb, seed, args.piter, cfg.get("zeta", 8)))
+             else sk.sketch_power(A, l, emb, seed, args.piter, cfg.get("zeta", 8), ortho=not args.plain_piter))
         next(nxt).record(stream)
         Js, Lf, _, _ = sk.select_cols(X, k, check=False)
         next(nxt).record(stream)
@@ -580,7 +591,7 @@ def main():
         t0 = time.perf_counter()
         from oracle.lupp import RankError
         try:
-            piv_o = oracle_selection(A_np, k, l, seed, emb, args.piter)
+            piv_o = oracle_selection(A_np, k, l, seed, emb, args.piter, args.plain_piter)
         except RankError as err:          # the selection is rank deficient at this k (both sides stop)
             piv_o = None
             fail_step = err.step

@@ -35,6 +35,7 @@
 #ifndef SKEL_H_
 #define SKEL_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -67,12 +68,18 @@ typedef enum { SK_EMB_GAUSSIAN = 0, SK_EMB_SPARSE_SIGN = 1, SK_EMB_SRTT = 2 } sk
  *   COL_ID    ||A - C C^+ A||              eq:def_column_id
  *   ROW_ID    ||A - A R^+ R||              eq:def_row_id,
  *   CUR       ||A - Q_C (Q_C^T A Q_R) Q_R^T||   stable CUR, Remark 2.3
- *   ID_COEFFS ||A - C Z||                  eq:colID, with Z from sk_id_coeffs */
+ *   ID_COEFFS ||A - C Z||                  eq:colID, with Z from sk_id_coeffs (or the
+ *                                          column-ID estimate X_1^+ X of sk_id_estimate_cols)
+ *   ROW_COEFFS ||A - W R||                 R = A(I_s, :), W (m x k) given -- e.g. the row-ID estimate
+ *                                          Y Y_1^+ of sk_id_estimate_rows
+ *   CUR_CSS   ||A - C S^{-1} R||           S = A(I_s, J_s): the sketch-free CUR estimate */
 typedef enum {
   SK_RES_COL_ID = 0,
   SK_RES_ROW_ID = 1,
   SK_RES_CUR = 2,
-  SK_RES_ID_COEFFS = 3
+  SK_RES_ID_COEFFS = 3,
+  SK_RES_ROW_COEFFS = 4,
+  SK_RES_CUR_CSS = 5
 } sk_residual_kind;
 
 /* ---- context ----------------------------------------------------------- */
@@ -164,6 +171,32 @@ sk_status sk_set_sketch_tuning(sk_ctx* ctx, int32_t path, int32_t bm, int32_t sp
  * and SRTT: the row sketch of a transposed copy of A. */
 sk_status sk_sketch_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
                          sk_embedding emb, int32_t zeta, uint64_t seed, double* Y, int64_t ldy);
+
+/* ---- Algorithm 3's dual sketch in ONE pass over A ----
+ * X = Gamma A (lx x n row-major, ldx >= n; Gamma over A's rows from seed_x, exactly sk_sketch's) and
+ * Y = A Omega^T (m x ly column-major, ldy >= m; Omega over A's columns from seed_y, exactly
+ * sk_sketch_cols') -- independent embeddings (Alg. 3 line 1) -- computed block by block: each
+ * L2-sized block of A (<= ~48 MB) is read from HBM once by the X product and again, from L2, by the Y
+ * product.  Gaussian only (SK_E_ARG otherwise); A 16-byte aligned with an even lda (the tensor-map
+ * rules; SK_E_ARG otherwise).  Requires 1 <= lx <= m, 1 <= ly <= n. */
+sk_status sk_sketch_dual(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t lx, int64_t ly,
+                         sk_embedding emb, uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y,
+                         int64_t ldy);
+
+/* ---- sketch-only ID estimates without revisiting A ----
+ * sk_id_estimate_cols: Z = X_1^+ X (k x n column-major, ldz >= k), X_1 = X(:, Js) the lx x k column
+ *   pivots of the row sketch (C^+ A ~ X_1^+ X; Z(:, Js) = I up to rounding).
+ * sk_id_estimate_rows: W = Y Y_1^+ (m x k column-major, ldw >= m), Y_1 = Y(Is, :) the k x ly row
+ *   pivots of the column sketch (A R^+ ~ Y Y_1^+).
+ * Both through the row LUPP of the pivot block (B1 = Lf U, |Lf| <= 1) and the Cholesky factor of
+ * Lf^T Lf, i.e. without forming the normal equations of B1.  Require 1 <= k <= min(l, n or m).
+ * info as for sk_select_cols (SK_E_RANK if the pivot block is numerically rank deficient).
+ * The residuals ||A - C Z|| / ||A - W R|| / ||A - C S^{-1} R|| are sk_residual kinds ID_COEFFS /
+ * ROW_COEFFS / CUR_CSS. */
+sk_status sk_id_estimate_cols(sk_ctx* ctx, const double* X, int64_t lx, int64_t n, int64_t ldx, const int64_t* Js,
+                              int64_t k, double* Z, int64_t ldz, int64_t* info);
+sk_status sk_id_estimate_rows(sk_ctx* ctx, const double* Y, int64_t m, int64_t ly, int64_t ldy, const int64_t* Is,
+                              int64_t k, double* W, int64_t ldw, int64_t* info);
 
 /* ---- S1 with power iterations (Rand-LUPP-1piter) ----
  * X = Omega (A^T A)^q, the plain power-iteration row-space approximator of eq:def_power_iter

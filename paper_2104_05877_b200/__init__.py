@@ -9,5 +9,6 @@ from .api import (  # noqa: F401
     DistSession, COL_ID, CUR, GAUSSIAN, ID_COEFFS, ROW_ID, SPARSE_SIGN, SkelError, context, fortran, gather_cols,
     gather_cols_shard, id_coeffs, launch_count, rand_lupp, residual, residual_cols, select_cols, select_cols_cpqr, select_cols_deim,
     LuppDist, LuppDistP2P, ipc_alloc, ipc_close, ipc_export, ipc_free, ipc_import, mailbox_bytes, select_rows,
-    set_sketch_tuning, sketch, sketch_cols, sketch_power, stream_select,
+    set_sketch_tuning, sketch, sketch_cols, sketch_dual, sketch_power, stream_select, id_estimate_cols,
+    id_estimate_rows, ROW_COEFFS, CUR_CSS,
 )

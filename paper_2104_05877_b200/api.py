@@ -17,11 +17,12 @@ import torch
 from . import _lib
 
 GAUSSIAN, SPARSE_SIGN, SRTT = 0, 1, 2
-COL_ID, ROW_ID, CUR, ID_COEFFS = 0, 1, 2, 3
+COL_ID, ROW_ID, CUR, ID_COEFFS, ROW_COEFFS, CUR_CSS = 0, 1, 2, 3, 4, 5
 _EMB = {"gaussian": GAUSSIAN, "sparse_sign": SPARSE_SIGN, "srtt": SRTT, GAUSSIAN: GAUSSIAN, SPARSE_SIGN: SPARSE_SIGN,
         SRTT: SRTT}
-_KIND = {"col_id": COL_ID, "row_id": ROW_ID, "cur": CUR, "id_coeffs": ID_COEFFS,
-         COL_ID: COL_ID, ROW_ID: ROW_ID, CUR: CUR, ID_COEFFS: ID_COEFFS}
+_KIND = {"col_id": COL_ID, "row_id": ROW_ID, "cur": CUR, "id_coeffs": ID_COEFFS, "row_coeffs": ROW_COEFFS,
+         "cur_css": CUR_CSS, COL_ID: COL_ID, ROW_ID: ROW_ID, CUR: CUR, ID_COEFFS: ID_COEFFS, ROW_COEFFS: ROW_COEFFS,
+         CUR_CSS: CUR_CSS}
 
 
 class SkelError(RuntimeError):
@@ -159,6 +160,46 @@ def sketch_cols(A, l, embedding="gaussian", seed=0, zeta=8):
     h = context(A.device.index)
     _check(lib().sk_sketch_cols(h, _ptr(A), m, n, lda, l, _EMB[embedding], zeta, seed & (2**64 - 1), _ptr(Y), m), h)
     return Y
+
+
+def sketch_dual(A, lx, ly, seed_x=0, seed_y=1):
+    """Algorithm 3 line 2: X = Gamma A (lx x n, row-major) and Y = A Omega^T (m x ly,
+    column-major) in one pass over A (Gaussian embeddings, independent seeds)."""
+    lda = _colmajor(A, "A")
+    m, n = A.shape
+    X = torch.empty((lx, n), dtype=torch.float64, device=A.device)
+    Y = torch.empty((ly, m), dtype=torch.float64, device=A.device).t()
+    h = context(A.device.index)
+    _check(lib().sk_sketch_dual(h, _ptr(A), m, n, lda, lx, ly, GAUSSIAN, seed_x & (2**64 - 1), seed_y & (2**64 - 1),
+                                _ptr(X), n, _ptr(Y), m), h)
+    return X, Y
+
+
+def id_estimate_cols(X, Js, check=True):
+    """C^+ A ~ X_1^+ X: Z (k x n, column-major) from the row sketch and its column pivots."""
+    lx, n = X.shape
+    k = Js.numel()
+    Z = torch.empty((n, k), dtype=torch.float64, device=X.device).t()
+    info = ctypes.c_int64(0)
+    h = context(X.device.index)
+    st = lib().sk_id_estimate_cols(h, _ptr(X), lx, n, max(X.stride(0), n), _ptr(Js), k, _ptr(Z), k,
+                                   ctypes.byref(info) if check else None)
+    _check(st, h, info.value)
+    return Z
+
+
+def id_estimate_rows(Y, Is, check=True):
+    """A R^+ ~ Y Y_1^+ (P:436): W (m x k, column-major) from the column sketch and its row pivots."""
+    ldy = _colmajor(Y, "Y")
+    m, ly = Y.shape
+    k = Is.numel()
+    W = torch.empty((k, m), dtype=torch.float64, device=Y.device).t()
+    info = ctypes.c_int64(0)
+    h = context(Y.device.index)
+    st = lib().sk_id_estimate_rows(h, _ptr(Y), m, ly, ldy, _ptr(Is), k, _ptr(W), m,
+                                   ctypes.byref(info) if check else None)
+    _check(st, h, info.value)
+    return W
 
 
 def stream_select(A, k, l=None, embedding="gaussian", seed_x=0, seed_y=1, zeta=8):

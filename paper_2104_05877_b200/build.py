@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libskel.so")
-SOURCES = ["capi.cu", "gemm.cu", "sketch.cu", "srtt.cu", "lupp.cu", "cpqr.cu", "dense.cu", "idcoef.cu", "residual.cu", "deim.cu", "lupp_dist.cu", "dist.cu"]
+SOURCES = ["capi.cu", "gemm.cu", "sketch.cu", "srtt.cu", "lupp.cu", "cpqr.cu", "dense.cu", "idcoef.cu", "residual.cu", "deim.cu", "lupp_dist.cu", "dist.cu", "estimates.cu"]
 HEADERS = ["common.cuh", "dmma.cuh", "philox.cuh", "internal.h", "sync.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

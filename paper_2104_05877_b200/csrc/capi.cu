@@ -460,11 +460,14 @@ sk_status sk_residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t 
   } else {
     SK_ARG(c, m >= 1 && n >= 1 && lda >= m && k >= 1 && k <= m && k <= n, "sk_residual: bad sizes");
   }
-  SK_ARG(c, kind >= SK_RES_COL_ID && kind <= SK_RES_ID_COEFFS, "sk_residual: unknown kind");
-  const bool need_js = kind != SK_RES_ROW_ID, need_is = kind == SK_RES_ROW_ID || kind == SK_RES_CUR;
+  SK_ARG(c, kind >= SK_RES_COL_ID && kind <= SK_RES_CUR_CSS, "sk_residual: unknown kind");
+  const bool need_js = kind != SK_RES_ROW_ID && kind != SK_RES_ROW_COEFFS;
+  const bool need_is = kind == SK_RES_ROW_ID || kind == SK_RES_CUR || kind == SK_RES_ROW_COEFFS || kind == SK_RES_CUR_CSS;
   SK_ARG(c, !need_js || Js, "sk_residual: Js required");
   SK_ARG(c, !need_is || Is, "sk_residual: Is required");
   SK_ARG(c, kind != SK_RES_ID_COEFFS || (Z && ldz >= k), "sk_residual: Z (ldz >= k) required");
+  SK_ARG(c, kind != SK_RES_ROW_COEFFS || (Z && ldz >= m), "sk_residual: W (passed as Z, ldz >= m) required");
+  SK_ARG(c, !dist_on(c) || kind <= SK_RES_ID_COEFFS, "sk_residual: the estimate kinds are single-GPU only");
   SK_CUDA(c, cudaSetDevice(c->device));
   DBuf sums, st;
   SK_TRY(sums.alloc(c, 2 * sizeof(double)));

@@ -518,8 +518,23 @@ sk_status trsm_right_lt(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t l
   return SK_OK;
 }
 
+template <int MODE>
+static sk_status trsm_right_l_impl(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L,
+                                   int64_t ldl);
+
 sk_status trsm_right_l_unit(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L,
                             int64_t ldl) {
+  return trsm_right_l_impl<1>(c, X, rows, k, ldx, L, ldl);
+}
+
+sk_status trsm_right_l(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L, int64_t ldl) {
+  return trsm_right_l_impl<2>(c, X, rows, k, ldx, L, ldl);
+}
+
+// X <- X L^{-1} for a unit (MODE 1) or non-unit (MODE 2) lower L
+template <int MODE>
+static sk_status trsm_right_l_impl(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L,
+                                   int64_t ldl) {
   SK_TRY(dense_attrs(c));
   // X_j <- (X_j - X_>j L_>j,j) L_jj^{-1} (unit lower), 64-wide blocks from the last
   DBuf Wd, Lc;
@@ -532,7 +547,7 @@ sk_status trsm_right_l_unit(sk_ctx* c, double* X, int64_t rows, int64_t k, int64
     const int64_t j1 = j0 + jb;
     SK_CUDA(c, cudaMemcpy2DAsync(Lc.p, TB2 * sizeof(double), L + j0 + j0 * ldl, ldl * sizeof(double),
                                  jb * sizeof(double), jb, cudaMemcpyDeviceToDevice, c->stream));
-    SK_TRY(launch_pdl(c, k_diag_inv<1>, dim3(1), dim3(256), kDiagInvSmem, Lc.as<double>(), (int64_t)TB2, jb,
+    SK_TRY(launch_pdl(c, k_diag_inv<MODE>, dim3(1), dim3(256), kDiagInvSmem, Lc.as<double>(), (int64_t)TB2, jb,
                       Wd.as<double>(), (int64_t)TB2, (int64_t)0, (int64_t*)nullptr));
     if (j1 < k) {
       c->pdl = true;

@@ -29,6 +29,10 @@ sk_status sketch_srtt(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t 
 // the sketch's TMA + DMMA GEMM with Omega = Q^T packed into its image (falls back to gemm()).
 sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int64_t m, int64_t n, int64_t lda,
                    int64_t l, double* X, int64_t ldx);
+// Algorithm 3's dual sketch in one pass over A: X = Gamma A (lx x n row-major), Y = A Omega^T (m x ly
+// col-major), both Gaussian (Gamma over A's rows from seed_x, Omega over A's columns from seed_y).
+sk_status sketch_dual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t lx, int64_t ly,
+                      uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y, int64_t ldy);
 // Y = A Omega^T (m x l col-major, ldy >= m), Omega l x n (Alg. 3 column sketch).
 sk_status sketch_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
                       int zeta, uint64_t seed, double* Y, int64_t ldy);
@@ -102,6 +106,13 @@ sk_status trsm_right_lt(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t l
 // X (rows x k, ldx) <- X * L^{-1} with L unit lower k x k.
 sk_status trsm_right_l_unit(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx,
                             const double* L, int64_t ldl);
+// X (rows x k, ldx) <- X * L^{-1} with L non-unit lower k x k.
+sk_status trsm_right_l(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L, int64_t ldl);
+// out (N x k, ldo) = D B1 (B1^T B1)^{-1} = D (B1^+)^T for B1 p x k (col-major, ld ldb, p >= k, full
+// column rank) and D N x p (ldd): through B1 = Lf U (row LUPP, |Lf| <= 1) so only the well-conditioned
+// Gram Lf^T Lf is factored: out = D Lf (Lf^T Lf)^{-1} U^{-T} (estimates.cu).
+sk_status pinv_apply(sk_ctx* c, const double* B1, int64_t ldb, int64_t p, int64_t k, const double* D, int64_t ldd,
+                     int64_t N, double* out, int64_t ldo, int64_t* status_dev);
 // Q (m x k, ldq) := orthonormal basis of range(Q) by two Cholesky-QR passes.
 sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64_t* status_dev);
 // out[0] = sum of in[0..n) pairs etc: finishes per-CTA partial sums deterministically.

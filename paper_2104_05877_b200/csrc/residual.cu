@@ -64,6 +64,26 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
     SK_TRY(gather_cols(c, A, m, lda, Js, k, C.as<double>(), m));
     return gemm_sumsq(c, false, false, m, n, k, -1.0, C.as<double>(), m, Z, ldz, 1.0, A, lda, sums);
   }
+  if (kind == SK_RES_ROW_COEFFS || kind == SK_RES_CUR_CSS) {
+    // ||A - W R||, R = A(I_s, :): W given (the row-ID estimate Y Y_1^+) or W = C S^{-1}
+    // (the CUR estimate C S^{-1} R) through the row LUPP of S^T (estimates.cu)
+    DBuf Rt, V, Cb, St;
+    SK_TRY(Rt.alloc(c, (size_t)n * k * sizeof(double)));
+    SK_TRY(gather_rows_t(c, A, m, n, lda, Is, k, Rt.as<double>(), n));
+    const double* Wp = Z;
+    int64_t ldw = ldz;
+    if (kind == SK_RES_CUR_CSS) {
+      SK_TRY(Cb.alloc(c, (size_t)m * k * sizeof(double)));
+      SK_TRY(St.alloc(c, (size_t)k * k * sizeof(double)));
+      SK_TRY(V.alloc(c, (size_t)m * k * sizeof(double)));
+      SK_TRY(gather_cols(c, A, m, lda, Js, k, Cb.as<double>(), m));
+      SK_TRY(gather_rows_t(c, Cb.as<double>(), m, k, m, Is, k, St.as<double>(), k));          // S^T = C(I_s, :)^T
+      SK_TRY(pinv_apply(c, St.as<double>(), k, k, k, Cb.as<double>(), m, m, V.as<double>(), m, status_dev));
+      Wp = V.as<double>();
+      ldw = m;
+    }
+    return gemm_sumsq(c, false, true, m, n, k, -1.0, Wp, ldw, Rt.as<double>(), n, 1.0, A, lda, sums);
+  }
   DBuf Qc, Qr, Cb, Rt, W;
   if (kind == SK_RES_COL_ID || kind == SK_RES_CUR) {
     SK_TRY(Cb.alloc(c, (size_t)m * k * sizeof(double)));

@@ -1016,6 +1016,87 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
   return best;
 }
 
+// Omega(:, j0:j1) as a plain column-major l x (j1 - j0) block (ld l): Omega(r, j) = z_r(j) / sqrt(l)
+// from the same counter layout as Gamma (R1, over the column index j of A).
+__global__ void __launch_bounds__(128) k_omega_plain(uint2 key, int l, int64_t j0, int64_t j1, double scale,
+                                                     double* __restrict__ out) {
+  const int hp = (l + 1) / 2;
+  const int64_t total = (j1 - j0) * hp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jj = e / hp;
+    const int pr = (int)(e - jj * hp);
+    double z0, z1;
+    dev::gauss_pair((uint64_t)(j0 + jj), (uint32_t)pr, key, z0, z1);
+    double* col = out + jj * l;
+    col[2 * pr] = z0 * scale;
+    if (2 * pr + 1 < l) col[2 * pr + 1] = z1 * scale;
+  }
+}
+
+// The tensor map of a column-major m x n A (box 16 rows x 64 columns, 128-byte swizzle).
+sk_status make_tmap(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, CUtensorMap* tm) {
+  const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)TBK, (cuuint32_t)PBOX};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tmap_encoder()(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, SK_E_CUDA, "cuTensorMapEncodeTiled failed for A");
+  return SK_OK;
+}
+
+// The Omega image of rows [i0, i1) of A (from Philox, or packed from Q when Qom != nullptr).
+template <int BM, int NW>
+sk_status omega_chunk_image(sk_ctx* c, uint2 key, const double* Qom, int64_t ldq, int64_t l, int64_t i0, int64_t i1,
+                            double* img) {
+  using C = PCfg<BM, NW>;
+  const int64_t mb = cdiv(l, BM), KT = cdiv(i1 - i0, TBK);
+  if (Qom) k_omega_pack<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(Qom, ldq, (int)l, i0, i1, BM, C::OS, KT, img);
+  else k_omega_image<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(key, (int)l, i0, i1, BM, C::OS, KT, img);
+  return launched(c);
+}
+
+// One K-chunk's GEMM: X (+)= Omega(:, p.k0:p.m) A(p.k0:p.m, :) with the chunk's image, K-split
+// `splits_req` ways (partials through `part` or cluster DSMEM); p.accum selects = or +=.
+template <int BM, int NW>
+sk_status pre_gemm_chunk(sk_ctx* c, const CUtensorMap& tm, DenseParams p, int64_t l, int64_t n, int splits_req,
+                         bool cl_allowed, const double* img, double* part) {
+  using C = PCfg<BM, NW>;
+  const int64_t mb = cdiv(l, BM), nb = cdiv(n, C::TBNP), KT = cdiv(p.m - p.k0, TBK);
+  p.k_per_split = cdiv(cdiv(p.m - p.k0, splits_req), TBK) * TBK;
+  const int splits = (int)cdiv(p.m - p.k0, p.k_per_split);
+  const bool clu = cl_allowed && splits > 1 && splits <= 8 && BM % splits == 0;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)mb, (unsigned)nb, (unsigned)splits);
+  lc.blockDim = dim3(C::NT);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (clu) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 1; at[na].val.clusterDim.y = 1; at[na].val.clusterDim.z = (unsigned)splits;
+    ++na;
+  }
+  at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL behind the image kernel
+  at[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  lc.attrs = at; lc.numAttrs = na;
+  if (splits == 1 || clu) {
+    auto kern = clu ? k_sketch_pre<BM, NW, 2> : k_sketch_pre<BM, NW, 0>;
+    SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, img, KT));
+    return launched(c);
+  }
+  p.part = part;
+  auto kern = k_sketch_pre<BM, NW, 1>;
+  SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, img, KT));
+  SK_TRY(launched(c));
+  return splitk_reduce(c, p.part, splits, l, n, p.scale, p.X, p.ldx, p.accum);
+}
+
 // X = Omega A chunk by chunk: per K-chunk, the chunk's Omega image (generated from Philox, or packed
 // from a given Q when Qom != nullptr) then the TMA + DMMA GEMM accumulating into X.
 template <int BM, int NW>
@@ -1024,67 +1105,74 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   using C = PCfg<BM, NW>;
   DenseParams p = p0;
   CUtensorMap tm;
-  const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
-  const cuuint64_t strides[1] = {(cuuint64_t)p.lda * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)TBK, (cuuint32_t)PBOX};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p.A), dims, strides,
-                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(c, SK_E_CUDA, "cuTensorMapEncodeTiled failed for A");
-  const int64_t mb = cdiv(l, BM), nb = cdiv(n, C::TBNP);
+  SK_TRY(make_tmap(c, p.A, m, n, p.lda, &tm));
+  const int64_t mb = cdiv(l, BM);
   const int64_t chunk = pl.chunk > 0 ? pl.chunk : m;
-  const int64_t KTmax = cdiv(chunk, TBK);
   DBuf img, part;
-  SK_TRY(img.alloc(c, (size_t)mb * KTmax * TBK * C::OS * sizeof(double)));   // one chunk's Omega: the slot
+  SK_TRY(img.alloc(c, (size_t)mb * cdiv(chunk, TBK) * TBK * C::OS * sizeof(double)));   // one chunk's Omega: the slot
   const int64_t kps_max = cdiv(cdiv(chunk, pl.splits), TBK) * TBK;
   const int sp_max = (int)cdiv(chunk, kps_max);
   const bool cl = pl.cluster && sp_max > 1 && sp_max <= 8 && BM % sp_max == 0;
   if (sp_max > 1 && !cl) SK_TRY(part.alloc(c, (size_t)sp_max * l * n * sizeof(double)));
   for (int64_t i0 = 0; i0 < m; i0 += chunk) {
     const int64_t i1 = std::min(m, i0 + chunk);
-    const int64_t KT = cdiv(i1 - i0, TBK);
-    if (Qom) {
-      k_omega_pack<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(Qom, ldq, (int)l, i0, i1, BM, C::OS, KT, img.as<double>());
-    } else {
-      k_omega_image<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(p.key, (int)l, i0, i1, BM, C::OS, KT, img.as<double>());
-    }
-    SK_TRY(launched(c));
+    SK_TRY((omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, i0, i1, img.as<double>())));
     p.k0 = i0;
     p.m = i1;
     p.accum = i0 > 0;
-    p.k_per_split = cdiv(cdiv(i1 - i0, pl.splits), TBK) * TBK;
-    const int splits = (int)cdiv(i1 - i0, p.k_per_split);
-    const bool clu = cl && splits == sp_max;
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3((unsigned)mb, (unsigned)nb, (unsigned)splits);
-    lc.blockDim = dim3(C::NT);
-    lc.dynamicSmemBytes = C::SMEM;
-    lc.stream = c->stream;
-    cudaLaunchAttribute at[2];
-    int na = 0;
-    if (clu) {
-      at[na].id = cudaLaunchAttributeClusterDimension;
-      at[na].val.clusterDim.x = 1; at[na].val.clusterDim.y = 1; at[na].val.clusterDim.z = (unsigned)splits;
-      ++na;
-    }
-    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL behind the image kernel
-    at[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-    lc.attrs = at; lc.numAttrs = na;
-    if (splits == 1 || clu) {
-      auto kern = clu ? k_sketch_pre<BM, NW, 2> : k_sketch_pre<BM, NW, 0>;
-      SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, (const double*)img.as<double>(), KT));
+    const int64_t kps = cdiv(cdiv(i1 - i0, pl.splits), TBK) * TBK;
+    const bool clu = cl && cdiv(i1 - i0, kps) == sp_max;
+    SK_TRY((pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, clu, img.as<double>(), part.as<double>())));
+  }
+  return SK_OK;
+}
+
+// Algorithm 3's dual sketch: X = Gamma A (lx x n) and Y = A Omega^T (m x ly) in ONE pass
+// over A in HBM.  A is walked in L2-sized blocks (Kc rows x Nc columns, <= ~48 MB); each block is
+// read by the X GEMM (TMA + DMMA, Gamma's chunk image for the block's rows generated once per row
+// panel) and right after by the Y GEMM (DMMA, Omega's block of columns generated per block), so the
+// second read hits L2.  X accumulates over row panels, Y over column blocks (fixed order).
+template <int BM, int NW>
+sk_status run_dual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t lx, int64_t ly,
+                   uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y, int64_t ldy, int splits) {
+  using C = PCfg<BM, NW>;
+  constexpr double kBlockBytes = 48.0 * (1 << 20);
+  int64_t Nc = std::max<int64_t>(C::TBNP, (int64_t)(kBlockBytes / (8.0 * m)) / C::TBNP * C::TBNP);
+  Nc = std::min(Nc, n);
+  int64_t Kc = m;
+  if ((double)Kc * Nc * 8.0 > kBlockBytes) Kc = std::max<int64_t>(1024, (int64_t)(kBlockBytes / (8.0 * Nc)) / 1024 * 1024);
+  Kc = std::min(Kc, m);
+  const int64_t mb = cdiv(lx, BM);
+  DBuf img, part, om;
+  SK_TRY(img.alloc(c, (size_t)mb * cdiv(Kc, TBK) * TBK * C::OS * sizeof(double)));
+  SK_TRY(om.alloc(c, (size_t)ly * Nc * sizeof(double)));
+  const int64_t kps = cdiv(cdiv(Kc, splits), TBK) * TBK;
+  if (cdiv(Kc, kps) > 1) SK_TRY(part.alloc(c, (size_t)cdiv(Kc, kps) * lx * Nc * sizeof(double)));
+  const uint2 kx = dev::seed_key(seed_x), ky = dev::seed_key(seed_y);
+  const double sy = 1.0 / std::sqrt((double)ly);
+  for (int64_t i0 = 0; i0 < m; i0 += Kc) {
+    const int64_t i1 = std::min(m, i0 + Kc);
+    SK_TRY((omega_chunk_image<BM, NW>(c, kx, nullptr, 0, lx, i0, i1, img.as<double>())));   // Gamma(:, i0:i1)
+    for (int64_t j0 = 0; j0 < n; j0 += Nc) {
+      const int64_t j1 = std::min(n, j0 + Nc);
+      const double* Ab = A + j0 * lda;
+      CUtensorMap tm;
+      SK_TRY(make_tmap(c, Ab, m, j1 - j0, lda, &tm));
+      DenseParams p{};
+      p.A = Ab; p.lda = lda; p.n = j1 - j0; p.l = (int)lx;
+      p.key = kx;
+      p.scale = 1.0 / std::sqrt((double)lx);
+      p.X = X + j0; p.ldx = ldx;
+      p.k0 = i0; p.m = i1; p.accum = i0 > 0;
+      SK_TRY((pre_gemm_chunk<BM, NW>(c, tm, p, lx, j1 - j0, splits, false, img.as<double>(), part.as<double>())));
+      // Y(i0:i1, :) (+)= A(i0:i1, j0:j1) Omega(:, j0:j1)^T -- the block again, now from L2
+      const int64_t work = (j1 - j0) * ((ly + 1) / 2);
+      k_omega_plain<<<(unsigned)std::min<int64_t>(cdiv(work, 128), 16LL * c->num_sms), 128, 0, c->stream>>>(
+          ky, (int)ly, j0, j1, sy, om.as<double>());
       SK_TRY(launched(c));
-      continue;
+      SK_TRY(gemm(c, false, true, i1 - i0, ly, j1 - j0, 1.0, A + i0 + j0 * lda, lda, om.as<double>(), ly,
+                  j0 > 0 ? 1.0 : 0.0, Y + i0, ldy));
     }
-    p.part = part.as<double>();
-    auto kern = k_sketch_pre<BM, NW, 1>;
-    SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, (const double*)img.as<double>(), KT));
-    SK_TRY(launched(c));
-    SK_TRY(splitk_reduce(c, p.part, splits, l, n, p.scale, p.X, p.ldx, p.accum));
   }
   return SK_OK;
 }
@@ -1144,6 +1232,21 @@ sk_status sketch_dense(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t
   return splitk_reduce(c, p.part, splits, l, n, p.scale, X, ldx);
 }
 
+sk_status sketch_dual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t lx, int64_t ly,
+                      uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y, int64_t ldy) {
+  if (n == 0 || m == 0) return SK_OK;
+  if (!tma_ok_for(A, m, n, lda)) return fail(c, SK_E_ARG, "sk_sketch_dual: A must be 16-byte aligned with an even lda");
+  const PrePlan pl = plan_pre(c, m, n, lx);
+  const int bm = pl.bm > 0 ? pl.bm : 48;
+  const int64_t tiles = cdiv(lx, bm) * cdiv(std::min<int64_t>(n, 4096), 256);
+  int splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, cdiv(2LL * c->num_sms, tiles)));
+  while (splits > 1 && m / splits < 512) --splits;
+  if (bm == 64) return run_dual<64, 8>(c, A, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy, splits);
+  if (bm == 32) return run_dual<32, 8>(c, A, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy, splits);
+  if (bm == 40) return run_dual<40, 8>(c, A, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy, splits);
+  return run_dual<48, 8>(c, A, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy, splits);
+}
+
 sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int64_t m, int64_t n, int64_t lda,
                    int64_t l, double* X, int64_t ldx) {
   if (n == 0 || l == 0) return SK_OK;
@@ -1158,23 +1261,6 @@ sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int
 }
 
 namespace {
-// Omega(:, j0:j1) as a plain column-major l x (j1 - j0) block (ld l): Omega(r, j) = z_r(j) / sqrt(l)
-// from the same counter layout as Gamma (R1, over the column index j of A).
-__global__ void __launch_bounds__(128) k_omega_plain(uint2 key, int l, int64_t j0, int64_t j1, double scale,
-                                                     double* __restrict__ out) {
-  const int hp = (l + 1) / 2;
-  const int64_t total = (j1 - j0) * hp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t jj = e / hp;
-    const int pr = (int)(e - jj * hp);
-    double z0, z1;
-    dev::gauss_pair((uint64_t)(j0 + jj), (uint32_t)pr, key, z0, z1);
-    double* col = out + jj * l;
-    col[2 * pr] = z0 * scale;
-    if (2 * pr + 1 < l) col[2 * pr + 1] = z1 * scale;
-  }
-}
-
 // Y (m x l, ldy) = A Omega^T for the Gaussian Omega (l x n over A's columns), one pass over A: Omega
 // is generated one block of A's columns at a time into an L2-sized slot and each block's product
 // is accumulated into Y by the DMMA GEMM (beta = 1 after the first block) -- no transpose of A.

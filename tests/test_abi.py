@@ -47,3 +47,14 @@ def test_missing_library_fails_loudly(tmp_path):
             _lib.load(str(tmp_path / "nope.so"))
         finally:
             _lib._lib = None
+
+
+def test_header_compiles_as_c_and_cxx(tmp_path):
+    """include/skel.h is self-contained for C and C++ callers (it declares the C ABI only)."""
+    import shutil
+    import subprocess
+    for cc, lang in (("gcc", "c"), ("g++", "c++")):
+        if shutil.which(cc) is None:
+            pytest.skip(f"{cc} not available")
+        r = subprocess.run([cc, "-fsyntax-only", "-Wall", "-Werror", "-x", lang, HEADER], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr

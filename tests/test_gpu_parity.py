@@ -135,6 +135,47 @@ def test_sketch_cols_parity(m, n, l, emb, seed):
     assert rel_fro(Y, o_sketch.sketch_cols(A, l, emb, seed)) <= 1e-12
 
 
+@pytest.mark.parametrize("m,n,lx,ly,seed", [(1000, 777, 61, 45, 1), (4096, 4096, 266, 266, 2),
+                                             (70000, 600, 40, 30, 3)])    # 2-D blocks: 3 row panels
+def test_sketch_dual_one_pass_parity(m, n, lx, ly, seed):
+    """Algorithm 3 line 2: X = Gamma A and Y = A Omega^T from one walk over A's blocks equal
+    the oracle's two sketches with the same (independent) seeds."""
+    A = rand_mat(m, n, seed)
+    X, Y = sk.sketch_dual(dev_f(A), lx, ly, seed_x=100 + seed, seed_y=200 + seed)
+    assert rel_fro(X.cpu().numpy(), o_sketch.sketch(A, lx, "gaussian", 100 + seed)) <= 1e-12
+    assert rel_fro(Y.cpu().numpy(), o_sketch.sketch_cols(A, ly, "gaussian", 200 + seed)) <= 1e-12
+
+
+@pytest.mark.parametrize("k,l", [(20, 40), (20, 20)])
+def test_alg3_sketch_only_estimates_c1(k, l):
+    """The sketch-only estimates of P:428-440 on C1: Z = X_1^+ X, W = Y Y_1^+ and the three residuals
+    ||A - C Z||, ||A - W R||, ||A - C S^{-1} R|| against the oracle's least-squares / solve."""
+    from oracle import estimates as o_est
+    A, sigma = make_c1(seed=1001)
+    Ad = dev_f(A)
+    X, Y = sk.sketch_dual(Ad, l, l, seed_x=2001, seed_y=3001)
+    Js, _, _, _ = sk.select_cols(X, k)
+    Is, _, _, _ = sk.select_rows(Y, k)
+    Z = sk.id_estimate_cols(X, Js)
+    W = sk.id_estimate_rows(Y, Is)
+    rz, nA = sk.residual(Ad, Js, None, "id_coeffs", Z)
+    rw, _ = sk.residual(Ad, None, Is, "row_coeffs", W)
+    rc, _ = sk.residual(Ad, Js, Is, "cur_css")
+    Xo = o_sketch.sketch(A, l, "gaussian", 2001)
+    Yo = o_sketch.sketch_cols(A, l, "gaussian", 3001)
+    (piv, _, _, _), _ = lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.select_cols(Xo, k, f))
+    (ipiv, _, _, _), _ = lupp_parity(Is.cpu().numpy(), lambda f: o_lupp.select_rows(Yo, k, f))
+    Zo = o_est.id_estimate_cols(Xo, piv)
+    Wo = o_est.id_estimate_rows(Yo, ipiv)
+    assert rel_fro(Z.cpu().numpy(), Zo) <= 1e-8
+    assert rel_fro(W.cpu().numpy(), Wo) <= 1e-8
+    nAo = float(np.linalg.norm(A))
+    for r, approx in ((rz, A[:, piv] @ Zo), (rw, Wo @ A[ipiv, :]), (rc, o_est.cur_css(A, ipiv, piv))):
+        ro = float(np.linalg.norm(A - approx))
+        assert abs(r - ro) <= 1e-8 * ro + 4 * U * nAo, (r, ro)
+        assert ro >= o_res.optimal_error(sigma, k) * (1 - 1e-9)
+
+
 def test_stream_select_alg3_c1():
     A, sigma = make_c1(seed=1001)
     k, l = 20, 40

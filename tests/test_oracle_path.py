@@ -441,3 +441,31 @@ def test_ortho_power_iteration_closed_forms():
     P2 = (lambda Q: Q @ Q.T)(np.linalg.qr(Xp2.T)[0])
     np.testing.assert_allclose(P1, P2, atol=1e-10)
     assert lupp.select_cols(Xo2, 10)[0].tolist() == lupp.select_cols(Xp2, 10)[0].tolist()
+
+
+def test_alg3_estimates_closed_forms():
+    """P:428-440 pinned by what the algebra fixes: on an exact-rank-k A with full-rank sketches the
+    estimates are exact -- X_1^+ X = C^+ A (A = C Z with Z = C^+ A, X = Gamma C Z, X_1 = Gamma C),
+    Y Y_1^+ = A R^+ and C S^{-1} R = A; for any A, X_1^+ X restricted to J_s is I_k and Y Y_1^+ restricted
+    to I_s is I_k."""
+    from oracle import estimates
+    rng = np.random.default_rng(23)
+    m, n, k, l = 90, 70, 6, 10
+    A = rng.standard_normal((m, k)) @ rng.standard_normal((k, n))            # rank k exactly
+    X = sketch.sketch(A, l, "gaussian", 1)
+    Y = sketch.sketch_cols(A, l, "gaussian", 2)
+    Js = lupp.select_cols(X, k)[0]
+    Is = lupp.select_rows(Y, k)[0]
+    C, R = A[:, Js], A[Is, :]
+    Z = estimates.id_estimate_cols(X, Js)
+    np.testing.assert_allclose(Z, np.linalg.lstsq(C, A, rcond=None)[0], atol=1e-10)
+    W = estimates.id_estimate_rows(Y, Is)
+    np.testing.assert_allclose(W, np.linalg.lstsq(R.T, A.T, rcond=None)[0].T, atol=1e-10)
+    np.testing.assert_allclose(estimates.cur_css(A, Is, Js), A, atol=1e-10 * np.abs(A).max())
+    B = make_lowrank(m, n, 0.7 ** np.arange(n), rng)                         # general A
+    Xb = sketch.sketch(B, l, "gaussian", 3)
+    Jb = lupp.select_cols(Xb, k)[0]
+    np.testing.assert_allclose(estimates.id_estimate_cols(Xb, Jb)[:, Jb], np.eye(k), atol=1e-12)
+    Yb = sketch.sketch_cols(B, l, "gaussian", 4)
+    Ib = lupp.select_rows(Yb, k)[0]
+    np.testing.assert_allclose(estimates.id_estimate_rows(Yb, Ib)[Ib, :], np.eye(k), atol=1e-12)
