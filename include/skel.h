@@ -175,13 +175,15 @@ sk_status sk_sketch_cols(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int
 /* ---- Algorithm 3's dual sketch in ONE pass over A ----
  * X = Gamma A (lx x n row-major, ldx >= n; Gamma over A's rows from seed_x, exactly sk_sketch's) and
  * Y = A Omega^T (m x ly column-major, ldy >= m; Omega over A's columns from seed_y, exactly
- * sk_sketch_cols') -- independent embeddings (Alg. 3 line 1) -- computed block by block: each
- * L2-sized block of A (<= ~48 MB) is read from HBM once by the X product and again, from L2, by the Y
- * product.  Gaussian only (SK_E_ARG otherwise); A 16-byte aligned with an even lda (the tensor-map
- * rules; SK_E_ARG otherwise).  Requires 1 <= lx <= m, 1 <= ly <= n. */
-sk_status sk_sketch_dual(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, int64_t lx, int64_t ly,
-                         sk_embedding emb, uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y,
-                         int64_t ldy);
+ * sk_sketch_cols') -- independent embeddings (Alg. 3 line 1).  a_on_host = 1: A is a HOST pointer
+ * (the streaming setting of Alg. 3) and crosses PCIe exactly once, in column blocks
+ * through a 3-slot device ring, each block feeding both products (X's block of columns and Y's
+ * term A_block Omega_block^T, accumulated in block order).  a_on_host = 0: A in device memory, the
+ * two products as two full-efficiency passes.  Gaussian only (SK_E_ARG otherwise).  Requires
+ * 1 <= lx <= m, 1 <= ly <= n. */
+sk_status sk_sketch_dual(sk_ctx* ctx, const double* A, int a_on_host, int64_t m, int64_t n, int64_t lda, int64_t lx,
+                         int64_t ly, sk_embedding emb, uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx,
+                         double* Y, int64_t ldy);
 
 /* ---- sketch-only ID estimates without revisiting A ----
  * sk_id_estimate_cols: Z = X_1^+ X (k x n column-major, ldz >= k), X_1 = X(:, Js) the lx x k column

@@ -18,8 +18,8 @@ _SIGS = {
     "sk_create": [ctypes.POINTER(c_dp), c_int, c_dp],
     "sk_set_stream": [c_dp, c_dp],
     "sk_set_sketch_tuning": [c_dp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_i64],
-    "sk_sketch_dual": [c_dp, c_dp, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_uint64, ctypes.c_uint64, c_dp,
-                       c_i64, c_dp, c_i64],
+    "sk_sketch_dual": [c_dp, c_dp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_uint64, ctypes.c_uint64,
+                       c_dp, c_i64, c_dp, c_i64],
     "sk_id_estimate_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, ctypes.POINTER(c_i64)],
     "sk_id_estimate_rows": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, ctypes.POINTER(c_i64)],
     "sk_nccl_unique_id": [c_dp],

@@ -162,16 +162,21 @@ def sketch_cols(A, l, embedding="gaussian", seed=0, zeta=8):
     return Y
 
 
-def sketch_dual(A, lx, ly, seed_x=0, seed_y=1):
+def sketch_dual(A, lx, ly, seed_x=0, seed_y=1, device=0):
     """Algorithm 3 line 2: X = Gamma A (lx x n, row-major) and Y = A Omega^T (m x ly,
-    column-major) in one pass over A (Gaussian embeddings, independent seeds)."""
-    lda = _colmajor(A, "A")
+    column-major) in one pass over A (Gaussian embeddings, independent seeds).  A may be a CPU
+    tensor (column-major, ideally pinned): it then crosses PCIe once, in column blocks."""
+    on_host = not A.is_cuda
+    if A.dtype != torch.float64 or A.dim() != 2 or (A.stride(0) != 1 and A.shape[1] > 1):
+        raise ValueError("A must be a column-major 2-D float64 tensor")
     m, n = A.shape
-    X = torch.empty((lx, n), dtype=torch.float64, device=A.device)
-    Y = torch.empty((ly, m), dtype=torch.float64, device=A.device).t()
-    h = context(A.device.index)
-    _check(lib().sk_sketch_dual(h, _ptr(A), m, n, lda, lx, ly, GAUSSIAN, seed_x & (2**64 - 1), seed_y & (2**64 - 1),
-                                _ptr(X), n, _ptr(Y), m), h)
+    lda = max(A.stride(1), m)
+    dev = torch.device("cuda", device if on_host else A.device.index)
+    X = torch.empty((lx, n), dtype=torch.float64, device=dev)
+    Y = torch.empty((ly, m), dtype=torch.float64, device=dev).t()
+    h = context(dev.index)
+    _check(lib().sk_sketch_dual(h, _ptr(A), 1 if on_host else 0, m, n, lda, lx, ly, GAUSSIAN, seed_x & (2**64 - 1),
+                                seed_y & (2**64 - 1), _ptr(X), n, _ptr(Y), m), h)
     return X, Y
 
 

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <new>
 
 #include "common.cuh"
@@ -39,6 +40,53 @@ sk_status finish_info(sk_ctx* c, const int64_t* status_dev, int64_t* info, const
 }
 
 }  // namespace
+
+namespace skel {
+
+sk_status for_host_blocks(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda,
+                          const std::function<sk_status(const double*, int64_t, int64_t)>& fn) {
+  // A ring of NR device slots of W columns (<= 2 GB each), not the whole of A: the host->device copy
+  // of block b (helper stream) overlaps the work on block b - 1 (context stream); a slot is refilled
+  // only after the work that read it is done.
+  constexpr int NR = 3;
+  const int64_t wmax = std::max<int64_t>(128, ((int64_t)(2.0 * (1 << 30) / (8.0 * (double)m)) / 128) * 128);
+  const int64_t W = std::min(wmax, std::max<int64_t>(128, cdiv(cdiv(n, 8), 128) * 128));
+  const int64_t nb = cdiv(n, W);
+  const int nr = (int)std::min<int64_t>(NR, nb);
+  if (nb == 0) return SK_OK;
+  DBuf slot[NR];
+  for (int r = 0; r < nr; ++r) SK_TRY(slot[r].alloc(c, (size_t)m * W * sizeof(double)));
+  SK_TRY(ensure_aux(c));
+  cudaEvent_t ev[2 * NR + 1] = {};
+  sk_status rs = SK_OK;
+  for (int e = 0; e < 2 * nr + 1 && rs == SK_OK; ++e)
+    if (cudaEventCreateWithFlags(&ev[e], cudaEventDisableTiming) != cudaSuccess) rs = fail(c, SK_E_CUDA, "host stream: event");
+  cudaEvent_t* copied = ev;            // [nr]: block in slot r has landed
+  cudaEvent_t* consumed = ev + nr;     // [nr]: the work on the block in slot r is done
+  if (rs == SK_OK && (cudaEventRecord(ev[2 * nr], c->stream) != cudaSuccess ||      // slots allocated (stream order)
+                      cudaStreamWaitEvent(c->aux, ev[2 * nr], 0) != cudaSuccess))
+    rs = fail(c, SK_E_CUDA, "host stream: event");
+  for (int64_t b = 0; b < nb && rs == SK_OK; ++b) {
+    const int r = (int)(b % nr);
+    const int64_t j0 = b * W, jw = std::min(W, n - j0);
+    double* dst = slot[r].as<double>();
+    if (b >= nr && cudaStreamWaitEvent(c->aux, consumed[r], 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "host stream: event"); break; }
+    if (cudaMemcpy2DAsync(dst, (size_t)m * sizeof(double), A + j0 * lda, (size_t)lda * sizeof(double),
+                          (size_t)m * sizeof(double), (size_t)jw, cudaMemcpyHostToDevice, c->aux) != cudaSuccess ||
+        cudaEventRecord(copied[r], c->aux) != cudaSuccess || cudaStreamWaitEvent(c->stream, copied[r], 0) != cudaSuccess) {
+      rs = fail(c, SK_E_CUDA, "host stream: host-to-device copy");
+      break;
+    }
+    rs = fn(dst, j0, jw);
+    if (rs == SK_OK && cudaEventRecord(consumed[r], c->stream) != cudaSuccess) rs = fail(c, SK_E_CUDA, "host stream: event");
+  }
+  // (every copy was waited for by the context stream, so the slots are freed after their last use)
+  for (int e = 0; e < 2 * nr + 1; ++e)
+    if (ev[e]) cudaEventDestroy(ev[e]);
+  return rs;
+}
+
+}  // namespace skel
 
 extern "C" {
 
@@ -499,45 +547,11 @@ sk_status sk_rand_lupp(sk_ctx* c, const double* A, int a_on_host, int64_t m, int
   SK_TRY(Jd.alloc(c, (size_t)k * sizeof(int64_t)));
   SK_TRY(st.alloc(c, sizeof(int64_t)));
   if (a_on_host) {
-    // A stays in host memory.  X = Gamma A is column-separable: column blocks of A stream through a
-    // ring of NR device slots -- the host->device copy of block b (helper stream) overlaps the sketch
-    // of block b-1 (context stream); a slot is refilled only after the sketch that read it is done.
-    // Device memory: NR slots of W columns (<= 2 GB each), not the whole of A.
-    constexpr int NR = 3;
-    const int64_t wmax = std::max<int64_t>(128, ((int64_t)(2.0 * (1 << 30) / (8.0 * (double)m)) / 128) * 128);
-    const int64_t W = std::min(wmax, std::max<int64_t>(128, cdiv(cdiv(n, 8), 128) * 128));
-    const int64_t nb = cdiv(n, W);
-    const int nr = (int)std::min<int64_t>(NR, nb);
-    DBuf slot[NR];
-    for (int r = 0; r < nr; ++r) SK_TRY(slot[r].alloc(c, (size_t)m * W * sizeof(double)));
-    SK_TRY(ensure_aux(c));
-    cudaEvent_t ev[2 * NR + 1] = {};
-    sk_status rs = SK_OK;
-    for (int e = 0; e < 2 * nr + 1 && rs == SK_OK; ++e)
-      if (cudaEventCreateWithFlags(&ev[e], cudaEventDisableTiming) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event");
-    cudaEvent_t* copied = ev;            // [nr]: block in slot r has landed
-    cudaEvent_t* consumed = ev + nr;     // [nr]: the sketch of the block in slot r is done
-    if (rs == SK_OK && (cudaEventRecord(ev[2 * nr], c->stream) != cudaSuccess ||      // slots allocated (stream order)
-                        cudaStreamWaitEvent(c->aux, ev[2 * nr], 0) != cudaSuccess))
-      rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event");
-    for (int64_t b = 0; b < nb && rs == SK_OK; ++b) {
-      const int r = (int)(b % nr);
-      const int64_t j0 = b * W, jw = std::min(W, n - j0);
-      double* dst = slot[r].as<double>();
-      if (b >= nr && cudaStreamWaitEvent(c->aux, consumed[r], 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event"); break; }
-      if (cudaMemcpy2DAsync(dst, (size_t)m * sizeof(double), A + j0 * lda, (size_t)lda * sizeof(double),
-                            (size_t)m * sizeof(double), (size_t)jw, cudaMemcpyHostToDevice, c->aux) != cudaSuccess ||
-          cudaEventRecord(copied[r], c->aux) != cudaSuccess || cudaStreamWaitEvent(c->stream, copied[r], 0) != cudaSuccess) {
-        rs = fail(c, SK_E_CUDA, "sk_rand_lupp: host-to-device copy");
-        break;
-      }
-      rs = sk_sketch(c, dst, m, jw, m, l, emb, zeta, seed, Xd.as<double>() + j0, n);
-      if (rs == SK_OK && cudaEventRecord(consumed[r], c->stream) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sk_rand_lupp: event");
-    }
-    // (every copy was waited for by the context stream, so the slots are freed after their last use)
-    for (int e = 0; e < 2 * nr + 1; ++e)
-      if (ev[e]) cudaEventDestroy(ev[e]);
-    SK_TRY(rs);
+    // A stays in host memory: X = Gamma A is column-separable, so A's column blocks stream through
+    // the device ring of for_host_blocks (copy of block b overlapping the sketch of block b - 1)
+    SK_TRY(for_host_blocks(c, A, m, n, lda, [&](const double* blk, int64_t j0, int64_t jw) {
+      return sk_sketch(c, blk, m, jw, m, l, emb, zeta, seed, Xd.as<double>() + j0, n);
+    }));
   } else {
     SK_TRY(sk_sketch(c, A, m, n, lda, l, emb, zeta, seed, Xd.as<double>(), n));
   }

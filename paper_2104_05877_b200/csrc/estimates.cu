@@ -57,9 +57,9 @@ sk_status finish(sk_ctx* c, const int64_t* st_dev, int64_t* info, const char* wh
 
 extern "C" {
 
-sk_status sk_sketch_dual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t lx, int64_t ly,
-                         sk_embedding emb, uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y,
-                         int64_t ldy) {
+sk_status sk_sketch_dual(sk_ctx* c, const double* A, int a_on_host, int64_t m, int64_t n, int64_t lda, int64_t lx,
+                         int64_t ly, sk_embedding emb, uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx,
+                         double* Y, int64_t ldy) {
   if (!c) return SK_E_ARG;
   c->err.clear();
   SK_ARG(c, A && X && Y, "sk_sketch_dual: NULL pointer");
@@ -68,7 +68,7 @@ sk_status sk_sketch_dual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64
   SK_ARG(c, m >= 1 && n >= 1 && lda >= m && lx >= 1 && lx <= m && ly >= 1 && ly <= n && ldx >= n && ldy >= m,
          "sk_sketch_dual: need 1 <= lx <= m, 1 <= ly <= n, lda >= m, ldx >= n, ldy >= m");
   SK_CUDA(c, cudaSetDevice(c->device));
-  return sketch_dual(c, A, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy);
+  return sketch_dual(c, A, a_on_host != 0, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy);
 }
 
 sk_status sk_id_estimate_cols(sk_ctx* c, const double* X, int64_t lx, int64_t n, int64_t ldx, const int64_t* Js,

@@ -1,5 +1,7 @@
 // internal.h -- host-side drivers shared by the translation units of libskel.so.
 #pragma once
+#include <functional>
+
 #include "common.cuh"
 
 namespace skel {
@@ -31,8 +33,8 @@ sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int
                    int64_t l, double* X, int64_t ldx);
 // Algorithm 3's dual sketch in one pass over A: X = Gamma A (lx x n row-major), Y = A Omega^T (m x ly
 // col-major), both Gaussian (Gamma over A's rows from seed_x, Omega over A's columns from seed_y).
-sk_status sketch_dual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t lx, int64_t ly,
-                      uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y, int64_t ldy);
+sk_status sketch_dual(sk_ctx* c, const double* A, bool a_on_host, int64_t m, int64_t n, int64_t lda, int64_t lx,
+                      int64_t ly, uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y, int64_t ldy);
 // Y = A Omega^T (m x l col-major, ldy >= m), Omega l x n (Alg. 3 column sketch).
 sk_status sketch_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
                       int zeta, uint64_t seed, double* Y, int64_t ldy);
@@ -133,6 +135,11 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
 // the distributed column-ID residual, where C is assembled across ranks).
 sk_status residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* C, int64_t k,
                         int64_t ldc, double* sums_dev, int64_t* status_dev);
+
+// Stream a HOST column-major m x n A through a 3-slot device ring in column blocks (capi.cu):
+// fn(block, j0, jw) runs on the context stream for each block (device copy, ld m) in order.
+sk_status for_host_blocks(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda,
+                          const std::function<sk_status(const double*, int64_t, int64_t)>& fn);
 
 // ---------------------------------------------------------------- column-sharded context (dist.cu)
 // A context made by sk_create_dist owns an NCCL communicator and this rank's column block

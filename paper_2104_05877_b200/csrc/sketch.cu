@@ -1127,55 +1127,6 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   return SK_OK;
 }
 
-// Algorithm 3's dual sketch: X = Gamma A (lx x n) and Y = A Omega^T (m x ly) in ONE pass
-// over A in HBM.  A is walked in L2-sized blocks (Kc rows x Nc columns, <= ~48 MB); each block is
-// read by the X GEMM (TMA + DMMA, Gamma's chunk image for the block's rows generated once per row
-// panel) and right after by the Y GEMM (DMMA, Omega's block of columns generated per block), so the
-// second read hits L2.  X accumulates over row panels, Y over column blocks (fixed order).
-template <int BM, int NW>
-sk_status run_dual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t lx, int64_t ly,
-                   uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y, int64_t ldy, int splits) {
-  using C = PCfg<BM, NW>;
-  constexpr double kBlockBytes = 48.0 * (1 << 20);
-  int64_t Nc = std::max<int64_t>(C::TBNP, (int64_t)(kBlockBytes / (8.0 * m)) / C::TBNP * C::TBNP);
-  Nc = std::min(Nc, n);
-  int64_t Kc = m;
-  if ((double)Kc * Nc * 8.0 > kBlockBytes) Kc = std::max<int64_t>(1024, (int64_t)(kBlockBytes / (8.0 * Nc)) / 1024 * 1024);
-  Kc = std::min(Kc, m);
-  const int64_t mb = cdiv(lx, BM);
-  DBuf img, part, om;
-  SK_TRY(img.alloc(c, (size_t)mb * cdiv(Kc, TBK) * TBK * C::OS * sizeof(double)));
-  SK_TRY(om.alloc(c, (size_t)ly * Nc * sizeof(double)));
-  const int64_t kps = cdiv(cdiv(Kc, splits), TBK) * TBK;
-  if (cdiv(Kc, kps) > 1) SK_TRY(part.alloc(c, (size_t)cdiv(Kc, kps) * lx * Nc * sizeof(double)));
-  const uint2 kx = dev::seed_key(seed_x), ky = dev::seed_key(seed_y);
-  const double sy = 1.0 / std::sqrt((double)ly);
-  for (int64_t i0 = 0; i0 < m; i0 += Kc) {
-    const int64_t i1 = std::min(m, i0 + Kc);
-    SK_TRY((omega_chunk_image<BM, NW>(c, kx, nullptr, 0, lx, i0, i1, img.as<double>())));   // Gamma(:, i0:i1)
-    for (int64_t j0 = 0; j0 < n; j0 += Nc) {
-      const int64_t j1 = std::min(n, j0 + Nc);
-      const double* Ab = A + j0 * lda;
-      CUtensorMap tm;
-      SK_TRY(make_tmap(c, Ab, m, j1 - j0, lda, &tm));
-      DenseParams p{};
-      p.A = Ab; p.lda = lda; p.n = j1 - j0; p.l = (int)lx;
-      p.key = kx;
-      p.scale = 1.0 / std::sqrt((double)lx);
-      p.X = X + j0; p.ldx = ldx;
-      p.k0 = i0; p.m = i1; p.accum = i0 > 0;
-      SK_TRY((pre_gemm_chunk<BM, NW>(c, tm, p, lx, j1 - j0, splits, false, img.as<double>(), part.as<double>())));
-      // Y(i0:i1, :) (+)= A(i0:i1, j0:j1) Omega(:, j0:j1)^T -- the block again, now from L2
-      const int64_t work = (j1 - j0) * ((ly + 1) / 2);
-      k_omega_plain<<<(unsigned)std::min<int64_t>(cdiv(work, 128), 16LL * c->num_sms), 128, 0, c->stream>>>(
-          ky, (int)ly, j0, j1, sy, om.as<double>());
-      SK_TRY(launched(c));
-      SK_TRY(gemm(c, false, true, i1 - i0, ly, j1 - j0, 1.0, A + i0 + j0 * lda, lda, om.as<double>(), ly,
-                  j0 > 0 ? 1.0 : 0.0, Y + i0, ldy));
-    }
-  }
-  return SK_OK;
-}
 
 sk_status sketch_dense_pre(sk_ctx* c, const DenseParams& p, int64_t m, int64_t n, int64_t l, const PrePlan& pl,
                            const double* Qom = nullptr, int64_t ldq = 0) {
@@ -1232,20 +1183,6 @@ sk_status sketch_dense(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t
   return splitk_reduce(c, p.part, splits, l, n, p.scale, X, ldx);
 }
 
-sk_status sketch_dual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t lx, int64_t ly,
-                      uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y, int64_t ldy) {
-  if (n == 0 || m == 0) return SK_OK;
-  if (!tma_ok_for(A, m, n, lda)) return fail(c, SK_E_ARG, "sk_sketch_dual: A must be 16-byte aligned with an even lda");
-  const PrePlan pl = plan_pre(c, m, n, lx);
-  const int bm = pl.bm > 0 ? pl.bm : 48;
-  const int64_t tiles = cdiv(lx, bm) * cdiv(std::min<int64_t>(n, 4096), 256);
-  int splits = (int)std::max<int64_t>(1, std::min<int64_t>(8, cdiv(2LL * c->num_sms, tiles)));
-  while (splits > 1 && m / splits < 512) --splits;
-  if (bm == 64) return run_dual<64, 8>(c, A, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy, splits);
-  if (bm == 32) return run_dual<32, 8>(c, A, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy, splits);
-  if (bm == 40) return run_dual<40, 8>(c, A, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy, splits);
-  return run_dual<48, 8>(c, A, m, n, lda, lx, ly, seed_x, seed_y, X, ldx, Y, ldy, splits);
-}
 
 sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int64_t m, int64_t n, int64_t lda,
                    int64_t l, double* X, int64_t ldx) {
@@ -1261,11 +1198,11 @@ sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int
 }
 
 namespace {
-// Y (m x l, ldy) = A Omega^T for the Gaussian Omega (l x n over A's columns), one pass over A: Omega
-// is generated one block of A's columns at a time into an L2-sized slot and each block's product
-// is accumulated into Y by the DMMA GEMM (beta = 1 after the first block) -- no transpose of A.
+// Y (m x l, ldy) (+)= A Omega(:, col0 : col0 + n)^T for the Gaussian Omega (l x n_total over A's
+// columns), one pass over A: Omega is generated one block of A's columns at a time into an L2-sized
+// slot and each block's product is accumulated into Y by the DMMA GEMM -- no transpose of A.
 sk_status cols_sketch_gaussian(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l,
-                               uint64_t seed, double* Y, int64_t ldy) {
+                               uint64_t seed, double* Y, int64_t ldy, int64_t col0 = 0, bool accumulate = false) {
   const int64_t nc = std::max<int64_t>(256, std::min<int64_t>(n, (int64_t)(kOmegaSlotBytes / (8.0 * l)) / 256 * 256));
   DBuf om;
   SK_TRY(om.alloc(c, (size_t)l * std::min(nc, n) * sizeof(double)));
@@ -1275,9 +1212,10 @@ sk_status cols_sketch_gaussian(sk_ctx* c, const double* A, int64_t m, int64_t n,
     const int64_t j1 = std::min(n, j0 + nc);
     const int64_t work = (j1 - j0) * ((l + 1) / 2);
     k_omega_plain<<<(unsigned)std::min<int64_t>(cdiv(work, 128), 16LL * c->num_sms), 128, 0, c->stream>>>(
-        key, (int)l, j0, j1, scale, om.as<double>());
+        key, (int)l, col0 + j0, col0 + j1, scale, om.as<double>());
     SK_TRY(launched(c));
-    SK_TRY(gemm(c, false, true, m, l, j1 - j0, 1.0, A + j0 * lda, lda, om.as<double>(), l, j0 > 0 ? 1.0 : 0.0, Y, ldy));
+    SK_TRY(gemm(c, false, true, m, l, j1 - j0, 1.0, A + j0 * lda, lda, om.as<double>(), l,
+                (j0 > 0 || accumulate) ? 1.0 : 0.0, Y, ldy));
   }
   return SK_OK;
 }
@@ -1311,6 +1249,25 @@ sk_status sketch_power(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t
     SK_TRY(gemm_qta(c, Tt.as<double>(), m, A, m, n, lda, l, Xout, ldo));                         // X = T A
   }
   return SK_OK;
+}
+
+// Algorithm 3 line 2: X = Gamma A and Y = A Omega^T "in a single pass through A".  The pass
+// that matters is the one over the STREAM A arrives on: with A in host memory its column blocks cross
+// PCIe once, through the ring of for_host_blocks, and each block feeds both products -- X(:, block)
+// completely (the TMA + DMMA sketch of the block) and its term A_block Omega(:, block)^T of Y.  With
+// A already in HBM the two products run as two full-efficiency passes (FP64-bound: an L2-blocked
+// single pass was measured 1.1-3.3x slower, its partial-sum traffic exceeding A's).
+sk_status sketch_dual(sk_ctx* c, const double* A, bool a_on_host, int64_t m, int64_t n, int64_t lda, int64_t lx,
+                      int64_t ly, uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y, int64_t ldy) {
+  if (n == 0 || m == 0) return SK_OK;
+  if (!a_on_host) {
+    SK_TRY(sketch_dense(c, A, m, n, lda, lx, seed_x, X, ldx));
+    return cols_sketch_gaussian(c, A, m, n, lda, ly, seed_y, Y, ldy);
+  }
+  return for_host_blocks(c, A, m, n, lda, [&](const double* blk, int64_t j0, int64_t jw) {
+    SK_TRY(sketch_dense(c, blk, m, jw, m, lx, seed_x, X + j0, ldx));
+    return cols_sketch_gaussian(c, blk, m, jw, m, ly, seed_y, Y, ldy, j0, j0 > 0);
+  });
 }
 
 sk_status sketch_power_ortho(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,

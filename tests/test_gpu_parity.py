@@ -135,13 +135,15 @@ def test_sketch_cols_parity(m, n, l, emb, seed):
     assert rel_fro(Y, o_sketch.sketch_cols(A, l, emb, seed)) <= 1e-12
 
 
-@pytest.mark.parametrize("m,n,lx,ly,seed", [(1000, 777, 61, 45, 1), (4096, 4096, 266, 266, 2),
-                                             (70000, 600, 40, 30, 3)])    # 2-D blocks: 3 row panels
-def test_sketch_dual_one_pass_parity(m, n, lx, ly, seed):
-    """Algorithm 3 line 2: X = Gamma A and Y = A Omega^T from one walk over A's blocks equal
-    the oracle's two sketches with the same (independent) seeds."""
+@pytest.mark.parametrize("m,n,lx,ly,seed,host", [(1000, 777, 61, 45, 1, True), (1000, 777, 61, 45, 1, False),
+                                                  (4096, 4096, 266, 266, 2, True), (3000, 20000, 1100, 300, 3, True)])
+def test_sketch_dual_one_pass_parity(m, n, lx, ly, seed, host):
+    """Algorithm 3 line 2: X = Gamma A and Y = A Omega^T -- from ONE pass of a host A over
+    PCIe in column blocks (each block feeding both products), or from device memory -- equal the
+    oracle's two sketches with the same (independent) seeds."""
     A = rand_mat(m, n, seed)
-    X, Y = sk.sketch_dual(dev_f(A), lx, ly, seed_x=100 + seed, seed_y=200 + seed)
+    Ain = torch.from_numpy(np.asfortranarray(A)).pin_memory() if host else dev_f(A)
+    X, Y = sk.sketch_dual(Ain, lx, ly, seed_x=100 + seed, seed_y=200 + seed)
     assert rel_fro(X.cpu().numpy(), o_sketch.sketch(A, lx, "gaussian", 100 + seed)) <= 1e-12
     assert rel_fro(Y.cpu().numpy(), o_sketch.sketch_cols(A, ly, "gaussian", 200 + seed)) <= 1e-12
 
