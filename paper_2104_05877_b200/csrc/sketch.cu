@@ -50,17 +50,6 @@ struct DenseParams {
   int64_t k_per_split;
   int64_t k0;            // first row of A in this K-chunk (rows k0 .. m-1 of A; m = the chunk's end)
   int accum;             // 1: X += the chunk's product (chunks after the first), 0: X = it
-  // K-chunk chain (k_sketch_pre MODE 0 over several chunks, launched back to back with PDL): this
-  // chunk's image is complete once *ready_cur >= ready_need; the first n_prod CTAs generate the NEXT
-  // chunk's image (rows next_i0 .. next_i1, next_KT k-tiles) into img_next after their mainloop and
-  // count themselves into *ready_next.  chain = 0: a single launch (griddep_wait at the top).
-  int chain;
-  double* img_next;
-  int64_t next_i0, next_i1, next_KT;
-  unsigned* ready_cur;
-  unsigned* ready_next;
-  unsigned ready_need;
-  int n_prod;
 };
 
 template <bool VEC>
@@ -327,7 +316,7 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
   using C = PCfg<BM, NW>;
   constexpr int TS = C::TS;
   constexpr int FI = BM / 8;
-  if (MODE != 0 || !p.chain) dev::griddep_wait();        // PDL: the Omega image is complete
+  dev::griddep_wait();                                   // PDL: the Omega image is complete
   extern __shared__ __align__(1024) unsigned char psm_raw[];
   unsigned char* base = psm_raw + ((1024u - (dev::smem_addr(psm_raw) & 1023u)) & 1023u);
   const unsigned base_u = dev::smem_addr(base);
@@ -346,20 +335,6 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     dev::prefetch_tmap(&tmA);
-  }
-  if (MODE == 0 && p.chain) {
-    // chained K-chunk: let the next chunk's grid launch as soon as every CTA of this one has started
-    // (its mainloop then overlaps this grid's last wave), and wait only for THIS chunk's image, made
-    // by the previous grid's first CTAs long before this grid could launch
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (tid == 0 && p.ready_cur) {
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ready_cur) : "memory");
-      } while (v < p.ready_need);
-      // the image was written with generic stores and is read by the bulk-copy (async) proxy
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
   }
   __syncthreads();
   const double* img_rt = img + ((int64_t)rt * KT) * (TBK * C::OS);
@@ -458,24 +433,6 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
     dev::cluster_arrive();                                  // no CTA leaves while peers read it
     dev::cluster_wait();
     return;
-  }
-  if (MODE == 0 && p.chain) {
-    // the previous chunk's grid has completed (its adds into X are visible, and the image slot it
-    // read -- the one the next chunk's image goes into -- is free)
-    dev::griddep_wait();
-    const int64_t lin = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
-    if (p.img_next && lin < p.n_prod) {
-      const int64_t tiles = (int64_t)gridDim.x * p.next_KT;          // row tiles x k tiles of the next image
-      const int64_t t0 = tiles * lin / p.n_prod, t1 = tiles * (lin + 1) / p.n_prod;
-      for (int64_t t = t0; t < t1; ++t)
-        omega_tile(p.key, p.l, p.next_i0, p.next_i1, BM, C::OS, p.next_KT, t, p.img_next, tid, C::NT);
-      asm volatile("fence.proxy.async.global;" ::: "memory");   // generic stores -> async-proxy reads
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        atomicAdd(p.ready_next, 1u);
-      }
-    }
   }
   if (!active) return;
 #pragma unroll
@@ -1169,51 +1126,6 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   const int sp_max = (int)cdiv(chunk, kps_max);
   const bool cl = pl.cluster && sp_max > 1 && sp_max <= 8 && BM % sp_max == 0;
   if (sp_max > 1 && !cl) SK_TRY(part.alloc(c, (size_t)sp_max * l * n * sizeof(double)));
-  const int64_t nch = cdiv(m, chunk);
-  if (nch > 1 && sp_max == 1 && !Qom) {
-    // chained chunks (one K range per chunk, Philox Omega): two image slots; the first chunk's image by
-    // k_omega_image, every later one by the first CTAs of the preceding chunk's GEMM; the GEMMs are
-    // launched back to back with programmatic dependent launch (tails overlap)
-    DBuf img2, ready;
-    SK_TRY(img2.alloc(c, img.bytes));
-    SK_TRY(ready.alloc(c, (size_t)(nch + 1) * sizeof(unsigned)));
-    SK_CUDA(c, cudaMemsetAsync(ready.p, 0, (size_t)(nch + 1) * sizeof(unsigned), c->stream));
-    double* slot[2] = {img.as<double>(), img2.as<double>()};
-    unsigned* rd = ready.as<unsigned>();
-    SK_TRY((omega_chunk_image<BM, NW>(c, p.key, nullptr, 0, l, 0, std::min(m, chunk), slot[0])));
-    const int64_t nb = cdiv(n, C::TBNP);
-    const int nprod = (int)std::min<int64_t>(mb * nb, 2LL * c->num_sms);
-    SK_CUDA(c, cudaFuncSetAttribute(k_sketch_pre<BM, NW, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    for (int64_t ci = 0; ci < nch; ++ci) {
-      const int64_t i0 = ci * chunk, i1 = std::min(m, i0 + chunk);
-      p.k0 = i0;
-      p.m = i1;
-      p.accum = ci > 0;
-      p.k_per_split = cdiv(i1 - i0, TBK) * TBK;
-      p.chain = 1;
-      p.ready_cur = ci > 0 ? rd + ci : nullptr;
-      p.ready_need = (unsigned)nprod;
-      p.ready_next = rd + ci + 1;
-      p.n_prod = nprod;
-      p.img_next = ci + 1 < nch ? slot[(ci + 1) & 1] : nullptr;
-      p.next_i0 = i1;
-      p.next_i1 = std::min(m, i1 + chunk);
-      p.next_KT = cdiv(p.next_i1 - p.next_i0, TBK);
-      cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3((unsigned)mb, (unsigned)nb, 1);
-      lc.blockDim = dim3(C::NT);
-      lc.dynamicSmemBytes = C::SMEM;
-      lc.stream = c->stream;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at[0].val.programmaticStreamSerializationAllowed = 1;
-      lc.attrs = at; lc.numAttrs = ci > 0 ? 1 : 0;         // chunk 0 waits for its image kernel in full
-      SK_CUDA(c, cudaLaunchKernelEx(&lc, k_sketch_pre<BM, NW, 0>, tm, p, (const double*)slot[ci & 1],
-                                    cdiv(i1 - i0, TBK)));
-      SK_TRY(launched(c));
-    }
-    return SK_OK;
-  }
   for (int64_t i0 = 0; i0 < m; i0 += chunk) {
     const int64_t i1 = std::min(m, i0 + chunk);
     SK_TRY((omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, i0, i1, img.as<double>())));
