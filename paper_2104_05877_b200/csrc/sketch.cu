@@ -306,6 +306,16 @@ __device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigne
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
 }
+__device__ __forceinline__ void bulk_load_hint(unsigned dst, const void* src, unsigned bytes, unsigned mbar,
+                                               unsigned long long policy) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar), "l"(policy) : "memory");
+}
+#ifndef SKEL_SKETCH_HINTS
+#define SKEL_SKETCH_HINTS 1
+#endif
+// L2 policy of the sketch GEMM's loads: the Omega image slot is re-read by every column tile of A
+// (keep: evict_last), a tile of A by the l / BM row-tile CTAs co-scheduled with it (evict_first)
 
 // MODE 0: one K range, X written directly; 1: K-split partials to HBM (+ k_sketch_splitk_reduce);
 // 2: the gridDim.z K-splits of a tile form one cluster and are summed through distributed shared
@@ -342,6 +352,8 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
   const int64_t nbox_all = (p.n - n0 + PBOX - 1) / PBOX;
   const int nbox = (int)(nbox_all < NW * 32 / PBOX ? nbox_all : NW * 32 / PBOX);
   int issued = 0;
+  const unsigned long long pol_a = SKEL_SKETCH_HINTS ? dev::policy_evict_first() : 0ull;
+  const unsigned long long pol_o = SKEL_SKETCH_HINTS ? dev::policy_evict_last() : 0ull;
   auto issue = [&](int upto, bool block) {
     while (issued < upto && issued < ktiles) {
       const int kq = issued, sq = kq % TS;
@@ -352,9 +364,16 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
       }
       const unsigned st = base_u + sq * C::ST_BYTES;
       dev::mbar_arm(fullB + 8 * sq, (unsigned)(nbox * PBOX * TBK * 8 + C::O_BYTES));
-      bulk_load(st + C::A_BYTES, img_rt + (kt0 + kq) * (TBK * C::OS), (unsigned)C::O_BYTES, fullB + 8 * sq);
-      for (int b = 0; b < nbox; ++b)
-        dev::tma_load_2d(st + b * PBOX * TBK * 8, &tmA, (int)(kbeg + (int64_t)kq * TBK), (int)(n0 + b * PBOX), fullB + 8 * sq);
+      if (SKEL_SKETCH_HINTS) {
+        bulk_load_hint(st + C::A_BYTES, img_rt + (kt0 + kq) * (TBK * C::OS), (unsigned)C::O_BYTES, fullB + 8 * sq, pol_o);
+        for (int b = 0; b < nbox; ++b)
+          dev::tma_load_2d_hint(st + b * PBOX * TBK * 8, &tmA, (int)(kbeg + (int64_t)kq * TBK), (int)(n0 + b * PBOX),
+                                fullB + 8 * sq, pol_a);
+      } else {
+        bulk_load(st + C::A_BYTES, img_rt + (kt0 + kq) * (TBK * C::OS), (unsigned)C::O_BYTES, fullB + 8 * sq);
+        for (int b = 0; b < nbox; ++b)
+          dev::tma_load_2d(st + b * PBOX * TBK * 8, &tmA, (int)(kbeg + (int64_t)kq * TBK), (int)(n0 + b * PBOX), fullB + 8 * sq);
+      }
       ++issued;
     }
   };
