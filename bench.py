@@ -521,7 +521,7 @@ def main():
     # roofline of the dominant kernel of the selection: the sketch (one launch per call)
     sk_ms = statistics.mean(stage_ms["sketch"])
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "round1", "sketch_dram_bytes.json")
+    tf = os.path.join(ROOT, "profiles", "round2", "sketch_dram_bytes.json")
     if os.path.exists(tf):
         try:
             traffic = json.load(open(tf)).get(f"{args.config}_k{k}")

@@ -1,5 +1,5 @@
-"""Sweep SKEL_PRE_PLAN (bm, nw, splits) for the dense sketch shapes (plan_pre reads the variable
-on every call, so one process serves all plans).  usage: python tools/sweep_pre.py"""
+"""Sweep the dense sketch's plans (sk_set_sketch_tuning: row-tile height, K-splits, HBM partials vs
+cluster DSMEM reduction) for the BASELINE shapes.  usage: python tools/sweep_pre.py"""
 import os
 import sys
 
@@ -11,7 +11,7 @@ import paper_2104_05877_b200 as sk  # noqa: E402
 SHAPES = [("C2 k=16", 4096, 4096, 26), ("C2 k=64", 4096, 4096, 74), ("C2 k=256", 4096, 4096, 266),
           ("C2 k=512", 4096, 4096, 522), ("C4 k=50", 65536, 784, 100), ("C4 k=100", 65536, 784, 200),
           ("C4 k=200", 65536, 784, 400), ("C5 block", 131072, 8192, 1100)]
-PLANS = [(64, 8), (48, 8), (32, 8)]
+PLANS = [(64, 8), (48, 8), (40, 8), (32, 8)]
 
 
 def timed(fn, reps=5):
@@ -32,7 +32,7 @@ def timed(fn, reps=5):
 for name, m, n, l in SHAPES:
     A = sk.fortran(torch.randn(m, n, dtype=torch.float64, device="cuda"))
     X = torch.empty((l, n), dtype=torch.float64, device="cuda")
-    os.environ.pop("SKEL_PRE_PLAN", None)
+    sk.set_sketch_tuning()
     ms = timed(lambda: sk.sketch(A, l, "gaussian", 7, out=X))
     ref = X.clone()
     print(f"{name:10s} default plan {ms:8.4f} ms {2 * l * m * n / ms / 1e9 / 37.13:6.1%}", flush=True)
@@ -42,7 +42,7 @@ for name, m, n, l in SHAPES:
             if sp > 1 and m // sp < 1024:
                 break
             for cl in ((0, 1) if sp > 1 and sp <= 8 and bm % sp == 0 else (0,)):
-                os.environ["SKEL_PRE_PLAN"] = f"{bm},{nw},{sp},{cl}"
+                sk.set_sketch_tuning(path=3 if cl else 2, bm=bm, splits=sp)
                 ms = timed(lambda: sk.sketch(A, l, "gaussian", 7, out=X))
                 err = float((X - ref).norm() / ref.norm())
                 res.append((ms, bm, nw, sp, cl, err))
@@ -51,4 +51,4 @@ for name, m, n, l in SHAPES:
         print(f"    {bm:3d} {nw:3d} {sp:3d} cl{cl}  {ms:8.4f} ms {2 * l * m * n / ms / 1e9 / 37.13:6.1%}  rel {err:.1e}",
               flush=True)
     del A, X
-    os.environ.pop("SKEL_PRE_PLAN", None)
+    sk.set_sketch_tuning()
