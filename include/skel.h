@@ -157,10 +157,12 @@ sk_status sk_sketch(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t 
  *               2 / 3 the TMA path with K-splits summed through HBM partials / through the
  *               distributed shared memory of a cluster of the splits
  *   bm          CTA row-tile height: 0 or one of 32, 40, 48, 64
+ *   warps       consumer warps per CTA = 32-column groups of the tile: 0, 7 (224 columns) or 8 (256)
  *   splits      K-splits per chunk (0 = planner, 1..64)
  *   chunk_rows  rows of A per K-chunk, rounded up to 16 (0 = the largest whose Gamma slot fits ~80 MB)
  * Results are identical up to summation order (parity tests use it to reach every plan). */
-sk_status sk_set_sketch_tuning(sk_ctx* ctx, int32_t path, int32_t bm, int32_t splits, int64_t chunk_rows);
+sk_status sk_set_sketch_tuning(sk_ctx* ctx, int32_t path, int32_t bm, int32_t warps, int32_t splits,
+                               int64_t chunk_rows);
 
 /* ---- column sketch for streaming two-sided selection (Algorithm 3) ----
  * Y = A Omega^T with Omega an l x n embedding drawn like sk_sketch's Gamma over the column index

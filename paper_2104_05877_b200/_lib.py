@@ -17,7 +17,7 @@ STATUS_NAMES = {0: "SK_OK", 1: "SK_E_ARG", 2: "SK_E_RANK", 3: "SK_E_CUDA", 4: "S
 _SIGS = {
     "sk_create": [ctypes.POINTER(c_dp), c_int, c_dp],
     "sk_set_stream": [c_dp, c_dp],
-    "sk_set_sketch_tuning": [c_dp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_i64],
+    "sk_set_sketch_tuning": [c_dp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_i64],
     "sk_sketch_dual": [c_dp, c_dp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, ctypes.c_uint64, ctypes.c_uint64,
                        c_dp, c_i64, c_dp, c_i64],
     "sk_id_estimate_cols": [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, ctypes.POINTER(c_i64)],

@@ -108,10 +108,10 @@ class DistSession:
             self.h = None
 
 
-def set_sketch_tuning(path=0, bm=0, splits=0, chunk_rows=0, device=None):
+def set_sketch_tuning(path=0, bm=0, splits=0, chunk_rows=0, warps=0, device=None):
     """sk_set_sketch_tuning: pin the dense sketch's plan on this device's context (0 = automatic)."""
     h = context(device)
-    _check(lib().sk_set_sketch_tuning(h, int(path), int(bm), int(splits), ctypes.c_int64(int(chunk_rows))), h)
+    _check(lib().sk_set_sketch_tuning(h, int(path), int(bm), int(warps), int(splits), ctypes.c_int64(int(chunk_rows))), h)
 
 
 def launch_count(device=None):

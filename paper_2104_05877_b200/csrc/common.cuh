@@ -26,8 +26,9 @@ struct sk_ctx {
   // pinned host scratch for small device->host results (info, scalars)
   void* host_scratch = nullptr;
   // dense-sketch tuning (sk_set_sketch_tuning; 0 = automatic): path 1 = the fallback kernel that
-  // generates Omega tiles in shared memory; row-tile height, K-splits per chunk, rows per K-chunk
-  int tune_sketch_path = 0, tune_sketch_bm = 0, tune_sketch_splits = 0;
+  // generates Omega tiles in shared memory; row-tile height, warps (x 32 columns), K-splits per chunk,
+  // rows per K-chunk
+  int tune_sketch_path = 0, tune_sketch_bm = 0, tune_sketch_nw = 0, tune_sketch_splits = 0;
   int64_t tune_sketch_chunk = 0;
   // lowest-priority helper stream + events for look-ahead overlap (LUPP trailing updates)
   cudaStream_t aux = nullptr;

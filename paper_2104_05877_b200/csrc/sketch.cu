@@ -248,10 +248,10 @@ __device__ __forceinline__ void mbar_arrive_local(unsigned addr) {
 // the copies up to a ring ahead.  Freed from the cluster-shared Box-Muller producers, the tile
 // can be chosen for the wave (plan_pre): BM in {32, 48, 64} rows x 256 columns, split-K to fill
 // the waves; C2 (l = 522) runs BM = 48 (1% padded rows instead of 10% at BM = 64) with 4 K-splits.
-constexpr int PBOX = 64;                                     // A tile rows (columns of A) per tensor load
 template <int BM, int NW> struct PCfg {
   static constexpr int OS = BM + 4;
   static constexpr int TBNP = NW * 32;
+  static constexpr int PBOX = TBNP % 64 == 0 ? 64 : 32;      // columns of A per tensor load (box 16 x PBOX)
   static constexpr int A_BYTES = TBNP * TBK * 8;
   static constexpr int O_BYTES = TBK * OS * 8;
   static constexpr int ST_BYTES = ((A_BYTES + O_BYTES) + 1023) & ~1023;
@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
   __syncthreads();
   const double* img_rt = img + ((int64_t)rt * KT) * (TBK * C::OS);
   // number of 64-column tensor loads with any column inside A (the rest of the tile stays stale)
+  constexpr int PBOX = C::PBOX;
   const int64_t nbox_all = (p.n - n0 + PBOX - 1) / PBOX;
   const int nbox = (int)(nbox_all < NW * 32 / PBOX ? nbox_all : NW * 32 / PBOX);
   int issued = 0;
@@ -988,6 +989,8 @@ template <int BM, int NW> int pre_max_ctas(int S) {
   return cached[S];
 }
 int pre_capacity(int bm, int nw, int S) {
+  if (bm == 40 && nw == 7) return pre_max_ctas<40, 7>(S);
+  if (bm == 48 && nw == 7) return pre_max_ctas<48, 7>(S);
   if (bm == 48 && nw == 8) return pre_max_ctas<48, 8>(S);
   if (bm == 64 && nw == 8) return pre_max_ctas<64, 8>(S);
   if (bm == 32 && nw == 8) return pre_max_ctas<32, 8>(S);
@@ -1011,10 +1014,12 @@ int64_t chunk_rows(int64_t m, int64_t l, int bm, int64_t forced) {
 // tuning (sk_set_sketch_tuning) can pin BM, the split count and the chunk height.
 PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
   PrePlan best;
-  const int cand[][2] = {{48, 8}, {64, 8}, {32, 8}, {40, 8}};
+  // 8 warps = 256-column tiles; 7 warps = 224 (C4's n = 784 fills 4 tiles of 224 to 87.5 %, of 256 to 77 %)
+  const int cand[][2] = {{48, 8}, {64, 8}, {32, 8}, {40, 8}, {40, 7}, {48, 7}};
   for (auto& cd : cand) {
     const int bm = cd[0], nw = cd[1];
     if (c->tune_sketch_bm && c->tune_sketch_bm != bm) continue;
+    if (c->tune_sketch_nw && c->tune_sketch_nw != nw) continue;
     const int64_t mb = cdiv(l, bm), nb = cdiv(n, nw * 32);
     const int64_t ch = chunk_rows(m, l, bm, c->tune_sketch_chunk);
     const int64_t nch = cdiv(m, ch);
@@ -1065,10 +1070,10 @@ __global__ void __launch_bounds__(128) k_omega_plain(uint2 key, int l, int64_t j
 }
 
 // The tensor map of a column-major m x n A (box 16 rows x 64 columns, 128-byte swizzle).
-sk_status make_tmap(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, CUtensorMap* tm) {
+sk_status make_tmap(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, CUtensorMap* tm, int pbox) {
   const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
   const cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)TBK, (cuuint32_t)PBOX};
+  const cuuint32_t box[2] = {(cuuint32_t)TBK, (cuuint32_t)pbox};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = tmap_encoder()(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides,
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1136,7 +1141,7 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   using C = PCfg<BM, NW>;
   DenseParams p = p0;
   CUtensorMap tm;
-  SK_TRY(make_tmap(c, p.A, m, n, p.lda, &tm));
+  SK_TRY(make_tmap(c, p.A, m, n, p.lda, &tm, C::PBOX));
   const int64_t mb = cdiv(l, BM);
   const int64_t chunk = pl.chunk > 0 ? pl.chunk : m;
   DBuf img, part;
@@ -1165,6 +1170,8 @@ sk_status sketch_dense_pre(sk_ctx* c, const DenseParams& p, int64_t m, int64_t n
   if (pl.bm == 64 && pl.nw == 8) return run_pre<64, 8>(c, p, m, n, l, pl, Qom, ldq);
   if (pl.bm == 32 && pl.nw == 8) return run_pre<32, 8>(c, p, m, n, l, pl, Qom, ldq);
   if (pl.bm == 40 && pl.nw == 8) return run_pre<40, 8>(c, p, m, n, l, pl, Qom, ldq);
+  if (pl.bm == 40 && pl.nw == 7) return run_pre<40, 7>(c, p, m, n, l, pl, Qom, ldq);
+  if (pl.bm == 48 && pl.nw == 7) return run_pre<48, 7>(c, p, m, n, l, pl, Qom, ldq);
   return fail(c, SK_E_ARG, "sketch: no tensor-core plan for this shape");
 }
 

@@ -527,6 +527,7 @@ def test_rand_lupp_host_pipelined(emb):
     (0, 48, 1, 0), (0, 64, 1, 0), (0, 32, 1, 0), (0, 40, 1, 0),        # tile heights, one K range
     (2, 48, 4, 0), (3, 48, 4, 0), (3, 64, 2, 0), (3, 32, 8, 0),        # K-splits via HBM partials / cluster DSMEM
     (0, 48, 1, 256), (2, 40, 3, 320), (3, 48, 2, 512),                  # K-chunked Omega (ragged last chunk)
+    (0, 40, 1, 0, 7), (2, 48, 3, 256, 7), (3, 40, 2, 0, 7),             # 7 warps: 224-column tiles, 32-column boxes
     (1, 0, 0, 0),                                                       # shared-memory generation fallback
 ])
 def test_sketch_dense_plans(plan):
@@ -536,7 +537,7 @@ def test_sketch_dense_plans(plan):
     fallback kernel.  Ragged l, m and n span several tiles."""
     m, n, l = 1000, 700, 61
     A = rand_mat(m, n, 41)
-    sk.set_sketch_tuning(*plan)
+    sk.set_sketch_tuning(*plan[:4], warps=plan[4] if len(plan) > 4 else 0)
     try:
         X = sk.sketch(dev_f(A), l, "gaussian", 77).cpu().numpy()
     finally:

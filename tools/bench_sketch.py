@@ -33,10 +33,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--only", default="", help="substring filter on the shape name")
-    ap.add_argument("--tune", default="", help="path,bm,splits,chunk for sk_set_sketch_tuning")
+    ap.add_argument("--tune", default="", help="path,bm,splits,chunk[,warps] for sk_set_sketch_tuning")
     a = ap.parse_args()
     if a.tune:
-        sk.set_sketch_tuning(*[int(x) for x in a.tune.split(",")])
+        t = [int(x) for x in a.tune.split(",")]
+        sk.set_sketch_tuning(*t[:4], warps=t[4] if len(t) > 4 else 0)
     dev = torch.device("cuda", 0)
     flush = torch.empty(512 << 18, dtype=torch.int32, device=dev)
     for name, m, n, l, emb in SHAPES:

@@ -11,7 +11,7 @@ import paper_2104_05877_b200 as sk  # noqa: E402
 SHAPES = [("C2 k=16", 4096, 4096, 26), ("C2 k=64", 4096, 4096, 74), ("C2 k=256", 4096, 4096, 266),
           ("C2 k=512", 4096, 4096, 522), ("C4 k=50", 65536, 784, 100), ("C4 k=100", 65536, 784, 200),
           ("C4 k=200", 65536, 784, 400), ("C5 block", 131072, 8192, 1100)]
-PLANS = [(64, 8), (48, 8), (40, 8), (32, 8)]
+PLANS = [(64, 8), (48, 8), (40, 8), (32, 8), (40, 7), (48, 7)]
 
 
 def timed(fn, reps=5):
@@ -29,7 +29,10 @@ def timed(fn, reps=5):
     return sorted(ts)[len(ts) // 2]
 
 
+only = sys.argv[1] if len(sys.argv) > 1 else ""
 for name, m, n, l in SHAPES:
+    if only and only not in name:
+        continue
     A = sk.fortran(torch.randn(m, n, dtype=torch.float64, device="cuda"))
     X = torch.empty((l, n), dtype=torch.float64, device="cuda")
     sk.set_sketch_tuning()
@@ -42,7 +45,7 @@ for name, m, n, l in SHAPES:
             if sp > 1 and m // sp < 1024:
                 break
             for cl in ((0, 1) if sp > 1 and sp <= 8 and bm % sp == 0 else (0,)):
-                sk.set_sketch_tuning(path=3 if cl else 2, bm=bm, splits=sp)
+                sk.set_sketch_tuning(path=3 if cl else 2, bm=bm, splits=sp, warps=nw)
                 ms = timed(lambda: sk.sketch(A, l, "gaussian", 7, out=X))
                 err = float((X - ref).norm() / ref.norm())
                 res.append((ms, bm, nw, sp, cl, err))
