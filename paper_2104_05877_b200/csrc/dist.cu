@@ -357,11 +357,7 @@ sk_status dist_residual(sk_ctx* c, const double* A, int64_t m, int64_t lda, cons
     SK_TRY(dist_cholqr_local(c, Qr.as<double>(), n, v.n_global, k, status_dev));
   }
   if (kind == SK_RES_COL_ID) {
-    if (n > 0) {
-      SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
-      SK_TRY(gemm_qta(c, Qc.as<double>(), m, A, m, n, lda, k, W.as<double>(), n));
-      SK_TRY(gemm_sumsq(c, false, true, m, n, k, -1.0, Qc.as<double>(), m, W.as<double>(), n, 1.0, A, lda, sums));
-    }
+    if (n > 0) SK_TRY(col_id_sumsq(c, Qc.as<double>(), A, m, n, lda, k, sums));
     return dist_allreduce_sum(c, sums, 2);
   }
   if (kind == SK_RES_ROW_ID) {   // A Q_R = sum_r A_r Q_R,r (m x k, one all-reduce), then local blocks

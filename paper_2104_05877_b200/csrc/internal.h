@@ -35,6 +35,10 @@ sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int
 // col-major), both Gaussian (Gamma over A's rows from seed_x, Omega over A's columns from seed_y).
 sk_status sketch_dual(sk_ctx* c, const double* A, bool a_on_host, int64_t m, int64_t n, int64_t lda, int64_t lx,
                       int64_t ly, uint64_t seed_x, uint64_t seed_y, double* X, int64_t ldx, double* Y, int64_t ldy);
+// sums[0] = ||A - Q W||_F^2, sums[1] = ||A||_F^2 (Q m x k col-major, W k x n col-major with an even
+// ldw, A m x n col-major) on the TMA + DMMA sketch pipeline with the residual epilogue (S6).
+sk_status residual_sumsq_tma(sk_ctx* c, const double* Q, int64_t ldq, const double* W, int64_t ldw, const double* A,
+                             int64_t lda, int64_t m, int64_t n, int64_t k, double* sums);
 // Y = A Omega^T (m x l col-major, ldy >= m), Omega l x n (Alg. 3 column sketch).
 sk_status sketch_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int64_t l, int emb,
                       int zeta, uint64_t seed, double* Y, int64_t ldy);
@@ -60,6 +64,9 @@ sk_status lupp(sk_ctx* c, const double* P, bool row_major, int64_t n, int64_t k,
 // Q (rows x k, ld rows) = an orthonormal basis of range(C) (C rows x k, ld rows): LUPP basis +
 // CholeskyQR2, or shifted CholeskyQR3 for panels taller than one cluster's LUPP (residual.cu).
 sk_status orthonormal_basis(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q, int64_t* status_dev);
+// sums[0] = ||A - Q Q^T A||_F^2, sums[1] = ||A||_F^2 for an orthonormal Q (m x k, ld m) (residual.cu).
+sk_status col_id_sumsq(sk_ctx* c, const double* Q, const double* A, int64_t m, int64_t n, int64_t lda, int64_t k,
+                       double* sums);
 // R (n x n, ldr) = upper triangle of B (first n columns, ldb), zeros below (dense.cu).
 sk_status upper_triangle(sk_ctx* c, const double* B, int64_t ldb, int64_t n, double* R, int64_t ldr);
 // RSVD-DEIM column skeletons from A and its row sketch X (deim.cu).

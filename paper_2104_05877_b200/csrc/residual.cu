@@ -46,6 +46,24 @@ static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows,
   return cholqr2(c, Q, rows, k, rows, status_dev);
 }
 
+sk_status col_id_sumsq(sk_ctx* c, const double* Q, const double* A, int64_t m, int64_t n, int64_t lda, int64_t k,
+                       double* sums) {
+  // W = Q^T A by the sketch's TMA + DMMA GEMM (Omega := Q^T; written as W^T, n x k column-major),
+  // turned column-major k x n (ld even, the tensor-map rule), then ||A - Q W||^2 and ||A||^2 on the
+  // same pipeline with the residual epilogue (Q packed as the row operand, A read once in the epilogue)
+  DBuf Wt, W;
+  SK_TRY(Wt.alloc(c, (size_t)k * n * sizeof(double)));
+  SK_TRY(gemm_qta(c, Q, m, A, m, n, lda, k, Wt.as<double>(), n));
+  const int64_t ldw = k + (k & 1);
+  if ((reinterpret_cast<uintptr_t>(A) & 7) == 0 && m < (1LL << 31)) {
+    SK_TRY(W.alloc(c, (size_t)ldw * n * sizeof(double)));
+    SK_TRY(transpose(c, Wt.as<double>(), n, k, n, W.as<double>(), ldw));
+    Wt.release();
+    return residual_sumsq_tma(c, Q, m, W.as<double>(), ldw, A, lda, m, n, k, sums);
+  }
+  return gemm_sumsq(c, false, true, m, n, k, -1.0, Q, m, Wt.as<double>(), n, 1.0, A, lda, sums);
+}
+
 sk_status orthonormal_basis(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q, int64_t* status_dev) {
   if (rows > lupp_max_rows(c)) return basis_shifted_cholqr3(c, C, rows, k, Q, status_dev);
   DBuf piv;
@@ -99,12 +117,7 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
     SK_TRY(orthonormal_basis(c, Rt.as<double>(), n, k, Qr.as<double>(), status_dev));
     Rt.release();
   }
-  if (kind == SK_RES_COL_ID) {
-    // W^T (n x k col-major) = (Qc^T A)^T by the sketch's TMA + DMMA GEMM (Omega = Qc^T)
-    SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
-    SK_TRY(gemm_qta(c, Qc.as<double>(), m, A, m, n, lda, k, W.as<double>(), n));
-    return gemm_sumsq(c, false, true, m, n, k, -1.0, Qc.as<double>(), m, W.as<double>(), n, 1.0, A, lda, sums);
-  }
+  if (kind == SK_RES_COL_ID) return col_id_sumsq(c, Qc.as<double>(), A, m, n, lda, k, sums);
   if (kind == SK_RES_ROW_ID) {
     SK_TRY(W.alloc(c, (size_t)m * k * sizeof(double)));
     SK_TRY(gemm(c, false, false, m, k, n, 1.0, A, lda, Qr.as<double>(), n, 0.0, W.as<double>(), m));
@@ -131,9 +144,7 @@ sk_status residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_
                                (size_t)k, cudaMemcpyDeviceToDevice, c->stream));
   SK_TRY(orthonormal_basis(c, Cc.as<double>(), m, k, Qc.as<double>(), status_dev));
   Cc.release();
-  SK_TRY(W.alloc(c, (size_t)k * n * sizeof(double)));
-  SK_TRY(gemm_qta(c, Qc.as<double>(), m, A, m, n, lda, k, W.as<double>(), n));
-  return gemm_sumsq(c, false, true, m, n, k, -1.0, Qc.as<double>(), m, W.as<double>(), n, 1.0, A, lda, sums);
+  return col_id_sumsq(c, Qc.as<double>(), A, m, n, lda, k, sums);
 }
 
 }  // namespace skel

@@ -50,6 +50,10 @@ struct DenseParams {
   int64_t k_per_split;
   int64_t k0;            // first row of A in this K-chunk (rows k0 .. m-1 of A; m = the chunk's end)
   int accum;             // 1: X += the chunk's product (chunks after the first), 0: X = it
+  // MODE 4 (residual): E = Csub - product over each output tile, never stored; per-CTA
+  // (sum E^2, sum Csub^2) into sums_part[2 * linear block]
+  const double* Csub; int64_t ldcs;
+  double* sums_part;
 };
 
 template <bool VEC>
@@ -302,6 +306,21 @@ __global__ void __launch_bounds__(128) k_omega_pack(const double* __restrict__ Q
   }
 }
 
+// The image of a GIVEN row operand Q (M x K, column-major, ld ldq) for the GEMM E = C - Q B: block
+// (row tile rt of M, k tile kt of K) = [TBK][OS] with img(kk, r) = Q(rt*BM + r, kt*TBK + kk); one CTA
+// per block, threads along r (contiguous in Q's columns).
+__global__ void __launch_bounds__(128) k_pack_rows(const double* __restrict__ Q, int64_t ldq, int64_t M, int64_t K,
+                                                   int BM, int OS, int64_t KT, double* __restrict__ img) {
+  const int64_t tile = blockIdx.x;
+  const int64_t rt = tile / KT, kt = tile - (tile / KT) * KT;
+  double* blk = img + tile * (int64_t)(TBK * OS);
+  for (int e = threadIdx.x; e < TBK * OS; e += 128) {
+    const int kk = e / OS, r = e - kk * OS;
+    const int64_t row = rt * BM + r, kq = kt * TBK + kk;
+    blk[e] = (r < BM && row < M && kq < K) ? Q[row + kq * ldq] : 0.0;
+  }
+}
+
 __device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigned bytes, unsigned mbar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
@@ -418,6 +437,48 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
     if (lane == 0) mbar_arrive_local(emptyB + 8 * s);
   }
   const int c0 = sig8(2 * q), c1 = sig8(2 * q + 1);
+  if (MODE == 4) {
+    // residual epilogue (S6): e = Csub(r, col) - acc, squared and summed with Csub^2; Csub (the
+    // m x n A, column-major) is read once, streamed; nothing of the m x n residual is written
+    double se = 0.0, sc = 0.0;
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < FI; ++i) {
+        const int64_t r = (int64_t)rt * BM + i * 8 + g;
+        if (r >= p.l) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t cb = n0 + wn + j * 8;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t col = cb + (h ? c1 : c0);
+            if (col < p.n) {
+              const double a = __ldcs(p.Csub + r + col * p.ldcs);
+              const double e = a - acc[i][j][h];
+              se = fma(e, e, se);
+              sc = fma(a, a, sc);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      se += __shfl_xor_sync(0xffffffffu, se, o);
+      sc += __shfl_xor_sync(0xffffffffu, sc, o);
+    }
+    __shared__ double wred[2 * NW];
+    if (lane == 0) { wred[2 * warp] = se; wred[2 * warp + 1] = sc; }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < NW; ++w) { a += wred[2 * w]; b += wred[2 * w + 1]; }
+      const int64_t lin = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
+      p.sums_part[2 * lin] = a;
+      p.sums_part[2 * lin + 1] = b;
+    }
+    return;
+  }
   if (MODE == 2) {
     constexpr int TST = C::TBNP + 1;                        // tile row stride (odd: fewer conflicts)
     static_assert((size_t)BM * TST * 8 <= (size_t)TS * C::ST_BYTES, "tile fits the ring");
@@ -1150,17 +1211,55 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   const int sp_max = (int)cdiv(chunk, kps_max);
   const bool cl = pl.cluster && sp_max > 1 && sp_max <= 8 && BM % sp_max == 0;
   if (sp_max > 1 && !cl) SK_TRY(part.alloc(c, (size_t)sp_max * l * n * sizeof(double)));
-  for (int64_t i0 = 0; i0 < m; i0 += chunk) {
-    const int64_t i1 = std::min(m, i0 + chunk);
-    SK_TRY((omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, i0, i1, img.as<double>())));
+  const int64_t nch = cdiv(m, chunk);
+  if (nch == 1) {
+    SK_TRY((omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, 0, m, img.as<double>())));
+    p.k0 = 0;
+    p.m = m;
+    p.accum = 0;
+    return pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, cl, img.as<double>(), part.as<double>());
+  }
+  // Several chunks: two image slots; the image of chunk c + 1 is generated on the helper stream while
+  // the GEMM of chunk c runs (its small CTAs fit beside a GEMM CTA on an SM), into the slot the GEMM of
+  // chunk c - 1 has finished reading.  Events order slot reuse and image -> GEMM.
+  DBuf img2;
+  SK_TRY(img2.alloc(c, img.bytes));
+  SK_TRY(ensure_aux(c));
+  double* slot[2] = {img.as<double>(), img2.as<double>()};
+  cudaEvent_t ev[5] = {};
+  sk_status rs = SK_OK;
+  for (int e = 0; e < 5 && rs == SK_OK; ++e)
+    if (cudaEventCreateWithFlags(&ev[e], cudaEventDisableTiming) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sketch: event");
+  cudaEvent_t* made = ev;         // [2] image of the chunk in slot s complete (helper stream)
+  cudaEvent_t* read = ev + 2;     // [2] GEMM that read slot s complete (context stream)
+  if (rs == SK_OK && (cudaEventRecord(ev[4], c->stream) != cudaSuccess || cudaStreamWaitEvent(c->aux, ev[4], 0) != cudaSuccess))
+    rs = fail(c, SK_E_CUDA, "sketch: event");
+  if (rs == SK_OK) rs = omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, 0, std::min(m, chunk), slot[0]);
+  for (int64_t ci = 0; ci < nch && rs == SK_OK; ++ci) {
+    const int64_t i0 = ci * chunk, i1 = std::min(m, i0 + chunk);
+    if (ci + 1 < nch) {           // next image on the helper stream, into the other slot
+      const int s = (int)((ci + 1) & 1);
+      cudaStream_t main_stream = c->stream;
+      if (ci >= 1 && cudaStreamWaitEvent(c->aux, read[s], 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sketch: event"); break; }
+      c->stream = c->aux;
+      rs = omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, i1, std::min(m, i1 + chunk), slot[s]);
+      c->stream = main_stream;
+      if (rs == SK_OK && cudaEventRecord(made[s], c->aux) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sketch: event");
+      if (rs != SK_OK) break;
+    }
+    if (ci >= 1 && cudaStreamWaitEvent(c->stream, made[ci & 1], 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sketch: event"); break; }
     p.k0 = i0;
     p.m = i1;
-    p.accum = i0 > 0;
+    p.accum = ci > 0;
     const int64_t kps = cdiv(cdiv(i1 - i0, pl.splits), TBK) * TBK;
     const bool clu = cl && cdiv(i1 - i0, kps) == sp_max;
-    SK_TRY((pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, clu, img.as<double>(), part.as<double>())));
+    rs = pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, clu, slot[ci & 1], part.as<double>());
+    if (rs == SK_OK && cudaEventRecord(read[ci & 1], c->stream) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sketch: event");
   }
-  return SK_OK;
+  // the context stream has waited for every image, so the slots are freed after their last use
+  for (int e = 0; e < 5; ++e)
+    if (ev[e]) cudaEventDestroy(ev[e]);
+  return rs;
 }
 
 
@@ -1221,6 +1320,49 @@ sk_status sketch_dense(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t
   return splitk_reduce(c, p.part, splits, l, n, p.scale, X, ldx);
 }
 
+
+namespace {
+// sums[0] = ||A - Q W||_F^2, sums[1] = ||A||_F^2 on the TMA + DMMA pipeline: rows of the output = the
+// M = m rows of Q (packed once into the row-operand image), K = k, the column operand W (k x n,
+// column-major) streamed by TMA, MODE 4 epilogue against A.
+template <int BM, int NW>
+sk_status run_sumsq(sk_ctx* c, const double* Q, int64_t ldq, const double* W, int64_t ldw, const double* A, int64_t lda,
+                    int64_t m, int64_t n, int64_t k, double* sums) {
+  using C = PCfg<BM, NW>;
+  CUtensorMap tm;
+  SK_TRY(make_tmap(c, W, k, n, ldw, &tm, C::PBOX));
+  const int64_t mb = cdiv(m, BM), nb = cdiv(n, C::TBNP), KT = cdiv(k, TBK);
+  DBuf img, part;
+  SK_TRY(img.alloc(c, (size_t)mb * KT * TBK * C::OS * sizeof(double)));
+  SK_TRY(part.alloc(c, (size_t)2 * mb * nb * sizeof(double)));
+  k_pack_rows<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(Q, ldq, m, k, BM, C::OS, KT, img.as<double>());
+  SK_TRY(launched(c));
+  DenseParams p{};
+  p.A = W; p.lda = ldw; p.m = k; p.n = n; p.l = (int)std::min<int64_t>(m, INT32_MAX);
+  p.scale = 1.0; p.k0 = 0; p.k_per_split = cdiv(k, TBK) * TBK;
+  p.Csub = A; p.ldcs = lda; p.sums_part = part.as<double>();
+  auto kern = k_sketch_pre<BM, NW, 4>;
+  SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)mb, (unsigned)nb, 1);
+  lc.blockDim = dim3(C::NT);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;     // PDL behind the pack kernel
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at; lc.numAttrs = 1;
+  SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, (const double*)img.as<double>(), KT));
+  SK_TRY(launched(c));
+  return reduce_pairs(c, part.as<double>(), mb * nb, sums);
+}
+}  // namespace
+
+sk_status residual_sumsq_tma(sk_ctx* c, const double* Q, int64_t ldq, const double* W, int64_t ldw, const double* A,
+                             int64_t lda, int64_t m, int64_t n, int64_t k, double* sums) {
+  if (!tma_ok_for(W, k, n, ldw) || m >= (1LL << 31)) return fail(c, SK_E_ARG, "residual_sumsq_tma: layout");
+  return run_sumsq<48, 8>(c, Q, ldq, W, ldw, A, lda, m, n, k, sums);
+}
 
 sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int64_t m, int64_t n, int64_t lda,
                    int64_t l, double* X, int64_t ldx) {
