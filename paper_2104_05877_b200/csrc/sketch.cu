@@ -54,11 +54,6 @@ struct DenseParams {
   // (sum E^2, sum Csub^2) into sums_part[2 * linear block]
   const double* Csub; int64_t ldcs;
   double* sums_part;
-  // MODE 0 with K-splits (gridDim.z > 1): the splits of an output tile add into X one after another
-  // (split z waits until tile_flags[tile] >= flag_base + z, then releases flag_base + z + 1), so X is
-  // accumulated in a fixed order without partial buffers; nullptr = one split
-  unsigned* tile_flags;
-  unsigned flag_base;
 };
 
 template <bool VEC>
@@ -522,43 +517,6 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
     }
     dev::cluster_arrive();                                  // no CTA leaves while peers read it
     dev::cluster_wait();
-    return;
-  }
-  if (MODE == 0 && p.tile_flags) {
-    // ordered split-K: the splits of this tile add into X in split order (split z = blockIdx.z is the
-    // slowest grid dimension, so split z - 1's CTA for this tile was dispatched earlier: no deadlock)
-    unsigned* flag = p.tile_flags + (blockIdx.x + (int64_t)gridDim.x * blockIdx.y);
-    const unsigned want = p.flag_base + blockIdx.z;
-    if (tid == 0) {
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-      } while (v < want);
-    }
-    __syncthreads();
-    const bool add = p.accum || blockIdx.z > 0;
-    if (active) {
-#pragma unroll
-      for (int i = 0; i < FI; ++i) {
-        const int r = rt * BM + i * 8 + g;
-        if (r >= p.l) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t cb = n0 + wn + j * 8;
-          double* dst = p.X + (int64_t)r * p.ldx;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t col = cb + (h ? c1 : c0);
-            if (col < p.n) dst[col] = add ? __ldcg(dst + col) + acc[i][j][h] * p.scale : acc[i][j][h] * p.scale;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(want + 1u) : "memory");
-    }
     return;
   }
   if (!active) return;
@@ -1145,12 +1103,11 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
         const double waves = (double)cdiv(ctas, cap);
         const double stage = (double)bm * nw * 32 * TBK;
         double cost = waves * (double)cdiv(kps, TBK) * stage;
-        // K-splits summed in-cluster through DSMEM (~0.05 FMA-equivalents per partial element), in
-        // order into X through the tile flags (an L2 read-modify-write, ~0.1), or through HBM
-        // partials + a reduce launch (tuning path 2); chunks after the first add X into X
-        if (sp > 1)
-          cost += clus ? 0.05 * (double)sp * l * n
-                       : (c->tune_sketch_path == 2 ? 0.3 * (double)sp * l * n + 3.6e5 : 0.1 * (double)sp * l * n);
+        // K-splits summed in-cluster through DSMEM (~0.05 FMA-equivalents per partial element) or
+        // through HBM partials + a reduce launch; chunks after the first add X into X.  (Adding the
+        // splits into X in split order through per-tile flags was measured slower: C2 k=512
+        // 0.594 -> 0.688 ms, k=16 0.06 -> 0.16 ms -- the splits of a tile then serialise.)
+        if (sp > 1) cost += clus ? 0.05 * (double)sp * l * n : 0.3 * (double)sp * l * n + 3.6e5;
         cost = cost * nch + (nch - 1) * (0.3 * (double)l * n + 3.6e5);
         if (cost < 0.99 * best.cost) {
           best.bm = bm; best.nw = nw; best.splits = (int)sp; best.cluster = clus != 0; best.cost = cost;
@@ -1207,8 +1164,7 @@ sk_status omega_chunk_image(sk_ctx* c, uint2 key, const double* Qom, int64_t ldq
 // `splits_req` ways (partials through `part` or cluster DSMEM); p.accum selects = or +=.
 template <int BM, int NW>
 sk_status pre_gemm_chunk(sk_ctx* c, const CUtensorMap& tm, DenseParams p, int64_t l, int64_t n, int splits_req,
-                         bool cl_allowed, const double* img, double* part, unsigned* flags = nullptr,
-                         unsigned flag_base = 0) {
+                         bool cl_allowed, const double* img, double* part) {
   using C = PCfg<BM, NW>;
   const int64_t mb = cdiv(l, BM), nb = cdiv(n, C::TBNP), KT = cdiv(p.m - p.k0, TBK);
   p.k_per_split = cdiv(cdiv(p.m - p.k0, splits_req), TBK) * TBK;
@@ -1230,10 +1186,7 @@ sk_status pre_gemm_chunk(sk_ctx* c, const CUtensorMap& tm, DenseParams p, int64_
   at[na].val.programmaticStreamSerializationAllowed = 1;
   ++na;
   lc.attrs = at; lc.numAttrs = na;
-  if (splits == 1 || clu || flags) {
-    // one K range, cluster-DSMEM splits, or splits accumulated in order through the tile flags
-    p.tile_flags = (splits > 1 && !clu) ? flags : nullptr;
-    p.flag_base = flag_base;
+  if (splits == 1 || clu) {
     auto kern = clu ? k_sketch_pre<BM, NW, 2> : k_sketch_pre<BM, NW, 0>;
     SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, img, KT));
@@ -1263,25 +1216,14 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   const int64_t kps_max = cdiv(cdiv(chunk, pl.splits), TBK) * TBK;
   const int sp_max = (int)cdiv(chunk, kps_max);
   const bool cl = pl.cluster && sp_max > 1 && sp_max <= 8 && BM % sp_max == 0;
-  // K-splits not reduced in a cluster add into X in split order through per-tile flags (no partial
-  // buffers, no reduce launch); tuning path 2 keeps the HBM partials + fixed-order reduce instead
-  const bool ordered = sp_max > 1 && !cl && c->tune_sketch_path != 2;
-  DBuf flg;
-  const int64_t ntile = cdiv(l, BM) * cdiv(n, C::TBNP);
-  if (ordered) {
-    SK_TRY(flg.alloc(c, (size_t)ntile * sizeof(unsigned)));
-    SK_CUDA(c, cudaMemsetAsync(flg.p, 0, (size_t)ntile * sizeof(unsigned), c->stream));
-  } else if (sp_max > 1 && !cl) {
-    SK_TRY(part.alloc(c, (size_t)sp_max * l * n * sizeof(double)));
-  }
-  unsigned* flags = ordered ? flg.as<unsigned>() : nullptr;
+  if (sp_max > 1 && !cl) SK_TRY(part.alloc(c, (size_t)sp_max * l * n * sizeof(double)));
   const int64_t nch = cdiv(m, chunk);
   if (nch == 1) {
     SK_TRY((omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, 0, m, img.as<double>())));
     p.k0 = 0;
     p.m = m;
     p.accum = 0;
-    return pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, cl, img.as<double>(), part.as<double>(), flags, 0);
+    return pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, cl, img.as<double>(), part.as<double>());
   }
   // Several chunks: two image slots; the image of chunk c + 1 is generated on the helper stream while
   // the GEMM of chunk c runs (its small CTAs fit beside a GEMM CTA on an SM), into the slot the GEMM of
@@ -1299,7 +1241,6 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   if (rs == SK_OK && (cudaEventRecord(ev[4], c->stream) != cudaSuccess || cudaStreamWaitEvent(c->aux, ev[4], 0) != cudaSuccess))
     rs = fail(c, SK_E_CUDA, "sketch: event");
   if (rs == SK_OK) rs = omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, 0, std::min(m, chunk), slot[0]);
-  unsigned flag_next = 0;             // flags of the ordered splits keep counting across chunks
   for (int64_t ci = 0; ci < nch && rs == SK_OK; ++ci) {
     const int64_t i0 = ci * chunk, i1 = std::min(m, i0 + chunk);
     if (ci + 1 < nch) {           // next image on the helper stream, into the other slot
@@ -1318,9 +1259,7 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
     p.accum = ci > 0;
     const int64_t kps = cdiv(cdiv(i1 - i0, pl.splits), TBK) * TBK;
     const bool clu = cl && cdiv(i1 - i0, kps) == sp_max;
-    const unsigned base = flag_next;
-    rs = pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, clu, slot[ci & 1], part.as<double>(), flags, base);
-    flag_next += (unsigned)cdiv(i1 - i0, kps);
+    rs = pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, clu, slot[ci & 1], part.as<double>());
     if (rs == SK_OK && cudaEventRecord(read[ci & 1], c->stream) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sketch: event");
   }
   // the context stream has waited for every image, so the slots are freed after their last use
