@@ -156,7 +156,7 @@ sk_status sk_sketch(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t 
  *               Gamma tile in shared memory (used automatically when A's layout rules out TMA),
  *               2 / 3 the TMA path with K-splits summed through HBM partials / through the
  *               distributed shared memory of a cluster of the splits
- *   bm          CTA row-tile height: 0 or one of 32, 40, 48, 64
+ *   bm          CTA row-tile height: 0 or one of 32, 40, 48, 56, 64
  *   warps       consumer warps per CTA = 32-column groups of the tile: 0, 7 (224 columns) or 8 (256)
  *   splits      K-splits per chunk (0 = planner, 1..64)
  *   chunk_rows  rows of A per K-chunk, rounded up to 16 (0 = the largest whose Gamma slot fits ~80 MB)

@@ -1054,6 +1054,7 @@ template <int BM, int NW> int pre_max_ctas(int S) {
   return cached[S];
 }
 int pre_capacity(int bm, int nw, int S) {
+  if (bm == 56 && nw == 8) return pre_max_ctas<56, 8>(S);
   if (bm == 40 && nw == 7) return pre_max_ctas<40, 7>(S);
   if (bm == 48 && nw == 7) return pre_max_ctas<48, 7>(S);
   if (bm == 48 && nw == 8) return pre_max_ctas<48, 8>(S);
@@ -1080,7 +1081,7 @@ int64_t chunk_rows(int64_t m, int64_t l, int bm, int64_t forced) {
 PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
   PrePlan best;
   // 8 warps = 256-column tiles; 7 warps = 224 (C4's n = 784 fills 4 tiles of 224 to 87.5 %, of 256 to 77 %)
-  const int cand[][2] = {{48, 8}, {64, 8}, {32, 8}, {40, 8}, {40, 7}, {48, 7}};
+  const int cand[][2] = {{48, 8}, {64, 8}, {32, 8}, {40, 8}, {56, 8}, {40, 7}, {48, 7}};
   for (auto& cd : cand) {
     const int bm = cd[0], nw = cd[1];
     if (c->tune_sketch_bm && c->tune_sketch_bm != bm) continue;
@@ -1275,6 +1276,7 @@ sk_status sketch_dense_pre(sk_ctx* c, const DenseParams& p, int64_t m, int64_t n
   if (pl.bm == 64 && pl.nw == 8) return run_pre<64, 8>(c, p, m, n, l, pl, Qom, ldq);
   if (pl.bm == 32 && pl.nw == 8) return run_pre<32, 8>(c, p, m, n, l, pl, Qom, ldq);
   if (pl.bm == 40 && pl.nw == 8) return run_pre<40, 8>(c, p, m, n, l, pl, Qom, ldq);
+  if (pl.bm == 56 && pl.nw == 8) return run_pre<56, 8>(c, p, m, n, l, pl, Qom, ldq);
   if (pl.bm == 40 && pl.nw == 7) return run_pre<40, 7>(c, p, m, n, l, pl, Qom, ldq);
   if (pl.bm == 48 && pl.nw == 7) return run_pre<48, 7>(c, p, m, n, l, pl, Qom, ldq);
   return fail(c, SK_E_ARG, "sketch: no tensor-core plan for this shape");

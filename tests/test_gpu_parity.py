@@ -524,7 +524,7 @@ def test_rand_lupp_host_pipelined(emb):
 
 
 @pytest.mark.parametrize("plan", [
-    (0, 48, 1, 0), (0, 64, 1, 0), (0, 32, 1, 0), (0, 40, 1, 0),        # tile heights, one K range
+    (0, 48, 1, 0), (0, 64, 1, 0), (0, 32, 1, 0), (0, 40, 1, 0), (0, 56, 1, 0),   # tile heights, one K range
     (2, 48, 4, 0), (3, 48, 4, 0), (3, 64, 2, 0), (3, 32, 8, 0),        # K-splits via HBM partials / cluster DSMEM
     (0, 48, 1, 256), (2, 40, 3, 320), (3, 48, 2, 512),                  # K-chunked Omega (ragged last chunk)
     (0, 40, 1, 0, 7), (2, 48, 3, 256, 7), (3, 40, 2, 0, 7),             # 7 warps: 224-column tiles, 32-column boxes
