@@ -343,7 +343,7 @@ sk_status dist_residual(sk_ctx* c, const double* A, int64_t m, int64_t lda, cons
     SK_TRY(dist_gather_cols(c, A, false, m, lda, Js, k, C.as<double>(), m));
   }
   if (kind == SK_RES_ID_COEFFS) {
-    if (n > 0) SK_TRY(gemm_sumsq(c, false, false, m, n, k, -1.0, C.as<double>(), m, Z, ldz, 1.0, A, lda, sums));
+    if (n > 0) SK_TRY(lowrank_sumsq(c, C.as<double>(), m, Z, ldz, nullptr, 0, A, lda, m, n, k, sums));
     return dist_allreduce_sum(c, sums, 2);
   }
   if (kind == SK_RES_COL_ID || kind == SK_RES_CUR) {
@@ -365,7 +365,7 @@ sk_status dist_residual(sk_ctx* c, const double* A, int64_t m, int64_t lda, cons
     if (n > 0) SK_TRY(gemm(c, false, false, m, k, n, 1.0, A, lda, Qr.as<double>(), n, 0.0, W.as<double>(), m));
     else SK_CUDA(c, cudaMemsetAsync(W.p, 0, (size_t)m * k * sizeof(double), c->stream));
     SK_TRY(dist_allreduce_sum(c, W.as<double>(), m * k));
-    if (n > 0) SK_TRY(gemm_sumsq(c, false, true, m, n, k, -1.0, W.as<double>(), m, Qr.as<double>(), n, 1.0, A, lda, sums));
+    if (n > 0) SK_TRY(lowrank_sumsq(c, W.as<double>(), m, nullptr, 0, Qr.as<double>(), n, A, lda, m, n, k, sums));
     return dist_allreduce_sum(c, sums, 2);
   }
   // CUR: Mid = Q_C^T A Q_R = sum_r (Q_C^T A_r) Q_R,r (k x k, one all-reduce); residual A_r - (Q_C Mid) Q_R,r^T
@@ -380,7 +380,7 @@ sk_status dist_residual(sk_ctx* c, const double* A, int64_t m, int64_t lda, cons
   }
   SK_TRY(dist_allreduce_sum(c, Mid.as<double>(), k * k));
   SK_TRY(gemm(c, false, false, m, k, k, 1.0, Qc.as<double>(), m, Mid.as<double>(), k, 0.0, Bm.as<double>(), m));
-  if (n > 0) SK_TRY(gemm_sumsq(c, false, true, m, n, k, -1.0, Bm.as<double>(), m, Qr.as<double>(), n, 1.0, A, lda, sums));
+  if (n > 0) SK_TRY(lowrank_sumsq(c, Bm.as<double>(), m, nullptr, 0, Qr.as<double>(), n, A, lda, m, n, k, sums));
   return dist_allreduce_sum(c, sums, 2);
 }
 

@@ -64,6 +64,10 @@ sk_status lupp(sk_ctx* c, const double* P, bool row_major, int64_t n, int64_t k,
 // Q (rows x k, ld rows) = an orthonormal basis of range(C) (C rows x k, ld rows): LUPP basis +
 // CholeskyQR2, or shifted CholeskyQR3 for panels taller than one cluster's LUPP (residual.cu).
 sk_status orthonormal_basis(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q, int64_t* status_dev);
+// sums[0] = ||A - L W||_F^2, sums[1] = ||A||_F^2, L m x k (ldl), W k x n given column-major (Wc, ldw)
+// or as its transpose (Wt n x k column-major, ldwt; pass the other nullptr) (residual.cu).
+sk_status lowrank_sumsq(sk_ctx* c, const double* L, int64_t ldl, const double* Wc, int64_t ldw, const double* Wt,
+                        int64_t ldwt, const double* A, int64_t lda, int64_t m, int64_t n, int64_t k, double* sums);
 // sums[0] = ||A - Q Q^T A||_F^2, sums[1] = ||A||_F^2 for an orthonormal Q (m x k, ld m) (residual.cu).
 sk_status col_id_sumsq(sk_ctx* c, const double* Q, const double* A, int64_t m, int64_t n, int64_t lda, int64_t k,
                        double* sums);

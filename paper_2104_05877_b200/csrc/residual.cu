@@ -46,6 +46,28 @@ static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows,
   return cholqr2(c, Q, rows, k, rows, status_dev);
 }
 
+// sums[0] = ||A - L W||_F^2, sums[1] = ||A||_F^2 for L (m x k, ldl) and W given either as a k x n
+// column-major matrix (Wc, ldw) or by its transpose (Wt, n x k column-major, ldwt): on the TMA + DMMA
+// pipeline with the residual epilogue when the layouts allow it (W column-major with an even ld),
+// else on the cp.async DMMA GEMM's sum-of-squares epilogue.
+sk_status lowrank_sumsq(sk_ctx* c, const double* L, int64_t ldl, const double* Wc, int64_t ldw, const double* Wt,
+                               int64_t ldwt, const double* A, int64_t lda, int64_t m, int64_t n, int64_t k, double* sums) {
+  const bool tma = (reinterpret_cast<uintptr_t>(A) & 7) == 0 && m < (1LL << 31);
+  if (tma && Wc && ldw % 2 == 0 && (reinterpret_cast<uintptr_t>(Wc) & 15) == 0)
+    return residual_sumsq_tma(c, L, ldl, Wc, ldw, A, lda, m, n, k, sums);
+  if (tma) {
+    DBuf W;
+    const int64_t ld = k + (k & 1);
+    SK_TRY(W.alloc(c, (size_t)ld * n * sizeof(double)));
+    if (Wt) SK_TRY(transpose(c, Wt, n, k, ldwt, W.as<double>(), ld));
+    else SK_CUDA(c, cudaMemcpy2DAsync(W.p, (size_t)ld * sizeof(double), Wc, (size_t)ldw * sizeof(double),
+                                      (size_t)k * sizeof(double), (size_t)n, cudaMemcpyDeviceToDevice, c->stream));
+    return residual_sumsq_tma(c, L, ldl, W.as<double>(), ld, A, lda, m, n, k, sums);
+  }
+  if (Wc) return gemm_sumsq(c, false, false, m, n, k, -1.0, L, ldl, Wc, ldw, 1.0, A, lda, sums);
+  return gemm_sumsq(c, false, true, m, n, k, -1.0, L, ldl, Wt, ldwt, 1.0, A, lda, sums);
+}
+
 sk_status col_id_sumsq(sk_ctx* c, const double* Q, const double* A, int64_t m, int64_t n, int64_t lda, int64_t k,
                        double* sums) {
   // W = Q^T A by the sketch's TMA + DMMA GEMM (Omega := Q^T; written as W^T, n x k column-major),
@@ -80,7 +102,7 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
     DBuf C;
     SK_TRY(C.alloc(c, (size_t)m * k * sizeof(double)));
     SK_TRY(gather_cols(c, A, m, lda, Js, k, C.as<double>(), m));
-    return gemm_sumsq(c, false, false, m, n, k, -1.0, C.as<double>(), m, Z, ldz, 1.0, A, lda, sums);
+    return lowrank_sumsq(c, C.as<double>(), m, Z, ldz, nullptr, 0, A, lda, m, n, k, sums);
   }
   if (kind == SK_RES_ROW_COEFFS || kind == SK_RES_CUR_CSS) {
     // ||A - W R||, R = A(I_s, :): W given (the row-ID estimate Y Y_1^+) or W = C S^{-1}
@@ -100,7 +122,7 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
       Wp = V.as<double>();
       ldw = m;
     }
-    return gemm_sumsq(c, false, true, m, n, k, -1.0, Wp, ldw, Rt.as<double>(), n, 1.0, A, lda, sums);
+    return lowrank_sumsq(c, Wp, ldw, nullptr, 0, Rt.as<double>(), n, A, lda, m, n, k, sums);
   }
   DBuf Qc, Qr, Cb, Rt, W;
   if (kind == SK_RES_COL_ID || kind == SK_RES_CUR) {
@@ -121,7 +143,7 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
   if (kind == SK_RES_ROW_ID) {
     SK_TRY(W.alloc(c, (size_t)m * k * sizeof(double)));
     SK_TRY(gemm(c, false, false, m, k, n, 1.0, A, lda, Qr.as<double>(), n, 0.0, W.as<double>(), m));
-    return gemm_sumsq(c, false, true, m, n, k, -1.0, W.as<double>(), m, Qr.as<double>(), n, 1.0, A, lda, sums);
+    return lowrank_sumsq(c, W.as<double>(), m, nullptr, 0, Qr.as<double>(), n, A, lda, m, n, k, sums);
   }
   // CUR: W = Qc^T A (k x n), Mid = W Qr (k x k), B = Qc Mid (m x k), residual A - B Qr^T
   DBuf Mid, B;
@@ -131,7 +153,7 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
   SK_TRY(gemm_qta(c, Qc.as<double>(), m, A, m, n, lda, k, W.as<double>(), n));            // W^T, n x k
   SK_TRY(gemm(c, true, false, k, k, n, 1.0, W.as<double>(), n, Qr.as<double>(), n, 0.0, Mid.as<double>(), k));
   SK_TRY(gemm(c, false, false, m, k, k, 1.0, Qc.as<double>(), m, Mid.as<double>(), k, 0.0, B.as<double>(), m));
-  return gemm_sumsq(c, false, true, m, n, k, -1.0, B.as<double>(), m, Qr.as<double>(), n, 1.0, A, lda, sums);
+  return lowrank_sumsq(c, B.as<double>(), m, nullptr, 0, Qr.as<double>(), n, A, lda, m, n, k, sums);
 }
 
 sk_status residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* C, int64_t k,
