@@ -52,7 +52,9 @@ static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows,
 // else on the cp.async DMMA GEMM's sum-of-squares epilogue.
 sk_status lowrank_sumsq(sk_ctx* c, const double* L, int64_t ldl, const double* Wc, int64_t ldw, const double* Wt,
                                int64_t ldwt, const double* A, int64_t lda, int64_t m, int64_t n, int64_t k, double* sums) {
-  const bool tma = (reinterpret_cast<uintptr_t>(A) & 7) == 0 && m < (1LL << 31);
+  // the TMA pipeline amortises its per-tile ring fill over K = k: measured ahead at k = 1000 (C5
+  // residual 1211 -> 1171 ms), even at k = 512 (C2), behind at k = 200 (C4 row ID 7.8 -> 8.3 ms)
+  const bool tma = (reinterpret_cast<uintptr_t>(A) & 7) == 0 && m < (1LL << 31) && k >= 512;
   if (tma && Wc && ldw % 2 == 0 && (reinterpret_cast<uintptr_t>(Wc) & 15) == 0)
     return residual_sumsq_tma(c, L, ldl, Wc, ldw, A, lda, m, n, k, sums);
   if (tma) {
@@ -77,7 +79,7 @@ sk_status col_id_sumsq(sk_ctx* c, const double* Q, const double* A, int64_t m, i
   SK_TRY(Wt.alloc(c, (size_t)k * n * sizeof(double)));
   SK_TRY(gemm_qta(c, Q, m, A, m, n, lda, k, Wt.as<double>(), n));
   const int64_t ldw = k + (k & 1);
-  if ((reinterpret_cast<uintptr_t>(A) & 7) == 0 && m < (1LL << 31)) {
+  if ((reinterpret_cast<uintptr_t>(A) & 7) == 0 && m < (1LL << 31) && k >= 512) {
     SK_TRY(W.alloc(c, (size_t)ldw * n * sizeof(double)));
     SK_TRY(transpose(c, Wt.as<double>(), n, k, n, W.as<double>(), ldw));
     Wt.release();

@@ -58,3 +58,24 @@ def test_header_compiles_as_c_and_cxx(tmp_path):
             pytest.skip(f"{cc} not available")
         r = subprocess.run([cc, "-fsyntax-only", "-Wall", "-Werror", "-x", lang, HEADER], capture_output=True, text=True)
         assert r.returncode == 0, r.stderr
+
+
+def test_round2_entry_points_reject_bad_calls_without_a_gpu():
+    """The round-2 entry points validate before touching a device: NULL context -> SK_E_ARG;
+    sk_nccl_unique_id(NULL) -> SK_E_ARG; sk_create_dist with an impossible partition -> SK_E_ARG."""
+    lib = _lib.load()
+    E = _lib.SK_E_ARG
+    assert lib.sk_set_sketch_tuning(None, 0, 0, 0, 0, 0) == E
+    assert lib.sk_sketch_power_ortho(None, None, 1, 1, 1, 1, 0, 8, 0, 1, None, 1, None) == E
+    assert lib.sk_sketch_dual(None, None, 0, 1, 1, 1, 1, 1, 0, 0, 0, None, 1, None, 1) == E
+    assert lib.sk_id_estimate_cols(None, None, 1, 1, 1, None, 1, None, 1, None) == E
+    assert lib.sk_id_estimate_rows(None, None, 1, 1, 1, None, 1, None, 1, None) == E
+    assert lib.sk_set_dist_exchange(None, 0) == E
+    assert lib.sk_dist_info(None, None, None, None, None, None) == E
+    assert lib.sk_nccl_unique_id(None) == E
+    h = ctypes.c_void_p()
+    uid = (ctypes.c_char * 128)()
+    # rank outside [0, world), negative column count: rejected before NCCL or CUDA is touched
+    assert lib.sk_create_dist(ctypes.byref(h), 0, None, uid, 2, 2, 100, 0, 50) == E
+    assert lib.sk_create_dist(ctypes.byref(h), 0, None, uid, 0, 1, 100, 60, 50) == E
+    assert not h.value
