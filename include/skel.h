@@ -328,8 +328,9 @@ sk_status sk_select_cols_cpqr(sk_ctx* ctx, const double* X, int64_t l, int64_t n
  * Q_X = ortho(X^T) (n x l), [U, S, V~] = svd(A Q_X, 'econ'), V^ = Q_X V~ (eq:rsvd_procedures,
  * P:237-243), then DEIM = column-wise LUPP on V^(:, 0:k)^T.  A m x n column-major,
  * X = Gamma A the l x n row-major sketch (ldx >= n).  Js device int64[k] in pivot order.
- * Requires 1 <= k <= l <= min(m, n).  The l x l SVD step is cuSOLVER's (geqrf + gesvd on the
- * triangular factor); everything else runs in this library's kernels.  info as sk_select_cols. */
+ * Requires 1 <= k <= l <= min(m, n).  Every step runs in this library's kernels: the l x l triangular
+ * factor of A Q_X from its row LUPP and Cholesky QR (no Householder QR), its right singular vectors by
+ * one-sided Jacobi in one cooperative launch.  info as sk_select_cols. */
 sk_status sk_select_cols_deim(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* X,
                               int64_t l, int64_t ldx, int64_t k, int64_t* Js, int64_t* info);
 

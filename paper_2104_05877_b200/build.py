@@ -63,7 +63,7 @@ def build(force=False, verbose=False):
             if out and verbose:
                 print(out)
     if force or jobs or _newer(LIB, objs):
-        cmd = [cc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcusolver", "-ldl"]
+        cmd = [cc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)

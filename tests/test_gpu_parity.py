@@ -543,3 +543,21 @@ def test_sketch_dense_plans(plan):
     finally:
         sk.set_sketch_tuning()
     assert rel_fro(X, o_sketch.sketch(A, l, "gaussian", 77)) <= 1e-12
+
+
+@pytest.mark.parametrize("k,l", [(64, 74), (256, 266)])
+def test_select_cols_deim_c2(k, l):
+    """RSVD-DEIM at C2 (4096^2, sigma_i = 10^(-i/50)): the l x l factor of A Q_X through the row LUPP +
+    Cholesky QR and its right singular vectors by one-sided Jacobi, against the oracle's Householder
+    QR + LAPACK SVD; singular values are distinct, so V^_k is unique up to column signs and the DEIM
+    pivots must agree."""
+    from inputs import make_c2
+    from oracle import deim as o_deim
+    A, sigma = make_c2(seed=1002)
+    Ad = dev_f(A)
+    X = sk.sketch(Ad, l, "gaussian", 2002 + k)
+    Js = sk.select_cols_deim(Ad, X, k)
+    Xo = o_sketch.sketch(A, l, "gaussian", 2002 + k)
+    V = o_deim.rsvd_vectors(A, Xo)
+    (piv, _, _, _), _ = lupp_parity(Js.cpu().numpy(), lambda f: o_lupp.lupp_panel(V[:, :k], k, f))
+    assert len(set(Js.cpu().tolist())) == k
