@@ -153,3 +153,91 @@ def test_rand_lupp_rank_failure_reports_the_step():
         with pytest.raises(sk.SkelError) as e:
             sk.rand_lupp(At, 4, 12, "gaussian", 1)
         assert e.value.status == SK_E_RANK and e.value.info == 3
+
+
+# ------------------------------------------------------------------ round-2 entry points at the edges
+def rand_cm(m, n, seed):
+    return np.random.default_rng(seed).standard_normal((m, n))
+
+
+@pytest.mark.parametrize("m,n,l,chunk", [(1037, 5, 3, 256), (33, 300, 1, 16), (2049, 129, 17, 1024)])
+def test_sketch_chunked_tiny_and_ragged(m, n, l, chunk):
+    """K-chunked Omega with ragged chunks (m not a multiple of the chunk or of 16), l = 1 and n < one tile."""
+    A = rand_cm(m, n, m + n)
+    sk.set_sketch_tuning(chunk_rows=chunk)
+    try:
+        X = sk.sketch(dev_f(A), l, "gaussian", 3).cpu().numpy()
+    finally:
+        sk.set_sketch_tuning()
+    ref = o_sketch.sketch(A, l, "gaussian", 3)
+    assert np.linalg.norm(X - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_sketch_dual_single_column_and_row(host):
+    A = rand_cm(40, 1, 1)
+    Ain = torch.from_numpy(np.asfortranarray(A)) if host else dev_f(A)
+    X, Y = sk.sketch_dual(Ain, 1, 1, seed_x=4, seed_y=5)
+    np.testing.assert_allclose(X.cpu().numpy(), o_sketch.sketch(A, 1, "gaussian", 4), rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(Y.cpu().numpy(), o_sketch.sketch_cols(A, 1, "gaussian", 5), rtol=1e-13, atol=1e-15)
+
+
+def test_estimates_k1_and_square_pivot_block():
+    """k = 1 and k = l (X_1 square: X_1^+ X = X_1^{-1} X, the sketch interpolation matrix itself)."""
+    from oracle import estimates as o_est
+    A = rand_cm(60, 50, 7)
+    Ad = dev_f(A)
+    for k, l in ((1, 4), (8, 8)):
+        X = sk.sketch(Ad, l, "gaussian", 11)
+        Js, _, _, _ = sk.select_cols(X, k)
+        Z = sk.id_estimate_cols(X, Js).cpu().numpy()
+        Zo = o_est.id_estimate_cols(o_sketch.sketch(A, l, "gaussian", 11), Js.cpu().numpy())
+        assert np.linalg.norm(Z - Zo) <= 1e-9 * np.linalg.norm(Zo)
+        Y = sk.sketch_cols(Ad, l, "gaussian", 12)
+        Is, _, _, _ = sk.select_rows(Y, k)
+        W = sk.id_estimate_rows(Y, Is).cpu().numpy()
+        Wo = o_est.id_estimate_rows(o_sketch.sketch_cols(A, l, "gaussian", 12), Is.cpu().numpy())
+        assert np.linalg.norm(W - Wo) <= 1e-9 * np.linalg.norm(Wo)
+        r, _ = sk.residual(Ad, Js, Is, "cur_css")
+        ro = float(np.linalg.norm(A - o_est.cur_css(A, Is.cpu().numpy(), Js.cpu().numpy())))
+        assert abs(r - ro) <= 1e-8 * ro
+
+
+def test_power_ortho_full_rank_l_equals_n():
+    """l = n: ortho(Y) spans everything, X = Q^T A with Q m x n orthonormal: X^T X = A^T A."""
+    A = rand_cm(70, 12, 9)
+    X = sk.sketch_power(dev_f(A), 12, "gaussian", 3, 2, ortho=True).cpu().numpy()
+    np.testing.assert_allclose(X.T @ X, A.T @ A, rtol=0, atol=1e-11 * np.abs(A.T @ A).max())
+
+
+def test_dist_context_k1_and_gaps_fallback():
+    """The distributed context at world size 1 with k = 1 (the per-step graph with one step) and with the
+    gaps output requested under the per-step exchange (served by the gather-then-replicate path)."""
+    import os
+    import socket
+    import torch.distributed as tdist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
+    try:
+        A = rand_cm(90, 40, 3)
+        Ad = dev_f(A)
+        sess = sk.DistSession(40, None, 0, "step")
+        try:
+            with sess:
+                X = sk.sketch(Ad, 6, "gaussian", 8)
+                J1, _, _, _ = sk.select_cols(X, 1)
+                J5, _, _, g5 = sk.select_cols(X, 5, want_gaps=True)
+        finally:
+            sess.close()
+        Xo = o_sketch.sketch(A, 6, "gaussian", 8)
+        assert J1.cpu().tolist() == o_lupp.select_cols(Xo, 1)[0].tolist()
+        piv, _, _, go = o_lupp.select_cols(Xo, 5)
+        assert J5.cpu().tolist() == piv.tolist()
+        np.testing.assert_allclose(g5.cpu().numpy(), go, atol=1e-9)
+    finally:
+        tdist.destroy_process_group()
