@@ -61,7 +61,9 @@ typedef enum {
  * Philox4x32-10 (R1, R2) and never stored in HBM.  SRTT:
  * sqrt(m/l) Pi_{m->l} T Phi Pi_{m->m} with T the unitary discrete Hartley transform, the random
  * permutation / selection as keyed Feistel bijections and the signs from Philox (R18); applied by
- * a per-column radix-2 FFT in shared memory, m a power of two <= 16384 (R19), SK_E_ARG otherwise. */
+ * a per-column radix-2 FFT in shared memory: m a power of two <= 16384 in one CTA per column, and
+ * 32768 <= m <= 131072 (with l <= 5800) in a cluster of m/16384 CTAs per column whose partial
+ * transforms are combined over distributed shared memory (R19); SK_E_ARG otherwise. */
 typedef enum { SK_EMB_GAUSSIAN = 0, SK_EMB_SPARSE_SIGN = 1, SK_EMB_SRTT = 2 } sk_embedding;
 
 /* Which approximation sk_residual measures (Frobenius norm, R12).

@@ -92,3 +92,25 @@ def test_c5_oracle_streamed(c5_data):
     assert abs(nA - nAo) <= 1e-12 * nAo
     assert abs(r - ro) <= 1e-9 * ro + 4 * 2.0 ** -53 * nAo, (r, ro)
     assert ro >= o_res.optimal_error(sigma, k) * (1 - 1e-9)
+
+
+def test_c5_srtt(c5_data):
+    """The SRTT embedding at C5's m = 131072 (the four-step cluster transform): sampled sketch
+    columns against the oracle's FFT route, then the column LUPP properties and the residual's
+    Eckart-Young bracket on the SRTT sketch."""
+    A, sigma, Y, Yp = c5_data
+    m, n = A.shape
+    k, l, seed = 1000, 1100, 2006
+    cols = [0, 1, 4097, 31337, n - 1]
+    X = sk.sketch(A, l, "srtt", seed)
+    acols = np.stack([c5.column_by_reflectors(j, Y, Yp, sigma) for j in cols], 1)
+    Xo = o_sketch.sketch_srtt_fft(acols, l, seed)
+    assert rel_fro(X[:, cols].cpu().numpy(), Xo) <= 1e-12
+    Js, Lf, _, _ = sk.select_cols(X, k)
+    J = Js.cpu().numpy()
+    assert J[0] == int(torch.argmax(X[0].abs()).item())
+    assert len(set(J.tolist())) == k
+    assert float(Lf.abs().max()) <= 1.0 + 1e-14
+    r, nA = sk.residual(A, Js, None, "col_id")
+    opt = o_res.optimal_error(sigma, k)
+    assert opt * (1 - 1e-9) <= r <= 100 * opt

@@ -191,11 +191,25 @@ def test_stream_select_alg3_c1():
 
 
 # ------------------------------------------------------------------ SRTT embedding (8(f) rank 3)
-@pytest.mark.parametrize("m,n,l,seed", [(8, 5, 3, 1), (256, 256, 40, 2001), (4096, 333, 266, 7), (16384, 70, 510, 3)])
+@pytest.mark.parametrize("m,n,l,seed", [(8, 5, 3, 1), (256, 256, 40, 2001), (4096, 333, 266, 7), (16384, 70, 510, 3),
+                                         (32768, 301, 300, 11), (65536, 37, 1100, 12), (131072, 160, 777, 13),
+                                         (131072, 3, 1, 14)])
 def test_sketch_srtt_parity(m, n, l, seed):
+    """m <= 16384 (l permitting): one CTA per column; beyond: the four-step transform, a cluster of
+    m / 16384 CTAs per column whose partial Hartley values meet in distributed shared memory."""
     A = rand_mat(m, n, seed)
     X = sk.sketch(dev_f(A), l, "srtt", seed).cpu().numpy()
     assert rel_fro(X, o_sketch.sketch_srtt_fft(A, l, seed)) <= 1e-12
+
+
+def test_sketch_srtt_large_m_limits():
+    """Beyond the four-step kernel's reach: m > 131072, or l past its shared-memory table."""
+    with pytest.raises(sk.SkelError) as e:
+        sk.sketch(dev_f(rand_mat(262144, 2, 1)), 8, "srtt", 1)
+    assert e.value.status == 1
+    with pytest.raises(sk.SkelError) as e:
+        sk.sketch(dev_f(rand_mat(32768, 2, 1)), 6000, "srtt", 1)
+    assert e.value.status == 1
 
 
 def test_srtt_rand_lupp_c1():

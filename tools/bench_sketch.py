@@ -26,6 +26,8 @@ SHAPES = [  # (name, m, n, l, embedding)
     ("C3 sparse", 16384, 16384, 510, "sparse_sign"),
     ("C2 srtt k=512", 4096, 4096, 522, "srtt"),
     ("C3 srtt", 16384, 16384, 510, "srtt"),
+    ("C4 srtt k=200", 65536, 784, 400, "srtt"),
+    ("C5 block srtt", 131072, 8192, 1100, "srtt"),
 ]
 
 
