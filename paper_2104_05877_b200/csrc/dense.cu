@@ -8,12 +8,16 @@
 
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "dmma.cuh"
 #include "internal.h"
 
 namespace skel {
 namespace {
+
+namespace cg = cooperative_groups;
 
 constexpr int TB = 32;   // diagonal block size
 
@@ -410,6 +414,361 @@ __global__ void k_upper_triangle(const double* B, int64_t ldb, int64_t n, double
   }
 }
 
+// ------------------------------------------------------------------ single-launch Cholesky and row solve
+// The CholeskyQR chain (G = Q^T Q, G = L L^T, Q <- Q L^{-T}) as two launches instead of ~50:
+//   k_potrf_cluster: right-looking Cholesky of a k x k SPD G (k <= 1024) by ONE cluster of 16 CTAs in
+//     32-wide block steps p, phases separated by cluster barriers (release/acquire: they order the
+//     global-memory updates; G stays in global memory, L2-resident, loads bypass L1):
+//       D  one warp factors the diagonal block in registers (row per lane; pivot by shuffle, column
+//          by shared memory, rsqrt by MUFU + one fourth-order step; tools/microbench/chol32_bench:
+//          ~6k cycles per 32 columns);
+//       P  L_ip = G_ip L_pp^{-T} by forward substitution (a warp per 32-row block, a row per lane),
+//          and, off the critical path, W_pp = L_pp^{-1} by the same substitution on unit rows;
+//       U  G_ij -= L_ip L_jp^T, 32 x 32 x 32 DMMA units spread over the cluster's 128 warps; the warp
+//          that updates the next diagonal block factors it right away (D of step p+1 under U of p).
+//   k_trsm_rows: X <- X L^{-T} (X rows x k) with no inter-CTA dependency: a CTA owns RB whole rows of X
+//     in shared memory and walks the 32-wide column blocks, X_j = (X_j - sum_c X_c L_jc^T) W_jj^T,
+//     row block j of L streamed in 32 x 64 chunks (then W_jj) through a cp.async ring.
+constexpr int CB = 32;           // block width of both kernels
+constexpr int CL = 16;           // cluster size of k_potrf_cluster
+constexpr int kCholMaxK = 1024;
+constexpr int LS = CB + 1;       // shared 32 x 32 tile stride
+
+// x = g L^{-T} for one row per lane: x_t = (g_t - sum_{q<t} x_q L(t, q)) / L(t, t); Ls = L (stride LS),
+// rinv[t] = 1 / L(t, t).  With g = e_lane it gives column `lane` of L^{-1}.
+__device__ __forceinline__ void rowsolve32(double (&g)[CB], const double* Ls, const double* rinv) {
+#pragma unroll
+  for (int t = 0; t < CB; ++t) {
+    g[t] *= rinv[t];
+#pragma unroll
+    for (int q = t + 1; q < CB; ++q) g[q] = fma(-g[t], Ls[q * LS + t], g[q]);
+  }
+}
+
+// 1/sqrt(d) for a normal d > 0 without the library routine's slow-path call (which would spill the
+// live row around every call site): the MUFU approximation refined by three Newton steps.
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  // one fourth-order step: e = 1 - d y^2, y' = y (1 + e/2 + 3e^2/8 + 5e^3/16), relative error ~e^4
+  const double e = fma(-d * y, y, 1.0);
+  const double p = fma(e, fma(0.3125, e, 0.375), 0.5);
+  return fma(y * e, p, y);
+}
+
+// column T of the register Cholesky (template recursion: every register index is a literal, so the
+// row never falls back to local memory)
+template <int T>
+struct Chol32Col {
+  static __device__ __forceinline__ void run(double (&r)[CB], double* colbuf, int lane, int& bad) {
+    double d = __shfl_sync(0xffffffffu, r[T], T);    // the pivot A(T, T), held by lane T
+    if (!(d > 0.0)) {
+      if (!bad) bad = T + 1;
+      d = 1.0;
+    }
+    const double rs = rsqrt_nr(d);
+    const double lit = lane == T ? d * rs : (lane > T ? r[T] * rs : 0.0);
+    r[T] = lit;
+    colbuf[(T & 1) * CB + lane] = lit;                 // column T of L, broadcast through shared memory
+    __syncwarp();                                      // (double-buffered: no second barrier per column)
+    double cj[CB];
+#pragma unroll
+    for (int j = T + 1; j < CB; ++j) cj[j] = colbuf[(T & 1) * CB + j];
+    // unpredicated: lanes above the diagonal update entries that are never read (lit = 0 for lanes < T)
+#pragma unroll
+    for (int j = T + 1; j < CB; ++j) r[j] = fma(-lit, cj[j], r[j]);
+    Chol32Col<T + 1>::run(r, colbuf, lane, bad);
+  }
+};
+template <>
+struct Chol32Col<CB> {
+  static __device__ __forceinline__ void run(double (&)[CB], double*, int, int&) {}
+};
+
+// one warp: Cholesky of a 32 x 32 block held row-per-lane in registers (r[j] = A(lane, j), j <= lane),
+// in place (r = row `lane` of L); colbuf: 64 doubles of shared scratch.  Returns the 1-based failing
+// column (a failed pivot continues with 1 so no NaN spreads), 0 if none.
+__device__ __forceinline__ int chol32_regs(double (&r)[CB], double* colbuf, int lane) {
+  int bad = 0;
+  Chol32Col<0>::run(r, colbuf, lane, bad);
+  return bad;
+}
+
+// one warp: D (32 x 32 at (d0r, d0c), ldd) = sgn Aop Bop^T (+ D if ACC), Aop(i, kk) = A(a0r + i, a0c + kk),
+// Bop(n, kk) = B(b0r + n, b0c + kk), K = 32 (column-major A, B, D), everything inside k x k.
+// LOWER: only the 8 x 8 tiles on or below the diagonal.
+template <bool ACC, bool LOWER>
+__device__ __forceinline__ void unit32(const double* A, int a0r, int a0c, const double* B, int b0r, int b0c, double* D,
+                                       int d0r, int d0c, int64_t ld, int k, double sgn, int lane) {
+  const int g = lane >> 2, q = lane & 3;
+  double bf[4][8];
+#pragma unroll
+  for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int rb = b0r + 8 * bb + g, cb = b0c + 4 * s + q;
+      bf[bb][s] = (rb < k && cb < k) ? __ldcg(B + rb + (int64_t)cb * ld) : 0.0;
+    }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    double af[8];
+    const int ra = a0r + 8 * a + g;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int ca = a0c + 4 * s + q;
+      af[s] = (ra < k && ca < k) ? sgn * __ldcg(A + ra + (int64_t)ca * ld) : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (LOWER && b > a) continue;
+      const int r = d0r + 8 * a + g, c = d0c + 8 * b + 2 * q;
+      const bool ok0 = r < k && c < k, ok1 = r < k && c + 1 < k;
+      double c0 = 0.0, c1 = 0.0;
+      if (ACC) {
+        if (ok0) c0 = __ldcg(D + r + (int64_t)c * ld);
+        if (ok1) c1 = __ldcg(D + r + (int64_t)(c + 1) * ld);
+      }
+#pragma unroll
+      for (int s = 0; s < 8; ++s) dev::dmma_8x8x4(c0, c1, af[s], bf[b][s]);
+      if (ok0) D[r + (int64_t)c * ld] = c0;
+      if (ok1) D[r + (int64_t)(c + 1) * ld] = c1;
+    }
+  }
+}
+
+// G (k x k, ld, lower part read) -> L in place (strict upper triangle zeroed), Wd (kp x 32, ld ldw):
+// rows 32p.. = L_pp^{-1}.  status: 1-based failing column on a non-positive pivot.
+__global__ void __launch_bounds__(256, 1)
+    k_potrf_cluster(double* G, int64_t ld, int k, double* Wd, int64_t ldw, int64_t* status) {
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ int fail;
+  __shared__ double Ls[CB * LS], rinv[CB];
+  const int rank = (int)cluster.block_rank(), warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = warp * CL + rank, nw = CL * 8;                     // consecutive units on different SMs
+  const int nb = (k + CB - 1) / CB;
+  if (threadIdx.x == 0) fail = status ? (int)(__ldcg(status) != 0) : 0;
+  cluster.sync();
+  const int* fail0 = cluster.map_shared_rank(&fail, 0);
+  const bool f0 = *fail0 != 0;
+  cluster.sync();                                                  // uniform decision, read before any write
+  if (f0) return;
+  // D (warp 0 of CTA 0): factor diagonal block p in registers, write L_pp back
+  auto diag = [&](int p) {
+    const int p0 = p * CB, i = p0 + lane;
+    double r[CB];
+#pragma unroll
+    for (int j = 0; j < CB; ++j)
+      r[j] = (i < k && j <= lane) ? __ldcg(G + i + (int64_t)(p0 + j) * ld) : (j == lane ? 1.0 : 0.0);
+    const int bad = chol32_regs(r, Ls, lane);                      // (Ls: broadcast scratch here)
+#pragma unroll
+    for (int j = 0; j < CB; ++j)
+      if (i < k && p0 + j < k) G[i + (int64_t)(p0 + j) * ld] = j <= lane ? r[j] : 0.0;
+    if (bad && p0 + bad <= k && lane == 0) {
+      fail = 1;
+      if (status) *status = p0 + bad;
+    }
+  };
+  if (gw == 0) diag(0);
+  for (int p = 0; p < nb; ++p) {
+    const int p0 = p * CB;
+    cluster.sync();                                                // L_pp (and the step-(p-1) update) in place
+    if (*fail0) {                                                  // every CTA sees the same flag
+      cluster.sync();                                              // CTA 0 stays until all have read it
+      return;
+    }
+    // P: L_ip = G_ip L_pp^{-T} (i > p) and W_pp = L_pp^{-1}; the mirrored upper block G_pi is zeroed
+    const int npu = nb - p;                                        // units: row blocks p+1.., then W_pp
+    if (rank < npu) {                                              // (unit u on CTA u % CL)
+      __syncthreads();
+      for (int e = threadIdx.x; e < CB * CB; e += 256) {
+        const int r = e & 31, cc = e >> 5;
+        Ls[r * LS + cc] = (p0 + r < k && cc <= r) ? __ldcg(G + (p0 + r) + (int64_t)(p0 + cc) * ld) : (r == cc ? 1.0 : 0.0);
+      }
+      __syncthreads();
+      if (threadIdx.x < CB) rinv[threadIdx.x] = __drcp_rn(Ls[threadIdx.x * LS + threadIdx.x]);
+      __syncthreads();
+      for (int u = gw; u < npu; u += nw) {
+        double x[CB];
+        if (u < npu - 1) {
+          const int i0 = (p + 1 + u) * CB, i = i0 + lane;
+#pragma unroll
+          for (int t = 0; t < CB; ++t) x[t] = (i < k && p0 + t < k) ? __ldcg(G + i + (int64_t)(p0 + t) * ld) : 0.0;
+          rowsolve32(x, Ls, rinv);
+#pragma unroll
+          for (int t = 0; t < CB; ++t)
+            if (i < k && p0 + t < k) {
+              G[i + (int64_t)(p0 + t) * ld] = x[t];
+              G[(p0 + t) + (int64_t)i * ld] = 0.0;
+            }
+        } else {
+#pragma unroll
+          for (int t = 0; t < CB; ++t) x[t] = t == lane ? 1.0 : 0.0;
+          rowsolve32(x, Ls, rinv);                                 // x_t = L_pp^{-1}(t, lane)
+#pragma unroll
+          for (int t = 0; t < CB; ++t) Wd[(p0 + t) + (int64_t)lane * ldw] = x[t];
+        }
+      }
+    }
+    cluster.sync();
+    // U: G_ij -= L_ip L_jp^T, p < j <= i (unit index -> (i, j) in the lower triangle).  Unit 0 is the
+    // next diagonal block; its warp (gw 0) factors it right after updating it (look-ahead: the D of
+    // step p+1 overlaps the rest of this update)
+    const int nt = nb - p - 1;
+    int ii = 0, jj = 0;
+    for (int u = gw; u < nt * (nt + 1) / 2; u += nw) {
+      while ((ii + 1) * (ii + 2) / 2 <= u) ++ii;                   // u increases: ii only moves forward
+      jj = u - ii * (ii + 1) / 2;
+      const int i0 = (p + 1 + ii) * CB, j0 = (p + 1 + jj) * CB;
+      if (ii == jj) unit32<true, true>(G, i0, p0, G, j0, p0, G, i0, j0, ld, k, -1.0, lane);
+      else unit32<true, false>(G, i0, p0, G, j0, p0, G, i0, j0, ld, k, -1.0, lane);
+      if (u == 0) diag(p + 1);
+    }
+  }
+}
+
+// Wd (kp x 32) rows 32p.. = L_pp^{-1} for a lower L (k x k, ld): one warp per diagonal block
+__global__ void __launch_bounds__(32) k_diag_inv32(const double* L, int64_t ld, int k, double* Wd, int64_t ldw) {
+  __shared__ double Ls[CB * LS], rinv[CB];
+  const int lane = threadIdx.x, p0 = blockIdx.x * CB;
+  for (int j = 0; j < CB; ++j) {
+    const int i = p0 + lane;
+    Ls[lane * LS + j] = (i < k && j <= lane) ? L[i + (int64_t)(p0 + j) * ld] : (j == lane ? 1.0 : 0.0);
+  }
+  __syncwarp();
+  rinv[lane] = __drcp_rn(Ls[lane * LS + lane]);
+  __syncwarp();
+  double x[CB];
+#pragma unroll
+  for (int t = 0; t < CB; ++t) x[t] = t == lane ? 1.0 : 0.0;
+  rowsolve32(x, Ls, rinv);
+#pragma unroll
+  for (int t = 0; t < CB; ++t) Wd[(p0 + t) + (int64_t)lane * ldw] = x[t];
+}
+
+constexpr int TRS = CB + 4;      // ring / temp tile stride (doubles): conflict-free fragment reads
+constexpr int TRR = 4;           // ring slots
+constexpr int TKC = 64;          // L columns per ring slot
+
+__host__ __device__ inline size_t trsm_rows_smem(int rb, int kp) {
+  return ((size_t)rb * (kp + 4) + (size_t)TRR * TKC * TRS + (size_t)rb * TRS) * sizeof(double);
+}
+
+// X (rows x k, ldx) <- X L^{-T}; L lower (k x k, ldl), Wd = diagonal-block inverses (kp x 32, ldw).
+// Stages, in order, for each column block j: chunks of row block j of L (columns [0, 32 j) in
+// TKC-wide pieces), then W_jj.  A stage is described by (j, c0, width); width 0 = the W_jj stage.
+template <int RB>
+__global__ void __launch_bounds__(256) k_trsm_rows(double* X, int64_t rows, int64_t ldx, int k, const double* L,
+                                                   int64_t ldl, const double* Wd, int64_t ldw) {
+  extern __shared__ __align__(16) double trs_sm[];
+  const int nb = (k + CB - 1) / CB, kp = nb * CB, xst = kp + 4;
+  double* xs = trs_sm;                                   // [RB][kp + 4]: xs[r][t] = X(r0 + r, t)
+  double* ring = xs + (size_t)RB * xst;                  // [TRR][TKC][TRS]: S[kk][n]
+  double* tt = ring + (size_t)TRR * TKC * TRS;           // [RB][TRS]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, q = lane & 3;
+  constexpr int TPW = RB / 16;                           // 8 x 8 tiles per warp (same column tile b)
+  const int b = w & 3, abase = TPW * (w >> 2);
+  const int64_t r0 = (int64_t)blockIdx.x * RB;
+  const bool vec = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0);
+  for (int e = tid; e < RB * kp; e += 256) {
+    const int rr = e % RB, t = e / RB;
+    const bool ok = r0 + rr < rows && t < k;
+    dev::cp_async8(xs + (size_t)rr * xst + t, ok ? X + (r0 + rr) + (int64_t)t * ldx : X, ok);
+  }
+  // issuer state (uniform): the next stage to load
+  int ij = 0, ic = 0, nis = 0;
+  auto issue = [&]() {
+    if (ij < nb) {
+      double* S = ring + (size_t)(nis % TRR) * TKC * TRS;
+      if (ic < ij * CB) {                                // L(32 ij + n, ic + kk), kk < width
+        const int wdt = min(TKC, ij * CB - ic);
+        if (vec) {
+          for (int e = tid; e < wdt * (CB / 2); e += 256) {
+            const int n2 = 2 * (e & 15), kk = e >> 4;
+            const int rowg = ij * CB + n2, colg = ic + kk;
+            const int nbytes = colg < k ? 8 * max(0, min(2, k - rowg)) : 0;
+            dev::cp_async16(S + kk * TRS + n2, nbytes ? L + rowg + (int64_t)colg * ldl : L, nbytes);
+          }
+        } else {
+          for (int e = tid; e < wdt * CB; e += 256) {
+            const int n = e & 31, kk = e >> 5;
+            const int rowg = ij * CB + n, colg = ic + kk;
+            const bool ok = rowg < k && colg < k;
+            dev::cp_async8(S + kk * TRS + n, ok ? L + rowg + (int64_t)colg * ldl : L, ok);
+          }
+        }
+        ic += wdt;
+      } else {                                           // W_jj(n, kk) = Wd(32 ij + n, kk)
+        for (int e = tid; e < CB * (CB / 2); e += 256) {
+          const int n2 = 2 * (e & 15), kk = e >> 4;
+          dev::cp_async16(S + kk * TRS + n2, Wd + (ij * CB + n2) + (int64_t)kk * ldw, 16);
+        }
+        ++ij;
+        ic = 0;
+      }
+      ++nis;
+    }
+    dev::cp_async_commit();
+  };
+  for (int st = 0; st < TRR - 1; ++st) issue();
+  double acc[TPW][2];
+  int j = 0, c = 0, st = 0;
+  while (j < nb) {
+    dev::cp_async_wait<TRR - 2>();
+    __syncthreads();
+    issue();
+    const double* S = ring + (size_t)(st % TRR) * TKC * TRS;
+    ++st;
+    if (c == 0) {
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) {
+        const double* xr = xs + (size_t)(8 * (abase + t) + g) * xst + j * CB + 8 * b + 2 * q;
+        acc[t][0] = xr[0];
+        acc[t][1] = xr[1];
+      }
+    }
+    if (c < j * CB) {                                    // acc -= X(:, c..c+wdt) L(j block, c..c+wdt)^T
+      const int wdt = min(TKC, j * CB - c);
+      for (int s = 0; s < wdt / 4; ++s) {
+        const double bv = S[(4 * s + q) * TRS + 8 * b + g];
+#pragma unroll
+        for (int t = 0; t < TPW; ++t)
+          dev::dmma_8x8x4(acc[t][0], acc[t][1], -xs[(size_t)(8 * (abase + t) + g) * xst + c + 4 * s + q], bv);
+      }
+      c += wdt;
+    } else {                                             // X_j = acc W_jj^T
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) {
+        double* tr = tt + (8 * (abase + t) + g) * TRS + 8 * b + 2 * q;
+        tr[0] = acc[t][0];
+        tr[1] = acc[t][1];
+        acc[t][0] = acc[t][1] = 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const double bv = S[(4 * s + q) * TRS + 8 * b + g];
+#pragma unroll
+        for (int t = 0; t < TPW; ++t)
+          dev::dmma_8x8x4(acc[t][0], acc[t][1], tt[(8 * (abase + t) + g) * TRS + 4 * s + q], bv);
+      }
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) {
+        double* xr = xs + (size_t)(8 * (abase + t) + g) * xst + j * CB + 8 * b + 2 * q;
+        xr[0] = acc[t][0];
+        xr[1] = acc[t][1];
+      }
+      ++j;
+      c = 0;
+    }
+  }
+  dev::cp_async_wait<0>();
+  __syncthreads();
+  for (int e = tid; e < RB * k; e += 256) {
+    const int rr = e % RB, t = e / RB;
+    if (r0 + rr < rows) X[(r0 + rr) + (int64_t)t * ldx] = xs[(size_t)rr * xst + t];
+  }
+}
+
 constexpr size_t kDiagInvSmem = (2 * TB2 * (TB2 + 1) + 3 * DB * DB) * sizeof(double);
 constexpr size_t kRtmSmem = 2 * TB2 * RTS * sizeof(double);
 
@@ -465,8 +824,51 @@ sk_status gather_rows_t(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_
   return launched(c);
 }
 
+namespace {
+// the single-launch pair (k <= kCholMaxK): Cholesky with the diagonal-block inverses kept in Wd
+// (kp x 32), and the row-block solve X <- X L^{-T}
+sk_status potrf_cluster(sk_ctx* c, double* G, int64_t k, int64_t ld, double* Wd, int64_t ldw, int64_t* status_dev) {
+  static bool attr_done[kMaxDevices] = {};
+  if (!attr_done[c->device % kMaxDevices]) {
+    SK_CUDA(c, cudaFuncSetAttribute(k_potrf_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_done[c->device % kMaxDevices] = true;
+  }
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(CL);
+  lc.blockDim = dim3(256);
+  lc.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  lc.attrs = at; lc.numAttrs = 1;
+  SK_CUDA(c, cudaLaunchKernelEx(&lc, k_potrf_cluster, G, ld, (int)k, Wd, ldw, status_dev));
+  return launched(c);
+}
+
+sk_status trsm_rows(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L, int64_t ldl,
+                    const double* Wd, int64_t ldw) {
+  if (rows == 0) return SK_OK;
+  const int kp = (int)cdiv(k, CB) * CB;
+  const int rb = kp <= 512 ? 32 : 16;
+  const size_t smem = trsm_rows_smem(rb, kp);
+  if (rb == 32) {
+    SK_CUDA(c, cudaFuncSetAttribute(k_trsm_rows<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_trsm_rows<32><<<(unsigned)cdiv(rows, 32), 256, smem, c->stream>>>(X, rows, ldx, (int)k, L, ldl, Wd, ldw);
+  } else {
+    SK_CUDA(c, cudaFuncSetAttribute(k_trsm_rows<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_trsm_rows<16><<<(unsigned)cdiv(rows, 16), 256, smem, c->stream>>>(X, rows, ldx, (int)k, L, ldl, Wd, ldw);
+  }
+  return launched(c);
+}
+}  // namespace
+
 sk_status potrf_lower(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t* status_dev) {
   SK_TRY(dense_attrs(c));
+  if (k <= kCholMaxK && !getenv("SKEL_BLOCKED_CHOL")) {
+    DBuf Wd;
+    SK_TRY(Wd.alloc(c, (size_t)cdiv(k, CB) * CB * CB * sizeof(double)));
+    return potrf_cluster(c, G, k, ld, Wd.as<double>(), cdiv(k, CB) * CB, status_dev);
+  }
   // right-looking, 64-wide blocks: L_jj and W_jj = L_jj^{-1} in one CTA, panel L_rj = G_rj W_jj^T
   // in place, trailing update by DMMA GEMM.  The W_jj blocks are kept (diagonal of c->tri_w) for
   // the triangular solve that follows.
@@ -494,6 +896,14 @@ sk_status potrf_lower(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t* stat
 sk_status trsm_right_lt(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L,
                         int64_t ldl) {
   SK_TRY(dense_attrs(c));
+  if (k <= kCholMaxK && !getenv("SKEL_BLOCKED_CHOL")) {
+    const int64_t kp = cdiv(k, CB) * CB;
+    DBuf Wd;
+    SK_TRY(Wd.alloc(c, (size_t)kp * CB * sizeof(double)));
+    k_diag_inv32<<<(unsigned)(kp / CB), 32, 0, c->stream>>>(L, ldl, (int)k, Wd.as<double>(), kp);
+    SK_TRY(launched(c));
+    return trsm_rows(c, X, rows, k, ldx, L, ldl, Wd.as<double>(), kp);
+  }
   // X_j <- (X_j - X_<j L_j,<j^T) L_jj^{-T}, 64-wide blocks; L_jj^{-1} re-formed per block (cheap)
   DBuf Wd;
   SK_TRY(Wd.alloc(c, (size_t)TB2 * TB2 * sizeof(double)));
@@ -565,6 +975,18 @@ static sk_status trsm_right_l_impl(sk_ctx* c, double* X, int64_t rows, int64_t k
 sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64_t* status_dev) {
   DBuf G;
   SK_TRY(G.alloc(c, (size_t)k * k * sizeof(double)));
+  if (k <= kCholMaxK && !getenv("SKEL_BLOCKED_CHOL")) {
+    // per pass: Gram (DMMA GEMM), Cholesky (one cluster launch), Q <- Q L^{-T} (one launch)
+    const int64_t kp = cdiv(k, CB) * CB;
+    DBuf Wd;
+    SK_TRY(Wd.alloc(c, (size_t)kp * CB * sizeof(double)));
+    for (int pass = 0; pass < 2; ++pass) {
+      SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
+      SK_TRY(potrf_cluster(c, G.as<double>(), k, k, Wd.as<double>(), kp, status_dev));
+      SK_TRY(trsm_rows(c, Q, m, k, ldq, G.as<double>(), k, Wd.as<double>(), kp));
+    }
+    return SK_OK;
+  }
   for (int pass = 0; pass < 2; ++pass) {
     SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
     SK_TRY(potrf_lower(c, G.as<double>(), k, k, status_dev));

@@ -1,0 +1,12 @@
+#!/bin/bash
+# single-launch Cholesky + row solve: parity (everything but C5), residual timings, launch list
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -x -q -m gpu --deselect tests/test_gpu_c5.py > gpurun_out/r2c_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r2c_pytest.log
+for c in "C2 col_id" "C3 cur" "C4 col_id" "C4 row_id"; do
+  set -- $c
+  timeout 300 python tools/probe_residual.py --config $1 --kind $2 >> gpurun_out/r2c_plain.log 2>&1
+done
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/r2c_launch_c2.csv python tools/probe_residual.py --config C2 --kind col_id --reps 1 --profile > gpurun_out/r2c_ncu.log 2>&1
+echo done
