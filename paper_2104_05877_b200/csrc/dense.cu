@@ -6,7 +6,9 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include <cooperative_groups.h>
 
@@ -645,6 +647,20 @@ __global__ void __launch_bounds__(32) k_diag_inv32(const double* L, int64_t ld, 
   for (int t = 0; t < CB; ++t) Wd[(p0 + t) + (int64_t)lane * ldw] = x[t];
 }
 
+// Newton-Schulz step for a nearly orthonormal Q (second CholeskyQR pass): M = (3 I - G) / 2 with
+// G = Q^T Q, and eta = max |G - I| (non-negative doubles order like their bit patterns).
+__global__ void k_ns_prep(const double* G, int64_t k, double* M, unsigned long long* eta) {
+  double mx = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k * k; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % k, j = e / k;
+    const double d = G[e] - (i == j ? 1.0 : 0.0);
+    mx = fmax(mx, fabs(d));
+    M[e] = (i == j ? 1.0 : 0.0) - 0.5 * d;
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(eta, (unsigned long long)__double_as_longlong(mx));
+}
+
 constexpr int TRS = CB + 4;      // ring / temp tile stride (doubles): conflict-free fragment reads
 constexpr int TRR = 4;           // ring slots
 constexpr int TKC = 64;          // L columns per ring slot
@@ -864,7 +880,7 @@ sk_status trsm_rows(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, 
 
 sk_status potrf_lower(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t* status_dev) {
   SK_TRY(dense_attrs(c));
-  if (k <= kCholMaxK && !getenv("SKEL_BLOCKED_CHOL")) {
+  if (k <= kCholMaxK) {
     DBuf Wd;
     SK_TRY(Wd.alloc(c, (size_t)cdiv(k, CB) * CB * CB * sizeof(double)));
     return potrf_cluster(c, G, k, ld, Wd.as<double>(), cdiv(k, CB) * CB, status_dev);
@@ -896,7 +912,7 @@ sk_status potrf_lower(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t* stat
 sk_status trsm_right_lt(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, const double* L,
                         int64_t ldl) {
   SK_TRY(dense_attrs(c));
-  if (k <= kCholMaxK && !getenv("SKEL_BLOCKED_CHOL")) {
+  if (k <= kCholMaxK) {
     const int64_t kp = cdiv(k, CB) * CB;
     DBuf Wd;
     SK_TRY(Wd.alloc(c, (size_t)kp * CB * sizeof(double)));
@@ -975,17 +991,40 @@ static sk_status trsm_right_l_impl(sk_ctx* c, double* X, int64_t rows, int64_t k
 sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64_t* status_dev) {
   DBuf G;
   SK_TRY(G.alloc(c, (size_t)k * k * sizeof(double)));
-  if (k <= kCholMaxK && !getenv("SKEL_BLOCKED_CHOL")) {
+  if (k <= kCholMaxK) {
     // per pass: Gram (DMMA GEMM), Cholesky (one cluster launch), Q <- Q L^{-T} (one launch)
     const int64_t kp = cdiv(k, CB) * CB;
     DBuf Wd;
     SK_TRY(Wd.alloc(c, (size_t)kp * CB * sizeof(double)));
-    for (int pass = 0; pass < 2; ++pass) {
-      SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
-      SK_TRY(potrf_cluster(c, G.as<double>(), k, k, Wd.as<double>(), kp, status_dev));
-      SK_TRY(trsm_rows(c, Q, m, k, ldq, G.as<double>(), k, Wd.as<double>(), kp));
+    SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
+    SK_TRY(potrf_cluster(c, G.as<double>(), k, k, Wd.as<double>(), kp, status_dev));
+    SK_TRY(trsm_rows(c, Q, m, k, ldq, G.as<double>(), k, Wd.as<double>(), kp));
+    // second pass: after the first, Q^T Q = I + E with |E| ~ u cond(Q_0)^2.  When |E| <= 1e-8 one
+    // Newton-Schulz step Q <- Q (3 I - Q^T Q) / 2 leaves |E|^2 ~ 1e-16 (the orthogonality CholeskyQR2
+    // reaches) with two GEMMs and no sequential chain; otherwise the Cholesky pass again.
+    SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
+    DBuf M, eta;
+    SK_TRY(M.alloc(c, (size_t)k * k * sizeof(double)));
+    SK_TRY(eta.alloc(c, sizeof(unsigned long long)));
+    SK_CUDA(c, cudaMemsetAsync(eta.p, 0, sizeof(unsigned long long), c->stream));
+    k_ns_prep<<<(unsigned)std::min<int64_t>(cdiv(k * k, 256), 2LL * c->num_sms), 256, 0, c->stream>>>(
+        G.as<double>(), k, M.as<double>(), eta.as<unsigned long long>());
+    SK_TRY(launched(c));
+    unsigned long long eb = 0;
+    SK_CUDA(c, cudaMemcpyAsync(&eb, eta.p, sizeof(eb), cudaMemcpyDeviceToHost, c->stream));
+    SK_CUDA(c, cudaStreamSynchronize(c->stream));
+    double e;
+    memcpy(&e, &eb, sizeof(e));
+    if (e <= 1e-8) {
+      DBuf T;
+      SK_TRY(T.alloc(c, (size_t)m * k * sizeof(double)));
+      SK_TRY(gemm(c, false, false, m, k, k, 1.0, Q, ldq, M.as<double>(), k, 0.0, T.as<double>(), m));
+      SK_CUDA(c, cudaMemcpy2DAsync(Q, (size_t)ldq * sizeof(double), T.p, (size_t)m * sizeof(double),
+                                   (size_t)m * sizeof(double), (size_t)k, cudaMemcpyDeviceToDevice, c->stream));
+      return SK_OK;
     }
-    return SK_OK;
+    SK_TRY(potrf_cluster(c, G.as<double>(), k, k, Wd.as<double>(), kp, status_dev));
+    return trsm_rows(c, Q, m, k, ldq, G.as<double>(), k, Wd.as<double>(), kp);
   }
   for (int pass = 0; pass < 2; ++pass) {
     SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));

@@ -4,12 +4,14 @@
 // Q_C (Q_C^T A Q_R) Q_R^T (Remark 2.3, eq:cur_stable; protocol P:554) and
 // A ~ C Z (eq:colID).  Frobenius norm (R12).
 //
-// ortho(C): the LUPP of C (row LUPP, the same kernel as S4) gives C = Lf_C U with
-// U invertible, so range(C) = range(Lf_C); Lf_C has |entries| <= 1 and a unit lower
-// triangular pivot block, hence is well conditioned even when C is not (cond(C) = 1.6e11
-// at C2 k=512), and two passes of Cholesky QR on Lf_C give an orthonormal basis to
-// working accuracy.  The residual A - Q (Q^T A) is never
-// materialised: the last GEMM squares and sums its tiles in the epilogue (EPI_SUMSQ).
+// ortho(C): shifted CholeskyQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020),
+// stable for cond(C) up to ~u^{-1} (cond(C) = 1.6e11 at C2 k=512): Gram + shift, then Cholesky
+// passes on the single-launch pair of dense.cu, the last pass a Newton-Schulz step when the one
+// before leaves Q nearly orthonormal.  If a pass breaks down (C numerically rank deficient), the
+// LUPP basis: the row LUPP of C (the S4 kernel) gives C = Lf_C U, range(C) = range(Lf_C), Lf_C
+// well conditioned by construction (|entries| <= 1, unit lower pivot block), then CholeskyQR2
+// (DESIGN.md section 7.6).  The residual A - Q (Q^T A) is never materialised: the last GEMM squares
+// and sums its tiles in the epilogue.
 #include "common.cuh"
 #include "internal.h"
 
@@ -32,7 +34,8 @@ sk_status add_shift(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t rows) {
   return launched(c);
 }
 
-// Columns of C whose row LUPP does not fit one cluster (rows > 16 x 256): shifted CholeskyQR3.
+// Shifted CholeskyQR3: Q = C, G = Q^T Q + s I, Q <- Q L^{-T}, then CholeskyQR2 (whose second pass
+// is a Newton-Schulz step when the first leaves |Q^T Q - I| <= 1e-8).
 static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q,
                                        int64_t* status_dev) {
   SK_CUDA(c, cudaMemcpyAsync(Q, C, (size_t)rows * k * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -89,7 +92,17 @@ sk_status col_id_sumsq(sk_ctx* c, const double* Q, const double* A, int64_t m, i
 }
 
 sk_status orthonormal_basis(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q, int64_t* status_dev) {
-  if (rows > lupp_max_rows(c)) return basis_shifted_cholqr3(c, C, rows, k, Q, status_dev);
+  // shifted CholeskyQR3 (all GEMMs + two single-launch Cholesky passes, the third pass a Newton-Schulz
+  // step when the second leaves |Q^T Q - I| <= 1e-8): stable for cond(C) up to ~u^{-1} (Fukaya et al.
+  // 2020).  When it reports a breakdown (C numerically rank deficient beyond that), the LUPP basis:
+  // range(C) = range(Lf_C), Lf_C well conditioned by construction, then CholeskyQR2.
+  SK_TRY(basis_shifted_cholqr3(c, C, rows, k, Q, status_dev));
+  if (rows > lupp_max_rows(c)) return SK_OK;
+  int64_t st = 0;
+  SK_CUDA(c, cudaMemcpyAsync(&st, status_dev, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+  SK_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (st == 0) return SK_OK;
+  SK_CUDA(c, cudaMemsetAsync(status_dev, 0, sizeof(int64_t), c->stream));
   DBuf piv;
   SK_TRY(piv.alloc(c, (size_t)k * sizeof(int64_t)));
   SK_TRY(lupp(c, C, false, rows, k, rows, piv.as<int64_t>(), Q, rows, nullptr, 0, nullptr, status_dev));
