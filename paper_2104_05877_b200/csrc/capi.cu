@@ -160,6 +160,7 @@ void sk_destroy(sk_ctx* c) {
   cudaStreamSynchronize(c->stream);
   dist_destroy(c);
   if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
+  if (c->img) { cudaStreamSynchronize(c->img); cudaStreamDestroy(c->img); }
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
   if (c->pool) cudaMemPoolDestroy(c->pool);

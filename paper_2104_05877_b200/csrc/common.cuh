@@ -33,6 +33,9 @@ struct sk_ctx {
   // lowest-priority helper stream + events for look-ahead overlap (LUPP trailing updates)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // helper stream of the K-chunked dense sketch (next chunk's Omega image beside the current GEMM);
+  // separate from aux, which carries the host -> device copies of the host-A ring
+  cudaStream_t img = nullptr;
   // column-sharded (distributed) context, sk_create_dist: this rank's block of A's columns and the
   // library-owned NCCL communicator (dist.cu); nullptr for a single-GPU context
   skel::DistState* dist = nullptr;

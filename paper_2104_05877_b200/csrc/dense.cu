@@ -999,9 +999,10 @@ sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64
     SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
     SK_TRY(potrf_cluster(c, G.as<double>(), k, k, Wd.as<double>(), kp, status_dev));
     SK_TRY(trsm_rows(c, Q, m, k, ldq, G.as<double>(), k, Wd.as<double>(), kp));
-    // second pass: after the first, Q^T Q = I + E with |E| ~ u cond(Q_0)^2.  When |E| <= 1e-8 one
-    // Newton-Schulz step Q <- Q (3 I - Q^T Q) / 2 leaves |E|^2 ~ 1e-16 (the orthogonality CholeskyQR2
-    // reaches) with two GEMMs and no sequential chain; otherwise the Cholesky pass again.
+    // second pass: after the first, Q^T Q = I + E with |E| ~ u cond(Q_0)^2.  When |E| <= 1e-10 one
+    // Newton-Schulz step Q <- Q (3 I - Q^T Q) / 2 leaves |E|^2 (below u: the orthogonality CholeskyQR2
+    // reaches) with two GEMMs and no sequential chain, and moves Q from the thin-QR factor by at most
+    // |E| / 2 (a symmetric right factor); otherwise the Cholesky pass again.
     SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
     DBuf M, eta;
     SK_TRY(M.alloc(c, (size_t)k * k * sizeof(double)));
@@ -1015,7 +1016,7 @@ sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64
     SK_CUDA(c, cudaStreamSynchronize(c->stream));
     double e;
     memcpy(&e, &eb, sizeof(e));
-    if (e <= 1e-8) {
+    if (e <= 1e-10) {
       DBuf T;
       SK_TRY(T.alloc(c, (size_t)m * k * sizeof(double)));
       SK_TRY(gemm(c, false, false, m, k, k, 1.0, Q, ldq, M.as<double>(), k, 0.0, T.as<double>(), m));

@@ -4,8 +4,8 @@
 // Q_C (Q_C^T A Q_R) Q_R^T (Remark 2.3, eq:cur_stable; protocol P:554) and
 // A ~ C Z (eq:colID).  Frobenius norm (R12).
 //
-// ortho(C): shifted CholeskyQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020),
-// stable for cond(C) up to ~u^{-1} (cond(C) = 1.6e11 at C2 k=512): Gram + shift, then Cholesky
+// ortho(C): shifted CholeskyQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020;
+// cond(C) = 1.6e11 at C2 k=512, R20): Gram + shift, then Cholesky
 // passes on the single-launch pair of dense.cu, the last pass a Newton-Schulz step when the one
 // before leaves Q nearly orthonormal.  If a pass breaks down (C numerically rank deficient), the
 // LUPP basis: the row LUPP of C (the S4 kernel) gives C = Lf_C U, range(C) = range(Lf_C), Lf_C
@@ -35,7 +35,7 @@ sk_status add_shift(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t rows) {
 }
 
 // Shifted CholeskyQR3: Q = C, G = Q^T Q + s I, Q <- Q L^{-T}, then CholeskyQR2 (whose second pass
-// is a Newton-Schulz step when the first leaves |Q^T Q - I| <= 1e-8).
+// is a Newton-Schulz step when the first leaves |Q^T Q - I| <= 1e-10).
 static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q,
                                        int64_t* status_dev) {
   SK_CUDA(c, cudaMemcpyAsync(Q, C, (size_t)rows * k * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -93,9 +93,10 @@ sk_status col_id_sumsq(sk_ctx* c, const double* Q, const double* A, int64_t m, i
 
 sk_status orthonormal_basis(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q, int64_t* status_dev) {
   // shifted CholeskyQR3 (all GEMMs + two single-launch Cholesky passes, the third pass a Newton-Schulz
-  // step when the second leaves |Q^T Q - I| <= 1e-8): stable for cond(C) up to ~u^{-1} (Fukaya et al.
-  // 2020).  When it reports a breakdown (C numerically rank deficient beyond that), the LUPP basis:
-  // range(C) = range(Lf_C), Lf_C well conditioned by construction, then CholeskyQR2.
+  // step when the second leaves |Q^T Q - I| <= 1e-10; Fukaya et al. 2020, R20 for its
+  // stability condition and the measured range).  When a pass breaks down (C numerically rank
+  // deficient), the LUPP basis: range(C) = range(Lf_C), Lf_C well conditioned by construction, then
+  // CholeskyQR2.
   SK_TRY(basis_shifted_cholqr3(c, C, rows, k, Q, status_dev));
   if (rows > lupp_max_rows(c)) return SK_OK;
   int64_t st = 0;

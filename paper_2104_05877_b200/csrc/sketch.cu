@@ -1230,12 +1230,12 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
     p.accum = 0;
     return pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, cl, img.as<double>(), part.as<double>());
   }
-  // Several chunks: two image slots; the image of chunk c + 1 is generated on the helper stream while
+  // Several chunks: two image slots; the image of chunk c + 1 is generated on the image stream while
   // the GEMM of chunk c runs (its small CTAs fit beside a GEMM CTA on an SM), into the slot the GEMM of
   // chunk c - 1 has finished reading.  Events order slot reuse and image -> GEMM.
   DBuf img2;
   SK_TRY(img2.alloc(c, img.bytes));
-  SK_TRY(ensure_aux(c));
+  if (!c->img) SK_CUDA(c, cudaStreamCreateWithFlags(&c->img, cudaStreamNonBlocking));
   double* slot[2] = {img.as<double>(), img2.as<double>()};
   cudaEvent_t ev[5] = {};
   sk_status rs = SK_OK;
@@ -1243,7 +1243,7 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
     if (cudaEventCreateWithFlags(&ev[e], cudaEventDisableTiming) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sketch: event");
   cudaEvent_t* made = ev;         // [2] image of the chunk in slot s complete (helper stream)
   cudaEvent_t* read = ev + 2;     // [2] GEMM that read slot s complete (context stream)
-  if (rs == SK_OK && (cudaEventRecord(ev[4], c->stream) != cudaSuccess || cudaStreamWaitEvent(c->aux, ev[4], 0) != cudaSuccess))
+  if (rs == SK_OK && (cudaEventRecord(ev[4], c->stream) != cudaSuccess || cudaStreamWaitEvent(c->img, ev[4], 0) != cudaSuccess))
     rs = fail(c, SK_E_CUDA, "sketch: event");
   if (rs == SK_OK) rs = omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, 0, std::min(m, chunk), slot[0]);
   for (int64_t ci = 0; ci < nch && rs == SK_OK; ++ci) {
@@ -1251,11 +1251,11 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
     if (ci + 1 < nch) {           // next image on the helper stream, into the other slot
       const int s = (int)((ci + 1) & 1);
       cudaStream_t main_stream = c->stream;
-      if (ci >= 1 && cudaStreamWaitEvent(c->aux, read[s], 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sketch: event"); break; }
-      c->stream = c->aux;
+      if (ci >= 1 && cudaStreamWaitEvent(c->img, read[s], 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sketch: event"); break; }
+      c->stream = c->img;
       rs = omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, i1, std::min(m, i1 + chunk), slot[s]);
       c->stream = main_stream;
-      if (rs == SK_OK && cudaEventRecord(made[s], c->aux) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sketch: event");
+      if (rs == SK_OK && cudaEventRecord(made[s], c->img) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sketch: event");
       if (rs != SK_OK) break;
     }
     if (ci >= 1 && cudaStreamWaitEvent(c->stream, made[ci & 1], 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sketch: event"); break; }
