@@ -653,7 +653,7 @@ __global__ void k_ns_prep(const double* G, int64_t k, double* M, unsigned long l
   double mx = 0.0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k * k; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e % k, j = e / k;
-    const double d = G[e] - (i == j ? 1.0 : 0.0);
+    const double d = G[i >= j ? e : j + i * k] - (i == j ? 1.0 : 0.0);   // G's lower triangle (gram_lower)
     mx = fmax(mx, fabs(d));
     M[e] = (i == j ? 1.0 : 0.0) - 0.5 * d;
   }
@@ -865,9 +865,13 @@ sk_status trsm_rows(sk_ctx* c, double* X, int64_t rows, int64_t k, int64_t ldx, 
                     const double* Wd, int64_t ldw) {
   if (rows == 0) return SK_OK;
   const int kp = (int)cdiv(k, CB) * CB;
-  const int rb = kp <= 512 ? 32 : 16;
+  // rows per CTA: as many as shared memory holds beside the ring (more rows amortise the L stream)
+  const int rb = kp <= 256 ? 64 : (kp <= 512 ? 32 : 16);
   const size_t smem = trsm_rows_smem(rb, kp);
-  if (rb == 32) {
+  if (rb == 64) {
+    SK_CUDA(c, cudaFuncSetAttribute(k_trsm_rows<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_trsm_rows<64><<<(unsigned)cdiv(rows, 64), 256, smem, c->stream>>>(X, rows, ldx, (int)k, L, ldl, Wd, ldw);
+  } else if (rb == 32) {
     SK_CUDA(c, cudaFuncSetAttribute(k_trsm_rows<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_trsm_rows<32><<<(unsigned)cdiv(rows, 32), 256, smem, c->stream>>>(X, rows, ldx, (int)k, L, ldl, Wd, ldw);
   } else {
@@ -992,18 +996,18 @@ sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64
   DBuf G;
   SK_TRY(G.alloc(c, (size_t)k * k * sizeof(double)));
   if (k <= kCholMaxK) {
-    // per pass: Gram (DMMA GEMM), Cholesky (one cluster launch), Q <- Q L^{-T} (one launch)
+    // per pass: Gram (DMMA GEMM, lower tiles), Cholesky (one cluster launch), Q <- Q L^{-T} (one launch)
     const int64_t kp = cdiv(k, CB) * CB;
     DBuf Wd;
     SK_TRY(Wd.alloc(c, (size_t)kp * CB * sizeof(double)));
-    SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
+    SK_TRY(gram_lower(c, Q, m, k, ldq, G.as<double>(), k));
     SK_TRY(potrf_cluster(c, G.as<double>(), k, k, Wd.as<double>(), kp, status_dev));
     SK_TRY(trsm_rows(c, Q, m, k, ldq, G.as<double>(), k, Wd.as<double>(), kp));
     // second pass: after the first, Q^T Q = I + E with |E| ~ u cond(Q_0)^2.  When |E| <= 1e-10 one
     // Newton-Schulz step Q <- Q (3 I - Q^T Q) / 2 leaves |E|^2 (below u: the orthogonality CholeskyQR2
     // reaches) with two GEMMs and no sequential chain, and moves Q from the thin-QR factor by at most
     // |E| / 2 (a symmetric right factor); otherwise the Cholesky pass again.
-    SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
+    SK_TRY(gram_lower(c, Q, m, k, ldq, G.as<double>(), k));
     DBuf M, eta;
     SK_TRY(M.alloc(c, (size_t)k * k * sizeof(double)));
     SK_TRY(eta.alloc(c, sizeof(unsigned long long)));

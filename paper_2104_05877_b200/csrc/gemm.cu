@@ -33,6 +33,7 @@ struct Params {
   double alpha, beta;
   int k_per_split;
   double* out;   // EPI_PARTIAL: [splits][M*N]; EPI_SUMSQ: [ctas][2]
+  int lower;     // M == N and only the tiles on or below the diagonal (blockIdx.x enumerates them)
 };
 
 template <bool TA>
@@ -70,7 +71,14 @@ template <bool TA, bool TB, int MODE>
 __global__ void __launch_bounds__(NT) k_gemm(Params p) {
   dev::griddep_wait();
   extern __shared__ __align__(16) double sm[];
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  int mb = blockIdx.x, nbk = blockIdx.y;
+  if (p.lower) {                                   // lower-triangle tile t -> (mb, nbk), mb >= nbk
+    mb = (int)((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);
+    while (mb * (mb + 1) / 2 > (int)blockIdx.x) --mb;
+    while ((mb + 1) * (mb + 2) / 2 <= (int)blockIdx.x) ++mb;
+    nbk = (int)blockIdx.x - mb * (mb + 1) / 2;
+  }
+  const int m0 = mb * BM, n0 = nbk * BN;
   const int kbeg = blockIdx.z * p.k_per_split;
   const int kend = min(p.K, kbeg + p.k_per_split);
   const int ktiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
@@ -187,10 +195,11 @@ __global__ void __launch_bounds__(NT) k_gemm(Params p) {
 // C(m, n) = alpha * sum_z part[z](m, n) + beta * C, z ascending.  Grid (row blocks, column n): no
 // 64-bit divisions; the split loads of an element are issued together.
 __global__ void k_splitk_reduce(const double* __restrict__ part, int splits, int M, int N, double alpha,
-                                double beta, double* __restrict__ C, int64_t ldc) {
+                                double beta, double* __restrict__ C, int64_t ldc, int lower) {
   const int64_t total = (int64_t)M * N;
   for (int64_t n = blockIdx.y; n < N; n += gridDim.y)
     for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < M; m += gridDim.x * blockDim.x) {
+      if (lower && m / BM < n / BN) continue;      // tile above the diagonal: never computed
       const double* src = part + m + n * M;
       double s = 0.0;
 #pragma unroll 8
@@ -280,7 +289,33 @@ sk_status gemm(sk_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
   p.out = part.as<double>();
   SK_TRY(dispatch<EPI_PARTIAL>(c, ta, tb, p, grid));
   const dim3 rg((unsigned)std::min<int64_t>(cdiv(M, 256), 64), (unsigned)std::min<int64_t>(N, 65535));
-  k_splitk_reduce<<<rg, 256, 0, c->stream>>>(part.as<double>(), splits, (int)M, (int)N, alpha, beta, C, ldc);
+  k_splitk_reduce<<<rg, 256, 0, c->stream>>>(part.as<double>(), splits, (int)M, (int)N, alpha, beta, C, ldc, 0);
+  return launched(c);
+}
+
+sk_status gram_lower(sk_ctx* c, const double* Q, int64_t m, int64_t k, int64_t ldq, double* G, int64_t ldg) {
+  // G = Q^T Q on the 64 x 64 tiles on or below the diagonal only (the consumers -- Cholesky, the
+  // Newton-Schulz prep, the shift -- read the lower triangle): ~T(T+1)/2 of T^2 tiles
+  if (k <= 0) return SK_OK;
+  if (m <= 0) return gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G, ldg);
+  Params p{};
+  p.M = (int)k; p.N = (int)k; p.K = (int)m;
+  p.A = Q; p.lda = ldq; p.B = Q; p.ldb = ldq; p.C = G; p.Cin = G; p.ldc = ldg;
+  p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
+  const int64_t T = cdiv(k, BM), tiles = T * (T + 1) / 2;
+  int splits = 1;
+  const int64_t target = 2LL * c->num_sms * 3;
+  while (tiles * splits * 2 <= target && m / (splits * 2) >= 256) splits *= 2;
+  p.k_per_split = (int)(cdiv(cdiv(m, splits), BK) * BK);
+  splits = (int)cdiv(m, p.k_per_split);
+  dim3 grid((unsigned)tiles, 1, (unsigned)splits);
+  if (splits == 1) return dispatch<EPI_STORE>(c, true, false, p, grid);
+  DBuf part;
+  SK_TRY(part.alloc(c, (size_t)splits * k * k * sizeof(double)));
+  p.out = part.as<double>();
+  SK_TRY(dispatch<EPI_PARTIAL>(c, true, false, p, grid));
+  const dim3 rg((unsigned)std::min<int64_t>(cdiv(k, 256), 64), (unsigned)std::min<int64_t>(k, 65535));
+  k_splitk_reduce<<<rg, 256, 0, c->stream>>>(part.as<double>(), splits, (int)k, (int)k, 1.0, 0.0, G, ldg, 1);
   return launched(c);
 }
 

@@ -12,6 +12,8 @@ namespace skel {
 sk_status gemm(sk_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
                const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
                int64_t ldc);
+// G = Q^T Q (k x k, ldg): only the 64 x 64 tiles on or below the diagonal are written
+sk_status gram_lower(sk_ctx* c, const double* Q, int64_t m, int64_t k, int64_t ldq, double* G, int64_t ldg);
 // sums[0] += ||beta*C + alpha*op(A)op(B)||_F^2 and sums[1] += ||C||_F^2, C read only
 // (the fused residual reduction).  sums: device double[2], overwritten.
 sk_status gemm_sumsq(sk_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,

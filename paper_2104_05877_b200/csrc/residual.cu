@@ -41,7 +41,7 @@ static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows,
   SK_CUDA(c, cudaMemcpyAsync(Q, C, (size_t)rows * k * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   DBuf G;
   SK_TRY(G.alloc(c, (size_t)k * k * sizeof(double)));
-  SK_TRY(gemm(c, true, false, k, k, rows, 1.0, Q, rows, Q, rows, 0.0, G.as<double>(), k));
+  SK_TRY(gram_lower(c, Q, rows, k, rows, G.as<double>(), k));
   k_add_shift<<<1, 1024, 0, c->stream>>>(G.as<double>(), k, k, rows);
   SK_TRY(launched(c));
   SK_TRY(potrf_lower(c, G.as<double>(), k, k, status_dev));
