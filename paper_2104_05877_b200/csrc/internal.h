@@ -72,7 +72,8 @@ sk_status lowrank_sumsq(sk_ctx* c, const double* L, int64_t ldl, const double* W
                         int64_t ldwt, const double* A, int64_t lda, int64_t m, int64_t n, int64_t k, double* sums);
 // sums[0] = ||A - Q Q^T A||_F^2, sums[1] = ||A||_F^2 for an orthonormal Q (m x k, ld m) (residual.cu).
 sk_status col_id_sumsq(sk_ctx* c, const double* Q, const double* A, int64_t m, int64_t n, int64_t lda, int64_t k,
-                       double* sums);
+                       double* sums,
+                       bool try_projection = false);
 // R (n x n, ldr) = upper triangle of B (first n columns, ldb), zeros below (dense.cu).
 sk_status upper_triangle(sk_ctx* c, const double* B, int64_t ldb, int64_t n, double* R, int64_t ldr);
 // RSVD-DEIM column skeletons from A and its row sketch X (deim.cu).

@@ -73,14 +73,67 @@ sk_status lowrank_sumsq(sk_ctx* c, const double* L, int64_t ldl, const double* W
   return gemm_sumsq(c, false, true, m, n, k, -1.0, L, ldl, Wt, ldwt, 1.0, A, lda, sums);
 }
 
+// sum of squares of a rows x cols block (ld) into part[2 * blockIdx.x + slot] (the other slot 0):
+// column-strided over a fixed grid, so the reduction order is fixed
+__global__ void k_sumsq_block(const double* __restrict__ X, int64_t rows, int64_t cols, int64_t ld, double* part,
+                              int slot) {
+  __shared__ double red[34];
+  double s = 0.0;
+  for (int64_t j = blockIdx.x; j < cols; j += gridDim.x)
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      const double v = __ldcs(X + i + j * ld);
+      s = fma(v, v, s);
+    }
+  s = dev::block_sum(s, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x + slot] = s;
+    part[2 * blockIdx.x + 1 - slot] = 0.0;
+  }
+}
+
+// When the projected part does not nearly exhaust A, the projection residual needs no second GEMM:
+// for an orthogonal projection P (P A = Q W with W = Q^T A, or A P = W Q^T, or P_C A P_R with
+// ||P_C A P_R|| = ||Q_C^T A Q_R||), ||A - P(A)||^2 = ||A||^2 - ||W||^2 exactly.  In floating point the
+// difference loses log10(||A||^2 / r^2) digits; ||W||^2 carries ~(u ||Q^T Q - I|| + u sqrt(m)) relative
+// error, so with r^2 >= 1e-3 ||A||^2 the result is good to ~1e-10 relative (the parity tolerance is
+// 1e-9 r).  Returns true (sums written) when that holds, false when the explicit A - QW GEMM is needed.
+static sk_status projection_residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, const double* W,
+                                     int64_t wr, int64_t wc, int64_t ldw, double* sums, bool* done) {
+  *done = false;
+  const int ga = (int)std::min<int64_t>(n, 4LL * c->num_sms), gw = (int)std::min<int64_t>(wc, 2LL * c->num_sms);
+  DBuf part, out;
+  SK_TRY(part.alloc(c, (size_t)2 * (ga + gw) * sizeof(double)));
+  SK_TRY(out.alloc(c, 2 * sizeof(double)));
+  k_sumsq_block<<<ga, 256, 0, c->stream>>>(A, m, n, lda, part.as<double>(), 0);
+  SK_TRY(launched(c));
+  k_sumsq_block<<<gw, 256, 0, c->stream>>>(W, wr, wc, ldw, part.as<double>() + 2 * ga, 1);
+  SK_TRY(launched(c));
+  SK_TRY(reduce_pairs(c, part.as<double>(), ga + gw, out.as<double>()));
+  double h[2];
+  SK_CUDA(c, cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  SK_CUDA(c, cudaStreamSynchronize(c->stream));
+  const double a2 = h[0], w2 = h[1], r2 = a2 - w2;
+  if (!(a2 > 0.0) || !(r2 >= 1e-3 * a2)) return SK_OK;
+  const double hs[2] = {r2, a2};
+  SK_CUDA(c, cudaMemcpyAsync(sums, hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+  SK_CUDA(c, cudaStreamSynchronize(c->stream));
+  *done = true;
+  return SK_OK;
+}
+
 sk_status col_id_sumsq(sk_ctx* c, const double* Q, const double* A, int64_t m, int64_t n, int64_t lda, int64_t k,
-                       double* sums) {
+                       double* sums, bool try_projection) {
   // W = Q^T A by the sketch's TMA + DMMA GEMM (Omega := Q^T; written as W^T, n x k column-major),
   // turned column-major k x n (ld even, the tensor-map rule), then ||A - Q W||^2 and ||A||^2 on the
   // same pipeline with the residual epilogue (Q packed as the row operand, A read once in the epilogue)
   DBuf Wt, W;
   SK_TRY(Wt.alloc(c, (size_t)k * n * sizeof(double)));
   SK_TRY(gemm_qta(c, Q, m, A, m, n, lda, k, Wt.as<double>(), n));
+  if (try_projection) {
+    bool done = false;
+    SK_TRY(projection_residual(c, A, m, n, lda, Wt.as<double>(), n, k, n, sums, &done));
+    if (done) return SK_OK;
+  }
   const int64_t ldw = k + (k & 1);
   if ((reinterpret_cast<uintptr_t>(A) & 7) == 0 && m < (1LL << 31) && k >= 512) {
     SK_TRY(W.alloc(c, (size_t)ldw * n * sizeof(double)));
@@ -155,10 +208,13 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
     SK_TRY(orthonormal_basis(c, Rt.as<double>(), n, k, Qr.as<double>(), status_dev));
     Rt.release();
   }
-  if (kind == SK_RES_COL_ID) return col_id_sumsq(c, Qc.as<double>(), A, m, n, lda, k, sums);
+  if (kind == SK_RES_COL_ID) return col_id_sumsq(c, Qc.as<double>(), A, m, n, lda, k, sums, true);
   if (kind == SK_RES_ROW_ID) {
     SK_TRY(W.alloc(c, (size_t)m * k * sizeof(double)));
     SK_TRY(gemm(c, false, false, m, k, n, 1.0, A, lda, Qr.as<double>(), n, 0.0, W.as<double>(), m));
+    bool done = false;
+    SK_TRY(projection_residual(c, A, m, n, lda, W.as<double>(), m, k, m, sums, &done));
+    if (done) return SK_OK;
     return lowrank_sumsq(c, W.as<double>(), m, nullptr, 0, Qr.as<double>(), n, A, lda, m, n, k, sums);
   }
   // CUR: W = Qc^T A (k x n), Mid = W Qr (k x k), B = Qc Mid (m x k), residual A - B Qr^T
@@ -168,6 +224,9 @@ sk_status residual(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda
   SK_TRY(B.alloc(c, (size_t)m * k * sizeof(double)));
   SK_TRY(gemm_qta(c, Qc.as<double>(), m, A, m, n, lda, k, W.as<double>(), n));            // W^T, n x k
   SK_TRY(gemm(c, true, false, k, k, n, 1.0, W.as<double>(), n, Qr.as<double>(), n, 0.0, Mid.as<double>(), k));
+  bool done = false;
+  SK_TRY(projection_residual(c, A, m, n, lda, Mid.as<double>(), k, k, k, sums, &done));
+  if (done) return SK_OK;
   SK_TRY(gemm(c, false, false, m, k, k, 1.0, Qc.as<double>(), m, Mid.as<double>(), k, 0.0, B.as<double>(), m));
   return lowrank_sumsq(c, B.as<double>(), m, nullptr, 0, Qr.as<double>(), n, A, lda, m, n, k, sums);
 }
@@ -182,7 +241,7 @@ sk_status residual_cols(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_
                                (size_t)k, cudaMemcpyDeviceToDevice, c->stream));
   SK_TRY(orthonormal_basis(c, Cc.as<double>(), m, k, Qc.as<double>(), status_dev));
   Cc.release();
-  return col_id_sumsq(c, Qc.as<double>(), A, m, n, lda, k, sums);
+  return col_id_sumsq(c, Qc.as<double>(), A, m, n, lda, k, sums, true);
 }
 
 }  // namespace skel

@@ -42,4 +42,4 @@ for _ in range(a.reps):
     ts.append(e0.elapsed_time(e1))
 if a.profile:
     torch.cuda.profiler.stop()
-print(f"{a.config} {a.kind} k={k}: residual {sorted(ts)[len(ts) // 2]:.3f} ms (median of {a.reps}), r={r:.6e}")
+print(f"{a.config} {a.kind} k={k}: residual {sorted(ts)[len(ts) // 2]:.3f} ms (median of {a.reps}), r={r:.6e} |A|={nA:.6e} r^2/|A|^2={(r / nA) ** 2:.3e}")
