@@ -241,3 +241,22 @@ def test_dist_context_k1_and_gaps_fallback():
         np.testing.assert_allclose(g5.cpu().numpy(), go, atol=1e-9)
     finally:
         tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["col_id", "row_id", "cur"])
+@pytest.mark.parametrize("scale", [1.0, 1e-2])
+def test_residual_projection_identity_large_residual(kind, scale):
+    """R25: when r^2 >= 1e-3 ||A||^2 the projection kinds take ||A||^2 - ||W||^2 (no second GEMM).
+    A Gaussian matrix with a planted rank-20 part: scale 1 keeps r^2/||A||^2 ~ 0.9 (identity path),
+    scale 1e-2 makes the noise small (r^2/||A||^2 ~ 1e-4: the explicit path) -- both vs the oracle."""
+    rng = np.random.default_rng(77)
+    m, n, k = 1500, 700, 20
+    A = rng.standard_normal((m, 20)) @ rng.standard_normal((20, n)) + scale * rng.standard_normal((m, n))
+    Ad = dev_f(A)
+    X = sk.sketch(Ad, k + 10, "gaussian", 3)
+    Js, _, _, _ = sk.select_cols(X, k)
+    Is, _, _, _ = sk.select_rows(sk.gather_cols(Ad, Js), k)
+    r, nA = sk.residual(Ad, Js, Is if kind != "col_id" else None, kind)
+    ro, nAo = o_res.residual(A, Js.cpu().numpy(), Is.cpu().numpy(), kind=kind)
+    assert abs(r - ro) <= 1e-9 * ro + 4 * 2.0 ** -53 * nAo, (kind, scale, r, ro, (ro / nAo) ** 2)
+    assert abs(nA - nAo) <= 1e-12 * nAo
