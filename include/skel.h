@@ -158,8 +158,10 @@ sk_status sk_sketch(sk_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t 
  *               Gamma tile in shared memory (used automatically when A's layout rules out TMA),
  *               2 / 3 the TMA path with K-splits summed through HBM partials / through the
  *               distributed shared memory of a cluster of the splits
- *   bm          CTA row-tile height: 0 or one of 32, 40, 48, 56, 64
- *   warps       consumer warps per CTA = 32-column groups of the tile: 0, 7 (224 columns) or 8 (256)
+ *   bm          CTA row-tile height: 0 or one of 32, 40, 48, 56, 64, 80
+ *   warps       consumer warps per CTA: 7 (224 columns) or 8 (256) of BM x 32 each; 4 (bm = 80) or
+ *               2 (bm = 40): the 112-column tiles of 40 x 56 warps; 0 = planner.  The (bm, warps)
+ *               pairs that exist: (32|40|48|56|64, 8), (40|48, 7), (80, 4), (40, 2)
  *   splits      K-splits per chunk (0 = planner, 1..64)
  *   chunk_rows  rows of A per K-chunk, rounded up to 16 (0 = the largest whose Gamma slot fits ~80 MB)
  * Results are identical up to summation order (parity tests use it to reach every plan). */

@@ -252,17 +252,29 @@ __device__ __forceinline__ void mbar_arrive_local(unsigned addr) {
 // the copies up to a ring ahead.  Freed from the cluster-shared Box-Muller producers, the tile
 // can be chosen for the wave (plan_pre): BM in {32, 48, 64} rows x 256 columns, split-K to fill
 // the waves; C2 (l = 522) runs BM = 48 (1% padded rows instead of 10% at BM = 64) with 4 K-splits.
-template <int BM, int NW> struct PCfg {
+// Tile geometry: BM rows of X (WM warp rows of FI = BM / (8 WM) MMA row fragments) x TBNP columns
+// (WN warp columns of FJ 8-column fragments), NW = WM * WN consumer warps, CPS CTAs per SM (the
+// ring takes ~200 KB / CPS of shared memory).  The wide-n family is WM = 1, FJ = 4 (warp = BM x 32);
+// the narrow-n family (C4's n = 784 = 7 x 112) is 2 x 2 warps of 40 x 56 at 2 CTAs per SM, which
+// tiles l = 400 and n = 784 exactly and loads all four SM sub-partitions equally.
+template <int BM_, int WM_, int WN_, int FJ_, int CPS_> struct PCfg {
+  static constexpr int BM = BM_, WM = WM_, WN = WN_, FJ = FJ_, CPS = CPS_;
+  static constexpr int NW = WM * WN;
+  static constexpr int FI = BM / (8 * WM);
+  static_assert(FI * 8 * WM == BM, "BM = 8 FI WM");
   static constexpr int OS = BM + 4;
-  static constexpr int TBNP = NW * 32;
-  static constexpr int PBOX = TBNP % 64 == 0 ? 64 : 32;      // columns of A per tensor load (box 16 x PBOX)
+  static constexpr int TBNP = WN * FJ * 8;
+  static constexpr int PBOX = TBNP % 64 == 0 ? 64 : (TBNP % 32 == 0 ? 32 : 16);   // columns per tensor load (box 16 x PBOX)
   static constexpr int A_BYTES = TBNP * TBK * 8;
   static constexpr int O_BYTES = TBK * OS * 8;
   static constexpr int ST_BYTES = ((A_BYTES + O_BYTES) + 1023) & ~1023;
-  static constexpr int TS = (200 * 1024) / ST_BYTES;          // ring depth within ~200 KB
+  static constexpr int TS = ((CPS == 1 ? 200 : 216 / CPS - 4) * 1024) / ST_BYTES;   // ring depth
   static constexpr size_t SMEM = (size_t)TS * ST_BYTES + 2 * TS * 8 + 1024;
   static constexpr int NT = NW * 32;
+  static_assert(TS >= 2, "ring depth");
 };
+// the wide-n family by (BM, warps)
+template <int BM, int NW> using PCfgW = PCfg<BM, 1, NW, 4, 1>;
 
 // One image block (row tile rt, k tile kt; tile = rt * KT + kt) of rows [i0, m) of A, generated by the
 // calling CTA's threads (nthr of them): pair e of the block -> column kk = e / (OS/2), rows 2 pr, 2 pr + 1.
@@ -343,12 +355,10 @@ __device__ __forceinline__ void bulk_load_hint(unsigned dst, const void* src, un
 // MODE 0: one K range, X written directly; 1: K-split partials to HBM (+ k_sketch_splitk_reduce);
 // 2: the gridDim.z K-splits of a tile form one cluster and are summed through distributed shared
 // memory in rank order (deterministic), each rank writing 1/S of the tile's rows.
-template <int BM, int NW, int MODE>
-__global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid_constant__ CUtensorMap tmA, DenseParams p,
-                                                                     const double* __restrict__ img, int64_t KT) {
-  using C = PCfg<BM, NW>;
-  constexpr int TS = C::TS;
-  constexpr int FI = BM / 8;
+template <class C, int MODE>
+__global__ void __launch_bounds__(C::NT, C::CPS) k_sketch_pre(const __grid_constant__ CUtensorMap tmA, DenseParams p,
+                                                               const double* __restrict__ img, int64_t KT) {
+  constexpr int TS = C::TS, BM = C::BM, NW = C::NW, FI = C::FI, FJ = C::FJ;
   dev::griddep_wait();                                   // PDL: the Omega image is complete
   extern __shared__ __align__(1024) unsigned char psm_raw[];
   unsigned char* base = psm_raw + ((1024u - (dev::smem_addr(psm_raw) & 1023u)) & 1023u);
@@ -374,7 +384,7 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
   // number of 64-column tensor loads with any column inside A (the rest of the tile stays stale)
   constexpr int PBOX = C::PBOX;
   const int64_t nbox_all = (p.n - n0 + PBOX - 1) / PBOX;
-  const int nbox = (int)(nbox_all < NW * 32 / PBOX ? nbox_all : NW * 32 / PBOX);
+  const int nbox = (int)(nbox_all < C::TBNP / PBOX ? nbox_all : C::TBNP / PBOX);
   int issued = 0;
   const unsigned long long pol_a = SKEL_SKETCH_HINTS ? dev::policy_evict_first() : 0ull;
   const unsigned long long pol_o = SKEL_SKETCH_HINTS ? dev::policy_evict_last() : 0ull;
@@ -402,13 +412,15 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
     }
   };
   const int g = lane >> 2, q = lane & 3;
-  const int wn = warp * 32;
+  const int wm = warp % C::WM;                             // warp row (FI fragments of 8 rows)
+  const int wr = wm * FI * 8;                              // first row of the warp within the tile
+  const int wn = (warp / C::WM) * FJ * 8;                  // first column of the warp within the tile
   const int sg = sig8(g);
-  double acc[FI][4][2];
+  double acc[FI][FJ][2];
 #pragma unroll
   for (int i = 0; i < FI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const bool lead = tid == 0;
   const bool active = n0 + wn < p.n;                       // warp has columns inside A
   for (int kt = 0; kt < ktiles; ++kt) {
@@ -421,20 +433,20 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
     dev::mbar_wait(fullB + 8 * s, (unsigned)(kt / TS) & 1u);
     if (active) {
       const unsigned char* st = base + (size_t)s * C::ST_BYTES;
-      const double* Os = reinterpret_cast<const double*>(st + C::A_BYTES) + q * C::OS + g;
+      const double* Os = reinterpret_cast<const double*>(st + C::A_BYTES) + q * C::OS + g + wr;
       const unsigned char* At = st + (size_t)(wn + sg) * 128 + ((q & 1) << 3);
 #pragma unroll
       for (int kk = 0; kk < TBK / 4; ++kk) {
-        double a[FI], b[4];
+        double a[FI], b[FJ];
 #pragma unroll
         for (int i = 0; i < FI; ++i) a[i] = Os[kk * 4 * C::OS + i * 8];
         const int inrow = ((2 * kk + (q >> 1)) ^ sg) << 4;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const double*>(At + j * 8 * 128 + inrow);
+        for (int j = 0; j < FJ; ++j) b[j] = *reinterpret_cast<const double*>(At + j * 8 * 128 + inrow);
 #pragma unroll
         for (int i = 0; i < FI; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dev::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+          for (int j = 0; j < FJ; ++j) dev::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
       }
     }
     __syncwarp();
@@ -448,10 +460,10 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
     if (active) {
 #pragma unroll
       for (int i = 0; i < FI; ++i) {
-        const int64_t r = (int64_t)rt * BM + i * 8 + g;
+        const int64_t r = (int64_t)rt * BM + wr + i * 8 + g;
         if (r >= p.l) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < FJ; ++j) {
           const int64_t cb = n0 + wn + j * 8;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -491,9 +503,9 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
 #pragma unroll
     for (int i = 0; i < FI; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        T[(i * 8 + g) * TST + wn + j * 8 + c0] = acc[i][j][0];
-        T[(i * 8 + g) * TST + wn + j * 8 + c1] = acc[i][j][1];
+      for (int j = 0; j < FJ; ++j) {
+        T[(wr + i * 8 + g) * TST + wn + j * 8 + c0] = acc[i][j][0];
+        T[(wr + i * 8 + g) * TST + wn + j * 8 + c1] = acc[i][j][1];
       }
     dev::cluster_arrive();
     dev::cluster_wait();
@@ -522,10 +534,10 @@ __global__ void __launch_bounds__(PCfg<BM, NW>::NT, 1) k_sketch_pre(const __grid
   if (!active) return;
 #pragma unroll
   for (int i = 0; i < FI; ++i) {
-    const int r = rt * BM + i * 8 + g;
+    const int r = rt * BM + wr + i * 8 + g;
     if (r >= p.l) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < FJ; ++j) {
       const int64_t cb = n0 + wn + j * 8;
       if (MODE == 1) {
         double* dst = p.part + ((int64_t)blockIdx.z * p.l + r) * p.n;
@@ -1019,7 +1031,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 struct PrePlan {
-  int bm = 0, nw = 0, splits = 1;
+  int geo = 0, bm = 0, nw = 0, splits = 1;
   bool cluster = true;     // K-splits reduced in-cluster when eligible (<= 8, dividing BM)
   int64_t chunk = 0;       // rows of A per K-chunk (the Omega image slot holds one chunk)
   double cost = 1e300;
@@ -1030,13 +1042,42 @@ struct PrePlan {
 // the per-chunk cost is the launch tail and the X read-modify-write, not L2 misses on the slot.
 constexpr double kOmegaSlotBytes = 80.0 * (1 << 20);
 
-// co-resident CTAs of k_sketch_pre<BM, NW> launched in clusters of S along z (cached per process)
-template <int BM, int NW> int pre_max_ctas(int S) {
+// The tile geometries of k_sketch_pre the planner chooses from (G_W56 only on request).
+enum PreGeo { G_W48 = 0, G_W64, G_W32, G_W40, G_W40_7, G_W48_7, G_W56, G_N80, G_N40, G_COUNT };
+struct GeoDesc { int bm, nw, tbn, cps; };
+constexpr GeoDesc kGeo[G_COUNT] = {{48, 8, 256, 1}, {64, 8, 256, 1}, {32, 8, 256, 1}, {40, 8, 256, 1},
+                                   {40, 7, 224, 1}, {48, 7, 224, 1}, {56, 8, 256, 1}, {80, 4, 112, 2},
+                                   {40, 2, 112, 4}};
+using CfgW48 = PCfgW<48, 8>;
+using CfgW64 = PCfgW<64, 8>;
+using CfgW32 = PCfgW<32, 8>;
+using CfgW40 = PCfgW<40, 8>;
+using CfgW40_7 = PCfgW<40, 7>;
+using CfgW48_7 = PCfgW<48, 7>;
+using CfgW56 = PCfgW<56, 8>;
+using CfgN80 = PCfg<80, 2, 2, 7, 2>;     // 80 x 112: 2 x 2 warps of 40 x 56, 2 CTAs per SM
+using CfgN40 = PCfg<40, 1, 2, 7, 4>;     // 40 x 112: 2 warps of 40 x 56, 4 CTAs per SM
+// Calls f(C{}) with the geometry's config type.
+template <class F> auto with_geo(int g, F&& f) {
+  switch (g) {
+    case G_W64: return f(CfgW64{});
+    case G_W32: return f(CfgW32{});
+    case G_W40: return f(CfgW40{});
+    case G_W40_7: return f(CfgW40_7{});
+    case G_W48_7: return f(CfgW48_7{});
+    case G_W56: return f(CfgW56{});
+    case G_N80: return f(CfgN80{});
+    case G_N40: return f(CfgN40{});
+    default: return f(CfgW48{});
+  }
+}
+
+// co-resident CTAs of k_sketch_pre<C> launched in clusters of S along z (cached per process)
+template <class C> int pre_max_ctas(int S) {
   static int cached[9] = {0};
   if (S < 1 || S > 8) return 0;
   if (cached[S] == 0) {
-    using C = PCfg<BM, NW>;
-    auto kern = S > 1 ? k_sketch_pre<BM, NW, 2> : k_sketch_pre<BM, NW, 0>;
+    auto kern = S > 1 ? k_sketch_pre<C, 2> : k_sketch_pre<C, 0>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(1, 1, (unsigned)S);
@@ -1053,15 +1094,8 @@ template <int BM, int NW> int pre_max_ctas(int S) {
   }
   return cached[S];
 }
-int pre_capacity(int bm, int nw, int S) {
-  if (bm == 56 && nw == 8) return pre_max_ctas<56, 8>(S);
-  if (bm == 40 && nw == 7) return pre_max_ctas<40, 7>(S);
-  if (bm == 48 && nw == 7) return pre_max_ctas<48, 7>(S);
-  if (bm == 48 && nw == 8) return pre_max_ctas<48, 8>(S);
-  if (bm == 64 && nw == 8) return pre_max_ctas<64, 8>(S);
-  if (bm == 32 && nw == 8) return pre_max_ctas<32, 8>(S);
-  if (bm == 40 && nw == 8) return pre_max_ctas<40, 8>(S);
-  return -1;
+int pre_capacity(int geo, int S) {
+  return with_geo(geo, [&](auto cfg) { return pre_max_ctas<decltype(cfg)>(S); });
 }
 
 // rows of A per K-chunk for a row-tile height bm: the largest multiple of 1024 whose Omega image
@@ -1073,24 +1107,27 @@ int64_t chunk_rows(int64_t m, int64_t l, int bm, int64_t forced) {
   return ch >= m ? m : ch;
 }
 
-// (BM, NW, K-splits per chunk) by a cost model: whole waves of the co-resident CTA count x per-CTA
-// DMMA work (padded tiles included) + split-K overhead, summed over the K-chunks; a candidate must
-// beat the incumbent by 1% (fewer splits, less partial traffic, win ties).  Checked against a
-// measured sweep of every plan (tools/sweep_pre.py, profiles/round1/sweep_pre.txt).  The context's
-// tuning (sk_set_sketch_tuning) can pin BM, the split count and the chunk height.
+// (geometry, K-splits per chunk) by a cost model: whole waves of the co-resident CTA count x per-CTA
+// DMMA work (padded tiles included) x the CTAs sharing an SM x the load of the busiest SM
+// sub-partition (warps are dealt to the 4 sub-partitions round-robin: 7 warps leave one with half
+// the work) + split-K overhead, summed over the K-chunks; a candidate must beat the incumbent by 1%
+// (fewer splits, less partial traffic, win ties).  Checked against a measured sweep of every plan
+// (tools/sweep_pre.py).  The context's tuning (sk_set_sketch_tuning) can pin BM, the warp count, the
+// split count and the chunk height.
 PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
   PrePlan best;
-  // 8 warps = 256-column tiles; 7 warps = 224 (C4's n = 784 fills 4 tiles of 224 to 87.5 %, of 256 to 77 %)
+  // 8 warps = 256-column tiles; 7 warps = 224; the narrow family 112 (C4's n = 784 = 7 x 112)
   // (BM = 56 is a tuning value only: measured 85.2 % at C5 vs 88.1 % for BM = 48)
-  const int cand[][2] = {{48, 8}, {64, 8}, {32, 8}, {40, 8}, {40, 7}, {48, 7}};
-  const int cand56[1][2] = {{56, 8}};
-  const int (*cl)[2] = c->tune_sketch_bm == 56 ? cand56 : cand;
+  const int cand[] = {G_W48, G_W64, G_W32, G_W40, G_W40_7, G_W48_7, G_N80, G_N40};
+  const int cand56[] = {G_W56};
+  const int* cl = c->tune_sketch_bm == 56 ? cand56 : cand;
   const int ncand = c->tune_sketch_bm == 56 ? 1 : (int)(sizeof(cand) / sizeof(cand[0]));
   for (int ci = 0; ci < ncand; ++ci) {
-    const int bm = cl[ci][0], nw = cl[ci][1];
+    const int geo = cl[ci];
+    const int bm = kGeo[geo].bm, nw = kGeo[geo].nw, tbn = kGeo[geo].tbn;
     if (c->tune_sketch_bm && c->tune_sketch_bm != bm) continue;
     if (c->tune_sketch_nw && c->tune_sketch_nw != nw) continue;
-    const int64_t mb = cdiv(l, bm), nb = cdiv(n, nw * 32);
+    const int64_t mb = cdiv(l, bm), nb = cdiv(n, tbn);
     const int64_t ch = chunk_rows(m, l, bm, c->tune_sketch_chunk);
     const int64_t nch = cdiv(m, ch);
     // K-splits per chunk 1..8 (any count: 5 fills the waves at C2 k=512), then powers of two up to 64
@@ -1102,12 +1139,18 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
       const int64_t ctas = mb * nb * sp;
       for (int clus = 0; clus < 2; ++clus) {
         if (clus && !(sp > 1 && sp <= 8 && bm % sp == 0)) continue;
+        // several CTAs per SM: the in-cluster reduction measured far slower (C4 k=200 N80: 41 % vs
+        // 75 % of the DMMA ceiling through HBM partials) -- planned through partials only
+        if (clus && kGeo[geo].cps > 1 && !c->tune_sketch_path) continue;
         if ((c->tune_sketch_path == 2 && clus) || (c->tune_sketch_path == 3 && !clus && sp > 1)) continue;
-        const int cap = pre_capacity(bm, nw, clus ? (int)sp : 1);   // clusters of 4/8 strand SMs per GPC
+        const int cap = pre_capacity(geo, clus ? (int)sp : 1);   // clusters of 4/8 strand SMs per GPC
         if (cap <= 0) continue;
         const double waves = (double)cdiv(ctas, cap);
-        const double stage = (double)bm * nw * 32 * TBK;
-        double cost = waves * (double)cdiv(kps, TBK) * stage;
+        const double per_sm = std::max(1.0, (double)cap / c->num_sms);      // CTAs sharing an SM
+        const double wps = per_sm * nw;                                     // warps per SM
+        const double smsp = std::ceil(wps / 4.0) * 4.0 / wps;                // busiest sub-partition
+        const double stage = (double)bm * tbn * TBK;
+        double cost = waves * (double)cdiv(kps, TBK) * stage * per_sm * smsp;
         // K-splits summed in-cluster through DSMEM (~0.05 FMA-equivalents per partial element) or
         // through HBM partials + a reduce launch; chunks after the first add X into X.  (Adding the
         // splits into X in split order through per-tile flags was measured slower: C2 k=512
@@ -1115,8 +1158,8 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
         if (sp > 1) cost += clus ? 0.05 * (double)sp * l * n : 0.3 * (double)sp * l * n + 3.6e5;
         cost = cost * nch + (nch - 1) * (0.3 * (double)l * n + 3.6e5);
         if (cost < 0.99 * best.cost) {
-          best.bm = bm; best.nw = nw; best.splits = (int)sp; best.cluster = clus != 0; best.cost = cost;
-          best.chunk = ch;
+          best.geo = geo; best.bm = bm; best.nw = nw; best.splits = (int)sp; best.cluster = clus != 0;
+          best.cost = cost; best.chunk = ch;
         }
       }
     }
@@ -1155,10 +1198,10 @@ sk_status make_tmap(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t ld
 }
 
 // The Omega image of rows [i0, i1) of A (from Philox, or packed from Q when Qom != nullptr).
-template <int BM, int NW>
+template <class C>
 sk_status omega_chunk_image(sk_ctx* c, uint2 key, const double* Qom, int64_t ldq, int64_t l, int64_t i0, int64_t i1,
                             double* img) {
-  using C = PCfg<BM, NW>;
+  constexpr int BM = C::BM;
   const int64_t mb = cdiv(l, BM), KT = cdiv(i1 - i0, TBK);
   if (Qom) k_omega_pack<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(Qom, ldq, (int)l, i0, i1, BM, C::OS, KT, img);
   else k_omega_image<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(key, (int)l, i0, i1, BM, C::OS, KT, img);
@@ -1167,10 +1210,10 @@ sk_status omega_chunk_image(sk_ctx* c, uint2 key, const double* Qom, int64_t ldq
 
 // One K-chunk's GEMM: X (+)= Omega(:, p.k0:p.m) A(p.k0:p.m, :) with the chunk's image, K-split
 // `splits_req` ways (partials through `part` or cluster DSMEM); p.accum selects = or +=.
-template <int BM, int NW>
+template <class C>
 sk_status pre_gemm_chunk(sk_ctx* c, const CUtensorMap& tm, DenseParams p, int64_t l, int64_t n, int splits_req,
                          bool cl_allowed, const double* img, double* part) {
-  using C = PCfg<BM, NW>;
+  constexpr int BM = C::BM;
   const int64_t mb = cdiv(l, BM), nb = cdiv(n, C::TBNP), KT = cdiv(p.m - p.k0, TBK);
   p.k_per_split = cdiv(cdiv(p.m - p.k0, splits_req), TBK) * TBK;
   const int splits = (int)cdiv(p.m - p.k0, p.k_per_split);
@@ -1192,13 +1235,13 @@ sk_status pre_gemm_chunk(sk_ctx* c, const CUtensorMap& tm, DenseParams p, int64_
   ++na;
   lc.attrs = at; lc.numAttrs = na;
   if (splits == 1 || clu) {
-    auto kern = clu ? k_sketch_pre<BM, NW, 2> : k_sketch_pre<BM, NW, 0>;
+    auto kern = clu ? k_sketch_pre<C, 2> : k_sketch_pre<C, 0>;
     SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, img, KT));
     return launched(c);
   }
   p.part = part;
-  auto kern = k_sketch_pre<BM, NW, 1>;
+  auto kern = k_sketch_pre<C, 1>;
   SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   SK_CUDA(c, cudaLaunchKernelEx(&lc, kern, tm, p, img, KT));
   SK_TRY(launched(c));
@@ -1207,10 +1250,10 @@ sk_status pre_gemm_chunk(sk_ctx* c, const CUtensorMap& tm, DenseParams p, int64_
 
 // X = Omega A chunk by chunk: per K-chunk, the chunk's Omega image (generated from Philox, or packed
 // from a given Q when Qom != nullptr) then the TMA + DMMA GEMM accumulating into X.
-template <int BM, int NW>
+template <class C>
 sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_t l, const PrePlan& pl,
                   const double* Qom = nullptr, int64_t ldq = 0) {
-  using C = PCfg<BM, NW>;
+  constexpr int BM = C::BM;
   DenseParams p = p0;
   CUtensorMap tm;
   SK_TRY(make_tmap(c, p.A, m, n, p.lda, &tm, C::PBOX));
@@ -1221,14 +1264,19 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   const int64_t kps_max = cdiv(cdiv(chunk, pl.splits), TBK) * TBK;
   const int sp_max = (int)cdiv(chunk, kps_max);
   const bool cl = pl.cluster && sp_max > 1 && sp_max <= 8 && BM % sp_max == 0;
-  if (sp_max > 1 && !cl) SK_TRY(part.alloc(c, (size_t)sp_max * l * n * sizeof(double)));
   const int64_t nch = cdiv(m, chunk);
+  // a ragged last chunk splits into fewer K ranges; when that count cannot form the cluster it goes
+  // through HBM partials, so those are allocated too
+  const int64_t last = m - (nch - 1) * chunk;
+  const int sp_last = (int)cdiv(last, cdiv(cdiv(last, pl.splits), TBK) * TBK);
+  if ((sp_max > 1 && !cl) || (sp_last > 1 && (!cl || sp_last != sp_max)))
+    SK_TRY(part.alloc(c, (size_t)sp_max * l * n * sizeof(double)));
   if (nch == 1) {
-    SK_TRY((omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, 0, m, img.as<double>())));
+    SK_TRY((omega_chunk_image<C>(c, p.key, Qom, ldq, l, 0, m, img.as<double>())));
     p.k0 = 0;
     p.m = m;
     p.accum = 0;
-    return pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, cl, img.as<double>(), part.as<double>());
+    return pre_gemm_chunk<C>(c, tm, p, l, n, pl.splits, cl, img.as<double>(), part.as<double>());
   }
   // Several chunks: two image slots; the image of chunk c + 1 is generated on the image stream while
   // the GEMM of chunk c runs (its small CTAs fit beside a GEMM CTA on an SM), into the slot the GEMM of
@@ -1245,7 +1293,7 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   cudaEvent_t* read = ev + 2;     // [2] GEMM that read slot s complete (context stream)
   if (rs == SK_OK && (cudaEventRecord(ev[4], c->stream) != cudaSuccess || cudaStreamWaitEvent(c->img, ev[4], 0) != cudaSuccess))
     rs = fail(c, SK_E_CUDA, "sketch: event");
-  if (rs == SK_OK) rs = omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, 0, std::min(m, chunk), slot[0]);
+  if (rs == SK_OK) rs = omega_chunk_image<C>(c, p.key, Qom, ldq, l, 0, std::min(m, chunk), slot[0]);
   for (int64_t ci = 0; ci < nch && rs == SK_OK; ++ci) {
     const int64_t i0 = ci * chunk, i1 = std::min(m, i0 + chunk);
     if (ci + 1 < nch) {           // next image on the helper stream, into the other slot
@@ -1253,7 +1301,7 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
       cudaStream_t main_stream = c->stream;
       if (ci >= 1 && cudaStreamWaitEvent(c->img, read[s], 0) != cudaSuccess) { rs = fail(c, SK_E_CUDA, "sketch: event"); break; }
       c->stream = c->img;
-      rs = omega_chunk_image<BM, NW>(c, p.key, Qom, ldq, l, i1, std::min(m, i1 + chunk), slot[s]);
+      rs = omega_chunk_image<C>(c, p.key, Qom, ldq, l, i1, std::min(m, i1 + chunk), slot[s]);
       c->stream = main_stream;
       if (rs == SK_OK && cudaEventRecord(made[s], c->img) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sketch: event");
       if (rs != SK_OK) break;
@@ -1264,7 +1312,7 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
     p.accum = ci > 0;
     const int64_t kps = cdiv(cdiv(i1 - i0, pl.splits), TBK) * TBK;
     const bool clu = cl && cdiv(i1 - i0, kps) == sp_max;
-    rs = pre_gemm_chunk<BM, NW>(c, tm, p, l, n, pl.splits, clu, slot[ci & 1], part.as<double>());
+    rs = pre_gemm_chunk<C>(c, tm, p, l, n, pl.splits, clu, slot[ci & 1], part.as<double>());
     if (rs == SK_OK && cudaEventRecord(read[ci & 1], c->stream) != cudaSuccess) rs = fail(c, SK_E_CUDA, "sketch: event");
   }
   // the context stream has waited for every image, so the slots are freed after their last use
@@ -1276,14 +1324,8 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
 
 sk_status sketch_dense_pre(sk_ctx* c, const DenseParams& p, int64_t m, int64_t n, int64_t l, const PrePlan& pl,
                            const double* Qom = nullptr, int64_t ldq = 0) {
-  if (pl.bm == 48 && pl.nw == 8) return run_pre<48, 8>(c, p, m, n, l, pl, Qom, ldq);
-  if (pl.bm == 64 && pl.nw == 8) return run_pre<64, 8>(c, p, m, n, l, pl, Qom, ldq);
-  if (pl.bm == 32 && pl.nw == 8) return run_pre<32, 8>(c, p, m, n, l, pl, Qom, ldq);
-  if (pl.bm == 40 && pl.nw == 8) return run_pre<40, 8>(c, p, m, n, l, pl, Qom, ldq);
-  if (pl.bm == 56 && pl.nw == 8) return run_pre<56, 8>(c, p, m, n, l, pl, Qom, ldq);
-  if (pl.bm == 40 && pl.nw == 7) return run_pre<40, 7>(c, p, m, n, l, pl, Qom, ldq);
-  if (pl.bm == 48 && pl.nw == 7) return run_pre<48, 7>(c, p, m, n, l, pl, Qom, ldq);
-  return fail(c, SK_E_ARG, "sketch: no tensor-core plan for this shape");
+  if (pl.bm <= 0) return fail(c, SK_E_ARG, "sketch: no tensor-core plan for this shape");
+  return with_geo(pl.geo, [&](auto cfg) { return run_pre<decltype(cfg)>(c, p, m, n, l, pl, Qom, ldq); });
 }
 
 bool tma_ok_for(const double* A, int64_t m, int64_t n, int64_t lda) {
@@ -1337,10 +1379,10 @@ namespace {
 // sums[0] = ||A - Q W||_F^2, sums[1] = ||A||_F^2 on the TMA + DMMA pipeline: rows of the output = the
 // M = m rows of Q (packed once into the row-operand image), K = k, the column operand W (k x n,
 // column-major) streamed by TMA, MODE 4 epilogue against A.
-template <int BM, int NW>
+template <class C>
 sk_status run_sumsq(sk_ctx* c, const double* Q, int64_t ldq, const double* W, int64_t ldw, const double* A, int64_t lda,
                     int64_t m, int64_t n, int64_t k, double* sums) {
-  using C = PCfg<BM, NW>;
+  constexpr int BM = C::BM;
   CUtensorMap tm;
   SK_TRY(make_tmap(c, W, k, n, ldw, &tm, C::PBOX));
   const int64_t mb = cdiv(m, BM), nb = cdiv(n, C::TBNP), KT = cdiv(k, TBK);
@@ -1353,7 +1395,7 @@ sk_status run_sumsq(sk_ctx* c, const double* Q, int64_t ldq, const double* W, in
   p.A = W; p.lda = ldw; p.m = k; p.n = n; p.l = (int)std::min<int64_t>(m, INT32_MAX);
   p.scale = 1.0; p.k0 = 0; p.k_per_split = cdiv(k, TBK) * TBK;
   p.Csub = A; p.ldcs = lda; p.sums_part = part.as<double>();
-  auto kern = k_sketch_pre<BM, NW, 4>;
+  auto kern = k_sketch_pre<C, 4>;
   SK_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3((unsigned)mb, (unsigned)nb, 1);
@@ -1373,7 +1415,11 @@ sk_status run_sumsq(sk_ctx* c, const double* Q, int64_t ldq, const double* W, in
 sk_status residual_sumsq_tma(sk_ctx* c, const double* Q, int64_t ldq, const double* W, int64_t ldw, const double* A,
                              int64_t lda, int64_t m, int64_t n, int64_t k, double* sums) {
   if (!tma_ok_for(W, k, n, ldw) || m >= (1LL << 31)) return fail(c, SK_E_ARG, "residual_sumsq_tma: layout");
-  return run_sumsq<48, 8>(c, Q, ldq, W, ldw, A, lda, m, n, k, sums);
+  // narrow n (C4's 784 = 7 x 112): the 112-column tiles fill the columns exactly where 256-column
+  // tiles would leave a quarter of the last one idle
+  auto fill = [&](int64_t tbn) { return (double)n / (double)(cdiv(n, tbn) * tbn); };
+  if (fill(112) > fill(256) + 0.05) return run_sumsq<CfgN80>(c, Q, ldq, W, ldw, A, lda, m, n, k, sums);
+  return run_sumsq<CfgW48>(c, Q, ldq, W, ldw, A, lda, m, n, k, sums);
 }
 
 sk_status gemm_qta(sk_ctx* c, const double* Q, int64_t ldq, const double* A, int64_t m, int64_t n, int64_t lda,

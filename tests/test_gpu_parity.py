@@ -542,6 +542,8 @@ def test_rand_lupp_host_pipelined(emb):
     (2, 48, 4, 0), (3, 48, 4, 0), (3, 64, 2, 0), (3, 32, 8, 0),        # K-splits via HBM partials / cluster DSMEM
     (0, 48, 1, 256), (2, 40, 3, 320), (3, 48, 2, 512),                  # K-chunked Omega (ragged last chunk)
     (0, 40, 1, 0, 7), (2, 48, 3, 256, 7), (3, 40, 2, 0, 7),             # 7 warps: 224-column tiles, 32-column boxes
+    (0, 80, 1, 0, 4), (3, 80, 4, 0, 4), (2, 80, 3, 256, 4),            # 112-column tiles: 2 x 2 warps of 40 x 56,
+    (0, 40, 1, 0, 2), (3, 40, 4, 320, 2), (2, 40, 2, 0, 2),             # or 2 warps of 40 x 56 (16-column boxes)
     (1, 0, 0, 0),                                                       # shared-memory generation fallback
 ])
 def test_sketch_dense_plans(plan):

@@ -11,7 +11,7 @@ import paper_2104_05877_b200 as sk  # noqa: E402
 SHAPES = [("C2 k=16", 4096, 4096, 26), ("C2 k=64", 4096, 4096, 74), ("C2 k=256", 4096, 4096, 266),
           ("C2 k=512", 4096, 4096, 522), ("C4 k=50", 65536, 784, 100), ("C4 k=100", 65536, 784, 200),
           ("C4 k=200", 65536, 784, 400), ("C5 block", 131072, 8192, 1100)]
-PLANS = [(64, 8), (48, 8), (40, 8), (32, 8), (40, 7), (48, 7)]
+PLANS = [(64, 8), (48, 8), (40, 8), (32, 8), (40, 7), (48, 7), (80, 4), (40, 2)]   # (bm, warps); 4 / 2 = 112-column tiles
 
 
 def timed(fn, reps=5):
@@ -41,10 +41,10 @@ for name, m, n, l in SHAPES:
     print(f"{name:10s} default plan {ms:8.4f} ms {2 * l * m * n / ms / 1e9 / 37.13:6.1%}", flush=True)
     res = []
     for bm, nw in PLANS:
-        for sp in (1, 2, 4, 8, 16, 32):
+        for sp in (1, 2, 4, 8, 16, 32, 64):
             if sp > 1 and m // sp < 1024:
                 break
-            for cl in ((0, 1) if sp > 1 and sp <= 8 and bm % sp == 0 else (0,)):
+            for cl in ((0, 1) if sp > 1 and sp <= 8 and bm % sp == 0 and nw > 4 else (0,)):
                 sk.set_sketch_tuning(path=3 if cl else 2, bm=bm, splits=sp, warps=nw)
                 ms = timed(lambda: sk.sketch(A, l, "gaussian", 7, out=X))
                 err = float((X - ref).norm() / ref.norm())
