@@ -137,10 +137,10 @@ sk_status sk_set_sketch_tuning(sk_ctx* c, int32_t path, int32_t bm, int32_t warp
   if (!c) return SK_E_ARG;
   c->err.clear();
   SK_ARG(c, path >= 0 && path <= 3, "sk_set_sketch_tuning: path must be 0..3");
-  SK_ARG(c, bm == 0 || bm == 32 || bm == 40 || bm == 48 || bm == 56 || bm == 64 || bm == 80,
-         "sk_set_sketch_tuning: bm must be 0, 32, 40, 48, 56, 64 or 80");
-  SK_ARG(c, warps == 0 || warps == 2 || warps == 4 || warps == 7 || warps == 8,
-         "sk_set_sketch_tuning: warps must be 0, 2, 4, 7 or 8");
+  SK_ARG(c, bm == 0 || bm == 32 || bm == 40 || bm == 48 || bm == 56 || bm == 64 || bm == 80 || bm == 96,
+         "sk_set_sketch_tuning: bm must be 0, 32, 40, 48, 56, 64, 80 or 96");
+  SK_ARG(c, warps == 0 || warps == 2 || warps == 4 || warps == 7 || warps == 8 || warps == 12,
+         "sk_set_sketch_tuning: warps must be 0, 2, 4, 7, 8 or 12");
   SK_ARG(c, splits >= 0 && splits <= 64 && chunk_rows >= 0, "sk_set_sketch_tuning: bad splits / chunk_rows");
   c->tune_sketch_path = path;
   c->tune_sketch_bm = bm;

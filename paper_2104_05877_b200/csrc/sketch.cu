@@ -268,7 +268,7 @@ template <int BM_, int WM_, int WN_, int FJ_, int CPS_> struct PCfg {
   static constexpr int A_BYTES = TBNP * TBK * 8;
   static constexpr int O_BYTES = TBK * OS * 8;
   static constexpr int ST_BYTES = ((A_BYTES + O_BYTES) + 1023) & ~1023;
-  static constexpr int TS = ((CPS == 1 ? 200 : 216 / CPS - 4) * 1024) / ST_BYTES;   // ring depth
+  static constexpr int TS = ((CPS == 1 ? (NW > 8 ? 220 : 200) : 216 / CPS - 4) * 1024) / ST_BYTES;   // ring depth
   static constexpr size_t SMEM = (size_t)TS * ST_BYTES + 2 * TS * 8 + 1024;
   static constexpr int NT = NW * 32;
   static_assert(TS >= 2, "ring depth");
@@ -1041,11 +1041,11 @@ struct PrePlan {
 constexpr double kOmegaSlotBytes = 80.0 * (1 << 20);
 
 // The tile geometries of k_sketch_pre the planner chooses from (G_W56 only on request).
-enum PreGeo { G_W48 = 0, G_W64, G_W32, G_W40, G_W40_7, G_W48_7, G_W56, G_N80, G_N40, G_COUNT };
+enum PreGeo { G_W48 = 0, G_W64, G_W32, G_W40, G_W40_7, G_W48_7, G_W56, G_N80, G_N40, G_T80, G_T48, G_T96, G_COUNT };
 struct GeoDesc { int bm, nw, tbn, cps; };
 constexpr GeoDesc kGeo[G_COUNT] = {{48, 8, 256, 1}, {64, 8, 256, 1}, {32, 8, 256, 1}, {40, 8, 256, 1},
                                    {40, 7, 224, 1}, {48, 7, 224, 1}, {56, 8, 256, 1}, {80, 4, 112, 2},
-                                   {40, 2, 112, 4}};
+                                   {40, 2, 112, 4}, {80, 12, 192, 1}, {48, 12, 384, 1}, {96, 8, 128, 1}};
 using CfgW48 = PCfgW<48, 8>;
 using CfgW64 = PCfgW<64, 8>;
 using CfgW32 = PCfgW<32, 8>;
@@ -1055,6 +1055,9 @@ using CfgW48_7 = PCfgW<48, 7>;
 using CfgW56 = PCfgW<56, 8>;
 using CfgN80 = PCfg<80, 2, 2, 7, 2>;     // 80 x 112: 2 x 2 warps of 40 x 56, 2 CTAs per SM
 using CfgN40 = PCfg<40, 1, 2, 7, 4>;     // 40 x 112: 2 warps of 40 x 56, 4 CTAs per SM
+using CfgT80 = PCfg<80, 2, 6, 4, 1>;     // 80 x 192: 2 x 6 warps of 40 x 32 (3 warps per SM sub-partition)
+using CfgT48 = PCfg<48, 1, 12, 4, 1>;    // 48 x 384: 12 warps of 48 x 32
+using CfgT96 = PCfg<96, 2, 4, 4, 1>;     // 96 x 128: 2 x 4 warps of 48 x 32
 // Calls f(C{}) with the geometry's config type.
 template <class F> auto with_geo(int g, F&& f) {
   switch (g) {
@@ -1066,6 +1069,9 @@ template <class F> auto with_geo(int g, F&& f) {
     case G_W56: return f(CfgW56{});
     case G_N80: return f(CfgN80{});
     case G_N40: return f(CfgN40{});
+    case G_T80: return f(CfgT80{});
+    case G_T48: return f(CfgT48{});
+    case G_T96: return f(CfgT96{});
     default: return f(CfgW48{});
   }
 }
@@ -1116,12 +1122,17 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
   PrePlan best;
   // 8 warps = 256-column tiles; 7 warps = 224; the narrow family 112 (C4's n = 784 = 7 x 112)
   // (BM = 56 is a tuning value only: measured 85.2 % at C5 vs 88.1 % for BM = 48)
-  const int cand[] = {G_W48, G_W64, G_W32, G_W40, G_W40_7, G_W48_7, G_N80, G_N40};
-  const int cand56[] = {G_W56};
-  const int* cl = c->tune_sketch_bm == 56 ? cand56 : cand;
-  const int ncand = c->tune_sketch_bm == 56 ? 1 : (int)(sizeof(cand) / sizeof(cand[0]));
-  for (int ci = 0; ci < ncand; ++ci) {
-    const int geo = cl[ci];
+  // the automatic candidates; an exact (bm, warps) pin may name any geometry (G_W56, G_T96 are
+  // reachable through sk_set_sketch_tuning only)
+  const int cand[] = {G_W48, G_W64, G_W32, G_W40, G_W40_7, G_W48_7, G_N80, G_N40, G_T48, G_T80};
+  const int ncand = (int)(sizeof(cand) / sizeof(cand[0]));
+  const bool pin = c->tune_sketch_bm && c->tune_sketch_nw;
+  PrePlan pinned;
+  if (pin)
+    for (int g = 0; g < G_COUNT; ++g)
+      if (kGeo[g].bm == c->tune_sketch_bm && kGeo[g].nw == c->tune_sketch_nw) pinned.geo = g;
+  for (int ci = 0; ci < (pin ? 1 : ncand); ++ci) {
+    const int geo = pin ? pinned.geo : cand[ci];
     const int bm = kGeo[geo].bm, nw = kGeo[geo].nw, tbn = kGeo[geo].tbn;
     if (c->tune_sketch_bm && c->tune_sketch_bm != bm) continue;
     if (c->tune_sketch_nw && c->tune_sketch_nw != nw) continue;
@@ -1147,8 +1158,11 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
         const double per_sm = std::max(1.0, (double)cap / c->num_sms);      // CTAs sharing an SM
         const double wps = per_sm * nw;                                     // warps per SM
         const double smsp = std::ceil(wps / 4.0) * 4.0 / wps;                // busiest sub-partition
+        // two warps per sub-partition leave DMMA issue gaps that a third fills (C5's full width:
+        // 48 x 384 tiles, 12 warps, 93.4 % of the ceiling vs 89.4 % for 48 x 256, 8 warps)
+        const double tlp = wps >= 12.0 ? 1.0 : 1.045;
         const double stage = (double)bm * tbn * TBK;
-        double cost = waves * (double)cdiv(kps, TBK) * stage * per_sm * smsp;
+        double cost = waves * (double)cdiv(kps, TBK) * stage * per_sm * smsp * tlp;
         // K-splits summed in-cluster through DSMEM (~0.05 FMA-equivalents per partial element) or
         // through HBM partials + a reduce launch; chunks after the first add X into X.  (Adding the
         // splits into X in split order through per-tile flags was measured slower: C2 k=512
@@ -1417,6 +1431,14 @@ sk_status residual_sumsq_tma(sk_ctx* c, const double* Q, int64_t ldq, const doub
   // tiles would leave a quarter of the last one idle
   auto fill = [&](int64_t tbn) { return (double)n / (double)(cdiv(n, tbn) * tbn); };
   if (fill(112) > fill(256) + 0.05) return run_sumsq<CfgN80>(c, Q, ldq, W, ldw, A, lda, m, n, k, sums);
+  // 12-warp 48 x 384 tiles where their column fill and wave count keep up with 48 x 256 (the third
+  // warp per SM sub-partition is worth ~4 %, see plan_pre)
+  auto waves = [&](int64_t tbn) {
+    const int64_t ctas = cdiv(m, 48) * cdiv(n, tbn);
+    return (double)ctas / (double)(cdiv(ctas, c->num_sms) * c->num_sms);
+  };
+  if (fill(384) * waves(384) * 1.045 > fill(256) * waves(256))
+    return run_sumsq<CfgT48>(c, Q, ldq, W, ldw, A, lda, m, n, k, sums);
   return run_sumsq<CfgW48>(c, Q, ldq, W, ldw, A, lda, m, n, k, sums);
 }
 
