@@ -1145,7 +1145,6 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
       if (splits > 1 && ch / splits < 512 && !c->tune_sketch_splits) break;
       const int64_t kps = cdiv(cdiv(ch, splits), TBK) * TBK;
       const int64_t sp = cdiv(ch, kps);
-      const int64_t ctas = mb * nb * sp;
       for (int clus = 0; clus < 2; ++clus) {
         if (clus && !(sp > 1 && sp <= 8 && bm % sp == 0)) continue;
         // several CTAs per SM: the in-cluster reduction measured far slower (C4 k=200 N80: 41 % vs
@@ -1154,7 +1153,6 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
         if ((c->tune_sketch_path == 2 && clus) || (c->tune_sketch_path == 3 && !clus && sp > 1)) continue;
         const int cap = pre_capacity(geo, clus ? (int)sp : 1);   // clusters of 4/8 strand SMs per GPC
         if (cap <= 0) continue;
-        const double waves = (double)cdiv(ctas, cap);
         const double per_sm = std::max(1.0, (double)cap / c->num_sms);      // CTAs sharing an SM
         const double wps = per_sm * nw;                                     // warps per SM
         const double smsp = std::ceil(wps / 4.0) * 4.0 / wps;                // busiest sub-partition
@@ -1162,13 +1160,22 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
         // 48 x 384 tiles, 12 warps, 93.4 % of the ceiling vs 89.4 % for 48 x 256, 8 warps)
         const double tlp = wps >= 12.0 ? 1.0 : 1.045;
         const double stage = (double)bm * tbn * TBK;
-        double cost = waves * (double)cdiv(kps, TBK) * stage * per_sm * smsp * tlp;
-        // K-splits summed in-cluster through DSMEM (~0.05 FMA-equivalents per partial element) or
-        // through HBM partials + a reduce launch; chunks after the first add X into X.  (Adding the
-        // splits into X in split order through per-tile flags was measured slower: C2 k=512
-        // 0.594 -> 0.688 ms, k=16 0.06 -> 0.16 ms -- the splits of a tile then serialise.)
-        if (sp > 1) cost += clus ? 0.05 * (double)sp * l * n : 0.3 * (double)sp * l * n + 3.6e5;
-        cost = cost * nch + (nch - 1) * (0.3 * (double)l * n + 3.6e5);
+        // one chunk of `rows` rows of A: whole waves x the per-CTA k tiles, + the split-K overhead:
+        // summed in-cluster through DSMEM (~0.05 FMA-equivalents per partial element) or through HBM
+        // partials + a reduce launch.  (Adding the splits into X in split order through per-tile flags
+        // was measured slower: C2 k=512 0.594 -> 0.688 ms, k=16 0.06 -> 0.16 ms -- the splits of a tile
+        // then serialise.)  The ragged last chunk is costed at its own height.
+        auto chunk_cost = [&](int64_t rows) {
+          const int64_t kr = cdiv(cdiv(rows, splits), TBK) * TBK;
+          const int64_t spr = cdiv(rows, kr);
+          const double waves = (double)cdiv(mb * nb * spr, cap);
+          double cc = waves * (double)cdiv(kr, TBK) * stage * per_sm * smsp * tlp;
+          if (spr > 1) cc += clus ? 0.05 * (double)spr * l * n : 0.3 * (double)spr * l * n + 3.6e5;
+          return cc;
+        };
+        // chunks after the first add X into X
+        double cost = (nch - 1) * chunk_cost(ch) + chunk_cost(m - (nch - 1) * ch) +
+                      (nch - 1) * (0.3 * (double)l * n + 3.6e5);
         if (cost < 0.99 * best.cost) {
           best.geo = geo; best.bm = bm; best.nw = nw; best.splits = (int)sp; best.cluster = clus != 0;
           best.cost = cost; best.chunk = ch;
