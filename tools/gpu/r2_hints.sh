@@ -1,14 +1,14 @@
 #!/bin/bash
-# A/B: L2 cache hints on the sketch GEMM's TMA loads (A evict_first, Omega slot evict_last)
+# A/B of the sketch GEMM's L2 hints at C5 width with 12-warp tiles: time and DRAM bytes per chunk GEMM
 mkdir -p gpurun_out
-cp paper_2104_05877_b200/libskel.so /tmp/libskel_cur.so
-for v in nohints hints; do
-  cp tools/ab/libskel_$v.so paper_2104_05877_b200/libskel.so
-  echo "== $v" >> gpurun_out/r2g_ab.log
-  timeout 300 python tools/bench_sketch.py --only "C" >> gpurun_out/r2g_ab.log 2>&1
-  CMD="python tools/bench_sketch.py --only C5 --reps 1"
-  timeout 300 $CMD > gpurun_out/r2g_plain_$v.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_sketch_pre|k_omega_image" -c 8 --csv --log-file gpurun_out/r2g_dram_$v.csv $CMD > gpurun_out/r2g_ncu_$v.log 2>&1
+cp paper_2104_05877_b200/libskel.so /tmp/libskel_orig.so
+for v in anorm hints1; do
+  cp ab/libskel_$v.so paper_2104_05877_b200/libskel.so
+  echo "== $v" >> gpurun_out/hints_ab.txt
+  timeout 300 python tools/bench_sketch.py --only "C5 rows" --reps 5 >> gpurun_out/hints_ab.txt 2>&1
+  timeout 300 python tools/bench_sketch.py --only "C5 block" --reps 3 >> gpurun_out/hints_ab.txt 2>&1
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:k_sketch_pre -s 2 -c 1 --csv \
+      python tools/bench_sketch.py --only "C5 rows" --reps 1 2>/dev/null | grep -E 'dram__|gpu__time' >> gpurun_out/hints_ab.txt
 done
-cp /tmp/libskel_cur.so paper_2104_05877_b200/libskel.so
+cp /tmp/libskel_orig.so paper_2104_05877_b200/libskel.so
 echo done

@@ -17,6 +17,8 @@ ap.add_argument("--n", type=int, default=65536)
 ap.add_argument("--k", type=int, default=1000)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--profile", action="store_true")
+ap.add_argument("--noise", type=float, default=1e-9, help="perturbation size (0: exact rank k)")
+ap.add_argument("--tune", default="", help="path,bm,splits,chunk[,warps] for sk_set_sketch_tuning")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(5)
@@ -25,7 +27,11 @@ Cf = torch.randn(a.k, a.n, dtype=torch.float64, device=dev, generator=g)
 Cf *= torch.arange(1, a.k + 1, dtype=torch.float64, device=dev).pow(-1.5)[:, None]
 A = sk.fortran(B @ Cf)
 del B, Cf
-A.add_(torch.randn(A.shape, dtype=torch.float64, device=dev, generator=g).t().contiguous().t(), alpha=1e-9)
+if a.noise > 0:
+    A.add_(torch.randn(A.shape, dtype=torch.float64, device=dev, generator=g).t().contiguous().t(), alpha=a.noise)
+if a.tune:
+    t = [int(x) for x in a.tune.split(",")]
+    sk.set_sketch_tuning(*t[:4], warps=t[4] if len(t) > 4 else 0)
 Js = torch.arange(a.k, dtype=torch.int64, device=dev)
 r, nA = sk.residual(A, Js, None, "col_id")
 torch.cuda.synchronize()
