@@ -524,7 +524,8 @@ def main():
     tf = os.path.join(ROOT, "profiles", "round2", "sketch_dram_bytes.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(f"{args.config}_k{k}")
+            # measured for the one-pass sketch only (tools/sketch_traffic.py); power iterations differ
+            traffic = None if args.piter else json.load(open(tf)).get(f"{args.config}_k{k}")
         except Exception:
             traffic = None
     if emb == "sparse_sign":
