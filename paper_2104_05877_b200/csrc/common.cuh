@@ -149,6 +149,8 @@ struct Cand {
 // PDL: block until the preceding grid in the stream has completed and its memory is visible (a
 // no-op when the launch was not programmatic).
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// PDL: let the next grid in the stream be scheduled (once every CTA of this grid has called it or exited)
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ Cand cand_none() { return Cand{-1.0, -1.0, 0x7fffffffffffffffLL}; }
 

@@ -54,6 +54,20 @@ struct DenseParams {
   // (sum E^2, sum Csub^2) into sums_part[2 * linear block]
   const double* Csub; int64_t ldcs;
   double* sums_part;
+  // chained K-chunks (run_pre_chained): each CTA adds 1 here when its tile is in X (release); the
+  // image kernel of the chunk that next overwrites this chunk's slot waits for the count
+  unsigned* done;
+  const unsigned* ready;  // chained chunks: generator CTAs done so far in this chunk's slot ...
+  unsigned ready_need;    // ... must reach this before the GEMM reads the slot
+  // chained chunks: CTAs [gen_lo, gen_lo + gen_n) of this GEMM also make the NEXT chunk's image (rows
+  // [gen_i0, gen_i1) of A, gen_kt k tiles) in gen_img, once gen_gate reaches gen_need (the GEMM that
+  // last read that slot is done), then count themselves in gen_ready
+  double* gen_img;
+  const double* gen_q; int64_t gen_ldq;       // packed from Q (Omega = Q^T) when non-null, else Philox
+  int64_t gen_i0, gen_i1, gen_kt;
+  unsigned gen_lo, gen_n;
+  const unsigned* gen_gate; unsigned gen_need;
+  unsigned* gen_ready;
 };
 
 template <bool VEC>
@@ -300,6 +314,34 @@ __device__ __forceinline__ void omega_tile(uint2 key, int l, int64_t i0, int64_t
   }
 }
 
+// Chained K-chunks: the image kernel of chunk c overwrites the slot chunk c - 2's GEMM read, so it
+// first waits (thread 0, bounded) until that GEMM's CTAs have all counted themselves done, then lets
+// the chunk's GEMM be scheduled (the GEMM's griddepcontrol.wait still waits for this image).
+__device__ __forceinline__ void wait_count(const unsigned* gate, unsigned need) {
+  if (gate) {
+    if (threadIdx.x == 0) {
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gate) : "memory");
+        if (v >= need) break;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20ull * 1000 * 1000 * 1000) __trap();   // 20 s: a scheduling bug, not a hang
+        __nanosleep(256);
+      }
+    }
+    __syncthreads();
+  }
+}
+__device__ __forceinline__ void count_done(unsigned* ctr) {
+  if (ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+  }
+}
+
 // One CTA per image block: blockIdx.x = rt * KT + kt.
 __global__ void __launch_bounds__(128) k_omega_image(uint2 key, int l, int64_t i0, int64_t m, int BM, int OS, int64_t KT,
                                                      double* __restrict__ img) {
@@ -309,17 +351,20 @@ __global__ void __launch_bounds__(128) k_omega_image(uint2 key, int l, int64_t i
 // The same image from a GIVEN Omega: Omega(r, i) = Q(i, r), Q m x l column-major (ld ldq), e.g. an
 // orthonormal basis for W = Q^T A in the residual.  One CTA per image block; thread -> (kk, r) with
 // kk fastest, so a warp reads 128-byte column segments of Q.
-__global__ void __launch_bounds__(128) k_omega_pack(const double* __restrict__ Q, int64_t ldq, int l, int64_t i0, int64_t m,
-                                                    int BM, int OS, int64_t KT, double* __restrict__ img) {
-  const int64_t tile = blockIdx.x;
+__device__ __forceinline__ void pack_tile(const double* __restrict__ Q, int64_t ldq, int l, int64_t i0, int64_t m, int BM,
+                                          int OS, int64_t KT, int64_t tile, double* __restrict__ img, int tid, int nthr) {
   const int64_t rt = tile / KT, kt = tile - (tile / KT) * KT;
   double* blk = img + tile * (int64_t)(TBK * OS);
-  for (int e = threadIdx.x; e < TBK * OS; e += 128) {
+  for (int e = tid; e < TBK * OS; e += nthr) {
     const int kk = e % TBK, r = e / TBK;
     const int64_t i = i0 + kt * TBK + kk;
     const int64_t row = rt * BM + r;
     blk[kk * OS + r] = (r < BM && row < l && i < m) ? Q[i + row * ldq] : 0.0;
   }
+}
+__global__ void __launch_bounds__(128) k_omega_pack(const double* __restrict__ Q, int64_t ldq, int l, int64_t i0, int64_t m,
+                                                    int BM, int OS, int64_t KT, double* __restrict__ img) {
+  pack_tile(Q, ldq, l, i0, m, BM, OS, KT, blockIdx.x, img, threadIdx.x, 128);
 }
 
 // The image of a GIVEN row operand Q (M x K, column-major, ld ldq) for the GEMM E = C - Q B: block
@@ -359,7 +404,26 @@ template <class C, int MODE>
 __global__ void __launch_bounds__(C::NT, C::CPS) k_sketch_pre(const __grid_constant__ CUtensorMap tmA, DenseParams p,
                                                                const double* __restrict__ img, int64_t KT) {
   constexpr int TS = C::TS, BM = C::BM, NW = C::NW, FI = C::FI, FJ = C::FJ;
-  dev::griddep_wait();                                   // PDL: the Omega image is complete
+  if (MODE == 0 && p.done) {
+    // chained chunks: this chunk's image was made by generator CTAs of the previous GEMM -- wait for
+    // them, not for that whole GEMM (whose last wave this grid's CTAs fill); let the next GEMM be
+    // scheduled; generator CTAs then make the next chunk's image before their own tile
+    if (p.ready) wait_count(p.ready, p.ready_need);
+    else dev::griddep_wait();                            // chunk 0: its image is the preceding kernel
+    dev::griddep_launch();
+    const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (p.gen_img && lin - p.gen_lo < p.gen_n) {
+      wait_count(p.gen_gate, p.gen_need);
+      const int64_t tiles = (int64_t)((p.l + BM - 1) / BM) * p.gen_kt;
+      for (int64_t t = lin - p.gen_lo; t < tiles; t += p.gen_n) {
+        if (p.gen_q) pack_tile(p.gen_q, p.gen_ldq, p.l, p.gen_i0, p.gen_i1, BM, C::OS, p.gen_kt, t, p.gen_img, threadIdx.x, C::NT);
+        else omega_tile(p.key, p.l, p.gen_i0, p.gen_i1, BM, C::OS, p.gen_kt, t, p.gen_img, threadIdx.x, C::NT);
+      }
+      count_done(p.gen_ready);
+    }
+  } else {
+    dev::griddep_wait();                                 // PDL: the Omega image is complete
+  }
   extern __shared__ __align__(1024) unsigned char psm_raw[];
   unsigned char* base = psm_raw + ((1024u - (dev::smem_addr(psm_raw) & 1023u)) & 1023u);
   const unsigned base_u = dev::smem_addr(base);
@@ -531,7 +595,7 @@ __global__ void __launch_bounds__(C::NT, C::CPS) k_sketch_pre(const __grid_const
     dev::cluster_wait();
     return;
   }
-  if (!active) return;
+  if (active) {
 #pragma unroll
   for (int i = 0; i < FI; ++i) {
     const int r = rt * BM + wr + i * 8 + g;
@@ -557,6 +621,11 @@ __global__ void __launch_bounds__(C::NT, C::CPS) k_sketch_pre(const __grid_const
         }
       }
     }
+  }
+  }
+  if (MODE == 0 && p.done) {                              // chained chunks: this tile is in X
+    __syncthreads();
+    if (tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.done) : "memory");
   }
 }
 
@@ -1219,12 +1288,40 @@ sk_status make_tmap(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t ld
 // The Omega image of rows [i0, i1) of A (from Philox, or packed from Q when Qom != nullptr).
 template <class C>
 sk_status omega_chunk_image(sk_ctx* c, uint2 key, const double* Qom, int64_t ldq, int64_t l, int64_t i0, int64_t i1,
-                            double* img) {
+                            double* img, bool pdl = false) {
   constexpr int BM = C::BM;
   const int64_t mb = cdiv(l, BM), KT = cdiv(i1 - i0, TBK);
-  if (Qom) k_omega_pack<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(Qom, ldq, (int)l, i0, i1, BM, C::OS, KT, img);
-  else k_omega_image<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(key, (int)l, i0, i1, BM, C::OS, KT, img);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)(mb * KT));
+  lc.blockDim = dim3(128);
+  lc.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // chained chunks: beside the GEMM's tail
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at; lc.numAttrs = pdl ? 1 : 0;
+  if (Qom) SK_CUDA(c, cudaLaunchKernelEx(&lc, k_omega_pack, Qom, ldq, (int)l, i0, i1, BM, C::OS, KT, img));
+  else SK_CUDA(c, cudaLaunchKernelEx(&lc, k_omega_image, key, (int)l, i0, i1, BM, C::OS, KT, img));
   return launched(c);
+}
+
+// Waits (one thread, bounded) until both slot counters reach their totals: every CTA of every chained
+// chunk GEMM has added its tile into X.  Launched normally after the chain, it restores plain stream
+// order for what follows (the chain's image kernels do not wait for their predecessors).
+__global__ void k_chain_join(const unsigned* done, unsigned need0, unsigned need1) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int s = 0; s < 2; ++s) {
+    const unsigned need = s ? need1 : need0;
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + s) : "memory");
+      if (v >= need) break;
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20ull * 1000 * 1000 * 1000) __trap();
+      __nanosleep(256);
+    }
+  }
 }
 
 // One K-chunk's GEMM: X (+)= Omega(:, p.k0:p.m) A(p.k0:p.m, :) with the chunk's image, K-split
@@ -1296,6 +1393,52 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
     p.m = m;
     p.accum = 0;
     return pre_gemm_chunk<C>(c, tm, p, l, n, pl.splits, cl, img.as<double>(), part.as<double>());
+  }
+  // Several chunks in one K range each (no split): the chunk GEMMs form ONE programmatic chain on the
+  // context stream, each letting its successor be scheduled once all its CTAs are resident, so the
+  // next chunk's CTAs take the SMs the last wave frees (no idle tail per chunk).  The next chunk's Omega
+  // image is made inside the current GEMM by kGenCtas CTAs starting kGenAt CTAs into the grid (well
+  // past the previous GEMM's tail); device counters carry the ordering the chain cannot: a GEMM waits
+  // for its image's generator CTAs (ready), generators wait for the GEMM that last read their slot
+  // (done) before overwriting it, k_chain_join waits for every GEMM CTA.  X is zeroed and every chunk
+  // adds (red.add) its product.
+  if (nch >= 3 && sp_max == 1 && sp_last == 1 && c->tune_sketch_path != 2 && c->tune_sketch_path != 3) {
+    DBuf img2, cnt;
+    SK_TRY(img2.alloc(c, img.bytes));
+    SK_TRY(cnt.alloc(c, 4 * sizeof(unsigned)));
+    SK_CUDA(c, cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned), c->stream));
+    SK_CUDA(c, cudaMemset2DAsync(p.X, p.ldx * sizeof(double), 0, n * sizeof(double), l, c->stream));
+    double* slot[2] = {img.as<double>(), img2.as<double>()};
+    unsigned* done = cnt.as<unsigned>();
+    unsigned* ready = done + 2;
+    const unsigned ctas = (unsigned)(cdiv(l, BM) * cdiv(n, C::TBNP));
+    const unsigned gen_n = std::min<unsigned>(ctas / 2, (unsigned)c->num_sms);
+    const unsigned gen_lo = std::min<unsigned>(ctas - gen_n, 3u * (unsigned)c->num_sms);
+    SK_TRY((omega_chunk_image<C>(c, p.key, Qom, ldq, l, 0, std::min(m, chunk), slot[0])));   // chunk 0's image
+    for (int64_t ci = 0; ci < nch; ++ci) {
+      const int64_t i0 = ci * chunk, i1 = std::min(m, i0 + chunk);
+      const int s = (int)(ci & 1);
+      DenseParams q = p;
+      q.k0 = i0;
+      q.m = i1;
+      q.accum = 1;
+      q.done = done + s;
+      q.ready = ci >= 1 ? ready + s : nullptr;              // chunk 0's image: a plain kernel before
+      q.ready_need = (unsigned)((ci + 1) / 2) * gen_n;      // generator CTAs of the chunks ci-1, ci-3, ...
+      if (ci + 1 < nch) {
+        const int64_t j0 = i1, j1 = std::min(m, j0 + chunk);
+        q.gen_img = slot[s ^ 1];
+        q.gen_q = Qom; q.gen_ldq = ldq;
+        q.gen_i0 = j0; q.gen_i1 = j1; q.gen_kt = cdiv(j1 - j0, TBK);
+        q.gen_lo = gen_lo; q.gen_n = gen_n;
+        q.gen_gate = ci >= 1 ? done + (s ^ 1) : nullptr;    // chunk ci-1's GEMM read slot s^1
+        q.gen_need = (unsigned)((ci + 1) / 2) * ctas;       // GEMMs ci-1, ci-3, ... used slot s^1
+        q.gen_ready = ready + (s ^ 1);
+      }
+      SK_TRY(pre_gemm_chunk<C>(c, tm, q, l, n, 1, false, slot[s], nullptr));
+    }
+    k_chain_join<<<1, 32, 0, c->stream>>>(done, (unsigned)((nch + 1) / 2) * ctas, (unsigned)(nch / 2) * ctas);
+    return launched(c);
   }
   // Several chunks: two image slots; the image of chunk c + 1 is generated on the image stream while
   // the GEMM of chunk c runs (its small CTAs fit beside a GEMM CTA on an SM), into the slot the GEMM of

@@ -546,6 +546,7 @@ def test_rand_lupp_host_pipelined(emb):
     (0, 40, 1, 0, 2), (3, 40, 4, 320, 2), (2, 40, 2, 0, 2),             # or 2 warps of 40 x 56 (16-column boxes)
     (0, 80, 1, 0, 12), (2, 80, 3, 256, 12), (0, 48, 1, 0, 12),          # 12 warps: 80 x 192 (2 x 6), 48 x 384
     (0, 96, 1, 0, 8), (3, 96, 2, 0, 8),                                 # 96 x 128 (2 x 4 warps of 48 x 32)
+    (0, 48, 1, 128, 12), (0, 80, 1, 96, 4), (0, 40, 1, 112, 7),         # >= 3 chunks, one K range: the chained path
     (1, 0, 0, 0),                                                       # shared-memory generation fallback
 ])
 def test_sketch_dense_plans(plan):

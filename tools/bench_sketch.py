@@ -24,6 +24,7 @@ SHAPES = [  # (name, m, n, l, embedding)
     ("C4 k=200", 65536, 784, 400, "gaussian"),
     ("C5 block", 131072, 8192, 1100, "gaussian"),
     ("C5 rows", 16384, 65536, 1100, "gaussian"),     # two of C5's 16 K-chunks at its full width (the N = 1 tile grid)
+    ("C5 half", 65536, 65536, 1100, "gaussian"),     # eight of C5's 16 K-chunks at its full width
     ("C3 sparse", 16384, 16384, 510, "sparse_sign"),
     ("C2 srtt k=512", 4096, 4096, 522, "srtt"),
     ("C3 srtt", 16384, 16384, 510, "srtt"),
