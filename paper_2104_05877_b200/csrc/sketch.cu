@@ -1234,10 +1234,15 @@ PrePlan plan_pre(sk_ctx* c, int64_t m, int64_t n, int64_t l) {
         // partials + a reduce launch.  (Adding the splits into X in split order through per-tile flags
         // was measured slower: C2 k=512 0.594 -> 0.688 ms, k=16 0.06 -> 0.16 ms -- the splits of a tile
         // then serialise.)  The ragged last chunk is costed at its own height.
+        // Chained chunks (>= 3 chunks in one K range each, run_pre) fill each chunk's last wave with the
+        // next chunk's CTAs: their waves count fractionally -- when a chunk has at least one full wave
+        // (a grid smaller than the GPU leaves it idle however the chunks overlap: C4 k=200 at one split
+        // per chunk, 35 CTAs, measured 8.0 ms vs 1.47 ms with 8 splits)
+        const bool chained = nch >= 3 && sp == 1 && !clus && mb * nb >= cap;
         auto chunk_cost = [&](int64_t rows) {
           const int64_t kr = cdiv(cdiv(rows, splits), TBK) * TBK;
           const int64_t spr = cdiv(rows, kr);
-          const double waves = (double)cdiv(mb * nb * spr, cap);
+          const double waves = chained ? (double)(mb * nb * spr) / cap : (double)cdiv(mb * nb * spr, cap);
           double cc = waves * (double)cdiv(kr, TBK) * stage * per_sm * smsp * tlp;
           if (spr > 1) cc += clus ? 0.05 * (double)spr * l * n : 0.3 * (double)spr * l * n + 3.6e5;
           return cc;
