@@ -1003,6 +1003,25 @@ sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64
     SK_TRY(gram_lower(c, Q, m, k, ldq, G.as<double>(), k));
     SK_TRY(potrf_cluster(c, G.as<double>(), k, k, Wd.as<double>(), kp, status_dev));
     SK_TRY(trsm_rows(c, Q, m, k, ldq, G.as<double>(), k, Wd.as<double>(), kp));
+    return cholqr_tail(c, Q, m, k, ldq, status_dev);
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
+    SK_TRY(potrf_lower(c, G.as<double>(), k, k, status_dev));
+    SK_TRY(trsm_right_lt(c, Q, m, k, ldq, G.as<double>(), k));
+  }
+  return SK_OK;
+}
+
+// The second CholeskyQR pass (k <= kCholMaxK): Gram, then one Newton-Schulz step when the pass before
+// left |Q^T Q - I| <= 1e-10, else a Cholesky pass.
+sk_status cholqr_tail(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64_t* status_dev) {
+  DBuf G;
+  SK_TRY(G.alloc(c, (size_t)k * k * sizeof(double)));
+  {
+    const int64_t kp = cdiv(k, CB) * CB;
+    DBuf Wd;
+    SK_TRY(Wd.alloc(c, (size_t)kp * CB * sizeof(double)));
     // second pass: after the first, Q^T Q = I + E with |E| ~ u cond(Q_0)^2.  When |E| <= 1e-10 one
     // Newton-Schulz step Q <- Q (3 I - Q^T Q) / 2 leaves |E|^2 (below u: the orthogonality CholeskyQR2
     // reaches) with two GEMMs and no sequential chain, and moves Q from the thin-QR factor by at most
@@ -1031,12 +1050,72 @@ sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64
     SK_TRY(potrf_cluster(c, G.as<double>(), k, k, Wd.as<double>(), kp, status_dev));
     return trsm_rows(c, Q, m, k, ldq, G.as<double>(), k, Wd.as<double>(), kp);
   }
-  for (int pass = 0; pass < 2; ++pass) {
-    SK_TRY(gemm(c, true, false, k, k, m, 1.0, Q, ldq, Q, ldq, 0.0, G.as<double>(), k));
-    SK_TRY(potrf_lower(c, G.as<double>(), k, k, status_dev));
-    SK_TRY(trsm_right_lt(c, Q, m, k, ldq, G.as<double>(), k));
+}
+
+// max L(i, i) / min L(i, i) of a Cholesky factor (a lower bound on its condition number) into out[0],
+// +inf when the factorisation reported a breakdown (status != 0); one CTA
+__global__ void k_diag_ratio(const double* L, int64_t k, int64_t ld, const int64_t* status, double* out) {
+  __shared__ double smx[32], smn[32];
+  double mx = 0.0, mn = INFINITY;
+  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+    const double d = fabs(L[i + i * ld]);
+    mx = fmax(mx, d);
+    mn = fmin(mn, d);
   }
-  return SK_OK;
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if ((threadIdx.x & 31) == 0) { smx[threadIdx.x >> 5] = mx; smn[threadIdx.x >> 5] = mn; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { mx = fmax(mx, smx[w]); mn = fmin(mn, smn[w]); }
+    out[0] = (*status != 0 || !(mn > 0.0)) ? INFINITY : mx / mn;
+  }
+}
+
+// The first pass of the residual's orthonormal basis (k <= kCholMaxK) with the shift only where it is
+// needed: G = Q^T Q is factored twice AT ONCE -- unshifted on the context stream, shifted (shifted
+// CholeskyQR3's s = 11 (m k + k (k + 1)) u tr G) on the helper stream, each one 16-CTA cluster -- and
+// the unshifted factor is used when it exists and max L_ii / min L_ii <= 1e3 (cond(Q) about that, so
+// the next Gram shows |Q^T Q - I| ~ cond^2 u <= 1e-10 and one Newton-Schulz step finishes: two passes
+// instead of three; C3 and C4 have cond(C) ~ 5e2, C2 1.6e11).  Then the CholeskyQR tail.
+sk_status cholqr_adaptive(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64_t* status_dev) {
+  const int64_t kp = cdiv(k, CB) * CB;
+  DBuf G, Gs, Wu, Ws, su, rb;
+  SK_TRY(G.alloc(c, (size_t)k * k * sizeof(double)));
+  SK_TRY(Gs.alloc(c, (size_t)k * k * sizeof(double)));
+  SK_TRY(Wu.alloc(c, (size_t)kp * CB * sizeof(double)));
+  SK_TRY(Ws.alloc(c, (size_t)kp * CB * sizeof(double)));
+  SK_TRY(su.alloc(c, sizeof(int64_t)));
+  SK_TRY(rb.alloc(c, sizeof(double)));
+  SK_TRY(gram_lower(c, Q, m, k, ldq, G.as<double>(), k));
+  SK_CUDA(c, cudaMemcpyAsync(Gs.p, G.p, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  SK_CUDA(c, cudaMemsetAsync(su.p, 0, sizeof(int64_t), c->stream));
+  SK_TRY(add_shift(c, Gs.as<double>(), k, k, m));
+  SK_TRY(ensure_aux(c));
+  SK_CUDA(c, cudaEventRecord(c->ev_a, c->stream));
+  SK_CUDA(c, cudaStreamWaitEvent(c->aux, c->ev_a, 0));
+  cudaStream_t main_stream = c->stream;
+  c->stream = c->aux;
+  const sk_status ss = potrf_cluster(c, Gs.as<double>(), k, k, Ws.as<double>(), kp, status_dev);
+  c->stream = main_stream;
+  SK_TRY(ss);
+  SK_CUDA(c, cudaEventRecord(c->ev_b, c->aux));
+  SK_TRY(potrf_cluster(c, G.as<double>(), k, k, Wu.as<double>(), kp, su.as<int64_t>()));
+  k_diag_ratio<<<1, 256, 0, c->stream>>>(G.as<double>(), k, k, su.as<int64_t>(), rb.as<double>());
+  SK_TRY(launched(c));
+  SK_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_b, 0));
+  double ratio = INFINITY;
+  SK_CUDA(c, cudaMemcpyAsync(&ratio, rb.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  SK_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (ratio <= 1e3) {
+    SK_CUDA(c, cudaMemsetAsync(status_dev, 0, sizeof(int64_t), c->stream));   // the shifted run is not used
+    SK_TRY(trsm_rows(c, Q, m, k, ldq, G.as<double>(), k, Wu.as<double>(), kp));
+    return cholqr_tail(c, Q, m, k, ldq, status_dev);
+  }
+  SK_TRY(trsm_rows(c, Q, m, k, ldq, Gs.as<double>(), k, Ws.as<double>(), kp));
+  return cholqr2(c, Q, m, k, ldq, status_dev);
 }
 
 sk_status lambda_max(sk_ctx* c, const double* G, int64_t k, int64_t ld, double* out_dev) {

@@ -131,6 +131,10 @@ sk_status pinv_apply(sk_ctx* c, const double* B1, int64_t ldb, int64_t p, int64_
                      int64_t N, double* out, int64_t ldo, int64_t* status_dev);
 // Q (m x k, ldq) := orthonormal basis of range(Q) by two Cholesky-QR passes.
 sk_status cholqr2(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64_t* status_dev);
+// the CholeskyQR tail (Gram, then Newton-Schulz when |Q^T Q - I| <= 1e-10, else a Cholesky pass), and the
+// basis's first pass with the shift only where needed (both for k <= 1024; dense.cu)
+sk_status cholqr_tail(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64_t* status_dev);
+sk_status cholqr_adaptive(sk_ctx* c, double* Q, int64_t m, int64_t k, int64_t ldq, int64_t* status_dev);
 // out[0] = sum of in[0..n) pairs etc: finishes per-CTA partial sums deterministically.
 sk_status reduce_pairs(sk_ctx* c, const double* partial, int64_t count, double* out);
 // largest eigenvalue of the SPD k x k matrix G by power iteration (device result).

@@ -39,6 +39,7 @@ sk_status add_shift(sk_ctx* c, double* G, int64_t k, int64_t ld, int64_t rows) {
 static sk_status basis_shifted_cholqr3(sk_ctx* c, const double* C, int64_t rows, int64_t k, double* Q,
                                        int64_t* status_dev) {
   SK_CUDA(c, cudaMemcpyAsync(Q, C, (size_t)rows * k * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (k <= 1024) return cholqr_adaptive(c, Q, rows, k, rows, status_dev);   // the shift only where needed
   DBuf G;
   SK_TRY(G.alloc(c, (size_t)k * k * sizeof(double)));
   SK_TRY(gram_lower(c, Q, rows, k, rows, G.as<double>(), k));
