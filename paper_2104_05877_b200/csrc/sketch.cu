@@ -68,6 +68,9 @@ struct DenseParams {
   unsigned gen_lo, gen_n;
   const unsigned* gen_gate; unsigned gen_need;
   unsigned* gen_ready;
+  // chained chunks: tile_ord[tile] = chunks already added into X's tile; chunk chunk_idx adds after it
+  // reaches chunk_idx, so every element of X sums its chunks in chunk order (deterministic)
+  unsigned* tile_ord; unsigned chunk_idx;
 };
 
 template <bool VEC>
@@ -595,6 +598,10 @@ __global__ void __launch_bounds__(C::NT, C::CPS) k_sketch_pre(const __grid_const
     dev::cluster_wait();
     return;
   }
+  if (MODE == 0 && p.tile_ord) {                        // chained chunks: the previous chunk's adds first
+    const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    wait_count(p.tile_ord + lin, p.chunk_idx);
+  }
   if (active) {
 #pragma unroll
   for (int i = 0; i < FI; ++i) {
@@ -625,7 +632,13 @@ __global__ void __launch_bounds__(C::NT, C::CPS) k_sketch_pre(const __grid_const
   }
   if (MODE == 0 && p.done) {                              // chained chunks: this tile is in X
     __syncthreads();
-    if (tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.done) : "memory");
+    if (tid == 0) {
+      if (p.tile_ord) {
+        const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.tile_ord + lin) : "memory");
+      }
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.done) : "memory");
+    }
   }
 }
 
@@ -1411,16 +1424,18 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   // for its image's generator CTAs (ready), generators wait for the GEMM that last read their slot
   // (done) before overwriting it, k_chain_join waits for every GEMM CTA.  X is zeroed and every chunk
   // adds (red.add) its product.
-  if (nch >= 3 && sp_max == 1 && sp_last == 1 && c->tune_sketch_path != 2 && c->tune_sketch_path != 3) {
+  if (nch >= 3 && sp_max == 1 && sp_last == 1 && c->tune_sketch_path != 2 && c->tune_sketch_path != 3 &&
+      cdiv(l, BM) * cdiv(n, C::TBNP) >= c->num_sms) {          // at least a wave per chunk (and generators)
+    const unsigned ctas = (unsigned)(cdiv(l, BM) * cdiv(n, C::TBNP));
     DBuf img2, cnt;
     SK_TRY(img2.alloc(c, img.bytes));
-    SK_TRY(cnt.alloc(c, 4 * sizeof(unsigned)));
-    SK_CUDA(c, cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned), c->stream));
+    SK_TRY(cnt.alloc(c, (4 + (size_t)ctas) * sizeof(unsigned)));
+    SK_CUDA(c, cudaMemsetAsync(cnt.p, 0, (4 + (size_t)ctas) * sizeof(unsigned), c->stream));
     SK_CUDA(c, cudaMemset2DAsync(p.X, p.ldx * sizeof(double), 0, n * sizeof(double), l, c->stream));
     double* slot[2] = {img.as<double>(), img2.as<double>()};
     unsigned* done = cnt.as<unsigned>();
     unsigned* ready = done + 2;
-    const unsigned ctas = (unsigned)(cdiv(l, BM) * cdiv(n, C::TBNP));
+    unsigned* tile_ord = done + 4;
     const unsigned gen_n = std::min<unsigned>(ctas / 2, (unsigned)c->num_sms);
     const unsigned gen_lo = std::min<unsigned>(ctas - gen_n, 3u * (unsigned)c->num_sms);
     SK_TRY((omega_chunk_image<C>(c, p.key, Qom, ldq, l, 0, std::min(m, chunk), slot[0])));   // chunk 0's image
@@ -1432,6 +1447,8 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
       q.m = i1;
       q.accum = 1;
       q.done = done + s;
+      q.tile_ord = tile_ord;
+      q.chunk_idx = (unsigned)ci;
       q.ready = ci >= 1 ? ready + s : nullptr;              // chunk 0's image: a plain kernel before
       q.ready_need = (unsigned)((ci + 1) / 2) * gen_n;      // generator CTAs of the chunks ci-1, ci-3, ...
       if (ci + 1 < nch) {

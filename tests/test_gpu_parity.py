@@ -546,7 +546,7 @@ def test_rand_lupp_host_pipelined(emb):
     (0, 40, 1, 0, 2), (3, 40, 4, 320, 2), (2, 40, 2, 0, 2),             # or 2 warps of 40 x 56 (16-column boxes)
     (0, 80, 1, 0, 12), (2, 80, 3, 256, 12), (0, 48, 1, 0, 12),          # 12 warps: 80 x 192 (2 x 6), 48 x 384
     (0, 96, 1, 0, 8), (3, 96, 2, 0, 8),                                 # 96 x 128 (2 x 4 warps of 48 x 32)
-    (0, 48, 1, 128, 12), (0, 80, 1, 96, 4), (0, 40, 1, 112, 7),         # >= 3 chunks, one K range: the chained path
+    (0, 48, 1, 128, 12), (0, 80, 1, 96, 4), (0, 40, 1, 112, 7),         # >= 3 chunks, one K range, small grids
     (1, 0, 0, 0),                                                       # shared-memory generation fallback
 ])
 def test_sketch_dense_plans(plan):
@@ -562,6 +562,25 @@ def test_sketch_dense_plans(plan):
     finally:
         sk.set_sketch_tuning()
     assert rel_fro(X, o_sketch.sketch(A, l, "gaussian", 77)) <= 1e-12
+
+
+@pytest.mark.parametrize("plan,n", [((0, 32, 1, 256, 8), 4100), ((0, 48, 1, 256, 12), 8200), ((0, 48, 1, 160, 8), 6000)])
+def test_sketch_dense_chained(plan, n):
+    """The chained K-chunk path (>= 3 chunks of one K range, >= one wave of tiles per chunk): chunk
+    GEMMs linked by programmatic dependent launch, the next chunk's Omega image made by generator CTAs
+    inside the current GEMM, device counters for image readiness and slot reuse.  Ragged last chunk
+    and column tile; l spans several row tiles.  Repeated calls give the same X."""
+    m, l = 800, 300
+    A = rand_mat(m, n, 43)
+    Ad = dev_f(A)
+    sk.set_sketch_tuning(*plan[:4], warps=plan[4])
+    try:
+        X = sk.sketch(Ad, l, "gaussian", 79).cpu().numpy()
+        X2 = sk.sketch(Ad, l, "gaussian", 79).cpu().numpy()
+    finally:
+        sk.set_sketch_tuning()
+    assert rel_fro(X, o_sketch.sketch(A, l, "gaussian", 79)) <= 1e-12
+    np.testing.assert_array_equal(X, X2)
 
 
 @pytest.mark.parametrize("k,l", [(64, 74), (256, 266)])
