@@ -1,3 +1,5 @@
+"""C1 sketch timing alone and right after a residual call (checks that no helper-stream work leaks into
+the next sketch).  usage: python tools/probe_c1_sketch.py"""
 import sys, torch
 sys.path.insert(0, '.')
 import paper_2104_05877_b200 as sk
@@ -15,10 +17,7 @@ def t(f, n=20):
     return e0.elapsed_time(e1) / n
 print('sketch only', t(lambda: sk.sketch(Ad, 40, 'gaussian', 2001, out=X)))
 Js, Lf, _, _ = sk.select_cols(X, 20)
-def step():
-    sk.sketch(Ad, 40, 'gaussian', 2001, out=X)
-    sk.residual(Ad, Js, None, 'col_id')
-print('sketch after residual', t(lambda: (sk.residual(Ad, Js, None, 'col_id'), None)[1] or None, 5))
+print('residual (col ID)', t(lambda: sk.residual(Ad, Js, None, 'col_id'), 5))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 sk.residual(Ad, Js, None, 'col_id')
 e0.record(); sk.sketch(Ad, 40, 'gaussian', 2001, out=X); e1.record(); torch.cuda.synchronize()
