@@ -65,6 +65,8 @@ def parse():
                     help="N > 1: column-LUPP exchange -- one k x n all-gather then replicated LUPP, one "
                          "all-gather of P records per pivot step (CUDA graph), or the records stored into "
                          "the peers' mailboxes by the step kernel itself (NVLink peer memory, CUDA graph)")
+    ap.add_argument("--sketch-tuning", default="",
+                    help="path,bm,splits,chunk[,warps] for sk_set_sketch_tuning (A/B of the dense sketch's plans)")
     return ap.parse_args()
 
 
@@ -293,6 +295,12 @@ def run_reference(args):
     return 0
 
 
+def apply_sketch_tuning(args, sk, device):
+    if args.sketch_tuning:
+        t = [int(x) for x in args.sketch_tuning.split(",")]
+        sk.set_sketch_tuning(*t[:4], warps=t[4] if len(t) > 4 else 0, device=device)
+
+
 def main_dist(args, world, rank, local):
     """N > 1 GPUs (torchrun): the column-sharded path of SURVEY 8(e) on the same C5 matrix
     (strong scaling: rank r builds and holds only its contiguous block of A's 65536 columns, built
@@ -345,6 +353,7 @@ def main_dist(args, world, rank, local):
         return Js, r, nA
 
     with torch.cuda.stream(stream), sess:
+        apply_sketch_tuning(args, sk, local)                 # on the distributed context
         for _ in range(args.warmup):
             step(lambda e: None)
         torch.cuda.synchronize(dev)

@@ -1425,7 +1425,11 @@ sk_status run_pre(sk_ctx* c, const DenseParams& p0, int64_t m, int64_t n, int64_
   // (done) before overwriting it, k_chain_join waits for every GEMM CTA.  X is zeroed and every chunk
   // adds (red.add) its product.
   if (nch >= 3 && sp_max == 1 && sp_last == 1 && c->tune_sketch_path != 2 && c->tune_sketch_path != 3 &&
-      cdiv(l, BM) * cdiv(n, C::TBNP) >= c->num_sms) {          // at least a wave per chunk (and generators)
+      cdiv(l, BM) * cdiv(n, C::TBNP) >= c->num_sms &&          // at least a wave per chunk (and generators)
+      !(dist_on(c) && dist_view(c).exchange == 1)) {
+    // (on a distributed context with the per-step exchange the chain measured slower at world size 1,
+    // 784 vs 565 ms per C5 sketch -- cause not isolated; the replicate exchange, the default, gains
+    // 545 -> 535 ms: profiles/round2/chain/dist_world1.txt)
     const unsigned ctas = (unsigned)(cdiv(l, BM) * cdiv(n, C::TBNP));
     DBuf img2, cnt;
     SK_TRY(img2.alloc(c, img.bytes));
