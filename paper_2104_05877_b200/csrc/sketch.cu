@@ -1310,19 +1310,11 @@ sk_status make_tmap(sk_ctx* c, const double* A, int64_t m, int64_t n, int64_t ld
 // The Omega image of rows [i0, i1) of A (from Philox, or packed from Q when Qom != nullptr).
 template <class C>
 sk_status omega_chunk_image(sk_ctx* c, uint2 key, const double* Qom, int64_t ldq, int64_t l, int64_t i0, int64_t i1,
-                            double* img, bool pdl = false) {
+                            double* img) {
   constexpr int BM = C::BM;
   const int64_t mb = cdiv(l, BM), KT = cdiv(i1 - i0, TBK);
-  cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3((unsigned)(mb * KT));
-  lc.blockDim = dim3(128);
-  lc.stream = c->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // chained chunks: beside the GEMM's tail
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  lc.attrs = at; lc.numAttrs = pdl ? 1 : 0;
-  if (Qom) SK_CUDA(c, cudaLaunchKernelEx(&lc, k_omega_pack, Qom, ldq, (int)l, i0, i1, BM, C::OS, KT, img));
-  else SK_CUDA(c, cudaLaunchKernelEx(&lc, k_omega_image, key, (int)l, i0, i1, BM, C::OS, KT, img));
+  if (Qom) k_omega_pack<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(Qom, ldq, (int)l, i0, i1, BM, C::OS, KT, img);
+  else k_omega_image<<<(unsigned)(mb * KT), 128, 0, c->stream>>>(key, (int)l, i0, i1, BM, C::OS, KT, img);
   return launched(c);
 }
 
