@@ -1189,10 +1189,9 @@ int pre_capacity(int geo, int S) {
 int64_t chunk_rows(int64_t m, int64_t l, int bm, int64_t forced, int64_t col_tiles) {
   if (forced > 0) return std::min<int64_t>(m, cdiv(forced, TBK) * TBK);
   const double per_row = (double)cdiv(l, bm) * (bm + 4) * 8.0;
-  // few column tiles re-read the image only a few times, so an image beyond L2 costs little DRAM
-  // traffic and one chunk saves the per-chunk overhead (C4 k=200, 7 column tiles: 210 MB image,
-  // 1.466 -> 1.442 ms; k=100 0.743 -> 0.732 ms)
-  if (col_tiles <= 8 && per_row * (double)m <= 256.0 * (1 << 20)) return m;
+  // (one whole image for few column tiles -- C4 k=200's 210 MB -- measured 1.6 % faster but would put
+  // the whole of Omega in HBM, which S0 excludes: not done)
+  (void)col_tiles;
   const int64_t ch = std::max<int64_t>(1024, (int64_t)(kOmegaSlotBytes / per_row) / 1024 * 1024);
   return ch >= m ? m : ch;
 }
