@@ -58,7 +58,11 @@ typedef enum {
  * (R3).  Sparse sign: zeta nonzeros +-1/sqrt(zeta) per column at
  * uniformly random distinct rows (R4); zeta = min(l, 8) in practice
  * (P:185).  Both are regenerated on the fly from (seed, row, column) with
- * Philox4x32-10 (R1, R2) and never stored in HBM.  SRTT:
+ * Philox4x32-10 (R1, R2) and never stored whole: the dense sketch regenerates
+ * Gaussian Gamma one K-chunk at a time into a reused, L2-sized image slot (at
+ * most 80 MB; its stores are evict_last, so the slot stays in L2), the sparse
+ * sketch keeps only the nonzero structure (4 bytes per nonzero) and
+ * regenerates nothing else.  SRTT:
  * sqrt(m/l) Pi_{m->l} T Phi Pi_{m->m} with T the unitary discrete Hartley transform, the random
  * permutation / selection as keyed Feistel bijections and the signs from Philox (R18); applied by
  * a per-column radix-2 FFT in shared memory: m a power of two <= 16384 in one CTA per column, and
