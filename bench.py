@@ -616,7 +616,7 @@ def main():
         line = {
             "metric": "skeleton-selection time (sketch+LUPP)", "value": value, "unit": "ms",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": False, "scaling": "weak" if world > 1 else "weak",
+            "higher_is_better": False, "scaling": "strong" if args.config == "C5" else "weak",   # C5: the same matrix column-sharded at N > 1
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "m": m, "n": n, "k": k, "l": l,
                        "l2": "flushed: 512 MiB overwrite between timed steps (untimed)",
