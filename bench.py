@@ -241,6 +241,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def lupp_report(ms, rows, k):
+    """SURVEY 8(d) figures of one LUPP call: rows x k panel, k pivot steps."""
+    flops, nbytes = float(rows) * k * k, 16.0 * rows * k
+    t_lb = max(flops / (FP64_PEAK_TFLOPS * 1e12), nbytes / (hbm_peak_gbs()[0] * 1e9)) * 1e3
+    return {"ms": ms, "us_per_step": ms * 1e3 / k, "gbs": nbytes / (ms * 1e-3) / 1e9,
+            "tflops": flops / (ms * 1e-3) / 1e12, "bound_ms": t_lb, "frac_of_bound": t_lb / ms,
+            "bound": "k sequential argmaxes (chain); bandwidth / flop bound max(F/P64, B/BW) as frac_of_bound"}
+
+
 def run_reference(args):
     """--impl reference: the oracle on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -401,6 +410,7 @@ def main_dist(args, world, rank, local):
                        "parallelism": f"column-sharded x{world}", "lupp_exchange": exchange,
                        "l2": "flushed: 512 MiB overwrite between timed steps (untimed); A (68.7 GB) >> L2"},
             "stages_ms": stage,
+            "lupp": {"select_cols": lupp_report(stage["select_cols_lupp"], n, k)},
             "residual": {"col_id_fro": r, "normA_fro": nA, "opt_fro": opt, "col_id_ratio": r / opt},
             "roofline": {"kernel": "sk_sketch Gaussian (k_omega_image + k_sketch_pre per K-chunk), rank 0's block",
                          "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
@@ -611,6 +621,21 @@ def main():
         cpu = {"value": cpu_ms, "unit": "ms", "cores": cores, "kind": "oracle",
                "sample": f"one full {args.config} selection (sketch{' with %d power iteration(s)' % args.piter if args.piter else ''} + LUPP), numpy/BLAS on {model}",
                "pivots_equal_to_gpu": same}
+        if args.config in ("C1", "C2"):   # the small configs also at one thread
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                t0 = time.perf_counter()
+                try:
+                    oracle_selection(A_np, k, l, seed, emb, args.piter, args.plain_piter)
+                except RankError:
+                    pass
+                cpu["value_1thread"] = (time.perf_counter() - t0) * 1e3
+
+    # every LUPP against max(F / P64, B / BW) with F = rows * k^2 flop and B = 16 * rows * k
+    # bytes (the panel read and the factor written once); the k sequential argmaxes bound it in practice
+    lupp = {"select_cols": lupp_report(statistics.mean(stage_ms["select_cols_lupp"]), n, k)}
+    if do_rows:
+        lupp["select_rows"] = lupp_report(statistics.mean(stage_ms["select_rows_lupp"]), m, k)
 
     if rank == 0:
         line = {
@@ -622,7 +647,9 @@ def main():
                        "l2": "flushed: 512 MiB overwrite between timed steps (untimed)",
                        "parallelism": "replicas" if world > 1 else "1 GPU"},
             "stages_ms": {nm: statistics.mean(v) for nm, v in stage_ms.items()},
+            "stages_median_ms": {nm: statistics.median(v) for nm, v in stage_ms.items()},
             "sketch_rate": {"value": achieved, "unit": roofline["unit"]},
+            "lupp": lupp,
             "residual": resid,
             "cpqr_overlap": int(len(set(Js.cpu().tolist()) & set(Jc.cpu().tolist()))) if Jc is not None else None,
             "roofline": roofline,
