@@ -539,12 +539,14 @@ def main():
 
     # roofline of the dominant kernel of the selection: the sketch (one launch per call)
     sk_ms = statistics.mean(stage_ms["sketch"])
-    traffic = None
+    traffic = traffic_note = None
     tf = os.path.join(ROOT, "profiles", "round2", "sketch_dram_bytes.json")
     if os.path.exists(tf):
         try:
             # measured for the one-pass sketch only (tools/sketch_traffic.py); power iterations differ
-            traffic = None if args.piter else json.load(open(tf)).get(f"{args.config}_k{k}")
+            tj = json.load(open(tf))
+            traffic = None if args.piter else tj.get(f"{args.config}_k{k}")
+            traffic_note = tj.get("_note") if traffic is not None else None
         except Exception:
             traffic = None
     if emb == "sparse_sign":
@@ -563,6 +565,8 @@ def main():
                     "peak_source": "measured FP64 DMMA ceiling (tools/microbench/fp64_pipes.cu, "
                                    "profiles/round1/fp64_pipes.txt); MEASURED_PEAKS.json has no FP64 entry; "
                                    "cuBLAS DGEMM measured 35.5"}
+    roofline["algorithmic_bytes"] = 8.0 * (m * n + l * n)
+    roofline["traffic_note"] = traffic_note
 
     # end to end through the public API with host buffers (Algorithm 2 entry point)
     e2e = None
