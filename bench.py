@@ -445,6 +445,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(dev)
+    apply_sketch_tuning(args, sk, local)                     # A/B only; the default line leaves the planner alone
 
     cfg, k, l, seed, desc = workload(args)
     emb = cfg["emb"]
