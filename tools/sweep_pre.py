@@ -11,7 +11,7 @@ import paper_2104_05877_b200 as sk  # noqa: E402
 SHAPES = [("C2 k=16", 4096, 4096, 26), ("C2 k=64", 4096, 4096, 74), ("C2 k=256", 4096, 4096, 266),
           ("C2 k=512", 4096, 4096, 522), ("C4 k=50", 65536, 784, 100), ("C4 k=100", 65536, 784, 200),
           ("C4 k=200", 65536, 784, 400), ("C5 block", 131072, 8192, 1100), ("C5 rows", 16384, 65536, 1100)]
-PLANS = [(64, 8), (48, 8), (40, 8), (32, 8), (40, 7), (48, 7), (80, 4), (40, 2), (48, 12), (80, 12)]   # (bm, warps); 4 / 2 = 112-column tiles, 12 = 384 / 192
+PLANS = [(64, 8), (56, 8), (96, 8), (48, 8), (40, 8), (32, 8), (40, 7), (48, 7), (80, 4), (40, 2), (48, 12), (80, 12)]   # (bm, warps); 4 / 2 = 112-column tiles, 12 = 384 / 192
 
 
 def timed(fn, reps=5):
