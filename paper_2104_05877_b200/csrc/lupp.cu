@@ -705,21 +705,42 @@ constexpr size_t v2_smem_bytes() {
 
 // U(c0+s, j) = M(piv_s, j) - sum_{s'<s} L11(s, s') U(c0+s', j), j in [c1, k).
 // One thread per column, the column of U in registers (bp <= U12_BP), L11 broadcast from smem.
+// Right-looking: step sp subtracts L11(:, sp) u[sp] from every later row -- the row updates of a step
+// are independent (no accumulator chains, the shared-memory loads of a step all in flight at once),
+// only u[sp + 1] of the next step waits for one FMA.  L11 is held transposed (L11T[sp][s], rows padded
+// to U12_LS) so that one 16-byte broadcast load feeds two rows.
+constexpr int U12_LS = U12_BP + 2;
+template <int BP>
+__device__ __forceinline__ void u12_subst(double (&u)[U12_BP], const double (*L11T)[U12_LS]) {
+  static_assert(BP % 2 == 0, "pairs");
+#pragma unroll
+  for (int sp = 0; sp + 1 < BP; ++sp) {
+    const double us = u[sp];
+    if ((sp + 1) & 1) u[sp + 1] = fma(-L11T[sp][sp + 1], us, u[sp + 1]);
+#pragma unroll
+    for (int s = (sp + 2) & ~1; s + 1 < BP; s += 2) {
+      const double2 l2 = *reinterpret_cast<const double2*>(&L11T[sp][s]);
+      u[s] = fma(-l2.x, us, u[s]);
+      u[s + 1] = fma(-l2.y, us, u[s + 1]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_lupp_u12(const double* W, int64_t n, int k, int c0, int bp,
                                                   const int64_t* Js, const double* Lf, int64_t ldlf,
                                                   double* Uw, const int64_t* status) {
   dev::griddep_wait();
   if (*status != 0) return;
   extern __shared__ __align__(16) double u12sm[];
-  double (*L11)[U12_BP + 1] = reinterpret_cast<double (*)[U12_BP + 1]>(u12sm);
-  double (*Wv)[33] = reinterpret_cast<double (*)[33]>(u12sm + U12_BP * (U12_BP + 1));
-  int64_t* piv = reinterpret_cast<int64_t*>(u12sm + U12_BP * (U12_BP + 1) + U12_BP * 33);
+  double (*L11T)[U12_LS] = reinterpret_cast<double (*)[U12_LS]>(u12sm);      // L11T[sp][s] = L11(s, sp)
+  double (*Wv)[33] = reinterpret_cast<double (*)[33]>(u12sm + U12_BP * U12_LS);
+  int64_t* piv = reinterpret_cast<int64_t*>(u12sm + U12_BP * U12_LS + U12_BP * 33);
   const int j0 = c0 + bp + blockIdx.x * 32;
   for (int s = threadIdx.x; s < bp; s += blockDim.x) piv[s] = Js[c0 + s];
   __syncthreads();
   for (int e = threadIdx.x; e < bp * bp; e += blockDim.x) {      // async gathers: all in flight
     const int s = e % bp, sp = e / bp;
-    if (sp < s) dev::cp_async8(&L11[s][sp], Lf + piv[s] + (int64_t)(c0 + sp) * ldlf, true);
+    if (sp < s) dev::cp_async8(&L11T[sp][s], Lf + piv[s] + (int64_t)(c0 + sp) * ldlf, true);
   }
   for (int e = threadIdx.x; e < bp * 32; e += blockDim.x) {
     const int s = e % bp, cc = e / bp;
@@ -735,20 +756,18 @@ __global__ void __launch_bounds__(256) k_lupp_u12(const double* W, int64_t n, in
   double u[U12_BP];
 #pragma unroll
   for (int s = 0; s < U12_BP; ++s) u[s] = s < bp ? Wv[s][threadIdx.x] : 0.0;
+  if (bp == U12_BP) u12_subst<U12_BP>(u, L11T);
+  else if (bp == 32) u12_subst<32>(u, L11T);
+  else if (bp == 16) u12_subst<16>(u, L11T);
+  else {
 #pragma unroll
-  for (int s = 1; s < U12_BP; ++s) {
-    if (s < bp) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int sp = 0; sp + 1 < U12_BP; ++sp) {
+      if (sp + 1 < bp) {
+        const double us = u[sp];
 #pragma unroll
-      for (int sp = 0; sp + 3 < s; sp += 4) {
-        a0 = fma(L11[s][sp], u[sp], a0);
-        a1 = fma(L11[s][sp + 1], u[sp + 1], a1);
-        a2 = fma(L11[s][sp + 2], u[sp + 2], a2);
-        a3 = fma(L11[s][sp + 3], u[sp + 3], a3);
+        for (int s = sp + 1; s < U12_BP; ++s)
+          if (s < bp) u[s] = fma(-L11T[sp][s], us, u[s]);
       }
-#pragma unroll
-      for (int sp = (s / 4) * 4; sp < s; ++sp) a0 = fma(L11[s][sp], u[sp], a0);
-      u[s] -= (a0 + a1) + (a2 + a3);
     }
   }
 #pragma unroll
@@ -756,7 +775,7 @@ __global__ void __launch_bounds__(256) k_lupp_u12(const double* W, int64_t n, in
     if (s < bp) Uw[(c0 + s) + (int64_t)j * k] = u[s];
 }
 
-constexpr size_t kU12Smem = sizeof(double) * (U12_BP * (U12_BP + 1) + U12_BP * 33 + U12_BP);
+constexpr size_t kU12Smem = sizeof(double) * (U12_BP * U12_LS + U12_BP * 33 + U12_BP);
 
 __global__ void k_copy_u(const double* Uw, int k, double* U, int64_t ldu) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
